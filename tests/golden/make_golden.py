@@ -1,0 +1,143 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (needs /root/reference, via oracle/_ref built by
+``make -C oracle``):
+
+    python tests/golden/make_golden.py
+
+Every array is produced by the unmodified reference library
+(oracle/_ref/libmlra_ref.so: /root/reference/proj/src + oracle/ref_driver.cpp).
+The fixtures pin the C oracle restatement (tests/test_oracle_golden.py) and are
+the known answers the GPU parity tests check the CUDA path against. They ship
+with the repo, so nothing at test time reads /root/reference.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "..", ".."))
+from oracle.oracle import Ref  # noqa: E402
+
+
+def bitpack_cases():
+    """test_bitpack.cpp:29-91 known answers."""
+    out = {}
+    out["kat_words_3120_b2"] = Ref.pack([3, 1, 2, 0], 2)
+    for bits in (2, 3, 4, 8):
+        for n in (0, 1, 5, 31, 32, 33, 64, 100, 200):
+            codes = Ref.random_codes(n, bits, 1000 + n * 10 + bits)  # test_bitpack.cpp:61
+            out[f"rt_b{bits}_n{n}_codes"] = codes
+            out[f"rt_b{bits}_n{n}_words"] = Ref.pack(codes, bits)
+    codes = Ref.random_codes(7 * 9, 3, 5)  # test_bitpack.cpp:78-91 row slices
+    out["rows7x9_codes"] = codes
+    out["rows7x9_words"] = Ref.pack(codes, 3)
+    return out
+
+
+# (rows, cols, bits, group, seed) — reference-test-like shapes (ragged, not
+# row-aligned, e.g. 7x9 at b=3) and LLaMA-aligned tiles (K*b % 128 == 0).
+QUANT_CASES = [
+    (2, 2, 2, 2, None),       # test_quantize.cpp:34-60 hand example (explicit)
+    (7, 9, 3, 3, 101),        # test_lowprec.cpp:98-119 shape, g=3
+    (7, 9, 4, 0, 102),
+    (16, 32, 2, 4, 103),
+    (16, 32, 8, 16, 104),
+    (24, 40, 3, 8, 105),
+    (64, 256, 4, 128, 106),
+    (96, 256, 3, 128, 107),
+    (48, 384, 2, 128, 108),
+    (32, 128, 8, 64, 109),
+]
+
+# (d_out, d_in, bits, group, rank, alpha, m, seed, bias, need_dx)
+LAYER_CASES = [
+    (7, 9, 3, 3, 2, 8.0, 4, 11, True, True),       # test_lora.cpp:123-150 shape
+    (6, 8, 4, 0, 2, 4.0, 3, 12, True, True),       # test_lora.cpp:152-201 shape
+    (24, 40, 2, 8, 4, 8.0, 5, 13, False, True),
+    (64, 128, 4, 32, 8, 32.0, 16, 14, True, False),   # dx skipped (autodiff.cpp:136)
+    (96, 256, 3, 128, 16, 32.0, 20, 15, True, True),
+    (256, 128, 4, 128, 8, 16.0, 12, 16, False, True),
+]
+
+
+def quant_cases():
+    out = {}
+    for i, (rows, cols, bits, group, seed) in enumerate(QUANT_CASES):
+        if seed is None:
+            from oracle.oracle import Ref as R
+            words = R.pack([0, 1, 2, 3], 2)
+            scales = np.array([0.5, 1.0], np.float32)
+            zeros = np.array([-1.0, 0.0], np.float32)
+            g = 2
+        else:
+            w = Ref.gaussian(seed, rows, cols, 0.0, 0.02 if i % 2 else 1.0)
+            words, scales, zeros = Ref.quantize_rtn(w, bits, group)
+            g = cols if group == 0 else group
+            out[f"q{i}_w"] = w
+        deq = Ref.dequantize(words, rows, cols, bits, g, scales, zeros)
+        out[f"q{i}_meta"] = np.array([rows, cols, bits, g], np.int64)
+        out[f"q{i}_words"] = words
+        out[f"q{i}_scales"] = scales
+        out[f"q{i}_zeros"] = zeros
+        out[f"q{i}_deq"] = deq
+    return out
+
+
+def layer_cases():
+    out = {}
+    for i, (d_out, d_in, bits, group, r, alpha, m, seed, bias, need_dx) in enumerate(LAYER_CASES):
+        w = Ref.gaussian(seed, d_out, d_in, 0.0, 0.02)
+        words, scales, zeros = Ref.quantize_rtn(w, bits, group)
+        g = d_in if group == 0 else group
+        b = np.empty((d_in, r))
+        Ref.get().ref_init_adapter_b(d_in, d_out, r, alpha, seed + 1, b)
+        a = Ref.gaussian(seed + 2, d_out, r, 0.0, 0.5)  # off its zero init (acceptance.cpp:116-117)
+        bvec = Ref.gaussian(seed + 3, 1, d_out, 0.0, 0.3) if bias else None
+        x = Ref.gaussian(seed + 4, m, d_in)
+        G = Ref.gaussian(seed + 5, m, d_out)
+        y, dx, da, db, dbias = Ref.layer_fwd_bwd(words, d_out, d_in, bits, g, scales, zeros,
+                                                 a, b, alpha, bvec, x, G, need_dx=need_dx,
+                                                 need_dbias=bias)
+        p = f"l{i}_"
+        out[p + "meta"] = np.array([d_out, d_in, bits, g, r, m, int(bias), int(need_dx)], np.int64)
+        out[p + "alpha"] = np.array([alpha])
+        out[p + "words"] = words
+        out[p + "scales"] = scales
+        out[p + "zeros"] = zeros
+        out[p + "a"] = a
+        out[p + "b"] = b
+        if bias:
+            out[p + "bias"] = bvec.ravel()
+            out[p + "dbias"] = dbias
+        out[p + "x"] = x
+        out[p + "g"] = G
+        out[p + "y"] = y
+        if need_dx:
+            out[p + "dx"] = dx
+        out[p + "da"] = da
+        out[p + "db"] = db
+    return out
+
+
+def main():
+    if not Ref.available():
+        raise SystemExit("oracle/_ref/libmlra_ref.so missing: run `make -C oracle` with /root/reference present")
+    np.savez_compressed(os.path.join(HERE, "bitpack.npz"), **bitpack_cases())
+    np.savez_compressed(os.path.join(HERE, "quantize.npz"), **quant_cases())
+    np.savez_compressed(os.path.join(HERE, "layer.npz"), **layer_cases())
+    meta = {"mix_seed_11_ada9": Ref.get().ref_mix_seed(11, 0xADA9)}
+    np.savez_compressed(os.path.join(HERE, "rng.npz"),
+                        gaussian_seed7=Ref.gaussian(7, 3, 5),
+                        gaussian_seed8_scaled=Ref.gaussian(8, 4, 4, 0.5, 0.02),
+                        mix_seed_11_ada9=np.array([meta["mix_seed_11_ada9"]], np.uint64))
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()
