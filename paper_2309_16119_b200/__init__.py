@@ -1,0 +1,11 @@
+"""B200-native ModuLoRA linear layer (arXiv 2309.16119): fused dequant +
+tcgen05 GEMM kernels for sm_100a behind the reference's hot-path API.
+
+The compute lives in libmlra.so (include/mlra.h); this package is the host-side
+mirror of the reference interface (see modulora.py)."""
+from ._lib import MlraError, build, lib  # noqa: F401
+from .modulora import (  # noqa: F401
+    DeviceQuantizedMatrix, LoraAdapter, LpLinearContext, MaterializationStrategy,
+    ModuLoraLayer, ModuLoraLinearFunction, PackedCodes, QuantizedMatrix, dequantize,
+    dequantize_row, grads_of_adapter, init_adapter, layer_backward, layer_forward, lp_backward,
+    lp_forward, make_layer, packed_word_count, parse_strategy, strategy_name)

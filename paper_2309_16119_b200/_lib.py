@@ -1,0 +1,95 @@
+"""ctypes binding of libmlra.so (include/mlra.h). Fails loudly: there is no
+CPU fallback anywhere in this package."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmlra.so")
+
+MLRA_OK = 0
+STATUS_NAMES = {
+    2: "DimensionError", 3: "ConfigError", 4: "RangeError", 5: "ContractError",
+    6: "NumericError", 7: "FormatError", 8: "CudaError", 9: "UnsupportedDevice",
+}
+WEIGHT, ROW, MATVEC = 0, 1, 2
+F32, BF16 = 0, 1
+
+# Every symbol include/mlra.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = [
+    "mlra_last_error", "mlra_abi_version", "mlra_device_check", "mlra_packed_word_count",
+    "mlra_qweight_create", "mlra_qweight_destroy", "mlra_qweight_info", "mlra_materialize",
+    "mlra_materialize_rows", "mlra_ledger_bytes", "mlra_lp_forward", "mlra_lp_backward",
+    "mlra_lora_forward", "mlra_lora_backward",
+]
+
+
+class MlraError(RuntimeError):
+    """Mirrors the reference exception taxonomy (errors.hpp:15-63)."""
+
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.kind = STATUS_NAMES.get(status, f"status{status}")
+        super().__init__(f"{self.kind}: {msg}")
+
+
+class MlraLora(C.Structure):
+    _fields_ = [
+        ("q", C.c_void_p), ("strategy", C.c_int), ("rank", C.c_int64), ("alpha", C.c_double),
+        ("a", C.c_void_p), ("b", C.c_void_p), ("bias", C.c_void_p),
+    ]
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", os.path.join(HERE, "csrc"), "-j8"], check=True)
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        i64, u64, vp, i32 = C.c_int64, C.c_uint64, C.c_void_p, C.c_int
+        L.mlra_last_error.restype = C.c_char_p
+        L.mlra_abi_version.restype = i32
+        L.mlra_device_check.restype = i32
+        L.mlra_packed_word_count.restype = u64
+        L.mlra_packed_word_count.argtypes = [u64, i32]
+        L.mlra_qweight_create.restype = i32
+        L.mlra_qweight_create.argtypes = [i64, i64, i32, i64, vp, u64, u64, vp, vp, u64, vp,
+                                          C.POINTER(vp)]
+        L.mlra_qweight_destroy.restype = None
+        L.mlra_qweight_destroy.argtypes = [vp]
+        L.mlra_qweight_info.restype = i32
+        L.mlra_qweight_info.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32),
+                                        C.POINTER(i64), C.POINTER(u64), C.POINTER(i64)]
+        L.mlra_materialize.restype = i32
+        L.mlra_materialize.argtypes = [vp, vp, i32, i64, vp]
+        L.mlra_materialize_rows.restype = i32
+        L.mlra_materialize_rows.argtypes = [vp, i64, i64, vp, i32, i64, vp]
+        L.mlra_ledger_bytes.restype = u64
+        L.mlra_ledger_bytes.argtypes = [vp, i32]
+        L.mlra_lp_forward.restype = i32
+        L.mlra_lp_forward.argtypes = [vp, i32, vp, i64, i64, vp, i32, i64, vp]
+        L.mlra_lp_backward.restype = i32
+        L.mlra_lp_backward.argtypes = [vp, i32, vp, i64, i64, vp, i32, i64, vp]
+        L.mlra_lora_forward.restype = i32
+        L.mlra_lora_forward.argtypes = [C.POINTER(MlraLora), vp, i64, i64, vp, i32, i64, vp, vp]
+        L.mlra_lora_backward.restype = i32
+        L.mlra_lora_backward.argtypes = [C.POINTER(MlraLora), vp, i64, vp, vp, i64, i64, vp, i32,
+                                         i64, vp, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != MLRA_OK:
+        raise MlraError(status, lib().mlra_last_error().decode())

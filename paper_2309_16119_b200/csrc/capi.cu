@@ -1,0 +1,524 @@
+// capi.cu — the C ABI of include/mlra.h: validation with the reference's error
+// taxonomy, device upload, workspace, and the kernel sequence of one
+// ModuLoRA linear forward / backward.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mlra.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "qgemm.h"
+
+using mlra::QWeightDev;
+
+struct mlra_qweight {
+  QWeightDev d{};
+  uint32_t* words = nullptr;
+  float2* grid = nullptr;
+  uint64_t device_bytes = 0;
+  int64_t uncertified = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+mlra_status fail(mlra_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(MLRA_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),     \
+                  __FILE__, __LINE__);                                                \
+  } while (0)
+
+bool supported_bits(int b) { return b == 2 || b == 3 || b == 4 || b == 8; }
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+mlra_status check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess)
+    return fail(MLRA_ERR_UNSUPPORTED, "no CUDA device: %s", cudaGetErrorString(e));
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(MLRA_ERR_UNSUPPORTED, "libmlra is built for sm_100a (B200); device is sm_%d%d",
+                major, minor);
+  return MLRA_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor [outer x inner] (row stride ld elements), SWIZZLE_128B box.
+mlra_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu",
+                static_cast<int>(r), (unsigned long long)inner, (unsigned long long)outer,
+                (unsigned long long)ld);
+  return MLRA_OK;
+}
+
+// Stream-ordered scratch owned by one API call.
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, count * sizeof(T) + 16, st) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+// Activations must be 16-byte aligned rows for TMA and the vectorized skinny
+// kernels; otherwise copy into an aligned scratch.
+mlra_status aligned_act(Scratch& sc, const void* p, int64_t ld, int64_t m, int64_t cols,
+                        const __nv_bfloat16** out, int64_t* out_ld) {
+  if (ld % 8 == 0 && reinterpret_cast<uintptr_t>(p) % 16 == 0) {
+    *out = static_cast<const __nv_bfloat16*>(p);
+    *out_ld = ld;
+    return MLRA_OK;
+  }
+  const int64_t nld = round_up(cols, 8);
+  auto* buf = sc.get<__nv_bfloat16>(static_cast<size_t>(m * nld));
+  if (!buf) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  CUDA_TRY(cudaMemcpy2DAsync(buf, nld * 2, p, ld * 2, cols * 2, m, cudaMemcpyDeviceToDevice,
+                             sc.st));
+  *out = buf;
+  *out_ld = nld;
+  return MLRA_OK;
+}
+
+mlra_status check_q(const mlra_qweight* q) {
+  if (!q) return fail(MLRA_ERR_CONTRACT, "lp_linear: missing quantized weights");
+  return MLRA_OK;
+}
+
+// One base GEMM (+ optional LoRA extra K) launch.
+struct GemmPlan {
+  bool mn;               // false: forward, true: dX
+  const __nv_bfloat16* act;
+  int64_t ld_act;
+  int64_t k_red_valid;   // valid reduction extent of the activations
+  const __nv_bfloat16* act_lora = nullptr;   // [m x rp]
+  const __nv_bfloat16* w_lora = nullptr;     // [m_total x rp]
+  int64_t rp = 0, rank = 0;
+  int64_t tokens;
+  void* out;
+  int64_t ldo;
+  bool out_f32;
+  const float* bias = nullptr;
+};
+
+mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPlan& gp,
+                     Scratch& sc) {
+  const QWeightDev& d = q->d;
+  mlra::GemmMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  mlra::GemmArgs a{};
+  a.m_total = gp.mn ? d.cols_pad : d.rows_pad;
+  a.m_valid = gp.mn ? d.cols : d.rows;
+  a.n_kb_main = static_cast<int>((gp.mn ? d.rows_pad : d.cols_pad) / 64);
+  a.n_kb_lora = gp.rank > 0 ? static_cast<int>(gp.rp / 64) : 0;
+  if (a.n_kb_lora) {
+    const int64_t last = gp.rank - 64 * (a.n_kb_lora - 1);
+    a.lora_k16_last = static_cast<int>((last + 15) / 16);
+  }
+  a.tokens = gp.tokens;
+  a.out = gp.out;
+  a.ldo = gp.ldo;
+  a.bias = gp.bias;
+  mlra_status st = make_map(&maps.act, gp.act, gp.k_red_valid, gp.tokens, gp.ld_act, 64, 256);
+  if (st) return st;
+  if (a.n_kb_lora) {
+    if ((st = make_map(&maps.act_lora, gp.act_lora, gp.rp, gp.tokens, gp.rp, 64, 256))) return st;
+    if ((st = make_map(&maps.w_lora, gp.w_lora, gp.rp, a.m_total, gp.rp, 64, 128))) return st;
+  } else {
+    maps.act_lora = maps.act;
+    maps.w_lora = maps.act;
+  }
+  const bool w_tma = strategy == MLRA_WEIGHT;
+  if (w_tma) {
+    // WeightMaterialize: the whole Ŵ in HBM for this pass (bf16), freed on return
+    auto* w = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows * d.cols_pad));
+    if (!w) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+    CUDA_TRY(mlra::launch_materialize(d, 0, d.rows, w, d.cols_pad, false, sc.st));
+    if ((st = make_map(&maps.w, w, d.cols, d.rows, d.cols_pad, 64, gp.mn ? 64 : 128))) return st;
+  } else {
+    maps.w = maps.act;
+  }
+  CUDA_TRY(mlra::qgemm_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
+  return MLRA_OK;
+}
+
+mlra_status check_lora(const mlra_lora* L) {
+  if (!L) return fail(MLRA_ERR_CONTRACT, "null layer");
+  if (mlra_status st = check_q(L->q)) return st;
+  if (L->rank < 1) return fail(MLRA_ERR_CONFIG, "adapter rank must be >= 1");
+  if (!(L->alpha > 0.0)) return fail(MLRA_ERR_CONFIG, "adapter alpha must be positive");
+  if (L->rank > 256) return fail(MLRA_ERR_CONFIG, "adapter rank %lld > 256 unsupported",
+                                 (long long)L->rank);
+  if (!L->a || !L->b) return fail(MLRA_ERR_CONTRACT, "adapter factors A/B missing");
+  if (L->strategy < MLRA_WEIGHT || L->strategy > MLRA_MATVEC)
+    return fail(MLRA_ERR_CONFIG, "unknown materialization strategy %d", (int)L->strategy);
+  return MLRA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mlra_last_error(void) { return g_last_error.c_str(); }
+int mlra_abi_version(void) { return 1; }
+mlra_status mlra_device_check(void) { return check_device(); }
+
+uint64_t mlra_packed_word_count(uint64_t count, int bits) {
+  return (count * static_cast<uint64_t>(bits) + 31) / 32;
+}
+
+mlra_status mlra_qweight_create(int64_t rows, int64_t cols, int bits, int64_t group,
+                                const uint32_t* words, uint64_t word_count,
+                                uint64_t code_count, const float* scales, const float* zeros,
+                                uint64_t grid_count, void* stream, mlra_qweight** out) {
+  if (!out) return fail(MLRA_ERR_CONTRACT, "null output handle");
+  *out = nullptr;
+  // QuantizedMatrix::validate — quantize.cpp:82-115 (same order, same types)
+  if (!supported_bits(bits))
+    return fail(MLRA_ERR_CONFIG, "QuantizedMatrix: unsupported bit width %d", bits);
+  if (rows <= 0 || cols <= 0 || group <= 0 || cols % group != 0)
+    return fail(MLRA_ERR_CONFIG, "QuantizedMatrix: group size %lld does not divide cols %lld",
+                (long long)group, (long long)cols);
+  if (code_count != static_cast<uint64_t>(rows * cols))
+    return fail(MLRA_ERR_FORMAT, "QuantizedMatrix: code count %llu != rows*cols",
+                (unsigned long long)code_count);
+  const uint64_t ng = static_cast<uint64_t>(rows * (cols / group));
+  if (grid_count != ng)
+    return fail(MLRA_ERR_FORMAT, "QuantizedMatrix: grid count mismatch (%llu, expected %llu)",
+                (unsigned long long)grid_count, (unsigned long long)ng);
+  if (!words || !scales || !zeros) return fail(MLRA_ERR_CONTRACT, "null weight buffers");
+  for (uint64_t i = 0; i < ng; ++i)
+    if (!(scales[i] > 0.0f)) return fail(MLRA_ERR_NUMERIC, "QuantizedMatrix: non-positive scale");
+  // bitpack validate_metadata — bitpack.cpp:37-60
+  const uint64_t expect = mlra_packed_word_count(code_count, bits);
+  if (word_count != expect)
+    return fail(MLRA_ERR_FORMAT,
+                "bitpack: corrupted length metadata: %llu words for %llu codes at %d bits "
+                "(expected %llu)",
+                (unsigned long long)word_count, (unsigned long long)code_count, bits,
+                (unsigned long long)expect);
+  const uint64_t tail = word_count * 32 - code_count * bits;
+  if (word_count && tail > 0 && tail < 32 && (words[word_count - 1] >> (32 - tail)) != 0)
+    return fail(MLRA_ERR_FORMAT, "bitpack: nonzero trailing bits in last word");
+  if (mlra_status st = check_device()) return st;
+
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto* q = new mlra_qweight();
+  QWeightDev& d = q->d;
+  d.rows = rows;
+  d.cols = cols;
+  d.rows_pad = round_up(rows, 256);
+  d.cols_pad = round_up(cols, 256);
+  d.bits = bits;
+  d.group = group;
+  d.ng_pad = (d.cols_pad + group - 1) / group;
+  d.row_words = d.cols_pad * bits / 32;
+  const size_t nwords = static_cast<size_t>(d.rows_pad * d.row_words) + 4;
+  const size_t ngrid = static_cast<size_t>(d.rows_pad * d.ng_pad);
+  auto cleanup = [&](mlra_status st) {
+    if (q->words) cudaFree(q->words);
+    if (q->grid) cudaFree(q->grid);
+    delete q;
+    return st;
+  };
+  if (cudaMalloc(&q->words, nwords * 4) != cudaSuccess ||
+      cudaMalloc(&q->grid, ngrid * sizeof(float2)) != cudaSuccess)
+    return cleanup(fail(MLRA_ERR_CUDA, "device allocation of %zu bytes failed",
+                        nwords * 4 + ngrid * 8));
+  q->device_bytes = nwords * 4 + ngrid * sizeof(float2);
+  d.words = q->words;
+  d.grid = q->grid;
+
+  uint32_t* src_words = nullptr;
+  float *dsc = nullptr, *dz = nullptr;
+  int* dcount = nullptr;
+  auto tmpfree = [&]() {
+    if (src_words) cudaFree(src_words);
+    if (dsc) cudaFree(dsc);
+    if (dz) cudaFree(dz);
+    if (dcount) cudaFree(dcount);
+  };
+  cudaError_t e = cudaSuccess;
+  const bool verbatim = (d.rows_pad == rows) && (d.cols_pad == cols);
+  if (verbatim) {
+    e = cudaMemcpyAsync(q->words, words, word_count * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(q->words + word_count, 0, 16, s);
+  } else {
+    e = cudaMalloc(&src_words, (word_count + 2) * 4);
+    if (e == cudaSuccess) e = cudaMemsetAsync(src_words, 0, (word_count + 2) * 4, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(src_words, words, word_count * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+      e = mlra::launch_relayout(src_words, rows, cols, bits, d.row_words, d.rows_pad, q->words, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(q->words + d.rows_pad * d.row_words, 0, 16, s);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&dsc, ng * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dz, ng * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dcount, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dsc, scales, ng * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dz, zeros, ng * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dcount, 0, sizeof(int), s);
+  if (e == cudaSuccess)
+    e = mlra::launch_grid(dsc, dz, rows, cols / group, d.rows_pad, d.ng_pad, bits, q->grid,
+                          dcount, s);
+  int unc = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&unc, dcount, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  tmpfree();
+  if (e != cudaSuccess)
+    return cleanup(fail(MLRA_ERR_CUDA, "qweight upload: %s", cudaGetErrorString(e)));
+  q->uncertified = unc;
+  *out = q;
+  return MLRA_OK;
+}
+
+void mlra_qweight_destroy(mlra_qweight* q) {
+  if (!q) return;
+  cudaFree(q->words);
+  cudaFree(q->grid);
+  delete q;
+}
+
+mlra_status mlra_qweight_info(const mlra_qweight* q, int64_t* rows, int64_t* cols, int* bits,
+                              int64_t* group, uint64_t* device_bytes, int64_t* uncertified) {
+  if (mlra_status st = check_q(q)) return st;
+  if (rows) *rows = q->d.rows;
+  if (cols) *cols = q->d.cols;
+  if (bits) *bits = q->d.bits;
+  if (group) *group = q->d.group;
+  if (device_bytes) *device_bytes = q->device_bytes;
+  if (uncertified) *uncertified = q->uncertified;
+  return MLRA_OK;
+}
+
+uint64_t mlra_ledger_bytes(const mlra_qweight* q, mlra_strategy strategy) {
+  if (!q || strategy != MLRA_WEIGHT) return 0;
+  return static_cast<uint64_t>(q->d.rows) * static_cast<uint64_t>(q->d.cols) * 2u;
+}
+
+mlra_status mlra_materialize_rows(const mlra_qweight* q, int64_t row0, int64_t nrows, void* out,
+                                  mlra_dtype dtype, int64_t ld, void* stream) {
+  if (mlra_status st = check_q(q)) return st;
+  if (row0 < 0 || nrows < 0 || row0 + nrows > q->d.rows)
+    return fail(MLRA_ERR_RANGE, "dequantize_row: rows [%lld, %lld) out of range [0, %lld)",
+                (long long)row0, (long long)(row0 + nrows), (long long)q->d.rows);
+  if (ld < q->d.cols)
+    return fail(MLRA_ERR_DIMENSION, "dequantize_into: buffer size mismatch (ld %lld < cols %lld)",
+                (long long)ld, (long long)q->d.cols);
+  if (dtype != MLRA_F32 && dtype != MLRA_BF16) return fail(MLRA_ERR_CONFIG, "bad dtype");
+  if (mlra_status st = check_device()) return st;
+  CUDA_TRY(mlra::launch_materialize(q->d, row0, nrows, out, ld, dtype == MLRA_F32,
+                                    static_cast<cudaStream_t>(stream)));
+  return MLRA_OK;
+}
+
+mlra_status mlra_materialize(const mlra_qweight* q, void* out, mlra_dtype dtype, int64_t ld,
+                             void* stream) {
+  if (mlra_status st = check_q(q)) return st;
+  return mlra_materialize_rows(q, 0, q->d.rows, out, dtype, ld, stream);
+}
+
+mlra_status mlra_lp_forward(const mlra_qweight* q, mlra_strategy strategy, const void* x,
+                            int64_t ldx, int64_t m, void* y, mlra_dtype y_dtype, int64_t ldy,
+                            void* stream) {
+  if (mlra_status st = check_q(q)) return st;
+  if (m < 0) return fail(MLRA_ERR_DIMENSION, "lp_forward: negative token count");
+  if (ldx < q->d.cols)
+    return fail(MLRA_ERR_DIMENSION, "lp_forward: input cols %lld != weight cols %lld",
+                (long long)ldx, (long long)q->d.cols);
+  if (ldy < q->d.rows) return fail(MLRA_ERR_DIMENSION, "lp_forward: output ld < rows");
+  if (strategy < MLRA_WEIGHT || strategy > MLRA_MATVEC)
+    return fail(MLRA_ERR_CONFIG, "unknown materialization strategy %d", (int)strategy);
+  if (mlra_status st = check_device()) return st;
+  if (m == 0) return MLRA_OK;
+  Scratch sc(static_cast<cudaStream_t>(stream));
+  GemmPlan gp{};
+  gp.mn = false;
+  if (mlra_status st = aligned_act(sc, x, ldx, m, q->d.cols, &gp.act, &gp.ld_act)) return st;
+  gp.k_red_valid = q->d.cols;
+  gp.tokens = m;
+  gp.out = y;
+  gp.ldo = ldy;
+  gp.out_f32 = y_dtype == MLRA_F32;
+  return run_gemm(q, strategy, gp, sc);
+}
+
+mlra_status mlra_lp_backward(const mlra_qweight* q, mlra_strategy strategy, const void* g,
+                             int64_t ldg, int64_t m, void* dx, mlra_dtype dx_dtype,
+                             int64_t lddx, void* stream) {
+  if (mlra_status st = check_q(q)) return st;
+  if (m < 0) return fail(MLRA_ERR_DIMENSION, "lp_backward: negative token count");
+  if (ldg < q->d.rows)
+    return fail(MLRA_ERR_DIMENSION, "lp_backward: grad cols %lld != weight rows %lld",
+                (long long)ldg, (long long)q->d.rows);
+  if (lddx < q->d.cols) return fail(MLRA_ERR_DIMENSION, "lp_backward: output ld < cols");
+  if (strategy < MLRA_WEIGHT || strategy > MLRA_MATVEC)
+    return fail(MLRA_ERR_CONFIG, "unknown materialization strategy %d", (int)strategy);
+  if (mlra_status st = check_device()) return st;
+  if (m == 0) return MLRA_OK;
+  Scratch sc(static_cast<cudaStream_t>(stream));
+  GemmPlan gp{};
+  gp.mn = true;
+  if (mlra_status st = aligned_act(sc, g, ldg, m, q->d.rows, &gp.act, &gp.ld_act)) return st;
+  gp.k_red_valid = q->d.rows;
+  gp.tokens = m;
+  gp.out = dx;
+  gp.ldo = lddx;
+  gp.out_f32 = dx_dtype == MLRA_F32;
+  return run_gemm(q, strategy, gp, sc);
+}
+
+mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, int64_t m, void* y,
+                              mlra_dtype y_dtype, int64_t ldy, float* xb, void* stream) {
+  if (mlra_status st = check_lora(L)) return st;
+  const QWeightDev& d = L->q->d;
+  if (m < 0) return fail(MLRA_ERR_DIMENSION, "layer: negative token count");
+  if (ldx < d.cols)
+    return fail(MLRA_ERR_DIMENSION, "layer: input cols %lld != d_in %lld", (long long)ldx,
+                (long long)d.cols);
+  if (ldy < d.rows) return fail(MLRA_ERR_DIMENSION, "layer: output ld < d_out");
+  if (!xb) return fail(MLRA_ERR_CONTRACT, "layer: xb buffer required (saved for backward)");
+  if (mlra_status st = check_device()) return st;
+  if (m == 0) return MLRA_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Scratch sc(s);
+  const int64_t r = L->rank, rp = round_up(r, 64);
+  const float scaling = static_cast<float>(L->alpha / static_cast<double>(r));
+  GemmPlan gp{};
+  gp.mn = false;
+  if (mlra_status st = aligned_act(sc, x, ldx, m, d.cols, &gp.act, &gp.ld_act)) return st;
+  auto* xbs = sc.get<__nv_bfloat16>(static_cast<size_t>(m * rp));
+  auto* apad = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows_pad * rp));
+  if (!xbs || !apad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  CUDA_TRY(cudaMemsetAsync(xbs, 0, m * rp * 2, s));
+  // K4: xb = x·B (matmul(t, x, B), lora.cpp:68) and bf16(s·xb) for the extra K
+  CUDA_TRY(mlra::launch_rowdot(gp.act, gp.ld_act, m, d.cols, L->b, r, scaling, xb, xbs, rp, s));
+  CUDA_TRY(mlra::launch_pad_bf16(L->a, d.rows, r, r, apad, d.rows_pad, rp, s));
+  gp.k_red_valid = d.cols;
+  gp.act_lora = xbs;
+  gp.w_lora = apad;
+  gp.rp = rp;
+  gp.rank = r;
+  gp.tokens = m;
+  gp.out = y;
+  gp.ldo = ldy;
+  gp.out_f32 = y_dtype == MLRA_F32;
+  gp.bias = L->bias;
+  // K2: y = x·Ŵᵀ + (s·xb)·Aᵀ + bias
+  return run_gemm(L->q, L->strategy, gp, sc);
+}
+
+mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, const float* xb,
+                               const void* dy, int64_t lddy, int64_t m, void* dx,
+                               mlra_dtype dx_dtype, int64_t lddx, float* da, float* db,
+                               float* dbias, void* stream) {
+  if (mlra_status st = check_lora(L)) return st;
+  const QWeightDev& d = L->q->d;
+  if (m < 0) return fail(MLRA_ERR_DIMENSION, "layer: negative token count");
+  if (ldx < d.cols) return fail(MLRA_ERR_DIMENSION, "layer: input ld < d_in");
+  if (lddy < d.rows)
+    return fail(MLRA_ERR_DIMENSION, "lp_backward: grad cols %lld != weight rows %lld",
+                (long long)lddy, (long long)d.rows);
+  if (dx && lddx < d.cols) return fail(MLRA_ERR_DIMENSION, "layer: dx ld < d_in");
+  if (!xb || !da || !db) return fail(MLRA_ERR_CONTRACT, "layer: xb/dA/dB buffers required");
+  if (mlra_status st = check_device()) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t r = L->rank, rp = round_up(r, 64);
+  CUDA_TRY(cudaMemsetAsync(da, 0, d.rows * r * 4, s));
+  CUDA_TRY(cudaMemsetAsync(db, 0, d.cols * r * 4, s));
+  if (dbias) CUDA_TRY(cudaMemsetAsync(dbias, 0, d.rows * 4, s));
+  if (m == 0) return MLRA_OK;
+  Scratch sc(s);
+  const float scaling = static_cast<float>(L->alpha / static_cast<double>(r));
+  const __nv_bfloat16 *xa, *dya;
+  int64_t ldxa, lddya;
+  if (mlra_status st = aligned_act(sc, x, ldx, m, d.cols, &xa, &ldxa)) return st;
+  if (mlra_status st = aligned_act(sc, dy, lddy, m, d.rows, &dya, &lddya)) return st;
+  auto* dyA = sc.get<float>(static_cast<size_t>(m * r));
+  auto* dyas = sc.get<__nv_bfloat16>(static_cast<size_t>(m * rp));
+  if (!dyA || !dyas) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  CUDA_TRY(cudaMemsetAsync(dyas, 0, m * rp * 2, s));
+  // K5a: dyA = dy·A ; d(xb) = s·dyA (autodiff.cpp:150-152 on record lora.cpp:69)
+  CUDA_TRY(mlra::launch_rowdot(dya, lddya, m, d.rows, L->a, r, scaling, dyA, dyas, rp, s));
+  // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
+  CUDA_TRY(mlra::launch_coldot(dya, lddya, m, d.rows, xb, r, scaling, da, dbias, s));
+  // K6: dB = s·xᵀ·dyA   (autodiff.cpp:153-155 on record lora.cpp:68)
+  CUDA_TRY(mlra::launch_coldot(xa, ldxa, m, d.cols, dyA, r, scaling, db, nullptr, s));
+  if (!dx) return MLRA_OK;  // frozen input: no dX (autodiff.cpp:136)
+  auto* bpad = sc.get<__nv_bfloat16>(static_cast<size_t>(d.cols_pad * rp));
+  if (!bpad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  CUDA_TRY(mlra::launch_pad_bf16(L->b, d.cols, r, r, bpad, d.cols_pad, rp, s));
+  GemmPlan gp{};
+  gp.mn = true;
+  gp.act = dya;
+  gp.ld_act = lddya;
+  gp.k_red_valid = d.rows;
+  gp.act_lora = dyas;
+  gp.w_lora = bpad;
+  gp.rp = rp;
+  gp.rank = r;
+  gp.tokens = m;
+  gp.out = dx;
+  gp.ldo = lddx;
+  gp.out_f32 = dx_dtype == MLRA_F32;
+  // K3: dx = dy·Ŵ + (s·dyA)·Bᵀ   (lp_backward + matmul-bwd dx, lora.cpp:68)
+  return run_gemm(L->q, L->strategy, gp, sc);
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// common.cuh — device-resident frozen weight layout and the exact dequant unit.
+//
+// Device layout of a QuantizedMatrix (quantize.hpp:29-48):
+//   * codes: the reference's LSB-first bitstream (bitpack.cpp:25-35), but laid
+//     out ROW-PADDED: rows_pad x cols_pad codes, each row starting on a word
+//     (rows_pad, cols_pad = multiples of 256). When rows and cols are already
+//     multiples of 256 this IS the reference's whole-matrix stream, uploaded
+//     verbatim (every BASELINE shape); otherwise a relayout kernel builds it.
+//     Pad codes are 0.
+//   * grid: float2 {s', z} per (row, group), rows_pad x ng_pad. s' = +s when the
+//     group is "fma-certified" (fmaf(s,c,z) == (float)(double(s)*c+double(z))
+//     for every code c), else -s (validate() guarantees s > 0, so the sign bit
+//     is free). Pad groups are {1, 0}, so pad entries dequantize to exactly 0.
+//
+// Dequant contract: the f32 value of an entry is
+// RN_f32(double(s)*c + double(z)) — bit-identical to (float) of the
+// reference's f64 dequantize (quantize.cpp:123-137). Certified groups compute
+// it with one fp32 FMA (exact: the f64 sum is exact there, so both roundings
+// coincide); uncertified groups take the f64 path. bf16 = RN(f32).
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace mlra {
+
+struct QWeightDev {
+  int64_t rows, cols;          // logical d_out (N), d_in (K)
+  int64_t rows_pad, cols_pad;  // multiples of 256
+  int bits;
+  int64_t group;               // group size along cols (divides cols)
+  int64_t ng_pad;              // groups per padded row = ceil(cols_pad / group)
+  int64_t row_words;           // 32-bit words per padded row = cols_pad*bits/32
+  const uint32_t* words;       // rows_pad * row_words (+ 4 words slack)
+  const float2* grid;          // rows_pad * ng_pad
+};
+
+// Bits of the 8 consecutive codes of unit `u` (codes 8u..8u+7) of a
+// word-aligned row, at the LSB of the result (bitpack.cpp:25-35 restated for
+// 8 codes at a time).
+template <int BITS>
+__device__ __forceinline__ uint64_t load_unit(const uint32_t* __restrict__ rw, int64_t u) {
+  if constexpr (BITS == 4) {
+    return __ldg(rw + u);
+  } else if constexpr (BITS == 8) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(rw) + u);
+    return static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32);
+  } else if constexpr (BITS == 2) {
+    const uint32_t w = __ldg(rw + (u >> 1));
+    return (w >> ((u & 1) * 16)) & 0xFFFFu;
+  } else {  // 3 bits: 24-bit unit at bit 24u, may straddle two words
+    const int64_t bit = u * 24;
+    const int64_t w0 = bit >> 5;
+    const uint32_t off = static_cast<uint32_t>(bit & 31);
+    uint64_t v = __ldg(rw + w0) >> off;
+    if (off > 8) v |= static_cast<uint64_t>(__ldg(rw + w0 + 1)) << (32 - off);
+    return v & 0xFFFFFFu;
+  }
+}
+
+__device__ __forceinline__ float code_to_f32(uint32_t c) {
+  // exact int -> float for c < 2^23 without the I2F pipe
+  return __int_as_float(0x4B000000u | c) - 8388608.0f;
+}
+
+// One dequantized entry, exact per the contract above. sg = signed scale.
+__device__ __forceinline__ float deq_entry(uint32_t c, float sg, float z) {
+  if (sg > 0.0f) return __fmaf_rn(sg, code_to_f32(c), z);
+  return __double2float_rn(__fma_rn(static_cast<double>(-sg), static_cast<double>(c),
+                                    static_cast<double>(z)));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// 8 codes sharing one grid entry -> 8 f32 values.
+template <int BITS>
+__device__ __forceinline__ void deq8_f32(uint64_t v, float2 g, float (&f)[8]) {
+  constexpr uint32_t mask = (1u << BITS) - 1u;
+  if (g.x > 0.0f) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      f[i] = __fmaf_rn(g.x, code_to_f32(static_cast<uint32_t>(v >> (BITS * i)) & mask), g.y);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      f[i] = deq_entry(static_cast<uint32_t>(v >> (BITS * i)) & mask, g.x, g.y);
+  }
+}
+
+template <int BITS>
+__device__ __forceinline__ uint4 deq8_bf16(uint64_t v, float2 g) {
+  float f[8];
+  deq8_f32<BITS>(v, g, f);
+  uint4 o;
+  o.x = pack_bf16x2(f[0], f[1]);
+  o.y = pack_bf16x2(f[2], f[3]);
+  o.z = pack_bf16x2(f[4], f[5]);
+  o.w = pack_bf16x2(f[6], f[7]);
+  return o;
+}
+
+// General unit: groups may change inside the 8 codes (group % 8 != 0; only the
+// small ragged reference-test shapes hit this).
+template <int BITS>
+__device__ __forceinline__ void deq8_f32_general(uint64_t v, const float2* __restrict__ grow,
+                                                 int64_t k0, int64_t group, float (&f)[8]) {
+  constexpr uint32_t mask = (1u << BITS) - 1u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 g = __ldg(grow + (k0 + i) / group);
+    f[i] = deq_entry(static_cast<uint32_t>(v >> (BITS * i)) & mask, g.x, g.y);
+  }
+}
+
+template <int BITS>
+__device__ __forceinline__ uint4 deq8_bf16_general(uint64_t v, const float2* __restrict__ grow,
+                                                   int64_t k0, int64_t group) {
+  float f[8];
+  deq8_f32_general<BITS>(v, grow, k0, group, f);
+  uint4 o;
+  o.x = pack_bf16x2(f[0], f[1]);
+  o.y = pack_bf16x2(f[2], f[3]);
+  o.z = pack_bf16x2(f[4], f[5]);
+  o.w = pack_bf16x2(f[6], f[7]);
+  return o;
+}
+
+}  // namespace mlra

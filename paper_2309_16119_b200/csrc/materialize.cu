@@ -1,0 +1,194 @@
+// materialize.cu — K1 (the plugin's materialize()) and the upload-time kernels.
+//
+//  * k_relayout: reference whole-matrix bitstream (bitpack.cpp:25-35) ->
+//    row-padded device layout (common.cuh). Only for shapes whose rows are
+//    not already word-aligned multiples of 256.
+//  * k_grid: f32 scales/zeros (quantize.hpp:36-37) -> signed float2 grid with
+//    the per-group fma certificate (common.cuh).
+//  * k_materialize: Ŵ = RN(double(s)·c + double(z)) (quantize.cpp:123-137,
+//    139-155) into f32 or bf16, bit-exact with (float)dequantize().
+//    HBM-bound: reads b/8 + 8/g bytes and writes 2 or 4 bytes per entry.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mlra {
+
+namespace {
+
+__device__ __forceinline__ uint32_t read_code_ref(const uint32_t* __restrict__ w, int bits,
+                                                  uint64_t index) {
+  // bitpack.cpp:25-35
+  const uint64_t bit = index * static_cast<uint64_t>(bits);
+  const uint64_t word = bit >> 5, off = bit & 31;
+  uint64_t v = w[word] >> off;
+  if (off + bits > 32) v |= static_cast<uint64_t>(w[word + 1]) << (32 - off);
+  return static_cast<uint32_t>(v) & ((1u << bits) - 1u);
+}
+
+__global__ void k_relayout(const uint32_t* __restrict__ src, int64_t rows, int64_t cols, int bits,
+                           int64_t row_words, int64_t rows_pad, uint32_t* __restrict__ dst) {
+  const int64_t total = rows_pad * row_words;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / row_words, w = i % row_words;
+    uint32_t out = 0;
+    if (r < rows) {
+      // codes whose bits intersect [32w, 32w+32) of this padded row
+      const int64_t b0 = w * 32;
+      const int64_t c_first = b0 / bits, c_last = (b0 + 31) / bits;
+      for (int64_t c = c_first; c <= c_last; ++c) {
+        if (c >= cols) break;
+        const uint32_t code = read_code_ref(src, bits, static_cast<uint64_t>(r * cols + c));
+        const int64_t sh = c * bits - b0;  // may be negative for the straddling first code
+        if (sh >= 0)
+          out |= code << sh;
+        else
+          out |= code >> (-sh);
+      }
+    }
+    dst[i] = out;
+  }
+}
+
+__global__ void k_grid(const float* __restrict__ scales, const float* __restrict__ zeros,
+                       int64_t rows, int64_t ng, int64_t rows_pad, int64_t ng_pad, int bits,
+                       float2* __restrict__ grid, int* __restrict__ n_uncertified) {
+  const int64_t total = rows_pad * ng_pad;
+  int local = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / ng_pad, g = i % ng_pad;
+    float s = 1.0f, z = 0.0f;
+    if (r < rows && g < ng) {
+      s = scales[r * ng + g];
+      z = zeros[r * ng + g];
+    }
+    bool cert = true;
+    const uint32_t levels = 1u << bits;
+    for (uint32_t c = 0; c < levels; ++c) {
+      const float fast = __fmaf_rn(s, code_to_f32(c), z);
+      const float exact = __double2float_rn(
+          __fma_rn(static_cast<double>(s), static_cast<double>(c), static_cast<double>(z)));
+      if (__float_as_uint(fast) != __float_as_uint(exact)) {
+        cert = false;
+        break;
+      }
+    }
+    if (!cert) ++local;
+    grid[i] = make_float2(cert ? s : -s, z);
+  }
+  if (local) atomicAdd(n_uncertified, local);
+}
+
+// One thread per 8-entry unit of the (logical) matrix.
+template <int BITS, bool F32, bool VEC>
+__global__ void __launch_bounds__(256) k_materialize(const QWeightDev q, int64_t row0,
+                                                     int64_t nrows, void* __restrict__ out,
+                                                     int64_t ld) {
+  const int64_t upr = (q.cols + 7) / 8;  // units per logical row
+  const int64_t total = nrows * upr;
+  const bool fast_group = (q.group % 8) == 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t rr = i / upr, u = i % upr;
+    const int64_t r = row0 + rr;
+    const uint64_t v = load_unit<BITS>(q.words + r * q.row_words, u);
+    const float2* grow = q.grid + r * q.ng_pad;
+    float f[8];
+    if (fast_group)
+      deq8_f32<BITS>(v, __ldg(grow + (u * 8) / q.group), f);
+    else
+      deq8_f32_general<BITS>(v, grow, u * 8, q.group, f);
+    const int64_t k0 = u * 8;
+    if constexpr (VEC) {  // cols % 8 == 0 and ld % 8 == 0: aligned vector stores
+      if constexpr (F32) {
+        float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * ld + k0);
+        o[0] = make_float4(f[0], f[1], f[2], f[3]);
+        o[1] = make_float4(f[4], f[5], f[6], f[7]);
+      } else {
+        uint4 o;
+        o.x = pack_bf16x2(f[0], f[1]);
+        o.y = pack_bf16x2(f[2], f[3]);
+        o.z = pack_bf16x2(f[4], f[5]);
+        o.w = pack_bf16x2(f[6], f[7]);
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * ld + k0) = o;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (k0 + j < q.cols) {
+          if constexpr (F32)
+            reinterpret_cast<float*>(out)[rr * ld + k0 + j] = f[j];
+          else
+            reinterpret_cast<__nv_bfloat16*>(out)[rr * ld + k0 + j] = __float2bfloat16_rn(f[j]);
+        }
+      }
+    }
+  }
+}
+
+int grid_for(int64_t work, int per_block) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t blocks = (work + per_block - 1) / per_block;
+  const int64_t cap = static_cast<int64_t>(sms) * 16;
+  if (blocks > cap) blocks = cap;
+  return static_cast<int>(blocks < 1 ? 1 : blocks);
+}
+
+template <int BITS>
+cudaError_t materialize_bits(const QWeightDev& q, int64_t row0, int64_t nrows, void* out,
+                             int64_t ld, bool f32, cudaStream_t st) {
+  const int64_t units = nrows * ((q.cols + 7) / 8);
+  const int blocks = grid_for(units, 256);
+  const bool vec = (q.cols % 8 == 0) && (ld % 8 == 0) &&
+                   (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  if (f32) {
+    if (vec)
+      k_materialize<BITS, true, true><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
+    else
+      k_materialize<BITS, true, false><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
+  } else {
+    if (vec)
+      k_materialize<BITS, false, true><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
+    else
+      k_materialize<BITS, false, false><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_relayout(const uint32_t* src, int64_t rows, int64_t cols, int bits,
+                            int64_t row_words, int64_t rows_pad, uint32_t* dst,
+                            cudaStream_t st) {
+  k_relayout<<<grid_for(rows_pad * row_words, 256), 256, 0, st>>>(src, rows, cols, bits,
+                                                                  row_words, rows_pad, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grid(const float* scales, const float* zeros, int64_t rows, int64_t ng,
+                        int64_t rows_pad, int64_t ng_pad, int bits, float2* grid,
+                        int* n_uncertified, cudaStream_t st) {
+  k_grid<<<grid_for(rows_pad * ng_pad, 256), 256, 0, st>>>(scales, zeros, rows, ng, rows_pad,
+                                                           ng_pad, bits, grid, n_uncertified);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_materialize(const QWeightDev& q, int64_t row0, int64_t nrows, void* out,
+                               int64_t ld, bool f32, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  switch (q.bits) {
+    case 2: return materialize_bits<2>(q, row0, nrows, out, ld, f32, st);
+    case 3: return materialize_bits<3>(q, row0, nrows, out, ld, f32, st);
+    case 4: return materialize_bits<4>(q, row0, nrows, out, ld, f32, st);
+    case 8: return materialize_bits<8>(q, row0, nrows, out, ld, f32, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mlra

@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Bars:
+  * materialize: bit-exact vs (float) of the reference f64 dequantize, and
+    bf16 = RN of that (the golden fixtures are the reference's own output);
+  * Y / dX tight: normwise rel-Frobenius <= 1e-5 (base GEMM) / 1e-4 (with the
+    bf16 LoRA extra-K block) vs an f64 oracle on the same bf16 operands;
+  * Y / dX loose: <= 4e-3 vs the exact f64 layer on the same inputs;
+  * dA / dB: <= 1e-4 vs the f64 oracle (fp32 intermediates).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from paper_2309_16119_b200 import MlraError
+from paper_2309_16119_b200 import modulora as M
+from tests.conftest import load_golden, rel_fro
+from tests.gpu_util import deq_bf16_f64, f64, qmatrix, random_quantized, to_bf16_dev
+
+pytestmark = pytest.mark.gpu
+
+STRATS = [M.MaterializationStrategy.WeightMaterialize, M.MaterializationStrategy.RowMaterialize,
+          M.MaterializationStrategy.QuantizerMatvec]
+
+
+def _golden_q(gq, i):
+    rows, cols, bits, g = (int(v) for v in gq[f"q{i}_meta"])
+    return rows, cols, bits, g, gq[f"q{i}_words"], gq[f"q{i}_scales"], gq[f"q{i}_zeros"]
+
+
+def test_device_is_b200():
+    assert M.lib().mlra_device_check() == 0, M.lib().mlra_last_error()
+
+
+def test_materialize_golden_bit_exact():
+    gq = load_golden("quantize.npz")
+    i = 0
+    while f"q{i}_meta" in gq:
+        rows, cols, bits, g, words, sc, z = _golden_q(gq, i)
+        dq = M.DeviceQuantizedMatrix(qmatrix(words, rows, cols, bits, g, sc, z))
+        want32 = gq[f"q{i}_deq"].astype(np.float32)
+        got32 = M.dequantize(dq, torch.float32).cpu().numpy()
+        assert np.array_equal(got32.view(np.uint32), want32.view(np.uint32)), f"case {i}"
+        got16 = M.dequantize(dq, torch.bfloat16).view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(got16, orc.f32_to_bf16_bits(want32)), f"case {i}"
+        # row-wise path (dequantize_row_into)
+        r = rows - 1
+        assert np.array_equal(M.dequantize_row(dq, r).cpu().numpy(), want32[r])
+        with pytest.raises(MlraError) as e:
+            M.dequantize_row(dq, rows)
+        assert e.value.kind == "RangeError"
+        i += 1
+    assert i >= 10
+
+
+@pytest.mark.parametrize("rows,cols,bits", [(4096, 4096, 4), (11008, 4096, 3), (4096, 11008, 3),
+                                            (512, 4096, 2), (512, 4096, 8), (256, 17920, 2)])
+def test_materialize_llama_shapes_bit_exact(rows, cols, bits):
+    q, words, sc, z = random_quantized(rows, cols, bits, 128, seed=rows + cols + bits)
+    dq = M.DeviceQuantizedMatrix(q)
+    want = orc.dequantize_f32(words, rows, cols, bits, 128, sc, z)
+    got = M.dequantize(dq, torch.float32).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    got16 = M.dequantize(dq, torch.bfloat16).view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(got16, orc.f32_to_bf16_bits(want))
+
+
+def test_materialize_pathological_grids_take_exact_f64_path():
+    # near-zero group minima: fmaf != (float)f64 for some codes,
+    # so these groups must go through the f64 path to stay bit-exact.
+    rows, cols, bits, g = 256, 512, 4, 128
+    rng = np.random.default_rng(5)
+    codes = rng.integers(0, 16, size=rows * cols, dtype=np.uint32)
+    words = orc.pack(codes, bits)
+    ng = rows * cols // g
+    scales = (2.0 ** -7 * (1 + rng.random(ng))).astype(np.float32)
+    zeros = (np.sign(rng.random(ng) - 0.5) * 2.0 ** -rng.uniform(20, 60, ng)).astype(np.float32)
+    dq = M.DeviceQuantizedMatrix(qmatrix(words, rows, cols, bits, g, scales, zeros))
+    assert dq.info()["uncertified_groups"] > 0
+    want = orc.dequantize_f32(words, rows, cols, bits, g, scales, zeros)
+    got = M.dequantize(dq, torch.float32).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def _lp_check(rows, cols, bits, group, m, strategy, seed):
+    q, words, sc, z = random_quantized(rows, cols, bits, group, seed)
+    g = cols if group == 0 else group
+    dq = M.DeviceQuantizedMatrix(q)
+    ctx = M.LpLinearContext(dq, strategy)
+    x64 = orc.bf16_round(orc.gaussian(seed + 1, m, cols))
+    gy64 = orc.bf16_round(orc.gaussian(seed + 2, m, rows))
+    y = f64(M.lp_forward(ctx, to_bf16_dev(x64), out_dtype=torch.float32))
+    dx = f64(M.lp_backward(ctx, to_bf16_dev(gy64), out_dtype=torch.float32))
+    wbf = deq_bf16_f64(words, rows, cols, bits, g, sc, z)
+    assert rel_fro(y, x64 @ wbf.T) <= 1e-5
+    assert rel_fro(dx, gy64 @ wbf) <= 1e-5
+    wex = orc.dequantize(words, rows, cols, bits, g, sc, z)
+    assert rel_fro(y, x64 @ wex.T) <= 4e-3
+    assert rel_fro(dx, gy64 @ wex) <= 4e-3
+    return y, dx
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("bits", [2, 3, 4, 8])
+def test_lp_forward_backward_tiles(bits, strategy):
+    _lp_check(256, 512, bits, 128, 300, strategy, seed=40 + bits)
+
+
+def test_strategies_bit_identical():
+    ys = [_lp_check(384, 768, 3, 128, 513, s, seed=77) for s in STRATS]
+    for y, dx in ys[1:]:
+        assert np.array_equal(y, ys[0][0]) and np.array_equal(dx, ys[0][1])
+
+
+@pytest.mark.parametrize("rows,cols,bits,group,m", [
+    (7, 9, 3, 3, 4), (24, 40, 2, 8, 5), (96, 256, 3, 128, 20), (300, 200, 4, 0, 33),
+    (4096, 4096, 4, 128, 512)])
+def test_lp_ragged_and_cfg1(rows, cols, bits, group, m):
+    _lp_check(rows, cols, bits, group, m, M.MaterializationStrategy.RowMaterialize,
+              seed=rows + cols)
+
+
+def _layer_run(golden, p, strategy, need_dx=True):
+    d_out, d_in, bits, g, r, m, has_bias, _ = (int(v) for v in golden[p + "meta"])
+    alpha = float(golden[p + "alpha"][0])
+    q = qmatrix(golden[p + "words"], d_out, d_in, bits, g, golden[p + "scales"],
+                golden[p + "zeros"])
+    dq = M.DeviceQuantizedMatrix(q)
+    a32 = golden[p + "a"].astype(np.float32)
+    b32 = golden[p + "b"].astype(np.float32)
+    bias32 = golden[p + "bias"].astype(np.float32) if has_bias else None
+    ad = M.LoraAdapter(a=torch.from_numpy(a32).cuda(), b=torch.from_numpy(b32).cuda(), rank=r,
+                       alpha=alpha)
+    layer = M.ModuLoraLayer("g", dq, ad,
+                            bias=None if bias32 is None else torch.from_numpy(bias32).cuda(),
+                            bias_trainable=bool(has_bias), strategy=strategy)
+    x64 = orc.bf16_round(golden[p + "x"])
+    g64 = orc.bf16_round(golden[p + "g"])
+    x = to_bf16_dev(x64)
+    y, xb = M.layer_forward(layer, x, out_dtype=torch.float32)
+    dx = M.layer_backward(layer, x, xb, to_bf16_dev(g64), need_dx=need_dx,
+                          dx_dtype=torch.float32)
+    w = orc.dequantize(golden[p + "words"], d_out, d_in, bits, g, golden[p + "scales"],
+                       golden[p + "zeros"])
+    # exact f64 reference layer on the same (bf16 activations, fp32 adapter) inputs
+    yr, xbr = orc.layer_forward(w, a32, b32, alpha, bias32, x64)
+    dxr, dar, dbr, dbiasr = orc.layer_backward(w, a32, b32, alpha, x64, xbr, g64, need_dx=need_dx,
+                                               need_dbias=bool(has_bias))
+    return dict(layer=layer, y=f64(y), xb=f64(xb), dx=None if dx is None else f64(dx),
+                yr=yr, xbr=xbr, dxr=dxr, dar=dar, dbr=dbr, dbiasr=dbiasr)
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_layer_golden_cases(strategy):
+    gl = load_golden("layer.npz")
+    i = 0
+    while f"l{i}_meta" in gl:
+        p = f"l{i}_"
+        need_dx = bool(gl[p + "meta"][7])
+        o = _layer_run(gl, p, strategy, need_dx)
+        assert rel_fro(o["xb"], o["xbr"]) <= 1e-5, i
+        assert rel_fro(o["y"], o["yr"]) <= 4e-3, i
+        if need_dx:
+            assert rel_fro(o["dx"], o["dxr"]) <= 4e-3, i
+        else:
+            assert o["dx"] is None
+        da, db = M.grads_of_adapter(o["layer"])
+        assert rel_fro(f64(da), o["dar"]) <= 1e-4, i
+        assert rel_fro(f64(db), o["dbr"]) <= 1e-4, i
+        if o["dbiasr"] is not None:
+            assert rel_fro(f64(o["layer"].grad_bias), o["dbiasr"]) <= 1e-5, i
+        i += 1
+    assert i == 6
+
+
+@pytest.mark.parametrize("d_out,d_in,bits,r,m", [(4096, 4096, 4, 8, 512), (1024, 2816, 3, 16, 700),
+                                                 (512, 1024, 4, 64, 256), (256, 512, 2, 100, 64)])
+def test_layer_llama_shapes(d_out, d_in, bits, r, m):
+    seed = d_out + d_in + r
+    q, words, sc, z = random_quantized(d_out, d_in, bits, 128, seed)
+    dq = M.DeviceQuantizedMatrix(q)
+    alpha = 32.0
+    s = alpha / r
+    a32 = orc.gaussian(seed + 1, d_out, r, 0.0, 0.02).astype(np.float32)
+    b32 = orc.gaussian(seed + 2, d_in, r, 0.0, 0.02).astype(np.float32)
+    ad = M.LoraAdapter(a=torch.from_numpy(a32).cuda(), b=torch.from_numpy(b32).cuda(), rank=r,
+                       alpha=alpha)
+    layer = M.ModuLoraLayer("l", dq, ad, strategy=M.MaterializationStrategy.RowMaterialize)
+    x64 = orc.bf16_round(orc.gaussian(seed + 3, m, d_in))
+    g64 = orc.bf16_round(orc.gaussian(seed + 4, m, d_out))
+    x = to_bf16_dev(x64)
+    y, xb = M.layer_forward(layer, x, out_dtype=torch.float32)
+    dx = M.layer_backward(layer, x, xb, to_bf16_dev(g64), dx_dtype=torch.float32)
+    wbf = deq_bf16_f64(words, d_out, d_in, bits, 128, sc, z)
+    A, B = a32.astype(np.float64), b32.astype(np.float64)
+    xbr = x64 @ B
+    dyar = g64 @ A
+    # tight: the GPU recipe (bf16 Ŵ, bf16(s·xb), bf16 A / B) in f64
+    y_recipe = x64 @ wbf.T + orc.bf16_round(s * xbr) @ orc.bf16_round(A).T
+    dx_recipe = g64 @ wbf + orc.bf16_round(s * dyar) @ orc.bf16_round(B).T
+    assert rel_fro(f64(xb), xbr) <= 1e-5
+    assert rel_fro(f64(y), y_recipe) <= 1e-4
+    assert rel_fro(f64(dx), dx_recipe) <= 1e-4
+    # loose: exact f64 layer (sampled rows for the O(m·N·K) part)
+    wex = orc.dequantize(words, d_out, d_in, bits, 128, sc, z)
+    rows = np.arange(0, m, max(1, m // 16))
+    assert rel_fro(f64(y)[rows], x64[rows] @ wex.T + s * xbr[rows] @ A.T) <= 4e-3
+    assert rel_fro(f64(dx)[rows], g64[rows] @ wex + s * dyar[rows] @ B.T) <= 4e-3
+    da, db = M.grads_of_adapter(layer)
+    assert rel_fro(f64(da), s * g64.T @ xbr) <= 1e-4
+    assert rel_fro(f64(db), s * x64.T @ dyar) <= 1e-4
+
+
+def test_bf16_outputs_and_autograd_function():
+    d_out, d_in, r, m = 512, 768, 16, 333
+    q, words, sc, z = random_quantized(d_out, d_in, 4, 128, 3)
+    dq = M.DeviceQuantizedMatrix(q)
+    a = (torch.randn(d_out, r) * 0.02).cuda()
+    b = (torch.randn(d_in, r) * 0.02).cuda()
+    layer = M.ModuLoraLayer("f", dq, M.LoraAdapter(a=a, b=b, rank=r, alpha=16.0))
+    x = torch.randn(m, d_in).to(torch.bfloat16).cuda().requires_grad_(True)
+    y = M.ModuLoraLinearFunction.apply(x, a, b, None, layer)
+    assert y.dtype == torch.bfloat16 and y.shape == (m, d_out)
+    y.float().sum().backward()
+    assert x.grad is not None and x.grad.shape == x.shape
+    wbf = torch.from_numpy(deq_bf16_f64(words, d_out, d_in, 4, 128, sc, z)).cuda()
+    ones = torch.ones(m, d_out, dtype=torch.float64, device="cuda")
+    want_dx = ones @ wbf + ((16.0 / r) * ones @ a.double()) @ b.double().T
+    assert rel_fro(f64(x.grad), want_dx.cpu().numpy()) <= 8e-3
+
+
+def test_empty_tokens_and_errors():
+    q, *_ = random_quantized(256, 256, 4, 128, 9)
+    dq = M.DeviceQuantizedMatrix(q)
+    ctx = M.LpLinearContext(dq, M.MaterializationStrategy.RowMaterialize)
+    y = M.lp_forward(ctx, torch.empty(0, 256, dtype=torch.bfloat16, device="cuda"))
+    assert y.shape == (0, 256)
+    with pytest.raises(MlraError) as e:
+        M.lp_forward(ctx, torch.zeros(4, 255, dtype=torch.bfloat16, device="cuda"))
+    assert e.value.kind == "DimensionError"
+    with pytest.raises(MlraError) as e:
+        M.lp_forward(M.LpLinearContext(None), torch.zeros(4, 256, dtype=torch.bfloat16, device="cuda"))
+    assert e.value.kind == "ContractError"
+    layer = M.make_layer("e", dq, 4, 8.0, 1)
+    with pytest.raises(MlraError) as e:
+        M.grads_of_adapter(layer)
+    assert e.value.kind == "ContractError"
+    # a fresh layer (A = 0) computes exactly the frozen base (test_lora.cpp:91-105)
+    x = torch.randn(40, 256).to(torch.bfloat16).cuda()
+    y1, _ = M.layer_forward(layer, x, out_dtype=torch.float32)
+    y0 = M.lp_forward(ctx, x, out_dtype=torch.float32)
+    assert torch.equal(y1, y0)
