@@ -8,6 +8,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -81,18 +82,21 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2-D bf16 tensor [outer x inner] (row stride ld elements), SWIZZLE_128B box.
+// 2-D tensor [outer x inner] (row stride ld elements). Default: bf16 with a
+// SWIZZLE_128B box (tcgen05 operands); the Q ring uses unswizzled u8 / f32.
 mlra_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                     uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+                     uint64_t ld, uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                     uint32_t esize = 2, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode();
   if (!enc) return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * esize};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu",
                 static_cast<int>(r), (unsigned long long)inner, (unsigned long long)outer,
@@ -194,6 +198,30 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
   } else {
     maps.w = maps.act;
   }
+  maps.codes = maps.act;
+  maps.grid = maps.act;
+  if (!w_tma && mlra::qgemm_q_tma_ok(d)) {
+    // Q ring: 128 codes x 128 weight rows per stage, plus their grid entries
+    const int64_t g = d.group;
+    const int gfl = 2 * static_cast<int>(g < 128 ? 128 / g : 2);  // floats per row in the box
+    a.q_codes_bytes = 128 * 16 * d.bits;
+    a.q_grid_bytes = 128 * gfl * 4;
+    a.q_stage_bytes = static_cast<int>(round_up(a.q_codes_bytes + a.q_grid_bytes, 128));
+    a.q_stages = mlra::qgemm_max_q_stages(a.q_stage_bytes);
+    a.q_group_shift = g < 128 ? (g == 32 ? 5 : 6) : -1;
+    a.q_group_div128 = g >= 128 ? static_cast<int>(g / 128) : 1;
+    if (a.q_stages >= 2) {
+      if ((st = make_map(&maps.codes, d.words, d.row_words * 4, d.rows_pad, d.row_words * 4,
+                         16 * d.bits, 128, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1,
+                         CU_TENSOR_MAP_SWIZZLE_NONE)))
+        return st;
+      if ((st = make_map(&maps.grid, d.grid, 2 * d.ng_pad, d.rows_pad, 2 * d.ng_pad, gfl, 128,
+                         CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_NONE)))
+        return st;
+    } else {
+      a.q_stages = 0;
+    }
+  }
   CUDA_TRY(mlra::qgemm_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
   return MLRA_OK;
 }
@@ -267,7 +295,7 @@ mlra_status mlra_qweight_create(int64_t rows, int64_t cols, int bits, int64_t gr
   d.cols_pad = round_up(cols, 256);
   d.bits = bits;
   d.group = group;
-  d.ng_pad = (d.cols_pad + group - 1) / group;
+  d.ng_pad = round_up((d.cols_pad + group - 1) / group, 2);  // even: 16-B grid rows for TMA
   d.row_words = d.cols_pad * bits / 32;
   const size_t nwords = static_cast<size_t>(d.rows_pad * d.row_words) + 4;
   const size_t ngrid = static_cast<size_t>(d.rows_pad * d.ng_pad);

@@ -28,7 +28,7 @@ struct QWeightDev {
   int64_t rows_pad, cols_pad;  // multiples of 256
   int bits;
   int64_t group;               // group size along cols (divides cols)
-  int64_t ng_pad;              // groups per padded row = ceil(cols_pad / group)
+  int64_t ng_pad;              // grid row stride in groups: ceil(cols_pad/group) rounded to even
   int64_t row_words;           // 32-bit words per padded row = cols_pad*bits/32
   const uint32_t* words;       // rows_pad * row_words (+ 4 words slack)
   const float2* grid;          // rows_pad * ng_pad

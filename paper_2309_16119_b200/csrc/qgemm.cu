@@ -10,15 +10,20 @@
 // The LoRA term rides as extra K blocks ("[X, s·XB]·[Ŵ, A]ᵀ").
 //
 // Tile = 128 weight-side rows (MMA M; the dequantized operand) x 256 tokens
-// (MMA N; activations via TMA) x 64 K per pipeline stage. The weight side is
-// produced per stage either by 8 dequant warps straight from the packed codes
-// (strategy row/matvec: the full-precision W never exists in HBM) or by TMA
-// from a materialized bf16 W (strategy weight). Accumulator: 128 lanes x 256
-// f32 columns of TMEM. Epilogue: TMEM -> registers -> (+bias) -> global, with
-// lane = weight-side index so stores are coalesced along the output row.
+// (MMA N; activations via TMA) x 64 K per pipeline stage. Persistent CTAs
+// (one per SM) walk the tile list; two TMEM accumulators (2 x 256 f32
+// columns) let the epilogue of tile i overlap the mainloop of tile i+1.
 //
-// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer + TMEM owner,
-// w2-3 idle, w4-11 dequant producers, w4-7 then run the epilogue.
+// Weight-side operand, per strategy:
+//  * row/matvec (fused): packed codes + grids arrive by TMA in their own ring
+//    ("Q ring", 128 codes x 128 rows per stage = two K blocks), and 8 dequant
+//    warps expand them to bf16 straight into the SW128 operand tile — the
+//    full-precision Ŵ never exists in HBM (PAPER.md:116-126 at tile level).
+//  * weight: Ŵ (bf16) materialized in HBM by K1, loaded by TMA.
+//
+// Warp roles (512 threads): w0 operand TMA, w1 MMA issuer + TMEM owner,
+// w2 Q-ring TMA, w3 idle, w4-7 epilogue (TMEM -> regs -> +bias -> global),
+// w8-15 dequant producers.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -35,97 +40,94 @@ constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 64;
 constexpr int STAGES = 4;
+constexpr int MAX_QS = 4;
 constexpr int W_TILE = BM * BK * 2;  // 16 KB
 constexpr int T_TILE = BN * BK * 2;  // 32 KB
-constexpr int DQ_WARP0 = 4;
+constexpr int EPI_WARP0 = 4;
+constexpr int DQ_WARP0 = 8;
 constexpr int NUM_DQ_WARPS = 8;
 constexpr int NUM_DQ_THREADS = NUM_DQ_WARPS * 32;
 constexpr int NUM_THREADS = (DQ_WARP0 + NUM_DQ_WARPS) * 32;
 constexpr int UNITS_PER_THREAD = (BM * BK / 8) / NUM_DQ_THREADS;  // 4
-constexpr uint32_t TMEM_COLS = 256;
-constexpr size_t SMEM_BYTES = 1024 + STAGES * (W_TILE + T_TILE) + 256;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int SMEM_LIMIT = 232448;
+constexpr int SMEM_FIXED = 1024 + STAGES * (W_TILE + T_TILE) + 512;
 
-struct UnitRegs {
-  uint64_t v[UNITS_PER_THREAD];
-  float2 g[UNITS_PER_THREAD];
-};
-
-// Unit u (0..1023) of a stage -> (weight row, unit index along that row) and
-// the byte offset of its 16-byte chunk inside the SW128 stage tile.
-//  K-major (forward):  tile = 128 rows x 64 k; unit = (r = u/8, k8 = u%8);
+// Unit u (0..1023) of a stage -> byte offset of its 16-byte chunk inside the
+// SW128 operand tile, plus its position in the packed tile.
+//  K-major (forward): tile = 128 rows x 64 k; unit = (r = u/8, k8 = u%8);
 //     canonical K-major SW128: row r at r*128, chunk k8 at (k8 ^ r%8)*16.
-//  MN-major (dX):      tile = 64 reduction rows (n) x 128 output cols (k);
-//     unit = (n = u/16, k8 = u%16); chunk c = k8/8 of 64 columns at c*8192,
+//  MN-major (dX):     tile = 64 reduction rows (n) x 128 output cols (k);
+//     unit = (n = u/16, k8 = u%16); 64-column chunk c = k8/8 at c*8192,
 //     row n at n*128, 16-byte column group (k8%8 ^ n%8).
 template <bool MN>
-__device__ __forceinline__ void unit_coords(int u, int m_tile, int kb, int64_t& wrow,
-                                            int64_t& wunit, uint32_t& soff) {
+__device__ __forceinline__ uint32_t unit_soff(int u) {
   if constexpr (!MN) {
     const int r = u >> 3, k8 = u & 7;
-    wrow = static_cast<int64_t>(m_tile) * BM + r;
-    wunit = static_cast<int64_t>(kb) * (BK / 8) + k8;
-    soff = r * 128 + ((k8 ^ (r & 7)) << 4);
+    return r * 128 + ((k8 ^ (r & 7)) << 4);
   } else {
     const int n = u >> 4, k8 = u & 15;
-    wrow = static_cast<int64_t>(kb) * BK + n;
-    wunit = static_cast<int64_t>(m_tile) * (BM / 8) + k8;
-    soff = (k8 >> 3) * 8192 + n * 128 + (((k8 & 7) ^ (n & 7)) << 4);
+    return (k8 >> 3) * 8192 + n * 128 + (((k8 & 7) ^ (n & 7)) << 4);
   }
 }
 
-template <int BITS, bool MN>
-__device__ __forceinline__ void dq_load(const QWeightDev& q, int m_tile, int kb, int tid,
-                                        bool fast_group, UnitRegs& ur) {
-#pragma unroll
-  for (int i = 0; i < UNITS_PER_THREAD; ++i) {
-    int64_t wrow, wunit;
-    uint32_t soff;
-    unit_coords<MN>(i * NUM_DQ_THREADS + tid, m_tile, kb, wrow, wunit, soff);
-    ur.v[i] = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
-    if (fast_group) ur.g[i] = __ldg(q.grid + wrow * q.ng_pad + (wunit * 8) / q.group);
+// Packed unit (8 codes) read from a Q-ring row (16*BITS bytes = 128 codes).
+template <int BITS>
+__device__ __forceinline__ uint32_t lds_unit(const uint8_t* row, int j) {
+  if constexpr (BITS == 4) {
+    return *reinterpret_cast<const uint32_t*>(row + j * 4);
+  } else if constexpr (BITS == 2) {
+    return *reinterpret_cast<const uint16_t*>(row + j * 2);
+  } else {
+    const int off = j * 3;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(row + (off & ~3));
+    return __funnelshift_r(w[0], w[1], (off & 3) * 8) & 0xFFFFFFu;
   }
 }
 
-template <int BITS, bool MN>
-__device__ __forceinline__ void dq_store(const QWeightDev& q, int m_tile, int kb, int tid,
-                                         bool fast_group, const UnitRegs& ur, uint8_t* stile) {
-#pragma unroll
-  for (int i = 0; i < UNITS_PER_THREAD; ++i) {
-    int64_t wrow, wunit;
-    uint32_t soff;
-    unit_coords<MN>(i * NUM_DQ_THREADS + tid, m_tile, kb, wrow, wunit, soff);
-    uint4 o;
-    if (fast_group)
-      o = deq8_bf16<BITS>(ur.v[i], ur.g[i]);
-    else
-      o = deq8_bf16_general<BITS>(ur.v[i], q.grid + wrow * q.ng_pad, wunit * 8, q.group);
-    *reinterpret_cast<uint4*>(stile + soff) = o;
-  }
+// Group index of the first code of 128-code block `blk` along the code rows.
+__device__ __forceinline__ int pair_group(int blk, const GemmArgs& p) {
+  return p.q_group_shift >= 0 ? (blk << (7 - p.q_group_shift)) : blk / p.q_group_div128;
 }
 
-template <int BITS, bool W_TMA, bool MN, bool OUT_F32>
+struct TileIter {
+  int m_tiles;
+  int n_tiles;
+  __device__ __forceinline__ void coords(int tile, int& m, int& n) const {
+    m = tile % m_tiles;
+    n = tile / m_tiles;
+  }
+};
+
+template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tm_act,
                  const __grid_constant__ CUtensorMap tm_act_lora,
                  const __grid_constant__ CUtensorMap tm_w,
-                 const __grid_constant__ CUtensorMap tm_w_lora, const QWeightDev q,
+                 const __grid_constant__ CUtensorMap tm_w_lora,
+                 const __grid_constant__ CUtensorMap tm_codes,
+                 const __grid_constant__ CUtensorMap tm_grid, const QWeightDev q,
                  const GemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sW = smem;
-  uint8_t* sT = smem + STAGES * W_TILE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sT + STAGES * T_TILE);
+  uint8_t* sT = sW + STAGES * W_TILE;
+  uint8_t* sQ = sT + STAGES * T_TILE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sQ + p.q_stages * p.q_stage_bytes);
   uint64_t* empty = full + STAGES;
-  uint64_t* accum_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
+  uint64_t* qfull = empty + STAGES;
+  uint64_t* qempty = qfull + MAX_QS;
+  uint64_t* tfull = qempty + MAX_QS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m_tile = blockIdx.x;
-  const int n_tile = blockIdx.y;
   const int n_kb_main = p.n_kb_main;
   const int n_kb = p.n_kb_main + p.n_kb_lora;
+  const TileIter it{static_cast<int>(p.m_total / BM), static_cast<int>((p.tokens + BN - 1) / BN)};
+  const int n_tiles = it.m_tiles * it.n_tiles;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_act);
@@ -134,11 +136,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tma_prefetch_desc(&tm_w_lora);
     }
     if (W_TMA) tma_prefetch_desc(&tm_w);
+    if (QTMA) {
+      tma_prefetch_desc(&tm_codes);
+      tma_prefetch_desc(&tm_grid);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1 + NUM_DQ_WARPS);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum_full, 1);
+    for (int s = 0; s < MAX_QS; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], NUM_DQ_WARPS);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -148,31 +161,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ operand TMA
     if (lane == 0) {
-      for (int kb = 0; kb < n_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        const bool lora = kb >= n_kb_main;
-        const bool w_tma = lora || W_TMA;
-        mbar_arrive_expect_tx(&full[s], T_TILE + (w_tma ? W_TILE : 0));
-        uint8_t* st = sT + s * T_TILE;
-        uint8_t* sw = sW + s * W_TILE;
-        if (!lora) {
-          tma_load_2d(st, &tm_act, &full[s], kb * BK, n_tile * BN);
-          if (W_TMA) {
-            if (!MN) {
-              tma_load_2d(sw, &tm_w, &full[s], kb * BK, m_tile * BM);
-            } else {
-              tma_load_2d(sw, &tm_w, &full[s], m_tile * BM, kb * BK);
-              tma_load_2d(sw + 8192, &tm_w, &full[s], m_tile * BM + 64, kb * BK);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int m_tile, n_tile;
+        it.coords(tile, m_tile, n_tile);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          const bool lora = kb >= n_kb_main;
+          const bool w_tma = lora || W_TMA;
+          mbar_arrive_expect_tx(&full[s], T_TILE + (w_tma ? W_TILE : 0));
+          uint8_t* st = sT + s * T_TILE;
+          uint8_t* sw = sW + s * W_TILE;
+          if (!lora) {
+            tma_load_2d(st, &tm_act, &full[s], kb * BK, n_tile * BN);
+            if (W_TMA) {
+              if (!MN) {
+                tma_load_2d(sw, &tm_w, &full[s], kb * BK, m_tile * BM);
+              } else {
+                tma_load_2d(sw, &tm_w, &full[s], m_tile * BM, kb * BK);
+                tma_load_2d(sw + 8192, &tm_w, &full[s], m_tile * BM + 64, kb * BK);
+              }
             }
+          } else {
+            const int lk = (kb - n_kb_main) * BK;
+            tma_load_2d(st, &tm_act_lora, &full[s], lk, n_tile * BN);
+            tma_load_2d(sw, &tm_w_lora, &full[s], lk, m_tile * BM);
           }
-        } else {
-          const int lk = (kb - n_kb_main) * BK;
-          tma_load_2d(st, &tm_act_lora, &full[s], lk, n_tile * BN);
-          tma_load_2d(sw, &tm_w_lora, &full[s], lk, m_tile * BM);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
@@ -181,76 +202,94 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_main = idesc_bf16(BM, BN, MN ? 1u : 0u, 0u);
       constexpr uint32_t idesc_kmaj = idesc_bf16(BM, BN, 0u, 0u);
-      for (int kb = 0; kb < n_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const bool lora = kb >= n_kb_main;
-        const int nk16 = (lora && kb == n_kb - 1) ? p.lora_k16_last : BK / 16;
-        const uint32_t sw = smem_u32(sW + s * W_TILE);
-        const uint32_t st = smem_u32(sT + s * T_TILE);
-        for (int k = 0; k < nk16; ++k) {
-          uint64_t adesc;
-          uint32_t idesc;
-          if (MN && !lora) {
-            adesc = sdesc_sw128(sw + k * 2048, 8192, 1024);
-            idesc = idesc_main;
-          } else {
-            adesc = sdesc_sw128(sw + k * 32, 16, 1024);
-            idesc = idesc_kmaj;
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const bool lora = kb >= n_kb_main;
+          const int nk16 = (lora && kb == n_kb - 1) ? p.lora_k16_last : BK / 16;
+          const uint32_t sw = smem_u32(sW + s * W_TILE);
+          const uint32_t st = smem_u32(sT + s * T_TILE);
+          for (int k = 0; k < nk16; ++k) {
+            uint64_t adesc;
+            uint32_t idesc;
+            if (MN && !lora) {
+              adesc = sdesc_sw128(sw + k * 2048, 8192, 1024);
+              idesc = idesc_main;
+            } else {
+              adesc = sdesc_sw128(sw + k * 32, 16, 1024);
+              idesc = idesc_kmaj;
+            }
+            const uint64_t bdesc = sdesc_sw128(st + k * 32, 16, 1024);
+            tc_mma_f16(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
           }
-          const uint64_t bdesc = sdesc_sw128(st + k * 32, 16, 1024);
-          tc_mma_f16(tmem_base, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          tc_commit(&empty[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
-        tc_commit(&empty[s]);
-      }
-      tc_commit(accum_full);
-    }
-  } else if (warp >= DQ_WARP0) {
-    // ------------------------------------------------------------ dequant producers
-    const int tid = threadIdx.x - DQ_WARP0 * 32;
-    if constexpr (!W_TMA) {
-      const bool fast_group = (q.group % 8) == 0;
-      UnitRegs cur, nxt;
-      if (n_kb_main > 0) dq_load<BITS, MN>(q, m_tile, 0, tid, fast_group, cur);
-      for (int kb = 0; kb < n_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        const bool main = kb < n_kb_main;
-        if (kb + 1 < n_kb_main) dq_load<BITS, MN>(q, m_tile, kb + 1, tid, fast_group, nxt);
-        mbar_wait(&empty[s], ph ^ 1);
-        if (main) {
-          dq_store<BITS, MN>(q, m_tile, kb, tid, fast_group, cur, sW + s * W_TILE);
-          fence_proxy_async_smem();
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[s]);
-        cur = nxt;
-      }
-    } else {
-      for (int kb = 0; kb < n_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[s]);
+        tc_commit(&tfull[acc]);
       }
     }
-
-    if (warp < DQ_WARP0 + 4) {
-      // ---------------------------------------------------------- epilogue
-      mbar_wait(accum_full, 0);
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ Q-ring TMA
+    if (QTMA && !W_TMA && lane == 0) {
+      const uint32_t qbytes = p.q_codes_bytes + p.q_grid_bytes;
+      int qs = 0;
+      uint32_t qph = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int m_tile, n_tile;
+        it.coords(tile, m_tile, n_tile);
+        for (int pr = 0; pr < n_kb_main / 2; ++pr) {
+          mbar_wait(&qempty[qs], qph ^ 1);
+          mbar_arrive_expect_tx(&qfull[qs], qbytes);
+          uint8_t* dst = sQ + qs * p.q_stage_bytes;
+          // grid boxes start on an even group: TMA box starts must be 16-byte aligned
+          if (!MN) {  // rows = weight rows of the tile, bytes = codes [pr*128, pr*128+128)
+            tma_load_2d(dst, &tm_codes, &qfull[qs], pr * 16 * BITS, m_tile * BM);
+            tma_load_2d(dst + p.q_codes_bytes, &tm_grid, &qfull[qs],
+                        2 * (pair_group(pr, p) & ~1), m_tile * BM);
+          } else {    // rows = weight rows [pr*128, +128), bytes = codes of tile columns
+            tma_load_2d(dst, &tm_codes, &qfull[qs], m_tile * 16 * BITS, pr * 128);
+            tma_load_2d(dst + p.q_codes_bytes, &tm_grid, &qfull[qs],
+                        2 * (pair_group(m_tile, p) & ~1), pr * 128);
+          }
+          if (++qs == p.q_stages) {
+            qs = 0;
+            qph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0 && warp < DQ_WARP0) {
+    // ------------------------------------------------------------ epilogue
+    const int qd = warp & 3;  // TMEM lane quadrant this warp may access
+    int local = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++local) {
+      int m_tile, n_tile;
+      it.coords(tile, m_tile, n_tile);
+      const int acc = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int qd = warp & 3;  // TMEM lane quadrant this warp may access
       const int64_t wrow = static_cast<int64_t>(m_tile) * BM + qd * 32 + lane;
       const bool row_ok = wrow < p.m_valid;
       const float bias = (p.bias != nullptr && row_ok) ? p.bias[wrow] : 0.0f;
       const int64_t t0 = static_cast<int64_t>(n_tile) * BN;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(qd * 32) << 16) + c * 32, r);
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
         tc_wait_ld();
         if (row_ok) {
 #pragma unroll
@@ -268,6 +307,136 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  } else if (warp >= DQ_WARP0) {
+    // ------------------------------------------------------------ dequant producers
+    const int tid = threadIdx.x - DQ_WARP0 * 32;
+    int s = 0;
+    uint32_t ph = 0;
+    if constexpr (W_TMA) {
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    } else if constexpr (QTMA) {
+      // per-thread constants: smem destinations and packed-tile positions
+      uint32_t soff[UNITS_PER_THREAD];
+      int qrow[UNITS_PER_THREAD], qunit[UNITS_PER_THREAD], qcode[UNITS_PER_THREAD];
+#pragma unroll
+      for (int i = 0; i < UNITS_PER_THREAD; ++i) {
+        const int u = i * NUM_DQ_THREADS + tid;
+        soff[i] = unit_soff<MN>(u);
+        if constexpr (!MN) {
+          qrow[i] = u >> 3;
+          qunit[i] = u & 7;  // + 8 * (kb & 1)
+          qcode[i] = (u & 7) * 8;
+        } else {
+          qrow[i] = u >> 4;  // + 64 * (kb & 1)
+          qunit[i] = u & 15;
+          qcode[i] = (u & 15) * 8;
+        }
+      }
+      const int gshift = p.q_group_shift;  // log2(group) when group < 128, else -1
+      const int gbox = p.q_grid_bytes / BM;  // bytes of grid per Q row
+      int qs = 0;
+      uint32_t qph = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int m_tile, n_tile;
+        it.coords(tile, m_tile, n_tile);
+        // g >= 128: one group per 128-code block; which half of the 2-group box
+        int gpar = MN ? (pair_group(m_tile, p) & 1) : 0;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          const bool main = kb < n_kb_main;
+          const int kp = kb & 1;
+          if (main && kp == 0) {
+            mbar_wait(&qfull[qs], qph);
+            if (!MN) gpar = pair_group(kb >> 1, p) & 1;
+          }
+          mbar_wait(&empty[s], ph ^ 1);
+          if (main) {
+            const uint8_t* qc = sQ + qs * p.q_stage_bytes;
+            const uint8_t* qg = qc + p.q_codes_bytes;
+            uint8_t* stile = sW + s * W_TILE;
+#pragma unroll
+            for (int i = 0; i < UNITS_PER_THREAD; ++i) {
+              int row, unit, code;
+              if constexpr (!MN) {
+                row = qrow[i];
+                unit = qunit[i] + 8 * kp;
+                code = qcode[i] + 64 * kp;
+              } else {
+                row = qrow[i] + 64 * kp;
+                unit = qunit[i];
+                code = qcode[i];
+              }
+              const uint32_t v = lds_unit<BITS>(qc + row * (16 * BITS), unit);
+              const int gsub = gshift >= 0 ? (code >> gshift) : gpar;
+              const float2 g = *reinterpret_cast<const float2*>(qg + row * gbox + gsub * 8);
+              *reinterpret_cast<uint4*>(stile + soff[i]) = deq8_bf16<BITS>(v, g);
+            }
+            fence_proxy_async_smem();
+          }
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&full[s]);
+            if (main && kp == 1) mbar_arrive(&qempty[qs]);
+          }
+          if (main && kp == 1) {
+            if (++qs == p.q_stages) {
+              qs = 0;
+              qph ^= 1;
+            }
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    } else {
+      // generic LDG path (odd group sizes / 8-bit codes)
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int m_tile, n_tile;
+        it.coords(tile, m_tile, n_tile);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (kb < n_kb_main) {
+            uint8_t* stile = sW + s * W_TILE;
+#pragma unroll
+            for (int i = 0; i < UNITS_PER_THREAD; ++i) {
+              const int u = i * NUM_DQ_THREADS + tid;
+              int64_t wrow, wunit;
+              if constexpr (!MN) {
+                wrow = static_cast<int64_t>(m_tile) * BM + (u >> 3);
+                wunit = static_cast<int64_t>(kb) * (BK / 8) + (u & 7);
+              } else {
+                wrow = static_cast<int64_t>(kb) * BK + (u >> 4);
+                wunit = static_cast<int64_t>(m_tile) * (BM / 8) + (u & 15);
+              }
+              const uint64_t v = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
+              *reinterpret_cast<uint4*>(stile + unit_soff<MN>(u)) =
+                  deq8_bf16_general<BITS>(v, q.grid + wrow * q.ng_pad, wunit * 8, q.group);
+            }
+            fence_proxy_async_smem();
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
     }
   }
 
@@ -276,50 +445,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) tmem_dealloc(tmem_base, TMEM_COLS);
 }
 
-template <int BITS, bool W_TMA, bool MN, bool OUT_F32>
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA>
 cudaError_t launch_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                      cudaStream_t stream) {
-  auto kern = qgemm_kernel<BITS, W_TMA, MN, OUT_F32>;
-  cudaError_t e =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  auto kern = qgemm_kernel<BITS, W_TMA, MN, OUT_F32, QTMA>;
+  const int smem = SMEM_FIXED + p.q_stages * p.q_stage_bytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>(p.m_total / BM),
-            static_cast<unsigned>((p.tokens + BN - 1) / BN));
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(maps.act, maps.act_lora, maps.w, maps.w_lora,
-                                                  q, p);
+  const int64_t tiles = (p.m_total / BM) * ((p.tokens + BN - 1) / BN);
+  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+  kern<<<grid, NUM_THREADS, smem, stream>>>(maps.act, maps.act_lora, maps.w, maps.w_lora,
+                                            maps.codes, maps.grid, q, p);
   return cudaGetLastError();
 }
 
-template <int BITS>
-cudaError_t launch_bits(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p, bool w_tma,
-                        bool mn, bool out_f32, cudaStream_t stream) {
-  if (w_tma) {
-    if (mn) return out_f32 ? launch_t<BITS, true, true, true>(maps, q, p, stream)
-                           : launch_t<BITS, true, true, false>(maps, q, p, stream);
-    return out_f32 ? launch_t<BITS, true, false, true>(maps, q, p, stream)
-                   : launch_t<BITS, true, false, false>(maps, q, p, stream);
-  }
-  if (mn) return out_f32 ? launch_t<BITS, false, true, true>(maps, q, p, stream)
-                         : launch_t<BITS, false, true, false>(maps, q, p, stream);
-  return out_f32 ? launch_t<BITS, false, false, true>(maps, q, p, stream)
-                 : launch_t<BITS, false, false, false>(maps, q, p, stream);
+template <int BITS, bool W_TMA, bool QTMA>
+cudaError_t launch_mo(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p, bool mn,
+                      bool out_f32, cudaStream_t st) {
+  if (mn) return out_f32 ? launch_t<BITS, W_TMA, true, true, QTMA>(maps, q, p, st)
+                         : launch_t<BITS, W_TMA, true, false, QTMA>(maps, q, p, st);
+  return out_f32 ? launch_t<BITS, W_TMA, false, true, QTMA>(maps, q, p, st)
+                 : launch_t<BITS, W_TMA, false, false, QTMA>(maps, q, p, st);
 }
 
 }  // namespace
 
-int qgemm_tile_m() { return BM; }
-int qgemm_tile_n() { return BN; }
-int qgemm_tile_k() { return BK; }
+bool qgemm_q_tma_ok(const QWeightDev& q) {
+  const int64_t g = q.group;
+  const bool g_ok = (g == 32 || g == 64 || g % 128 == 0);
+  return (q.bits == 2 || q.bits == 3 || q.bits == 4) && g_ok;
+}
+
+int qgemm_max_q_stages(int q_stage_bytes) {
+  int qs = (SMEM_LIMIT - SMEM_FIXED) / q_stage_bytes;
+  return qs > MAX_QS ? MAX_QS : qs;
+}
 
 cudaError_t qgemm_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                          bool w_tma, bool mn, bool out_f32, cudaStream_t stream) {
   if (p.tokens <= 0 || p.m_total <= 0) return cudaSuccess;
-  if (w_tma) return launch_bits<4>(maps, q, p, true, mn, out_f32, stream);  // bits unused
+  if (w_tma) return launch_mo<4, true, false>(maps, q, p, mn, out_f32, stream);
+  const bool qtma = p.q_stages > 0;
   switch (q.bits) {
-    case 2: return launch_bits<2>(maps, q, p, false, mn, out_f32, stream);
-    case 3: return launch_bits<3>(maps, q, p, false, mn, out_f32, stream);
-    case 4: return launch_bits<4>(maps, q, p, false, mn, out_f32, stream);
-    case 8: return launch_bits<8>(maps, q, p, false, mn, out_f32, stream);
+    case 2: return qtma ? launch_mo<2, false, true>(maps, q, p, mn, out_f32, stream)
+                        : launch_mo<2, false, false>(maps, q, p, mn, out_f32, stream);
+    case 3: return qtma ? launch_mo<3, false, true>(maps, q, p, mn, out_f32, stream)
+                        : launch_mo<3, false, false>(maps, q, p, mn, out_f32, stream);
+    case 4: return qtma ? launch_mo<4, false, true>(maps, q, p, mn, out_f32, stream)
+                        : launch_mo<4, false, false>(maps, q, p, mn, out_f32, stream);
+    case 8: return launch_mo<8, false, false>(maps, q, p, mn, out_f32, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -13,23 +13,32 @@ struct GemmMaps {
   CUtensorMap act_lora;  // LoRA activations [tokens x 64*nlb] bf16, box 64 x 256
   CUtensorMap w;         // materialized W bf16 (strategy weight): box 64x128 (K-major) or 64x64 (MN)
   CUtensorMap w_lora;    // adapter factor padded [m_total x 64*nlb] bf16, box 64 x 128
+  CUtensorMap codes;     // packed codes as u8 [rows_pad x row_bytes], box 16*bits x 128
+  CUtensorMap grid;      // signed grid as f32 [rows_pad x 2*ng_pad], box 2*max(2,128/g) x 128
 };
 
 struct GemmArgs {
-  int64_t m_total;   // weight-side extent, multiple of 128 (grid.x = m_total/128)
+  int64_t m_total;   // weight-side extent, multiple of 128
   int64_t m_valid;   // weight-side extent actually stored
-  int n_kb_main;     // 64-wide reduction blocks over the quantized operand
+  int n_kb_main;     // 64-wide reduction blocks over the quantized operand (even)
   int n_kb_lora;     // extra 64-wide LoRA blocks (ceil(r/64)), 0 = none
   int lora_k16_last; // useful 16-wide MMA steps in the last LoRA block
   int64_t tokens;    // m
   void* out;         // [tokens x ldo], f32 or bf16
   int64_t ldo;
   const float* bias; // [m_valid] or nullptr
+  // Q ring (fused path with TMA-fed codes); q_stages == 0 selects the LDG path
+  int q_stages;
+  int q_stage_bytes;
+  int q_codes_bytes;
+  int q_grid_bytes;
+  int q_group_shift; // log2(group) when group < 128, else -1
+  int q_group_div128; // group / 128 when group >= 128
 };
 
-int qgemm_tile_m();
-int qgemm_tile_n();
-int qgemm_tile_k();
+// true when the fused path can stream codes/grids through the TMA Q ring
+bool qgemm_q_tma_ok(const QWeightDev& q);
+int qgemm_max_q_stages(int q_stage_bytes);
 
 // mn = false: forward (Ŵ K-major on the weight side); true: dX (Ŵᵀ, MN-major).
 cudaError_t qgemm_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
