@@ -79,6 +79,8 @@ typedef struct mlra_lora {
 /* Last error message of this thread ("" if none). */
 MLRA_API const char* mlra_last_error(void);
 MLRA_API int mlra_abi_version(void);
+/* Number of CUDA kernels this library has launched in this process. */
+MLRA_API uint64_t mlra_kernel_launches(void);
 
 /* MLRA_OK iff the current CUDA device is sm_100 (B200). */
 MLRA_API mlra_status mlra_device_check(void);

@@ -19,7 +19,7 @@ F32, BF16 = 0, 1
 
 # Every symbol include/mlra.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = [
-    "mlra_last_error", "mlra_abi_version", "mlra_device_check", "mlra_packed_word_count",
+    "mlra_last_error", "mlra_abi_version", "mlra_kernel_launches", "mlra_device_check", "mlra_packed_word_count",
     "mlra_qweight_create", "mlra_qweight_destroy", "mlra_qweight_info", "mlra_materialize",
     "mlra_materialize_rows", "mlra_ledger_bytes", "mlra_lp_forward", "mlra_lp_backward",
     "mlra_lora_forward", "mlra_lora_backward",
@@ -60,6 +60,7 @@ def lib() -> C.CDLL:
         i64, u64, vp, i32 = C.c_int64, C.c_uint64, C.c_void_p, C.c_int
         L.mlra_last_error.restype = C.c_char_p
         L.mlra_abi_version.restype = i32
+        L.mlra_kernel_launches.restype = u64
         L.mlra_device_check.restype = i32
         L.mlra_packed_word_count.restype = u64
         L.mlra_packed_word_count.argtypes = [u64, i32]

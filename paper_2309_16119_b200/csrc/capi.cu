@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -20,6 +21,11 @@
 #include "qgemm.h"
 
 using mlra::QWeightDev;
+
+namespace mlra {
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace mlra
 
 struct mlra_qweight {
   QWeightDev d{};
@@ -245,6 +251,7 @@ extern "C" {
 
 const char* mlra_last_error(void) { return g_last_error.c_str(); }
 int mlra_abi_version(void) { return 1; }
+uint64_t mlra_kernel_launches(void) { return mlra::g_launches.load(); }
 mlra_status mlra_device_check(void) { return check_device(); }
 
 uint64_t mlra_packed_word_count(uint64_t count, int bits) {

@@ -8,6 +8,9 @@
 
 namespace mlra {
 
+// Counts every kernel this library launches (mlra_kernel_launches()).
+void note_launch();
+
 cudaError_t launch_relayout(const uint32_t* src, int64_t rows, int64_t cols, int bits,
                             int64_t row_words, int64_t rows_pad, uint32_t* dst, cudaStream_t st);
 cudaError_t launch_grid(const float* scales, const float* zeros, int64_t rows, int64_t ng,

@@ -206,6 +206,7 @@ cudaError_t rowdot_rc(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int64_t blocks = (m + 8 * TT - 1) / (8 * TT);
+  note_launch();
   kern<<<static_cast<unsigned>(blocks), 256, smem, st>>>(act, lda, m, kd, W, ldw, rc, scale,
                                                          out, ldo, pad, ldp);
   return cudaGetLastError();
@@ -224,6 +225,7 @@ cudaError_t coldot_rc(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   tpb = (tpb + 63) / 64 * 64;
   splits = (m + tpb - 1) / tpb;
   dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(splits));
+  note_launch();
   k_coldot<RC><<<grid, 128, 0, st>>>(act, lda, m, nd, V, ldv, rc, scale, tpb, out, ldo, colsum);
   return cudaGetLastError();
 }
@@ -278,6 +280,7 @@ cudaError_t launch_pad_bf16(const float* src, int64_t rows, int64_t cols, int64_
   int64_t blocks = (rows_pad * ldd + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
+  note_launch();
   k_pad_bf16<<<static_cast<unsigned>(blocks), 256, 0, st>>>(src, rows, cols, lds, dst, rows_pad,
                                                             ldd);
   return cudaGetLastError();

@@ -147,6 +147,7 @@ cudaError_t materialize_bits(const QWeightDev& q, int64_t row0, int64_t nrows, v
   const int blocks = grid_for(units, 256);
   const bool vec = (q.cols % 8 == 0) && (ld % 8 == 0) &&
                    (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  note_launch();
   if (f32) {
     if (vec)
       k_materialize<BITS, true, true><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
@@ -166,6 +167,7 @@ cudaError_t materialize_bits(const QWeightDev& q, int64_t row0, int64_t nrows, v
 cudaError_t launch_relayout(const uint32_t* src, int64_t rows, int64_t cols, int bits,
                             int64_t row_words, int64_t rows_pad, uint32_t* dst,
                             cudaStream_t st) {
+  note_launch();
   k_relayout<<<grid_for(rows_pad * row_words, 256), 256, 0, st>>>(src, rows, cols, bits,
                                                                   row_words, rows_pad, dst);
   return cudaGetLastError();
@@ -174,6 +176,7 @@ cudaError_t launch_relayout(const uint32_t* src, int64_t rows, int64_t cols, int
 cudaError_t launch_grid(const float* scales, const float* zeros, int64_t rows, int64_t ng,
                         int64_t rows_pad, int64_t ng_pad, int bits, float2* grid,
                         int* n_uncertified, cudaStream_t st) {
+  note_launch();
   k_grid<<<grid_for(rows_pad * ng_pad, 256), 256, 0, st>>>(scales, zeros, rows, ng, rows_pad,
                                                            ng_pad, bits, grid, n_uncertified);
   return cudaGetLastError();

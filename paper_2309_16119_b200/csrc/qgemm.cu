@@ -30,6 +30,7 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "kernels.h"
 #include "qgemm.h"
 
 namespace mlra {
@@ -464,6 +465,7 @@ cudaError_t launch_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& 
   if (e != cudaSuccess) return e;
   const int64_t tiles = (p.m_total / BM) * ((p.tokens + BN - 1) / BN);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+  note_launch();
   kern<<<grid, NUM_THREADS, smem, stream>>>(maps.act, maps.act_lora, maps.w, maps.w_lora,
                                             maps.codes, maps.grid, q, p);
   return cudaGetLastError();

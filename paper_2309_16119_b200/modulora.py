@@ -294,16 +294,24 @@ def layer_forward(layer: ModuLoraLayer, x: torch.Tensor, out_dtype=torch.bfloat1
 
 
 def layer_backward(layer: ModuLoraLayer, x: torch.Tensor, xb: torch.Tensor, dy: torch.Tensor,
-                   need_dx: bool = True, dx_dtype=torch.bfloat16):
+                   need_dx: bool = True, dx_dtype=torch.bfloat16,
+                   da: Optional[torch.Tensor] = None, db: Optional[torch.Tensor] = None):
     """Tape replay of layer_forward's records (autodiff.cpp:101-193) for the
     upstream gradient dy. Stores dA/dB (and dbias when trainable) on the layer
-    (grads_of_adapter) and returns dx (None when need_dx is False)."""
+    (grads_of_adapter) and returns dx (None when need_dx is False). da/db may
+    be caller-provided contiguous fp32 views (e.g. slices of one flat
+    gradient bucket for the data-parallel all-reduce)."""
     _check_act(dy, layer.d_out(), f"layer '{layer.name}' backward")
     _check_act(x, layer.d_in(), f"layer '{layer.name}' backward")
     m = x.shape[0]
     r = layer.adapter.rank
-    da = torch.empty(layer.d_out(), r, dtype=torch.float32, device=x.device)
-    db = torch.empty(layer.d_in(), r, dtype=torch.float32, device=x.device)
+    if da is None:
+        da = torch.empty(layer.d_out(), r, dtype=torch.float32, device=x.device)
+    if db is None:
+        db = torch.empty(layer.d_in(), r, dtype=torch.float32, device=x.device)
+    for t, shape in ((da, (layer.d_out(), r)), (db, (layer.d_in(), r))):
+        if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_contiguous():
+            raise MlraError(2, f"gradient buffer must be contiguous fp32 {shape}")
     dbias = torch.empty(layer.d_out(), dtype=torch.float32, device=x.device) if layer.bias_trainable else None
     dx = torch.empty(m, layer.d_in(), dtype=dx_dtype, device=x.device) if need_dx else None
     L = layer._c()
