@@ -101,6 +101,66 @@ __device__ __forceinline__ uint4 deq8_bf16(uint64_t v, float2 g) {
   return o;
 }
 
+// Packed-f32x2 ops (sm_100 FADD2 / FFMA2): same IEEE rounding per lane as the
+// scalar forms, so results stay bit-identical to deq8_f32.
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t p) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;"
+      : "=r"(d)
+      : "f"(__uint_as_float(static_cast<uint32_t>(p >> 32))),
+        "f"(__uint_as_float(static_cast<uint32_t>(p))));
+  return d;
+}
+
+// Magic-float words (0x4B000000 | c) of the 8 codes of a unit, in order.
+template <int BITS>
+__device__ __forceinline__ void unit_magic(uint32_t v, uint32_t (&m)[8]) {
+  if constexpr (BITS == 4) {
+    // nibbles 2j / 2j+1 live in byte j of lo / hi; PRMT drops each byte under
+    // the 0x4B exponent byte in one instruction
+    const uint32_t lo = v & 0x0F0F0F0Fu, hi = (v >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      m[2 * j] = __byte_perm(lo, 0x4B000000u, 0x7540u | j);
+      m[2 * j + 1] = __byte_perm(hi, 0x4B000000u, 0x7540u | j);
+    }
+  } else {
+    constexpr uint32_t mask = (1u << BITS) - 1u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = ((v >> (BITS * i)) & mask) | 0x4B000000u;
+  }
+}
+
+// Fast unit: 8 codes (BITS <= 4, packed in v) sharing grid g -> 8 bf16.
+// Certified groups: FADD2 (exact code -> float) + FFMA2 (one rounding) +
+// cvt.rn.bf16x2; uncertified groups take the exact f64 path.
+template <int BITS>
+__device__ __forceinline__ uint4 deq8_bf16_fast(uint32_t v, float2 g) {
+  if (!(g.x > 0.0f)) return deq8_bf16<BITS>(v, g);
+  uint32_t m[8];
+  unit_magic<BITS>(v, m);
+  const uint64_t neg = 0xCB000000CB000000ull;  // (-2^23, -2^23)
+  const uint64_t s2 = (static_cast<uint64_t>(__float_as_uint(g.x)) << 32) | __float_as_uint(g.x);
+  const uint64_t z2 = (static_cast<uint64_t>(__float_as_uint(g.y)) << 32) | __float_as_uint(g.y);
+  uint32_t o[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint64_t pr = (static_cast<uint64_t>(m[2 * j + 1]) << 32) | m[2 * j];
+    o[j] = f2_to_bf16x2(f2_fma(f2_add(pr, neg), s2, z2));
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 // General unit: groups may change inside the 8 codes (group % 8 != 0; only the
 // small ragged reference-test shapes hit this).
 template <int BITS>

@@ -49,7 +49,7 @@ constexpr int DQ_WARP0 = 8;
 constexpr int NUM_DQ_WARPS = 8;
 constexpr int NUM_DQ_THREADS = NUM_DQ_WARPS * 32;
 constexpr int NUM_THREADS = (DQ_WARP0 + NUM_DQ_WARPS) * 32;
-constexpr int UNITS_PER_THREAD = (BM * BK / 8) / NUM_DQ_THREADS;  // 4
+constexpr int UNITS_PER_GROUP_THREAD = (BM * BK / 8) / (NUM_DQ_THREADS / 2);  // 8
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int SMEM_LIMIT = 232448;
 constexpr int SMEM_FIXED = 1024 + STAGES * (W_TILE + T_TILE) + 512;
@@ -72,17 +72,18 @@ __device__ __forceinline__ uint32_t unit_soff(int u) {
   }
 }
 
-// Packed unit (8 codes) read from a Q-ring row (16*BITS bytes = 128 codes).
+// Packed unit j (8 codes) of a Q-ring row (16*BITS bytes = 128 codes) at
+// shared address `row`.
 template <int BITS>
-__device__ __forceinline__ uint32_t lds_unit(const uint8_t* row, int j) {
+__device__ __forceinline__ uint32_t q_unit(uint32_t row, int j) {
   if constexpr (BITS == 4) {
-    return *reinterpret_cast<const uint32_t*>(row + j * 4);
+    return lds32(row + j * 4);
   } else if constexpr (BITS == 2) {
-    return *reinterpret_cast<const uint16_t*>(row + j * 2);
+    return lds16(row + j * 2);
   } else {
     const int off = j * 3;
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(row + (off & ~3));
-    return __funnelshift_r(w[0], w[1], (off & 3) * 8) & 0xFFFFFFu;
+    const uint32_t a = row + (off & ~3);
+    return __funnelshift_r(lds32(a), lds32(a + 4), (off & 3) * 8) & 0xFFFFFFu;
   }
 }
 
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tma_prefetch_desc(&tm_grid);
     }
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1 + NUM_DQ_WARPS);
+      mbar_init(&full[s], 1 + NUM_DQ_WARPS / 2);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < MAX_QS; ++s) {
@@ -314,15 +315,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= DQ_WARP0) {
     // ------------------------------------------------------------ dequant producers
-    const int tid = threadIdx.x - DQ_WARP0 * 32;
+    // Two groups of 4 warps; group g owns the pipeline stages with (s & 1) == g,
+    // so each stage waits on 4 warps and the groups run a stage apart.
+    const int grp = (warp - DQ_WARP0) >> 2;
+    const int gtid = threadIdx.x - (DQ_WARP0 + 4 * grp) * 32;  // 0..127
     int s = 0;
     uint32_t ph = 0;
     if constexpr (W_TMA) {
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full[s]);
+          if ((s & 1) == grp) {
+            mbar_wait(&empty[s], ph ^ 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+          }
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
@@ -330,67 +336,56 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     } else if constexpr (QTMA) {
-      // per-thread constants: smem destinations and packed-tile positions
-      uint32_t soff[UNITS_PER_THREAD];
-      int qrow[UNITS_PER_THREAD], qunit[UNITS_PER_THREAD], qcode[UNITS_PER_THREAD];
+      // Per-thread constants. Unit u = i*128 + gtid (i < 8) of a 1024-unit stage:
+      //   K-major: row r = i*16 + gtid/8 (Q row r), unit k8 = gtid%8 (+8 for odd kb)
+      //   MN:      row n = i*8 + gtid/16 (Q row n, +64 for odd kb), unit k8 = gtid%16
+      constexpr int UPT = UNITS_PER_GROUP_THREAD;
+      uint32_t soff[UPT];
 #pragma unroll
-      for (int i = 0; i < UNITS_PER_THREAD; ++i) {
-        const int u = i * NUM_DQ_THREADS + tid;
-        soff[i] = unit_soff<MN>(u);
-        if constexpr (!MN) {
-          qrow[i] = u >> 3;
-          qunit[i] = u & 7;  // + 8 * (kb & 1)
-          qcode[i] = (u & 7) * 8;
-        } else {
-          qrow[i] = u >> 4;  // + 64 * (kb & 1)
-          qunit[i] = u & 15;
-          qcode[i] = (u & 15) * 8;
-        }
-      }
+      for (int i = 0; i < UPT; ++i) soff[i] = unit_soff<MN>(i * 128 + gtid);
+      const int k8 = MN ? (gtid & 15) : (gtid & 7);
+      const int row0 = MN ? (gtid >> 4) : (gtid >> 3);
+      constexpr int ROW_STEP = MN ? 8 : 16;
+      constexpr int QROW = 16 * BITS;  // bytes per Q row (128 codes)
       const int gshift = p.q_group_shift;  // log2(group) when group < 128, else -1
-      const int gbox = p.q_grid_bytes / BM;  // bytes of grid per Q row
+      const int gbox = p.q_grid_bytes / BM;  // grid bytes per Q row
+      const uint32_t sQ32 = smem_u32(sQ), sW32 = smem_u32(sW);
       int qs = 0;
       uint32_t qph = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         int m_tile, n_tile;
         it.coords(tile, m_tile, n_tile);
         // g >= 128: one group per 128-code block; which half of the 2-group box
-        int gpar = MN ? (pair_group(m_tile, p) & 1) : 0;
+        const int gpar_mn = pair_group(m_tile, p) & 1;
         for (int kb = 0; kb < n_kb; ++kb) {
           const bool main = kb < n_kb_main;
           const int kp = kb & 1;
-          if (main && kp == 0) {
-            mbar_wait(&qfull[qs], qph);
-            if (!MN) gpar = pair_group(kb >> 1, p) & 1;
-          }
-          mbar_wait(&empty[s], ph ^ 1);
-          if (main) {
-            const uint8_t* qc = sQ + qs * p.q_stage_bytes;
-            const uint8_t* qg = qc + p.q_codes_bytes;
-            uint8_t* stile = sW + s * W_TILE;
+          if ((s & 1) == grp) {
+            if (main) mbar_wait(&qfull[qs], qph);
+            mbar_wait(&empty[s], ph ^ 1);
+            if (main) {
+              const uint32_t qc = sQ32 + qs * p.q_stage_bytes;
+              const uint32_t qg = qc + p.q_codes_bytes;
+              const uint32_t st = sW32 + s * W_TILE;
+              const int unit = MN ? k8 : (k8 + 8 * kp);
+              const int code = unit * 8;  // first code of the unit within the 128-code block
+              const int gsub = gshift >= 0 ? (code >> gshift)
+                                           : (MN ? gpar_mn : (pair_group(kb >> 1, p) & 1));
+              const int rbase = MN ? (row0 + 64 * kp) : row0;
 #pragma unroll
-            for (int i = 0; i < UNITS_PER_THREAD; ++i) {
-              int row, unit, code;
-              if constexpr (!MN) {
-                row = qrow[i];
-                unit = qunit[i] + 8 * kp;
-                code = qcode[i] + 64 * kp;
-              } else {
-                row = qrow[i] + 64 * kp;
-                unit = qunit[i];
-                code = qcode[i];
+              for (int i = 0; i < UPT; ++i) {
+                const int row = rbase + i * ROW_STEP;
+                const uint32_t v = q_unit<BITS>(qc + row * QROW, unit);
+                const float2 g = lds_f2(qg + row * gbox + gsub * 8);
+                sts128(st + soff[i], deq8_bf16_fast<BITS>(v, g));
               }
-              const uint32_t v = lds_unit<BITS>(qc + row * (16 * BITS), unit);
-              const int gsub = gshift >= 0 ? (code >> gshift) : gpar;
-              const float2 g = *reinterpret_cast<const float2*>(qg + row * gbox + gsub * 8);
-              *reinterpret_cast<uint4*>(stile + soff[i]) = deq8_bf16<BITS>(v, g);
+              fence_proxy_async_smem();
             }
-            fence_proxy_async_smem();
-          }
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&full[s]);
-            if (main && kp == 1) mbar_arrive(&qempty[qs]);
+            __syncwarp();
+            if (lane == 0) {
+              mbar_arrive(&full[s]);
+              if (main) mbar_arrive(&qempty[qs]);
+            }
           }
           if (main && kp == 1) {
             if (++qs == p.q_stages) {
@@ -410,28 +405,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int m_tile, n_tile;
         it.coords(tile, m_tile, n_tile);
         for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          if (kb < n_kb_main) {
-            uint8_t* stile = sW + s * W_TILE;
-#pragma unroll
-            for (int i = 0; i < UNITS_PER_THREAD; ++i) {
-              const int u = i * NUM_DQ_THREADS + tid;
-              int64_t wrow, wunit;
-              if constexpr (!MN) {
-                wrow = static_cast<int64_t>(m_tile) * BM + (u >> 3);
-                wunit = static_cast<int64_t>(kb) * (BK / 8) + (u & 7);
-              } else {
-                wrow = static_cast<int64_t>(kb) * BK + (u >> 4);
-                wunit = static_cast<int64_t>(m_tile) * (BM / 8) + (u & 15);
+          if ((s & 1) == grp) {
+            mbar_wait(&empty[s], ph ^ 1);
+            if (kb < n_kb_main) {
+              uint8_t* stile = sW + s * W_TILE;
+#pragma unroll 2
+              for (int i = 0; i < UNITS_PER_GROUP_THREAD; ++i) {
+                const int u = i * 128 + gtid;
+                int64_t wrow, wunit;
+                if constexpr (!MN) {
+                  wrow = static_cast<int64_t>(m_tile) * BM + (u >> 3);
+                  wunit = static_cast<int64_t>(kb) * (BK / 8) + (u & 7);
+                } else {
+                  wrow = static_cast<int64_t>(kb) * BK + (u >> 4);
+                  wunit = static_cast<int64_t>(m_tile) * (BM / 8) + (u & 15);
+                }
+                const uint64_t v = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
+                *reinterpret_cast<uint4*>(stile + unit_soff<MN>(u)) =
+                    deq8_bf16_general<BITS>(v, q.grid + wrow * q.ng_pad, wunit * 8, q.group);
               }
-              const uint64_t v = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
-              *reinterpret_cast<uint4*>(stile + unit_soff<MN>(u)) =
-                  deq8_bf16_general<BITS>(v, q.grid + wrow * q.ng_pad, wunit * 8, q.group);
+              fence_proxy_async_smem();
             }
-            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full[s]);
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
