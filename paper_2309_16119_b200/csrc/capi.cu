@@ -245,6 +245,40 @@ mlra_status check_lora(const mlra_lora* L) {
   return MLRA_OK;
 }
 
+// out[m x r] = act[m x kd] · W[kd x r]  (K4 / K5a on tensor cores; W fp32),
+// in column chunks of at most 64.
+mlra_status thin_rows_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int64_t m,
+                              int64_t kd, const float* W, int64_t r, float* out) {
+  const int64_t ldt = round_up(kd, 64);
+  auto* hi = sc.get<__nv_bfloat16>(static_cast<size_t>(2 * 64 * ldt));
+  if (!hi) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  CUDA_TRY(cudaMemsetAsync(out, 0, m * r * 4, sc.st));
+  for (int64_t j0 = 0; j0 < r; j0 += 64) {
+    const int64_t rc = r - j0 < 64 ? r - j0 : 64;
+    __nv_bfloat16* lo = hi + mlra::thin_rows(rc, false) * ldt;
+    CUDA_TRY(mlra::launch_split_t(W + j0, kd, rc, r, false, hi, lo, ldt, sc.st));
+    CUDA_TRY(mlra::launch_rowmma(act, lda, m, kd, hi, lo, ldt, out + j0, r, rc, sc.st));
+  }
+  return MLRA_OK;
+}
+
+// out[nd x r] += scale · actᵀ · V[m x r] (+ colsum[n] += Σ_t act[t, n])  (K5b / K6).
+mlra_status thin_cols_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int64_t m,
+                              int64_t nd, const float* V, int64_t r, float scale, float* out,
+                              float* colsum) {
+  const int64_t ldt = round_up(m, 64);
+  auto* hi = sc.get<__nv_bfloat16>(static_cast<size_t>(2 * 72 * ldt));
+  if (!hi) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  for (int64_t j0 = 0; j0 < r; j0 += 64) {
+    const int64_t rc = r - j0 < 64 ? r - j0 : 64;
+    float* cs = j0 == 0 ? colsum : nullptr;
+    __nv_bfloat16* lo = hi + mlra::thin_rows(rc, cs != nullptr) * ldt;
+    CUDA_TRY(mlra::launch_split_t(V + j0, m, rc, r, cs != nullptr, hi, lo, ldt, sc.st));
+    CUDA_TRY(mlra::launch_colmma(act, lda, m, nd, hi, lo, ldt, scale, out + j0, r, rc, cs, sc.st));
+  }
+  return MLRA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -483,7 +517,8 @@ mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, in
   if (!xbs || !apad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
   CUDA_TRY(cudaMemsetAsync(xbs, 0, m * rp * 2, s));
   // K4: xb = x·B (matmul(t, x, B), lora.cpp:68) and bf16(s·xb) for the extra K
-  CUDA_TRY(mlra::launch_rowdot(gp.act, gp.ld_act, m, d.cols, L->b, r, scaling, xb, xbs, rp, s));
+  if (mlra_status st = thin_rows_product(sc, gp.act, gp.ld_act, m, d.cols, L->b, r, xb)) return st;
+  CUDA_TRY(mlra::launch_scale_pad(xb, m, r, scaling, xbs, rp, s));
   CUDA_TRY(mlra::launch_pad_bf16(L->a, d.rows, r, r, apad, d.rows_pad, rp, s));
   gp.k_red_valid = d.cols;
   gp.act_lora = xbs;
@@ -530,11 +565,14 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   if (!dyA || !dyas) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
   CUDA_TRY(cudaMemsetAsync(dyas, 0, m * rp * 2, s));
   // K5a: dyA = dy·A ; d(xb) = s·dyA (autodiff.cpp:150-152 on record lora.cpp:69)
-  CUDA_TRY(mlra::launch_rowdot(dya, lddya, m, d.rows, L->a, r, scaling, dyA, dyas, rp, s));
+  if (mlra_status st = thin_rows_product(sc, dya, lddya, m, d.rows, L->a, r, dyA)) return st;
+  CUDA_TRY(mlra::launch_scale_pad(dyA, m, r, scaling, dyas, rp, s));
   // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
-  CUDA_TRY(mlra::launch_coldot(dya, lddya, m, d.rows, xb, r, scaling, da, dbias, s));
+  if (mlra_status st = thin_cols_product(sc, dya, lddya, m, d.rows, xb, r, scaling, da, dbias))
+    return st;
   // K6: dB = s·xᵀ·dyA   (autodiff.cpp:153-155 on record lora.cpp:68)
-  CUDA_TRY(mlra::launch_coldot(xa, ldxa, m, d.cols, dyA, r, scaling, db, nullptr, s));
+  if (mlra_status st = thin_cols_product(sc, xa, ldxa, m, d.cols, dyA, r, scaling, db, nullptr))
+    return st;
   if (!dx) return MLRA_OK;  // frozen input: no dX (autodiff.cpp:136)
   auto* bpad = sc.get<__nv_bfloat16>(static_cast<size_t>(d.cols_pad * rp));
   if (!bpad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
