@@ -231,23 +231,19 @@ def main():
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn(m, CFG["d_model"], device=dev, generator=gen).to(torch.bfloat16)
     dy2 = torch.randn(m, CFG["d_model"], device=dev, generator=gen).to(torch.bfloat16)
-    # one flat LoRA-gradient bucket: [dA_up | dB_up | dA_down | dB_down]
-    sizes = [up.d_out() * r, up.d_in() * r, down.d_out() * r, down.d_in() * r]
-    bucket = torch.empty(sum(sizes), device=dev, dtype=torch.float32)
-    views, o = [], 0
-    for s in sizes:
-        views.append(bucket[o:o + s])
-        o += s
-    da_up, db_up = views[0].view(up.d_out(), r), views[1].view(up.d_in(), r)
-    da_dn, db_dn = views[2].view(down.d_out(), r), views[3].view(down.d_in(), r)
+    # one flat LoRA-gradient bucket: [dA_up | dB_up | dA_down | dB_down] -> one all-reduce
+    from paper_2309_16119_b200.dp import GradBucket
+    grads = GradBucket.for_layers([up, down], dev)
+    bucket = grads.flat
+    da_up, db_up = grads.views["l0.dA"], grads.views["l0.dB"]
+    da_dn, db_dn = grads.views["l1.dA"], grads.views["l1.dB"]
 
     def step(xin, dyin):
         y1, xb1 = M.layer_forward(up, xin)
         y2, xb2 = M.layer_forward(down, y1)
         dx2 = M.layer_backward(down, y1, xb2, dyin, da=da_dn, db=db_dn)
         M.layer_backward(up, xin, xb1, dx2, da=da_up, db=db_up)
-        if world > 1:
-            dist.all_reduce(bucket)
+        grads.allreduce()
         return y2
 
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -327,8 +323,7 @@ def main():
         stream.wait_stream(copy_stream)
         dx2 = M.layer_backward(down, y1, xb2, dyd, da=da_dn, db=db_dn)
         M.layer_backward(up, xd, xb1, dx2, da=da_up, db=db_up)
-        if world > 1:
-            dist.all_reduce(bucket)
+        grads.allreduce()
         gh.copy_(bucket, non_blocking=True)
 
     for _ in range(2):

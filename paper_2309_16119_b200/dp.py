@@ -1,0 +1,61 @@
+"""Data parallelism over token micro-batches.
+
+The frozen packed weights, grids and bias are replicated; tokens are sharded
+across ranks; the only exchange per step is a sum all-reduce of the LoRA
+gradients {dA [d_out x r], dB [d_in x r]} (+ dbias when trainable) — dA and dB
+are sums over tokens (autodiff.cpp:153-155), so the sum of per-shard gradients
+equals the full-batch gradient. The reference has no distribution at all
+(SPEC.md:453); this is the B200 build's own plumbing over torch.distributed
+(NCCL over NVLink on the GPU box, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Sequence, Tuple
+
+import torch
+
+
+def shard_tokens(m: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous token range [begin, end) of `rank` (sizes differ by <= 1)."""
+    base, extra = divmod(m, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+@dataclass
+class GradBucket:
+    """One flat fp32 buffer holding every LoRA gradient of a step, so the
+    data-parallel exchange is a single all-reduce (one NCCL launch, latency
+    bound at these sizes: 2-16 MB per step)."""
+
+    flat: torch.Tensor
+    views: Dict[str, torch.Tensor]
+
+    @staticmethod
+    def create(shapes: Sequence[Tuple[str, Tuple[int, ...]]], device) -> "GradBucket":
+        total = sum(int(torch.tensor(s).prod()) for _, s in shapes)
+        flat = torch.zeros(total, dtype=torch.float32, device=device)
+        views, o = {}, 0
+        for name, s in shapes:
+            n = int(torch.tensor(s).prod())
+            views[name] = flat[o:o + n].view(*s)
+            o += n
+        return GradBucket(flat, views)
+
+    @staticmethod
+    def for_layers(layers: List, device) -> "GradBucket":
+        """dA/dB (and dbias if trainable) of each ModuLoRA layer, in order."""
+        shapes = []
+        for L in layers:
+            r = L.adapter.rank
+            shapes.append((f"{L.name}.dA", (L.d_out(), r)))
+            shapes.append((f"{L.name}.dB", (L.d_in(), r)))
+            if L.bias_trainable:
+                shapes.append((f"{L.name}.dbias", (L.d_out(),)))
+        return GradBucket.create(shapes, device)
+
+    def allreduce(self, group=None) -> None:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=group)
