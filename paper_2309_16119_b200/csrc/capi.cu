@@ -185,10 +185,15 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
   a.out = gp.out;
   a.ldo = gp.ldo;
   a.bias = gp.bias;
-  mlra_status st = make_map(&maps.act, gp.act, gp.k_red_valid, gp.tokens, gp.ld_act, 64, 256);
+  // CTA-pair kernel (512 tokens per tile) once there are enough tokens to fill
+  // it; MLRA_GEMM=1|2 forces the 1-CTA / pair kernel (tests cover both).
+  bool pair = gp.tokens > 256;
+  if (const char* force = getenv("MLRA_GEMM")) pair = atoi(force) == 2;
+  const uint32_t tbox = pair ? 128 : 256;
+  mlra_status st = make_map(&maps.act, gp.act, gp.k_red_valid, gp.tokens, gp.ld_act, 64, tbox);
   if (st) return st;
   if (a.n_kb_lora) {
-    if ((st = make_map(&maps.act_lora, gp.act_lora, gp.rp, gp.tokens, gp.rp, 64, 256))) return st;
+    if ((st = make_map(&maps.act_lora, gp.act_lora, gp.rp, gp.tokens, gp.rp, 64, tbox))) return st;
     if ((st = make_map(&maps.w_lora, gp.w_lora, gp.rp, a.m_total, gp.rp, 64, 128))) return st;
   } else {
     maps.act_lora = maps.act;
@@ -228,7 +233,10 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
       a.q_stages = 0;
     }
   }
-  CUDA_TRY(mlra::qgemm_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
+  if (pair)
+    CUDA_TRY(mlra::qgemm2_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
+  else
+    CUDA_TRY(mlra::qgemm_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
   return MLRA_OK;
 }
 

@@ -43,5 +43,9 @@ int qgemm_max_q_stages(int q_stage_bytes);
 // mn = false: forward (Ŵ K-major on the weight side); true: dX (Ŵᵀ, MN-major).
 cudaError_t qgemm_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                          bool w_tma, bool mn, bool out_f32, cudaStream_t stream);
+// CTA-pair variant (qgemm2.cu): 256 weight rows x 512 tokens per pair tile.
+// Same maps, except the activation boxes are 64 x 128 (each CTA stages half).
+cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
+                          bool w_tma, bool mn, bool out_f32, cudaStream_t stream);
 
 }  // namespace mlra

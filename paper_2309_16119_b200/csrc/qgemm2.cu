@@ -1,0 +1,442 @@
+// qgemm2.cu — K2/K3 on CTA pairs: cta_group::2 tcgen05 with two accumulators.
+//
+// Same products as qgemm.cu (forward Y = X·Ŵᵀ + LoRA, dX = dY·Ŵ + LoRA;
+// lowprec_linear.cpp:150-247, lora.cpp:68-71, autodiff.cpp:150-152), but each
+// pair tile is 256 weight-side rows (128 per CTA, each CTA dequantizes only its
+// own half) x 512 tokens (two N=256 accumulators of 256 TMEM columns each; each
+// CTA stages 128 tokens of every 256-token half). Every dequantized weight
+// element now feeds 512 tokens of MMA instead of 256, and every activation tile
+// read from L2 feeds 256 weight rows instead of 128 — halving both the
+// dequant-issue and the L2-traffic cost per FLOP relative to the 1-CTA kernel.
+//
+// Pair protocol (the leader is cluster rank 0):
+//  * operand TMA: each CTA loads its own halves with cta_group::2 TMA whose
+//    completion counts on the LEADER's full barrier; only the leader arms it
+//    (expect_tx = both CTAs' bytes);
+//  * dequant warps of both CTAs arrive (remote, release.cluster) on the
+//    leader's full barrier after fence.proxy.async;
+//  * the leader's single MMA thread issues tcgen05.mma.cta_group::2 (M=256,
+//    N=256) for both accumulators and commits empty/tfull to both CTAs
+//    (multicast);
+//  * each CTA's epilogue drains its own 128 TMEM lanes, then arrives (remote)
+//    on the leader's tempty before the next tile may overwrite TMEM.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "ptx.cuh"
+#include "qgemm.h"
+#include "qgemm_dev.cuh"
+
+namespace mlra {
+
+namespace {
+
+using namespace qg;
+
+constexpr int HB = 128;            // tokens per CTA per accumulator (MMA N=256 split in two)
+constexpr int HB_TILE = HB * BK * 2;  // 16 KB
+constexpr int PAIR_ROWS = 2 * BM;  // 256 weight-side rows per pair tile
+constexpr int PAIR_TOK = 2 * 2 * HB;  // 512 tokens per pair tile
+static_assert(2 * HB_TILE == T_TILE, "stage layout shared with the 1-CTA kernel");
+
+template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    qgemm2_kernel(const __grid_constant__ CUtensorMap tm_act,
+                  const __grid_constant__ CUtensorMap tm_act_lora,
+                  const __grid_constant__ CUtensorMap tm_w,
+                  const __grid_constant__ CUtensorMap tm_w_lora,
+                  const __grid_constant__ CUtensorMap tm_codes,
+                  const __grid_constant__ CUtensorMap tm_grid, const QWeightDev q,
+                  const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sW = smem;
+  uint8_t* sT = sW + STAGES * W_TILE;
+  uint8_t* sQ = sT + STAGES * T_TILE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sQ + p.q_stages * p.q_stage_bytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* qfull = empty + STAGES;
+  uint64_t* qempty = qfull + MAX_QS;
+  uint64_t* tfull = qempty + MAX_QS;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int n_kb_main = p.n_kb_main;
+  const int n_kb = p.n_kb_main + p.n_kb_lora;
+  const int m_pairs = static_cast<int>(p.m_total / PAIR_ROWS);
+  const int n_pairs = static_cast<int>((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
+  const int n_tiles = m_pairs * n_pairs;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_act);
+    if (p.n_kb_lora) {
+      tma_prefetch_desc(&tm_act_lora);
+      tma_prefetch_desc(&tm_w_lora);
+    }
+    if (W_TMA) tma_prefetch_desc(&tm_w);
+    if (QTMA) {
+      tma_prefetch_desc(&tm_codes);
+      tma_prefetch_desc(&tm_grid);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1 + 2 * (NUM_DQ_WARPS / 2));  // leader's is the live one
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < MAX_QS; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], NUM_DQ_WARPS);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 2 * 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();  // barrier inits visible to the peer before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ operand TMA (both CTAs)
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        const int mp = tile % m_pairs, np = tile / m_pairs;
+        const int cb = mp * 2 + static_cast<int>(rank);  // this CTA's 128-row block
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          const bool lora = kb >= n_kb_main;
+          const bool w_tma = lora || W_TMA;
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * (T_TILE + (w_tma ? W_TILE : 0)));
+          uint8_t* st = sT + s * T_TILE;
+          uint8_t* sw = sW + s * W_TILE;
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const int tok = np * PAIR_TOK + a * 2 * HB + static_cast<int>(rank) * HB;
+            if (!lora)
+              tma_load_2d_2sm(st + a * HB_TILE, &tm_act, &full[s], kb * BK, tok);
+            else
+              tma_load_2d_2sm(st + a * HB_TILE, &tm_act_lora, &full[s], (kb - n_kb_main) * BK, tok);
+          }
+          if (lora) {
+            tma_load_2d_2sm(sw, &tm_w_lora, &full[s], (kb - n_kb_main) * BK, cb * BM);
+          } else if (W_TMA) {
+            if (!MN) {
+              tma_load_2d_2sm(sw, &tm_w, &full[s], kb * BK, cb * BM);
+            } else {
+              tma_load_2d_2sm(sw, &tm_w, &full[s], cb * BM, kb * BK);
+              tma_load_2d_2sm(sw + 8192, &tm_w, &full[s], cb * BM + 64, kb * BK);
+            }
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc_main = idesc_bf16(2 * BM, 2 * HB, MN ? 1u : 0u, 0u);
+      constexpr uint32_t idesc_kmaj = idesc_bf16(2 * BM, 2 * HB, 0u, 0u);
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int tile = cid; tile < n_tiles; tile += ncl, ++local) {
+        mbar_wait_acq_cluster(tempty, (local & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait_acq_cluster(&full[s], ph);
+          tc_fence_after();
+          const bool lora = kb >= n_kb_main;
+          const int nk16 = (lora && kb == n_kb - 1) ? p.lora_k16_last : BK / 16;
+          const uint32_t sw = smem_u32(sW + s * W_TILE);
+          const uint32_t st = smem_u32(sT + s * T_TILE);
+          for (int k = 0; k < nk16; ++k) {
+            uint64_t adesc;
+            uint32_t idesc;
+            if (MN && !lora) {
+              adesc = sdesc_sw128(sw + k * 2048, 8192, 1024);
+              idesc = idesc_main;
+            } else {
+              adesc = sdesc_sw128(sw + k * 32, 16, 1024);
+              idesc = idesc_kmaj;
+            }
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+              const uint64_t bdesc = sdesc_sw128(st + a * HB_TILE + k * 32, 16, 1024);
+              tc_mma_f16_2sm(tmem_base + a * (2 * HB), adesc, bdesc, idesc,
+                             (kb | k) != 0 ? 1u : 0u);
+            }
+          }
+          tc_commit_2sm_mc(&empty[s], 0x3);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit_2sm_mc(tfull, 0x3);
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ Q-ring TMA (both CTAs, local)
+    if (QTMA && !W_TMA && lane == 0) {
+      const uint32_t qbytes = p.q_codes_bytes + p.q_grid_bytes;
+      int qs = 0;
+      uint32_t qph = 0;
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        const int mp = tile % m_pairs;
+        const int cb = mp * 2 + static_cast<int>(rank);
+        for (int pr = 0; pr < n_kb_main / 2; ++pr) {
+          mbar_wait(&qempty[qs], qph ^ 1);
+          mbar_arrive_expect_tx(&qfull[qs], qbytes);
+          uint8_t* dst = sQ + qs * p.q_stage_bytes;
+          if (!MN) {
+            tma_load_2d(dst, &tm_codes, &qfull[qs], pr * 16 * BITS, cb * BM);
+            tma_load_2d(dst + p.q_codes_bytes, &tm_grid, &qfull[qs],
+                        2 * (pair_group(pr, p) & ~1), cb * BM);
+          } else {
+            tma_load_2d(dst, &tm_codes, &qfull[qs], cb * 16 * BITS, pr * 128);
+            tma_load_2d(dst + p.q_codes_bytes, &tm_grid, &qfull[qs],
+                        2 * (pair_group(cb, p) & ~1), pr * 128);
+          }
+          if (++qs == p.q_stages) {
+            qs = 0;
+            qph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0 && warp < DQ_WARP0) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int qd = warp & 3;
+    const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
+    int local = 0;
+    for (int tile = cid; tile < n_tiles; tile += ncl, ++local) {
+      const int mp = tile % m_pairs, np = tile / m_pairs;
+      mbar_wait(tfull, local & 1);
+      tc_fence_after();
+      const int64_t wrow = static_cast<int64_t>(mp) * PAIR_ROWS + rank * BM + qd * 32 + lane;
+      const bool row_ok = wrow < p.m_valid;
+      const float bias = (p.bias != nullptr && row_ok) ? p.bias[wrow] : 0.0f;
+#pragma unroll 1
+      for (int a = 0; a < 2; ++a) {
+        const int64_t t0 = static_cast<int64_t>(np) * PAIR_TOK + a * 2 * HB;
+        const uint32_t taddr =
+            tmem_base + (static_cast<uint32_t>(qd * 32) << 16) + a * (2 * HB);
+#pragma unroll 1
+        for (int c = 0; c < 2 * HB / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + c * 32, r);
+          tc_wait_ld();
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int64_t t = t0 + c * 32 + j;
+              if (t < p.tokens) {
+                const float v = __uint_as_float(r[j]) + bias;
+                if constexpr (OUT_F32) {
+                  reinterpret_cast<float*>(p.out)[t * p.ldo + wrow] = v;
+                } else {
+                  reinterpret_cast<__nv_bfloat16*>(p.out)[t * p.ldo + wrow] =
+                      __float2bfloat16_rn(v);
+                }
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader);
+    }
+  } else if (warp >= DQ_WARP0) {
+    // ------------------------------------------------------------ dequant producers (both CTAs)
+    const int grp = (warp - DQ_WARP0) >> 2;
+    const int gtid = threadIdx.x - (DQ_WARP0 + 4 * grp) * 32;  // 0..127
+    const uint32_t full_leader0 = mapa(smem_u32(full), 0);
+    int s = 0;
+    uint32_t ph = 0;
+    if constexpr (W_TMA) {
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        for (int kb = 0; kb < n_kb; ++kb) {
+          if ((s & 1) == grp) {
+            mbar_wait(&empty[s], ph ^ 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(full_leader0 + 8 * s);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    } else if constexpr (QTMA) {
+      constexpr int UPT = UNITS_PER_GROUP_THREAD;
+      uint32_t soff[UPT];
+#pragma unroll
+      for (int i = 0; i < UPT; ++i) soff[i] = unit_soff<MN>(i * 128 + gtid);
+      const int k8 = MN ? (gtid & 15) : (gtid & 7);
+      const int row0 = MN ? (gtid >> 4) : (gtid >> 3);
+      constexpr int ROW_STEP = MN ? 8 : 16;
+      constexpr int QROW = 16 * BITS;
+      const int gshift = p.q_group_shift;
+      const int gbox = p.q_grid_bytes / BM;
+      const uint32_t sQ32 = smem_u32(sQ), sW32 = smem_u32(sW);
+      int qs = 0;
+      uint32_t qph = 0;
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        const int mp = tile % m_pairs;
+        const int cb = mp * 2 + static_cast<int>(rank);
+        const int gpar_mn = pair_group(cb, p) & 1;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          const bool main = kb < n_kb_main;
+          const int kp = kb & 1;
+          if ((s & 1) == grp) {
+            if (main) mbar_wait(&qfull[qs], qph);
+            mbar_wait(&empty[s], ph ^ 1);
+            if (main) {
+              const uint32_t qc = sQ32 + qs * p.q_stage_bytes;
+              const uint32_t qg = qc + p.q_codes_bytes;
+              const uint32_t st = sW32 + s * W_TILE;
+              const int unit = MN ? k8 : (k8 + 8 * kp);
+              const int code = unit * 8;
+              const int gsub = gshift >= 0 ? (code >> gshift)
+                                           : (MN ? gpar_mn : (pair_group(kb >> 1, p) & 1));
+              const int rbase = MN ? (row0 + 64 * kp) : row0;
+#pragma unroll
+              for (int i = 0; i < UPT; ++i) {
+                const int row = rbase + i * ROW_STEP;
+                const uint32_t v = q_unit<BITS>(qc + row * QROW, unit);
+                const float2 g = lds_f2(qg + row * gbox + gsub * 8);
+                sts128(st + soff[i], deq8_bf16_fast<BITS>(v, g));
+              }
+              fence_proxy_async_smem();
+            }
+            __syncwarp();
+            if (lane == 0) {
+              mbar_arrive_cluster(full_leader0 + 8 * s);
+              if (main) mbar_arrive(&qempty[qs]);
+            }
+          }
+          if (main && kp == 1) {
+            if (++qs == p.q_stages) {
+              qs = 0;
+              qph ^= 1;
+            }
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    } else {
+      // generic LDG path (odd group sizes / 8-bit codes)
+      for (int tile = cid; tile < n_tiles; tile += ncl) {
+        const int mp = tile % m_pairs;
+        const int cb = mp * 2 + static_cast<int>(rank);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          if ((s & 1) == grp) {
+            mbar_wait(&empty[s], ph ^ 1);
+            if (kb < n_kb_main) {
+              uint8_t* stile = sW + s * W_TILE;
+#pragma unroll 2
+              for (int i = 0; i < UNITS_PER_GROUP_THREAD; ++i) {
+                const int u = i * 128 + gtid;
+                int64_t wrow, wunit;
+                if constexpr (!MN) {
+                  wrow = static_cast<int64_t>(cb) * BM + (u >> 3);
+                  wunit = static_cast<int64_t>(kb) * (BK / 8) + (u & 7);
+                } else {
+                  wrow = static_cast<int64_t>(kb) * BK + (u >> 4);
+                  wunit = static_cast<int64_t>(cb) * (BM / 8) + (u & 15);
+                }
+                const uint64_t v = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
+                *reinterpret_cast<uint4*>(stile + unit_soff<MN>(u)) =
+                    deq8_bf16_general<BITS>(v, q.grid + wrow * q.ng_pad, wunit * 8, q.group);
+              }
+              fence_proxy_async_smem();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(full_leader0 + 8 * s);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc2(tmem_base, TMEM_COLS);
+}
+
+int sm_total() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA>
+cudaError_t launch2_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
+                      cudaStream_t stream) {
+  auto kern = qgemm2_kernel<BITS, W_TMA, MN, OUT_F32, QTMA>;
+  const int smem = SMEM_FIXED + p.q_stages * p.q_stage_bytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
+  const int64_t pairs = tiles < sm_total() / 2 ? tiles : sm_total() / 2;
+  note_launch();
+  kern<<<static_cast<unsigned>(2 * pairs), NUM_THREADS, smem, stream>>>(
+      maps.act, maps.act_lora, maps.w, maps.w_lora, maps.codes, maps.grid, q, p);
+  return cudaGetLastError();
+}
+
+template <int BITS, bool W_TMA, bool QTMA>
+cudaError_t launch2_mo(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p, bool mn,
+                       bool out_f32, cudaStream_t st) {
+  if (mn) return out_f32 ? launch2_t<BITS, W_TMA, true, true, QTMA>(maps, q, p, st)
+                         : launch2_t<BITS, W_TMA, true, false, QTMA>(maps, q, p, st);
+  return out_f32 ? launch2_t<BITS, W_TMA, false, true, QTMA>(maps, q, p, st)
+                 : launch2_t<BITS, W_TMA, false, false, QTMA>(maps, q, p, st);
+}
+
+}  // namespace
+
+cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
+                          bool w_tma, bool mn, bool out_f32, cudaStream_t stream) {
+  if (p.tokens <= 0 || p.m_total <= 0) return cudaSuccess;
+  if (w_tma) return launch2_mo<4, true, false>(maps, q, p, mn, out_f32, stream);
+  const bool qtma = p.q_stages > 0;
+  switch (q.bits) {
+    case 2: return qtma ? launch2_mo<2, false, true>(maps, q, p, mn, out_f32, stream)
+                        : launch2_mo<2, false, false>(maps, q, p, mn, out_f32, stream);
+    case 3: return qtma ? launch2_mo<3, false, true>(maps, q, p, mn, out_f32, stream)
+                        : launch2_mo<3, false, false>(maps, q, p, mn, out_f32, stream);
+    case 4: return qtma ? launch2_mo<4, false, true>(maps, q, p, mn, out_f32, stream)
+                        : launch2_mo<4, false, false>(maps, q, p, mn, out_f32, stream);
+    case 8: return launch2_mo<8, false, false>(maps, q, p, mn, out_f32, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mlra

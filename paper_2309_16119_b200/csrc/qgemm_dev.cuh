@@ -1,0 +1,78 @@
+// qgemm_dev.cuh — device helpers shared by the 1-CTA (qgemm.cu) and CTA-pair
+// (qgemm2.cu) fused dequant GEMMs.
+#pragma once
+#include <stdint.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+#include "qgemm.h"
+
+namespace mlra {
+namespace qg {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int MAX_QS = 4;
+constexpr int W_TILE = BM * BK * 2;  // 16 KB
+constexpr int T_TILE = BN * BK * 2;  // 32 KB
+constexpr int EPI_WARP0 = 4;
+constexpr int DQ_WARP0 = 8;
+constexpr int NUM_DQ_WARPS = 8;
+constexpr int NUM_DQ_THREADS = NUM_DQ_WARPS * 32;
+constexpr int NUM_THREADS = (DQ_WARP0 + NUM_DQ_WARPS) * 32;
+constexpr int UNITS_PER_GROUP_THREAD = (BM * BK / 8) / (NUM_DQ_THREADS / 2);  // 8
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int SMEM_LIMIT = 232448;
+constexpr int SMEM_FIXED = 1024 + STAGES * (W_TILE + T_TILE) + 512;
+
+// Unit u (0..1023) of a stage -> byte offset of its 16-byte chunk inside the
+// SW128 operand tile, plus its position in the packed tile.
+//  K-major (forward): tile = 128 rows x 64 k; unit = (r = u/8, k8 = u%8);
+//     canonical K-major SW128: row r at r*128, chunk k8 at (k8 ^ r%8)*16.
+//  MN-major (dX):     tile = 64 reduction rows (n) x 128 output cols (k);
+//     unit = (n = u/16, k8 = u%16); 64-column chunk c = k8/8 at c*8192,
+//     row n at n*128, 16-byte column group (k8%8 ^ n%8).
+template <bool MN>
+__device__ __forceinline__ uint32_t unit_soff(int u) {
+  if constexpr (!MN) {
+    const int r = u >> 3, k8 = u & 7;
+    return r * 128 + ((k8 ^ (r & 7)) << 4);
+  } else {
+    const int n = u >> 4, k8 = u & 15;
+    return (k8 >> 3) * 8192 + n * 128 + (((k8 & 7) ^ (n & 7)) << 4);
+  }
+}
+
+// Packed unit j (8 codes) of a Q-ring row (16*BITS bytes = 128 codes) at
+// shared address `row`.
+template <int BITS>
+__device__ __forceinline__ uint32_t q_unit(uint32_t row, int j) {
+  if constexpr (BITS == 4) {
+    return lds32(row + j * 4);
+  } else if constexpr (BITS == 2) {
+    return lds16(row + j * 2);
+  } else {
+    const int off = j * 3;
+    const uint32_t a = row + (off & ~3);
+    return __funnelshift_r(lds32(a), lds32(a + 4), (off & 3) * 8) & 0xFFFFFFu;
+  }
+}
+
+// Group index of the first code of 128-code block `blk` along the code rows.
+__device__ __forceinline__ int pair_group(int blk, const GemmArgs& p) {
+  return p.q_group_shift >= 0 ? (blk << (7 - p.q_group_shift)) : blk / p.q_group_div128;
+}
+
+struct TileIter {
+  int m_tiles;
+  int n_tiles;
+  __device__ __forceinline__ void coords(int tile, int& m, int& n) const {
+    m = tile % m_tiles;
+    n = tile / m_tiles;
+  }
+};
+
+}  // namespace qg
+}  // namespace mlra

@@ -251,3 +251,23 @@ def test_empty_tokens_and_errors():
     y1, _ = M.layer_forward(layer, x, out_dtype=torch.float32)
     y0 = M.lp_forward(ctx, x, out_dtype=torch.float32)
     assert torch.equal(y1, y0)
+
+
+@pytest.mark.parametrize("bits,mn", [(3, False), (3, True), (4, False), (2, True)])
+def test_pair_kernel_matches_single_cta(bits, mn, monkeypatch):
+    """The CTA-pair (cta_group::2) GEMM and the 1-CTA GEMM compute the same
+    products on the same bf16 operands (same K order) -> identical outputs."""
+    rows, cols, m = 768, 1024, 1100
+    q, words, sc, z = random_quantized(rows, cols, bits, 128, seed=bits + 10 * mn)
+    dq = M.DeviceQuantizedMatrix(q)
+    ctx = M.LpLinearContext(dq, M.MaterializationStrategy.RowMaterialize)
+    a = to_bf16_dev(orc.bf16_round(orc.gaussian(5, m, rows if mn else cols)))
+    outs = []
+    for mode in ("1", "2"):
+        monkeypatch.setenv("MLRA_GEMM", mode)
+        f = M.lp_backward if mn else M.lp_forward
+        outs.append(f64(f(ctx, a, out_dtype=torch.float32)))
+    assert np.array_equal(outs[0], outs[1])
+    wbf = deq_bf16_f64(words, rows, cols, bits, 128, sc, z)
+    ref = f64(a) @ (wbf if mn else wbf.T)
+    assert rel_fro(outs[1], ref) <= 1e-5
