@@ -71,6 +71,17 @@ mlra_status check_device() {
   if (major != 10 || minor != 0)
     return fail(MLRA_ERR_UNSUPPORTED, "libmlra is built for sm_100a (B200); device is sm_%d%d",
                 major, minor);
+  // Per-call workspaces come from the device's stream-ordered pool; keep freed
+  // blocks cached instead of returning them to the driver at every sync.
+  static bool pool_set[64] = {};
+  if (dev < 64 && !pool_set[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_set[dev] = true;
+  }
   return MLRA_OK;
 }
 

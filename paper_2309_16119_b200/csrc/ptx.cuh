@@ -173,9 +173,12 @@ __device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
   return r;
 }
+// Arrive on a (possibly remote) barrier by shared::cluster address, default
+// (release.cta) semantics as CUTLASS's ClusterBarrier::arrive(cta_id): the
+// producer's fence.proxy.async + this arrive is the 2-SM UMMA producer protocol.
+// An explicit .release.cluster costs a MEMBAR.ALL.GPU per arrive (ncu).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
