@@ -1,0 +1,103 @@
+"""Throughput sweep over BASELINE.json configs on one B200 (reported beside the
+headline bench; writes one JSON line per config).
+
+  cfg1  4096x4096, 4-bit g128, r=8, m=512, fwd+bwd
+  cfg2  LLaMA-7B MLP up+down, 3-bit, r=16, m=4096 (the bench.py headline)
+  cfg3  LLaMA-7B decoder linear stack Q,K,V,O,gate,up,down, 3-bit, r=8, m=8192
+  cfg4  LLaMA-65B up 22016x8192 + down 8192x22016, b in {3,4}, r=64, m=2048 (per GPU of 8)
+  cfg5  2-bit 6656x17920 materialize() bandwidth sweep (bf16 and f32 out)
+
+Timing: CUDA events, 3 warm-up + 10 timed steps, L2 flushed between steps.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from bench import synthetic_qmatrix
+from paper_2309_16119_b200 import modulora as M
+
+
+def layers_for(shapes, bits, r, strat):
+    out = []
+    for i, (rows, cols) in enumerate(shapes):
+        q, *_ = synthetic_qmatrix(rows, cols, bits, 128, 300 + i)
+        dq = M.DeviceQuantizedMatrix(q)
+        a = torch.randn(rows, r, device="cuda") * 0.02
+        b = torch.randn(cols, r, device="cuda") * 0.02
+        out.append(M.ModuLoraLayer(f"l{i}", dq, M.LoraAdapter(a, b, r, 32.0), strategy=strat))
+    return out
+
+
+def time_steps(fn, flush, steps=10, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        tot += s.elapsed_time(e)
+    return tot / steps
+
+
+def independent_layers_step(layers, m):
+    """fwd+bwd of each linear on its own input (a decoder's linears see
+    different inputs; this times the linears, not the glue between them)."""
+    xs = [torch.randn(m, L.d_in(), device="cuda").to(torch.bfloat16) for L in layers]
+    dys = [torch.randn(m, L.d_out(), device="cuda").to(torch.bfloat16) for L in layers]
+
+    def step():
+        for L, x, dy in zip(layers, xs, dys):
+            y, xb = M.layer_forward(L, x)
+            M.layer_backward(L, x, xb, dy)
+    return step
+
+
+def main():
+    strat = M.parse_strategy(os.environ.get("STRATEGY", "row"))
+    flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    pk = 1646.4
+    cfgs = {
+        "cfg1": ([(4096, 4096)], 4, 8, 512),
+        "cfg2": ([(11008, 4096), (4096, 11008)], 3, 16, 4096),
+        "cfg3": ([(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)], 3, 8, 8192),
+        "cfg4_b3": ([(22016, 8192), (8192, 22016)], 3, 64, 2048),
+        "cfg4_b4": ([(22016, 8192), (8192, 22016)], 4, 64, 2048),
+    }
+    only = sys.argv[1:]
+    for name, (shapes, bits, r, m) in cfgs.items():
+        if only and name not in only:
+            continue
+        layers = layers_for(shapes, bits, r, strat)
+        ms = time_steps(independent_layers_step(layers, m), flush)
+        flops = sum(4.0 * m * a * b + 6.0 * m * r * (a + b) for a, b in shapes)
+        print(json.dumps({"config": name, "shapes": shapes, "bits": bits, "rank": r, "tokens": m,
+                          "strategy": M.strategy_name(strat), "ms_per_step": ms,
+                          "tokens_per_s": m / (ms / 1e3), "tflops": flops / (ms / 1e3) / 1e12,
+                          "pct_measured_bf16_peak": 100 * flops / (ms / 1e3) / 1e12 / pk}),
+              flush=True)
+        del layers
+        torch.cuda.empty_cache()
+    if not only or "cfg5" in only:
+        q, *_ = synthetic_qmatrix(6656, 17920, 2, 128, 500)
+        dq = M.DeviceQuantizedMatrix(q)
+        for dt, eb in ((torch.bfloat16, 2), (torch.float32, 4)):
+            out = torch.empty(6656, 17920, dtype=dt, device="cuda")
+            ms = time_steps(lambda: M.dequantize(dq, dt, out=out), flush)
+            nbytes = 6656 * 17920 * (2 / 8 + eb) + 6656 * (17920 // 128) * 8
+            print(json.dumps({"config": "cfg5_materialize", "shape": [6656, 17920], "bits": 2,
+                              "out": str(dt), "us": ms * 1e3,
+                              "gbs": nbytes / (ms / 1e3) / 1e9,
+                              "frac_measured_hbm": nbytes / (ms / 1e3) / 1e9 / 6544.3}),
+                  flush=True)
+
+
+if __name__ == "__main__":
+    main()
