@@ -130,6 +130,57 @@ __global__ void __launch_bounds__(256) k_materialize(const QWeightDev q, int64_t
   }
 }
 
+// Bandwidth path (2-D grid, one row per blockIdx.y, no 64-bit divides): each
+// thread owns 4 items strided by 32 so every warp store covers a contiguous
+// 512 B. Items are 8-code units (bf16 out, one 16-B store) or 4-code quads
+// (f32 out, one 16-B store). Requires group % 8 == 0 (one grid entry per item).
+template <int BITS>
+__device__ __forceinline__ uint32_t quad_bits(const uint32_t* __restrict__ rw, int64_t qd) {
+  const int64_t bit = qd * 4 * BITS;
+  const int64_t w0 = bit >> 5;
+  const uint32_t off = static_cast<uint32_t>(bit & 31);
+  const uint32_t lo = __ldg(rw + w0);
+  const uint32_t hi = off + 4 * BITS > 32 ? __ldg(rw + w0 + 1) : 0u;
+  constexpr uint32_t qmask = 4 * BITS >= 32 ? 0xFFFFFFFFu : ((1u << (4 * BITS)) - 1u);
+  return __funnelshift_r(lo, hi, off) & qmask;
+}
+
+template <int BITS, bool F32>
+__global__ void __launch_bounds__(128) k_materialize_fast(const QWeightDev q, int64_t row0,
+                                                          void* __restrict__ out, int64_t ld,
+                                                          int64_t items, int gshift) {
+  constexpr int CODES = F32 ? 4 : 8;
+  const int64_t rr = blockIdx.y;
+  const int64_t r = row0 + rr;
+  const uint32_t* rw = q.words + r * q.row_words;
+  const float2* grow = q.grid + r * q.ng_pad;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * 512 + (threadIdx.x >> 5) * 128 + (threadIdx.x & 31);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t it = base + 32 * j;
+    if (it >= items) break;
+    const int64_t k0 = it * CODES;
+    const float2 g = __ldg(grow + (gshift >= 0 ? (k0 >> gshift) : k0 / q.group));
+    if constexpr (F32) {
+      const uint32_t v = quad_bits<BITS>(rw, it);
+      constexpr uint32_t mask = (1u << BITS) - 1u;
+      float f[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) f[i] = deq_entry((v >> (BITS * i)) & mask, g.x, g.y);
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * ld + k0) =
+          make_float4(f[0], f[1], f[2], f[3]);
+    } else {
+      const uint64_t v = load_unit<BITS>(rw, it);
+      uint4 o;
+      if constexpr (BITS <= 4)
+        o = deq8_bf16_fast<BITS>(static_cast<uint32_t>(v), g);
+      else
+        o = deq8_bf16<BITS>(v, g);
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * ld + k0) = o;
+    }
+  }
+}
+
 int grid_for(int64_t work, int per_block) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -143,10 +194,23 @@ int grid_for(int64_t work, int per_block) {
 template <int BITS>
 cudaError_t materialize_bits(const QWeightDev& q, int64_t row0, int64_t nrows, void* out,
                              int64_t ld, bool f32, cudaStream_t st) {
-  const int64_t units = nrows * ((q.cols + 7) / 8);
-  const int blocks = grid_for(units, 256);
   const bool vec = (q.cols % 8 == 0) && (ld % 8 == 0) &&
                    (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  if (vec && q.group % 8 == 0 && nrows <= 65535) {
+    const int64_t items = f32 ? q.cols / 4 : q.cols / 8;
+    int gshift = -1;
+    for (int sft = 3; sft < 31; ++sft)
+      if ((int64_t{1} << sft) == q.group) gshift = sft;
+    dim3 grid(static_cast<unsigned>((items + 511) / 512), static_cast<unsigned>(nrows));
+    note_launch();
+    if (f32)
+      k_materialize_fast<BITS, true><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
+    else
+      k_materialize_fast<BITS, false><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
+    return cudaGetLastError();
+  }
+  const int64_t units = nrows * ((q.cols + 7) / 8);
+  const int blocks = grid_for(units, 256);
   note_launch();
   if (f32) {
     if (vec)
