@@ -264,37 +264,50 @@ mlra_status check_lora(const mlra_lora* L) {
   return MLRA_OK;
 }
 
-// out[m x r] = act[m x kd] · W[kd x r]  (K4 / K5a on tensor cores; W fp32),
-// in column chunks of at most 64.
-mlra_status thin_rows_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int64_t m,
-                              int64_t kd, const float* W, int64_t r, float* out) {
-  const int64_t ldt = round_up(kd, 64);
-  auto* hi = sc.get<__nv_bfloat16>(static_cast<size_t>(2 * 64 * ldt));
-  if (!hi) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  CUDA_TRY(cudaMemsetAsync(out, 0, m * r * 4, sc.st));
-  for (int64_t j0 = 0; j0 < r; j0 += 64) {
-    const int64_t rc = r - j0 < 64 ? r - j0 : 64;
-    __nv_bfloat16* lo = hi + mlra::thin_rows(rc, false) * ldt;
-    CUDA_TRY(mlra::launch_split_t(W + j0, kd, rc, r, false, hi, lo, ldt, sc.st));
-    CUDA_TRY(mlra::launch_rowmma(act, lda, m, kd, hi, lo, ldt, out + j0, r, rc, sc.st));
+// Transposed hi/lo bf16 planes of an fp32 factor F [rows x r], one plane pair
+// per 64-column chunk (thin_mma.cu consumes <= 64 columns per launch). The
+// split jobs are queued on a PrepBatch, so they cost no launch of their own.
+struct Planes {
+  int n = 0;
+  __nv_bfloat16* hi[4];
+  __nv_bfloat16* lo[4];
+  int64_t rc[4];
+  int64_t ldt = 0;
+};
+
+mlra_status make_planes(Scratch& sc, mlra::PrepBatch& pb, const float* F, int64_t rows, int64_t r,
+                        bool ones, Planes* pl) {
+  pl->ldt = round_up(rows, 64);
+  pl->n = static_cast<int>((r + 63) / 64);
+  for (int c = 0; c < pl->n; ++c) {
+    const int64_t j0 = 64 * c, rc = r - j0 < 64 ? r - j0 : 64;
+    const bool o = ones && c == 0;
+    const int64_t rows_t = mlra::thin_rows(rc, o);
+    auto* hi = sc.get<__nv_bfloat16>(static_cast<size_t>(2 * rows_t * pl->ldt));
+    if (!hi) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+    pl->hi[c] = hi;
+    pl->lo[c] = hi + rows_t * pl->ldt;
+    pl->rc[c] = rc;
+    pb.split_t(F + j0, rows, rc, r, o, pl->hi[c], pl->lo[c], rows_t, pl->ldt);
   }
   return MLRA_OK;
 }
 
-// out[nd x r] += scale · actᵀ · V[m x r] (+ colsum[n] += Σ_t act[t, n])  (K5b / K6).
-mlra_status thin_cols_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int64_t m,
-                              int64_t nd, const float* V, int64_t r, float scale, float* out,
-                              float* colsum) {
-  const int64_t ldt = round_up(m, 64);
-  auto* hi = sc.get<__nv_bfloat16>(static_cast<size_t>(2 * 72 * ldt));
-  if (!hi) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  for (int64_t j0 = 0; j0 < r; j0 += 64) {
-    const int64_t rc = r - j0 < 64 ? r - j0 : 64;
-    float* cs = j0 == 0 ? colsum : nullptr;
-    __nv_bfloat16* lo = hi + mlra::thin_rows(rc, cs != nullptr) * ldt;
-    CUDA_TRY(mlra::launch_split_t(V + j0, m, rc, r, cs != nullptr, hi, lo, ldt, sc.st));
-    CUDA_TRY(mlra::launch_colmma(act, lda, m, nd, hi, lo, ldt, scale, out + j0, r, rc, cs, sc.st));
-  }
+// out[m x r] += act[m x kd] · W   (K4 / K5a; out pre-zeroed; W as planes)
+mlra_status rows_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
+                         const Planes& W, float* out, int64_t r) {
+  for (int c = 0; c < W.n; ++c)
+    CUDA_TRY(mlra::launch_rowmma(act, lda, m, kd, W.hi[c], W.lo[c], W.ldt, out + 64 * c, r,
+                                 W.rc[c], sc.st));
+  return MLRA_OK;
+}
+
+// out[nd x r] += scale · actᵀ · V  (+ colsum[n] += Σ_t act[t, n])  (K5b / K6)
+mlra_status cols_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t nd,
+                         const Planes& V, float scale, float* out, int64_t r, float* colsum) {
+  for (int c = 0; c < V.n; ++c)
+    CUDA_TRY(mlra::launch_colmma(act, lda, m, nd, V.hi[c], V.lo[c], V.ldt, scale, out + 64 * c, r,
+                                 V.rc[c], c == 0 ? colsum : nullptr, sc.st));
   return MLRA_OK;
 }
 
@@ -534,11 +547,19 @@ mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, in
   auto* xbs = sc.get<__nv_bfloat16>(static_cast<size_t>(m * rp));
   auto* apad = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows_pad * rp));
   if (!xbs || !apad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  CUDA_TRY(cudaMemsetAsync(xbs, 0, m * rp * 2, s));
-  // K4: xb = x·B (matmul(t, x, B), lora.cpp:68) and bf16(s·xb) for the extra K
-  if (mlra_status st = thin_rows_product(sc, gp.act, gp.ld_act, m, d.cols, L->b, r, xb)) return st;
-  CUDA_TRY(mlra::launch_scale_pad(xb, m, r, scaling, xbs, rp, s));
-  CUDA_TRY(mlra::launch_pad_bf16(L->a, d.rows, r, r, apad, d.rows_pad, rp, s));
+  // one launch: B -> transposed hi/lo planes, A -> padded bf16 operand, xb = 0
+  mlra::PrepBatch pb;
+  Planes bt;
+  if (mlra_status st = make_planes(sc, pb, L->b, d.cols, r, false, &bt)) return st;
+  pb.pad(L->a, d.rows, r, r, 1.0f, apad, d.rows_pad, rp);
+  pb.zero_f32(xb, m * r);
+  CUDA_TRY(mlra::launch_prep(pb, s));
+  // K4: xb = x·B (matmul(t, x, B), lora.cpp:68)
+  if (mlra_status st = rows_product(sc, gp.act, gp.ld_act, m, d.cols, bt, xb, r)) return st;
+  // bf16(s·xb), zero padded: the extra-K LoRA operand
+  mlra::PrepBatch pb2;
+  pb2.pad(xb, m, r, r, scaling, xbs, m, rp);
+  CUDA_TRY(mlra::launch_prep(pb2, s));
   gp.k_red_valid = d.cols;
   gp.act_lora = xbs;
   gp.w_lora = apad;
@@ -569,10 +590,12 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   if (mlra_status st = check_device()) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t r = L->rank, rp = round_up(r, 64);
-  CUDA_TRY(cudaMemsetAsync(da, 0, d.rows * r * 4, s));
-  CUDA_TRY(cudaMemsetAsync(db, 0, d.cols * r * 4, s));
-  if (dbias) CUDA_TRY(cudaMemsetAsync(dbias, 0, d.rows * 4, s));
-  if (m == 0) return MLRA_OK;
+  if (m == 0) {
+    CUDA_TRY(cudaMemsetAsync(da, 0, d.rows * r * 4, s));
+    CUDA_TRY(cudaMemsetAsync(db, 0, d.cols * r * 4, s));
+    if (dbias) CUDA_TRY(cudaMemsetAsync(dbias, 0, d.rows * 4, s));
+    return MLRA_OK;
+  }
   Scratch sc(s);
   const float scaling = static_cast<float>(L->alpha / static_cast<double>(r));
   const __nv_bfloat16 *xa, *dya;
@@ -581,21 +604,32 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   if (mlra_status st = aligned_act(sc, dy, lddy, m, d.rows, &dya, &lddya)) return st;
   auto* dyA = sc.get<float>(static_cast<size_t>(m * r));
   auto* dyas = sc.get<__nv_bfloat16>(static_cast<size_t>(m * rp));
-  if (!dyA || !dyas) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  CUDA_TRY(cudaMemsetAsync(dyas, 0, m * rp * 2, s));
+  auto* bpad = dx ? sc.get<__nv_bfloat16>(static_cast<size_t>(d.cols_pad * rp)) : nullptr;
+  if (!dyA || !dyas || (dx && !bpad)) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  // one launch: A, xb -> transposed hi/lo planes, B -> padded operand, zero the outputs
+  mlra::PrepBatch pb;
+  Planes at, xbt, dyat;
+  if (mlra_status st = make_planes(sc, pb, L->a, d.rows, r, false, &at)) return st;
+  if (mlra_status st = make_planes(sc, pb, xb, m, r, dbias != nullptr, &xbt)) return st;
+  if (dx) pb.pad(L->b, d.cols, r, r, 1.0f, bpad, d.cols_pad, rp);
+  pb.zero_f32(dyA, m * r);
+  pb.zero_f32(da, d.rows * r);
+  pb.zero_f32(db, d.cols * r);
+  if (dbias) pb.zero_f32(dbias, d.rows);
+  CUDA_TRY(mlra::launch_prep(pb, s));
   // K5a: dyA = dy·A ; d(xb) = s·dyA (autodiff.cpp:150-152 on record lora.cpp:69)
-  if (mlra_status st = thin_rows_product(sc, dya, lddya, m, d.rows, L->a, r, dyA)) return st;
-  CUDA_TRY(mlra::launch_scale_pad(dyA, m, r, scaling, dyas, rp, s));
+  if (mlra_status st = rows_product(sc, dya, lddya, m, d.rows, at, dyA, r)) return st;
+  mlra::PrepBatch pb2;
+  pb2.pad(dyA, m, r, r, scaling, dyas, m, rp);  // extra-K operand of the dX GEMM
+  if (mlra_status st = make_planes(sc, pb2, dyA, m, r, false, &dyat)) return st;
+  CUDA_TRY(mlra::launch_prep(pb2, s));
   // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
-  if (mlra_status st = thin_cols_product(sc, dya, lddya, m, d.rows, xb, r, scaling, da, dbias))
+  if (mlra_status st = cols_product(sc, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias))
     return st;
   // K6: dB = s·xᵀ·dyA   (autodiff.cpp:153-155 on record lora.cpp:68)
-  if (mlra_status st = thin_cols_product(sc, xa, ldxa, m, d.cols, dyA, r, scaling, db, nullptr))
+  if (mlra_status st = cols_product(sc, xa, ldxa, m, d.cols, dyat, scaling, db, r, nullptr))
     return st;
   if (!dx) return MLRA_OK;  // frozen input: no dX (autodiff.cpp:136)
-  auto* bpad = sc.get<__nv_bfloat16>(static_cast<size_t>(d.cols_pad * rp));
-  if (!bpad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  CUDA_TRY(mlra::launch_pad_bf16(L->b, d.cols, r, r, bpad, d.cols_pad, rp, s));
   GemmPlan gp{};
   gp.mn = true;
   gp.act = dya;

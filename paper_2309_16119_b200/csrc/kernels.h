@@ -19,13 +19,55 @@ cudaError_t launch_grid(const float* scales, const float* zeros, int64_t rows, i
 cudaError_t launch_materialize(const QWeightDev& q, int64_t row0, int64_t nrows, void* out,
                                int64_t ld, bool f32, cudaStream_t st);
 
+// Batched small jobs of one layer pass, one launch (thin_mma.cu k_prep).
+struct PrepTask {
+  enum Kind : int { kZeroF32 = 0, kZeroBf16 = 1, kSplitT = 2, kPadBf16 = 3 };
+  int kind;
+  int ones;            // kSplitT: append a ones row at index cols
+  const float* src;
+  void* dst;
+  void* dst2;          // kSplitT: lo plane
+  int64_t rows, cols;  // source extent (kSplitT: rows = source rows, cols = r)
+  int64_t lds;         // source leading dimension
+  int64_t rows_out;    // output rows
+  int64_t ldd;         // output leading dimension
+  float scale;         // kPadBf16
+};
+constexpr int kMaxPrep = 16;
+struct PrepBatch {
+  PrepTask t[kMaxPrep];
+  int64_t offs[kMaxPrep + 1];
+  int n = 0;
+  void add(const PrepTask& k, int64_t count) {
+    if (n == 0) offs[0] = 0;
+    t[n] = k;
+    offs[n + 1] = offs[n] + count;
+    ++n;
+  }
+  void zero_f32(float* p, int64_t count) {
+    add(PrepTask{PrepTask::kZeroF32, 0, nullptr, p, nullptr, 0, 0, 0, 0, 0, 0.f}, count);
+  }
+  void zero_bf16(void* p, int64_t count) {
+    add(PrepTask{PrepTask::kZeroBf16, 0, nullptr, p, nullptr, 0, 0, 0, 0, 0, 0.f}, count);
+  }
+  // hi/lo bf16 planes [rows_t x ldt] of the transpose of src [rows x r] (ld lds)
+  void split_t(const float* src, int64_t rows, int64_t r, int64_t lds, bool ones, void* hi,
+               void* lo, int64_t rows_t, int64_t ldt) {
+    add(PrepTask{PrepTask::kSplitT, ones ? 1 : 0, src, hi, lo, rows, r, lds, rows_t, ldt, 0.f},
+        rows_t * ldt);
+  }
+  // dst [rows_out x ldd] = bf16(scale * src[rows x cols]) zero padded
+  void pad(const float* src, int64_t rows, int64_t cols, int64_t lds, float scale, void* dst,
+           int64_t rows_out, int64_t ldd) {
+    add(PrepTask{PrepTask::kPadBf16, 0, src, dst, nullptr, rows, cols, lds, rows_out, ldd, scale},
+        rows_out * ldd);
+  }
+};
+cudaError_t launch_prep(const PrepBatch& b, cudaStream_t st);
+
 // Skinny rank-r products on tensor cores (thin_mma.cu); r <= 64 per call. Factors are passed
-// transposed and split into bf16 hi/lo planes [thin_rows(r) x ld] (launch_split_t).
+// transposed and split into bf16 hi/lo planes [thin_rows(r) x ld] (PrepBatch::split_t).
 int thin_rows(int64_t r, bool ones);
-cudaError_t launch_split_t(const float* src, int64_t rows, int64_t r, int64_t lds, bool ones,
-                           __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ldt, cudaStream_t st);
-cudaError_t launch_scale_pad(const float* src, int64_t m, int64_t r, float scale,
-                             __nv_bfloat16* pad, int64_t ldp, cudaStream_t st);
 // out[m x r] += act[m x kd] · W      (W given as Wt hi/lo [rows x ldw])
 cudaError_t launch_rowmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
                           const __nv_bfloat16* wt_hi, const __nv_bfloat16* wt_lo, int64_t ldw,
@@ -35,7 +77,5 @@ cudaError_t launch_colmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int6
                           const __nv_bfloat16* vt_hi, const __nv_bfloat16* vt_lo, int64_t ldv,
                           float scale, float* out, int64_t ldo, int64_t r, float* colsum,
                           cudaStream_t st);
-cudaError_t launch_pad_bf16(const float* src, int64_t rows, int64_t cols, int64_t lds,
-                            __nv_bfloat16* dst, int64_t rows_pad, int64_t ldd, cudaStream_t st);
 
 }  // namespace mlra

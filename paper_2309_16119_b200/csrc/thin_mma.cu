@@ -25,6 +25,8 @@ namespace {
 
 constexpr int TILE = 64;      // rows (tokens or n) per CTA tile, and K chunk
 constexpr int PADW = 72;      // padded smem row (bf16): conflict-free ldmatrix
+constexpr int NS = 4;         // cp.async pipeline depth (chunks in flight per CTA)
+constexpr int thin_smem_bytes(int nt) { return (NS * TILE * PADW + NS * 2 * 8 * nt * PADW) * 2; }
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -100,8 +102,8 @@ __global__ void __launch_bounds__(128)
              int64_t ldw, int64_t k_per_split, float* __restrict__ out, int64_t ldo, int rc) {
   constexpr int ROWS = 8 * NT;
   extern __shared__ __align__(16) __nv_bfloat16 thin_smem[];
-  __nv_bfloat16* sa[2] = {thin_smem, thin_smem + TILE * PADW};
-  __nv_bfloat16* sw[2] = {thin_smem + 2 * TILE * PADW, thin_smem + 2 * TILE * PADW + 2 * ROWS * PADW};
+  __nv_bfloat16* const sa0 = thin_smem;                      // NS act tiles
+  __nv_bfloat16* const sw0 = thin_smem + NS * TILE * PADW;   // NS factor tiles (hi+lo)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * TILE;
@@ -111,24 +113,25 @@ __global__ void __launch_bounds__(128)
   float acc[NT][4];
 #pragma unroll
   for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
-  if (nch > 0) {
-    load_tile(su32(sa[0]), act, lda, m, ke, t0, ks);
-    load_factor<NT>(su32(sw[0]), wt_hi, wt_lo, ldw, ks);
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nch) {
+      load_tile(su32(sa0 + c * TILE * PADW), act, lda, m, ke, t0, ks + c * TILE);
+      load_factor<NT>(su32(sw0 + c * 2 * ROWS * PADW), wt_hi, wt_lo, ldw, ks + c * TILE);
+    }
     cp_commit();
   }
   for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    if (c + 1 < nch) {
-      load_tile(su32(sa[b ^ 1]), act, lda, m, ke, t0, ks + (c + 1) * TILE);
-      load_factor<NT>(su32(sw[b ^ 1]), wt_hi, wt_lo, ldw, ks + (c + 1) * TILE);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+    const int pf = c + NS - 1, b = c % NS;
+    if (pf < nch) {
+      load_tile(su32(sa0 + (pf % NS) * TILE * PADW), act, lda, m, ke, t0, ks + pf * TILE);
+      load_factor<NT>(su32(sw0 + (pf % NS) * 2 * ROWS * PADW), wt_hi, wt_lo, ldw, ks + pf * TILE);
     }
+    cp_commit();
+    cp_wait<NS - 1>();
     __syncthreads();
-    const uint32_t abase = su32(sa[b]) + ((warp * 16 + (lane & 15)) * PADW + (lane >> 4) * 8) * 2;
-    const __nv_bfloat16* wsm = sw[b];
+    const uint32_t abase =
+        su32(sa0 + b * TILE * PADW) + ((warp * 16 + (lane & 15)) * PADW + (lane >> 4) * 8) * 2;
+    const __nv_bfloat16* wsm = sw0 + b * 2 * ROWS * PADW;
 #pragma unroll
     for (int k16 = 0; k16 < 4; ++k16) {
       uint32_t a[4];
@@ -170,8 +173,8 @@ __global__ void __launch_bounds__(128)
              int rc, float* __restrict__ colsum) {
   constexpr int ROWS = 8 * NT;
   extern __shared__ __align__(16) __nv_bfloat16 thin_smem[];
-  __nv_bfloat16* sa[2] = {thin_smem, thin_smem + TILE * PADW};
-  __nv_bfloat16* sv[2] = {thin_smem + 2 * TILE * PADW, thin_smem + 2 * TILE * PADW + 2 * ROWS * PADW};
+  __nv_bfloat16* const sa0 = thin_smem;
+  __nv_bfloat16* const sv0 = thin_smem + NS * TILE * PADW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int64_t n0 = static_cast<int64_t>(blockIdx.x) * TILE;
@@ -181,27 +184,28 @@ __global__ void __launch_bounds__(128)
   float acc[NT][4];
 #pragma unroll
   for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
-  if (nch > 0) {
-    load_tile(su32(sa[0]), act, lda, te, nd, ts, n0);
-    load_factor<NT>(su32(sv[0]), vt_hi, vt_lo, ldv, ts);
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nch) {
+      load_tile(su32(sa0 + c * TILE * PADW), act, lda, te, nd, ts + c * TILE, n0);
+      load_factor<NT>(su32(sv0 + c * 2 * ROWS * PADW), vt_hi, vt_lo, ldv, ts + c * TILE);
+    }
     cp_commit();
   }
   for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    if (c + 1 < nch) {
-      load_tile(su32(sa[b ^ 1]), act, lda, te, nd, ts + (c + 1) * TILE, n0);
-      load_factor<NT>(su32(sv[b ^ 1]), vt_hi, vt_lo, ldv, ts + (c + 1) * TILE);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+    const int pf = c + NS - 1, b = c % NS;
+    if (pf < nch) {
+      load_tile(su32(sa0 + (pf % NS) * TILE * PADW), act, lda, te, nd, ts + pf * TILE, n0);
+      load_factor<NT>(su32(sv0 + (pf % NS) * 2 * ROWS * PADW), vt_hi, vt_lo, ldv, ts + pf * TILE);
     }
+    cp_commit();
+    cp_wait<NS - 1>();
     __syncthreads();
     // A fragment (M = n, K = t) from the [t][n] tile via transposed ldmatrix:
     // lane l addresses row t = (l & 7) + 8*(l >> 4), col n = warp*16 + 8*((l >> 3) & 1)
-    const uint32_t abase =
-        su32(sa[b]) + (((lane & 7) + ((lane >> 4) << 3)) * PADW + warp * 16 + ((lane >> 3) & 1) * 8) * 2;
-    const __nv_bfloat16* vsm = sv[b];
+    const uint32_t abase = su32(sa0 + b * TILE * PADW) +
+                           (((lane & 7) + ((lane >> 4) << 3)) * PADW + warp * 16 +
+                            ((lane >> 3) & 1) * 8) * 2;
+    const __nv_bfloat16* vsm = sv0 + b * 2 * ROWS * PADW;
 #pragma unroll
     for (int k16 = 0; k16 < 4; ++k16) {
       uint32_t a[4];
@@ -235,51 +239,46 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// hi/lo bf16 split of an fp32 [rows x r] matrix, transposed to [8NT x ldt]
-// (zero padded); optional ones row at index r (for column sums).
-__global__ void k_split_t(const float* __restrict__ src, int64_t rows, int64_t r, int64_t lds,
-                          int64_t rows_t, int64_t ldt, int ones_row,
-                          __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
-  const int64_t total = rows_t * ldt;
+// One launch for a layer pass's small conversion / zeroing jobs (PrepBatch):
+// grid-stride over the concatenated index spaces of up to kMaxPrep tasks.
+__global__ void k_prep(const PrepBatch b) {
+  const int64_t total = b.offs[b.n];
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = i / ldt, k = i % ldt;
-    float v = 0.0f;
-    if (k < rows) {
-      if (j < r)
-        v = src[k * lds + j];
-      else if (j == r && ones_row)
-        v = 1.0f;
+    int t = 0;
+    while (i >= b.offs[t + 1]) ++t;
+    const PrepTask& k = b.t[t];
+    const int64_t j = i - b.offs[t];
+    switch (k.kind) {
+      case PrepTask::kZeroF32:
+        reinterpret_cast<float*>(k.dst)[j] = 0.0f;
+        break;
+      case PrepTask::kZeroBf16:
+        reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = __float2bfloat16_rn(0.0f);
+        break;
+      case PrepTask::kSplitT: {  // hi/lo planes [rows_out x ldd] of src^T (cols = r)
+        const int64_t row = j / k.ldd, col = j % k.ldd;
+        float v = 0.0f;
+        if (col < k.rows) {
+          if (row < k.cols)
+            v = k.src[col * k.lds + row];
+          else if (row == k.cols && k.ones)
+            v = 1.0f;
+        }
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = h;
+        reinterpret_cast<__nv_bfloat16*>(k.dst2)[j] = __float2bfloat16_rn(v - __bfloat162float(h));
+        break;
+      }
+      case PrepTask::kPadBf16: {  // dst [rows_out x ldd] = bf16(scale * src) zero-padded
+        const int64_t row = j / k.ldd, col = j % k.ldd;
+        const float v = (row < k.rows && col < k.cols) ? k.scale * k.src[row * k.lds + col] : 0.0f;
+        reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = __float2bfloat16_rn(v);
+        break;
+      }
     }
-    const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    hi[i] = h;
-    lo[i] = __float2bfloat16_rn(v - __bfloat162float(h));
   }
 }
-
-// pad[t, j] = bf16(scale · out[t, j]) for j < r (pad pre-zeroed beyond r).
-__global__ void k_scale_pad(const float* __restrict__ src, int64_t m, int64_t r, float scale,
-                            __nv_bfloat16* __restrict__ pad, int64_t ldp) {
-  const int64_t total = m * r;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = i / r, j = i % r;
-    pad[t * ldp + j] = __float2bfloat16_rn(scale * src[i]);
-  }
-}
-
-__global__ void k_pad_bf16(const float* __restrict__ src, int64_t rows, int64_t cols,
-                           int64_t lds, __nv_bfloat16* __restrict__ dst, int64_t rows_pad,
-                           int64_t ldd) {
-  const int64_t total = rows_pad * ldd;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / ldd, c = i % ldd;
-    dst[i] = __float2bfloat16_rn((r < rows && c < cols) ? src[r * lds + c] : 0.0f);
-  }
-}
-
-constexpr int thin_smem_bytes(int nt) { return (2 * TILE * PADW + 4 * 8 * nt * PADW) * 2; }
 
 int sms() {
   static int n = 0;
@@ -341,23 +340,14 @@ cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
 
 }  // namespace
 
+cudaError_t launch_prep(const PrepBatch& b, cudaStream_t st) {
+  if (b.n == 0 || b.offs[b.n] == 0) return cudaSuccess;
+  note_launch();
+  k_prep<<<blocks_for(b.offs[b.n]), 256, 0, st>>>(b);
+  return cudaGetLastError();
+}
+
 int thin_rows(int64_t r, bool ones) { return static_cast<int>((r + (ones ? 1 : 0) + 7) / 8 * 8); }
-
-cudaError_t launch_split_t(const float* src, int64_t rows, int64_t r, int64_t lds, bool ones,
-                           __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t ldt, cudaStream_t st) {
-  const int64_t rows_t = thin_rows(r, ones);
-  note_launch();
-  k_split_t<<<blocks_for(rows_t * ldt), 256, 0, st>>>(src, rows, r, lds, rows_t, ldt,
-                                                      ones ? 1 : 0, hi, lo);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_scale_pad(const float* src, int64_t m, int64_t r, float scale,
-                             __nv_bfloat16* pad, int64_t ldp, cudaStream_t st) {
-  note_launch();
-  k_scale_pad<<<blocks_for(m * r), 256, 0, st>>>(src, m, r, scale, pad, ldp);
-  return cudaGetLastError();
-}
 
 #define MLRA_NT_DISPATCH(NTV, CALL)            \
   switch (NTV) {                               \
@@ -390,17 +380,6 @@ cudaError_t launch_colmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int6
 #define CALL_COL(N) colmma_nt<N>(act, lda, m, nd, vt_hi, vt_lo, ldv, scale, out, ldo, r, colsum, st)
   MLRA_NT_DISPATCH(thin_rows(r, colsum != nullptr) / 8, CALL_COL)
 #undef CALL_COL
-}
-
-cudaError_t launch_pad_bf16(const float* src, int64_t rows, int64_t cols, int64_t lds,
-                            __nv_bfloat16* dst, int64_t rows_pad, int64_t ldd, cudaStream_t st) {
-  int64_t blocks = (rows_pad * ldd + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
-  note_launch();
-  k_pad_bf16<<<static_cast<unsigned>(blocks), 256, 0, st>>>(src, rows, cols, lds, dst, rows_pad,
-                                                            ldd);
-  return cudaGetLastError();
 }
 
 }  // namespace mlra
