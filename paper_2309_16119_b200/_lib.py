@@ -7,7 +7,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmlra.so")
+LIB_PATH = os.environ.get("MLRA_LIB") or os.path.join(HERE, "libmlra.so")
 
 MLRA_OK = 0
 STATUS_NAMES = {

@@ -303,11 +303,34 @@ mlra_status rows_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int
 }
 
 // out[nd x r] += scale · actᵀ · V  (+ colsum[n] += Σ_t act[t, n])  (K5b / K6)
-mlra_status cols_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t nd,
-                         const Planes& V, float scale, float* out, int64_t r, float* colsum) {
+mlra_status cols_product(cudaStream_t st, const __nv_bfloat16* act, int64_t lda, int64_t m,
+                         int64_t nd, const Planes& V, float scale, float* out, int64_t r,
+                         float* colsum) {
   for (int c = 0; c < V.n; ++c)
     CUDA_TRY(mlra::launch_colmma(act, lda, m, nd, V.hi[c], V.lo[c], V.ldt, scale, out + 64 * c, r,
-                                 V.rc[c], c == 0 ? colsum : nullptr, sc.st));
+                                 V.rc[c], c == 0 ? colsum : nullptr, st));
+  return MLRA_OK;
+}
+
+// Per-thread, per-device side stream: the dA/dB products of a backward pass run
+// on it concurrently with the dX GEMM (they fill the SMs its last tile wave
+// leaves idle) and are joined back to the caller's stream before return.
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+mlra_status side_stream(SideStream** out) {
+  thread_local SideStream per_dev[64];
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 64) return fail(MLRA_ERR_UNSUPPORTED, "device index %d", dev);
+  SideStream& ss = per_dev[dev];
+  if (!ss.st) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ss.st, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
   return MLRA_OK;
 }
 
@@ -623,11 +646,20 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   pb2.pad(dyA, m, r, r, scaling, dyas, m, rp);  // extra-K operand of the dX GEMM
   if (mlra_status st = make_planes(sc, pb2, dyA, m, r, false, &dyat)) return st;
   CUDA_TRY(mlra::launch_prep(pb2, s));
+  // K5b / K6 go to the side stream when a dX GEMM follows (overlap), else inline
+  SideStream* side = nullptr;
+  cudaStream_t cs = s;
+  if (dx) {
+    if (mlra_status st = side_stream(&side)) return st;
+    cs = side->st;
+    CUDA_TRY(cudaEventRecord(side->fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(cs, side->fork, 0));
+  }
   // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
-  if (mlra_status st = cols_product(sc, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias))
+  if (mlra_status st = cols_product(cs, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias))
     return st;
   // K6: dB = s·xᵀ·dyA   (autodiff.cpp:153-155 on record lora.cpp:68)
-  if (mlra_status st = cols_product(sc, xa, ldxa, m, d.cols, dyat, scaling, db, r, nullptr))
+  if (mlra_status st = cols_product(cs, xa, ldxa, m, d.cols, dyat, scaling, db, r, nullptr))
     return st;
   if (!dx) return MLRA_OK;  // frozen input: no dX (autodiff.cpp:136)
   GemmPlan gp{};
@@ -644,7 +676,11 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   gp.ldo = lddx;
   gp.out_f32 = dx_dtype == MLRA_F32;
   // K3: dx = dy·Ŵ + (s·dyA)·Bᵀ   (lp_backward + matmul-bwd dx, lora.cpp:68)
-  return run_gemm(L->q, L->strategy, gp, sc);
+  const mlra_status gst = run_gemm(L->q, L->strategy, gp, sc);
+  // join: the caller's stream (and the scratch frees queued on it) waits for dA/dB
+  CUDA_TRY(cudaEventRecord(side->join, cs));
+  CUDA_TRY(cudaStreamWaitEvent(s, side->join, 0));
+  return gst;
 }
 
 }  // extern "C"

@@ -13,7 +13,10 @@ namespace qg {
 constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 64;
-constexpr int STAGES = 4;
+#ifndef MLRA_STAGES
+#define MLRA_STAGES 4
+#endif
+constexpr int STAGES = MLRA_STAGES;
 constexpr int MAX_QS = 4;
 constexpr int W_TILE = BM * BK * 2;  // 16 KB
 constexpr int T_TILE = BN * BK * 2;  // 32 KB
