@@ -244,6 +244,8 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
       a.q_stages = 0;
     }
   }
+  if (const char* tr = getenv("MLRA_TRACE"))  // dev-only: MMA-thread wait cycles per CTA pair
+    a.trace = reinterpret_cast<unsigned long long*>(strtoull(tr, nullptr, 0));
   if (pair)
     CUDA_TRY(mlra::qgemm2_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
   else

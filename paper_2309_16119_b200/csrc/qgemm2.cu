@@ -153,11 +153,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int local = 0;
+      unsigned long long t_full = 0, t_tempty = 0;
+      const unsigned long long t_start = p.trace ? clock64() : 0;
       for (int tile = cid; tile < n_tiles; tile += ncl, ++local) {
+        const unsigned long long tw0 = p.trace ? clock64() : 0;
         mbar_wait_acq_cluster(tempty, (local & 1) ^ 1);
+        if (p.trace) t_tempty += clock64() - tw0;
         tc_fence_after();
         for (int kb = 0; kb < n_kb; ++kb) {
+          const unsigned long long tf0 = p.trace ? clock64() : 0;
           mbar_wait_acq_cluster(&full[s], ph);
+          if (p.trace) t_full += clock64() - tf0;
           tc_fence_after();
           const bool lora = kb >= n_kb_main;
           const int nk16 = (lora && kb == n_kb - 1) ? p.lora_k16_last : BK / 16;
@@ -187,6 +193,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           }
         }
         tc_commit_2sm_mc(tfull, 0x3);
+      }
+      if (p.trace) {  // dev-only instrumentation (MLRA_TRACE)
+        p.trace[4 * cid + 0] = clock64() - t_start;
+        p.trace[4 * cid + 1] = t_full;
+        p.trace[4 * cid + 2] = t_tempty;
+        p.trace[4 * cid + 3] = static_cast<unsigned long long>(local);
       }
     }
   } else if (warp == 2) {
@@ -230,36 +242,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int64_t wrow = static_cast<int64_t>(mp) * PAIR_ROWS + rank * BM + qd * 32 + lane;
       const bool row_ok = wrow < p.m_valid;
       const float bias = (p.bias != nullptr && row_ok) ? p.bias[wrow] : 0.0f;
-#pragma unroll 1
-      for (int a = 0; a < 2; ++a) {
-        const int64_t t0 = static_cast<int64_t>(np) * PAIR_TOK + a * 2 * HB;
-        const uint32_t taddr =
-            tmem_base + (static_cast<uint32_t>(qd * 32) << 16) + a * (2 * HB);
-#pragma unroll 1
-        for (int c = 0; c < 2 * HB / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + c * 32, r);
-          tc_wait_ld();
-          if (row_ok) {
+      // 16 chunks of 32 TMEM columns = tokens [np*512 + 32cc, +32) (acc0 then acc1).
+      // TMEM loads are double-buffered so their latency hides under the previous
+      // chunk's stores; TMEM is released right after the last load completes.
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
+      const int64_t tbase = static_cast<int64_t>(np) * PAIR_TOK;
+      auto store_chunk = [&](const uint32_t(&r)[32], int cc) {
+        if (!row_ok) return;
+        const int64_t t0 = tbase + cc * 32;
+        if (t0 + 32 <= p.tokens) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int64_t t = t0 + c * 32 + j;
-              if (t < p.tokens) {
-                const float v = __uint_as_float(r[j]) + bias;
-                if constexpr (OUT_F32) {
-                  reinterpret_cast<float*>(p.out)[t * p.ldo + wrow] = v;
-                } else {
-                  reinterpret_cast<__nv_bfloat16*>(p.out)[t * p.ldo + wrow] =
-                      __float2bfloat16_rn(v);
-                }
-              }
+          for (int j = 0; j < 32; ++j) {
+            const float v = __uint_as_float(r[j]) + bias;
+            if constexpr (OUT_F32)
+              reinterpret_cast<float*>(p.out)[(t0 + j) * p.ldo + wrow] = v;
+            else
+              reinterpret_cast<__nv_bfloat16*>(p.out)[(t0 + j) * p.ldo + wrow] =
+                  __float2bfloat16_rn(v);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (t0 + j < p.tokens) {
+              const float v = __uint_as_float(r[j]) + bias;
+              if constexpr (OUT_F32)
+                reinterpret_cast<float*>(p.out)[(t0 + j) * p.ldo + wrow] = v;
+              else
+                reinterpret_cast<__nv_bfloat16*>(p.out)[(t0 + j) * p.ldo + wrow] =
+                    __float2bfloat16_rn(v);
             }
           }
         }
+      };
+      uint32_t ra[32], rb[32];
+      tmem_ld_32x32b_x32(taddr, ra);
+      tc_wait_ld();
+#pragma unroll 1
+      for (int cc = 0; cc < 16; cc += 2) {
+        tmem_ld_32x32b_x32(taddr + (cc + 1) * 32, rb);
+        store_chunk(ra, cc);
+        tc_wait_ld();
+        if (cc + 2 < 16) {
+          tmem_ld_32x32b_x32(taddr + (cc + 2) * 32, ra);
+        } else {
+          tc_fence_before();  // all TMEM reads of this tile are complete
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        }
+        store_chunk(rb, cc + 1);
+        if (cc + 2 < 16) tc_wait_ld();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader);
     }
   } else if (warp >= DQ_WARP0) {
     // ------------------------------------------------------------ dequant producers (both CTAs)

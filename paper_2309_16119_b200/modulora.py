@@ -136,10 +136,13 @@ class DeviceQuantizedMatrix:
                     device_bytes=nbytes.value, uncertified_groups=u.value)
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib._lib is not None:
-            lib().mlra_qweight_destroy(h)
-            self._h = C.c_void_p()
+        try:
+            h = getattr(self, "_h", None)
+            if h is not None and h.value and _lib._lib is not None:
+                lib().mlra_qweight_destroy(h)
+                self._h = C.c_void_p()
+        except Exception:  # interpreter shutdown: module globals already torn down
+            pass
 
 
 def dequantize(q: DeviceQuantizedMatrix, dtype: torch.dtype = torch.float32,
