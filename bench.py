@@ -54,6 +54,7 @@ def _config_dict(strategy: str, n: int):
         "lora_alpha": CFG["alpha"], "tokens_per_gpu": CFG["m"], "global_tokens": CFG["m"] * n,
         "strategy": strategy, "parallelism": f"dp{n}" if n > 1 else "single",
         "l2": "flushed between timed steps (512 MiB write, outside the events)",
+        "launch": "eager (--graph: CUDA graph replay)",
     }
 
 
@@ -198,6 +199,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--strategy", default="row", choices=["weight", "row", "matvec"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the step as a captured CUDA graph (default: eager launches; "
+                         "measured equal at cfg2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -249,9 +253,33 @@ def main():
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    def compute(xin, dyin):
+        y1, xb1 = M.layer_forward(up, xin)
+        y2, xb2 = M.layer_forward(down, y1)
+        dx2 = M.layer_backward(down, y1, xb2, dyin, da=da_dn, db=db_dn)
+        M.layer_backward(up, xin, xb1, dx2, da=da_up, db=db_up)
+
     for _ in range(args.warmup):
         step(x, dy2)
     torch.cuda.synchronize(dev)
+    use_graph = args.graph
+    if use_graph:
+        # The whole fwd+bwd of the layer pair (~20 kernels, stream-ordered scratch,
+        # side-stream fork/join) captured once and replayed: no per-launch host
+        # overhead or inter-kernel gaps. The NCCL all-reduce stays eager.
+        graph = torch.cuda.CUDAGraph()
+        c0 = lib().mlra_kernel_launches()
+        with torch.cuda.graph(graph):
+            compute(x, dy2)
+        graph_kernels = lib().mlra_kernel_launches() - c0  # libmlra kernels in one replay
+        torch.cuda.synchronize(dev)
+
+        def step(xin, dyin):  # noqa: F811  (same inputs as captured)
+            graph.replay()
+            grads.allreduce()
+        for _ in range(2):
+            step(x, dy2)
+        torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
 
@@ -266,6 +294,8 @@ def main():
             ev[i][1].record(stream)
         torch.cuda.synchronize(dev)
     launches = lib().mlra_kernel_launches() - launches0
+    if use_graph:  # replays launch the captured kernels without touching the host counter
+        launches += graph_kernels * args.steps
     step_ms = [s.elapsed_time(e) for s, e in ev]
     total_ms = sum(step_ms)
     if world > 1:
