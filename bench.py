@@ -54,7 +54,6 @@ def _config_dict(strategy: str, n: int):
         "lora_alpha": CFG["alpha"], "tokens_per_gpu": CFG["m"], "global_tokens": CFG["m"] * n,
         "strategy": strategy, "parallelism": f"dp{n}" if n > 1 else "single",
         "l2": "flushed between timed steps (512 MiB write, outside the events)",
-        "launch": "eager (--graph: CUDA graph replay)",
     }
 
 
@@ -409,7 +408,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (uniform 3-bit codes, RTN-like grids; N(0,1) activations)",
-            "config": _config_dict(args.strategy, world),
+            "config": dict(_config_dict(args.strategy, world),
+                           launch="cuda-graph replay" if use_graph else "eager"),
             "tflops": step_flops / (ms_per_step / 1e3) / 1e12,
             "pct_bf16_peak": 100.0 * step_flops / (ms_per_step / 1e3) / 1e12 / peak_tf,
             "roofline": {"bound": "tensor", "kernel": "qgemm (fused dequant tcgen05 GEMM)",
