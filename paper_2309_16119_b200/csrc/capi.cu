@@ -232,6 +232,10 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
     a.q_stages = mlra::qgemm_max_q_stages(a.q_stage_bytes);
     a.q_group_shift = g < 128 ? (g == 32 ? 5 : 6) : -1;
     a.q_group_div128 = g >= 128 ? static_cast<int>(g / 128) : 1;
+    {
+      const uint64_t d = static_cast<uint64_t>(a.q_group_div128);
+      a.q_group_magic = d > 1 ? static_cast<uint32_t>(((1ull << 32) + d - 1) / d) : 0u;
+    }
     if (a.q_stages >= 2) {
       if ((st = make_map(&maps.codes, d.words, d.row_words * 4, d.rows_pad, d.row_words * 4,
                          16 * d.bits, 128, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1,

@@ -142,11 +142,11 @@ __device__ __forceinline__ void unit_magic(uint32_t v, uint32_t (&m)[8]) {
 }
 
 // Fast unit: 8 codes (BITS <= 4, packed in v) sharing grid g -> 8 bf16.
+// deq8_bf16_cert assumes a certified group (caller checked g.x > 0).
 // Certified groups: FADD2 (exact code -> float) + FFMA2 (one rounding) +
 // cvt.rn.bf16x2; uncertified groups take the exact f64 path.
 template <int BITS>
-__device__ __forceinline__ uint4 deq8_bf16_fast(uint32_t v, float2 g) {
-  if (!(g.x > 0.0f)) return deq8_bf16<BITS>(v, g);
+__device__ __forceinline__ uint4 deq8_bf16_cert(uint32_t v, float2 g) {
   uint32_t m[8];
   unit_magic<BITS>(v, m);
   const uint64_t neg = 0xCB000000CB000000ull;  // (-2^23, -2^23)
@@ -159,6 +159,11 @@ __device__ __forceinline__ uint4 deq8_bf16_fast(uint32_t v, float2 g) {
     o[j] = f2_to_bf16x2(f2_fma(f2_add(pr, neg), s2, z2));
   }
   return make_uint4(o[0], o[1], o[2], o[3]);
+}
+template <int BITS>
+__device__ __forceinline__ uint4 deq8_bf16_fast(uint32_t v, float2 g) {
+  if (!(g.x > 0.0f)) return deq8_bf16<BITS>(v, g);
+  return deq8_bf16_cert<BITS>(v, g);
 }
 
 // General unit: groups may change inside the 8 codes (group % 8 != 0; only the

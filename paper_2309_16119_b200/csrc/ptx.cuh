@@ -58,6 +58,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(0x989680)
       : "memory");
 }
+// Backoff wait for waiters OFF the critical path (producers that run stages
+// ahead, the epilogue between tiles). try_wait's suspend is woken by every
+// barrier event in the CTA, so under heavy barrier traffic the loop above
+// re-issues constantly (ncu: the activation-TMA warp took ~half of SMSP0's
+// issue slots, starving the dequant warps sharing that scheduler). A
+// non-blocking test + nanosleep costs a few instructions per `NS`.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+template <int NS>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) __nanosleep(NS);
+}
 
 // 32-bit shared-memory accesses by explicit .shared address (no 64-bit
 // generic-address arithmetic in the dequant inner loop).

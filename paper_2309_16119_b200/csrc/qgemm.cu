@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int m_tile, n_tile;
         it.coords(tile, m_tile, n_tile);
         for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_backoff<PROD_NS>(&empty[s], ph ^ 1);
           const bool lora = kb >= n_kb_main;
           const bool w_tma = lora || W_TMA;
           mbar_arrive_expect_tx(&full[s], T_TILE + (w_tma ? W_TILE : 0));
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int m_tile, n_tile;
         it.coords(tile, m_tile, n_tile);
         for (int pr = 0; pr < n_kb_main / 2; ++pr) {
-          mbar_wait(&qempty[qs], qph ^ 1);
+          mbar_wait_backoff<PROD_NS>(&qempty[qs], qph ^ 1);
           mbar_arrive_expect_tx(&qfull[qs], qbytes);
           uint8_t* dst = sQ + qs * p.q_stage_bytes;
           // grid boxes start on an even group: TMA box starts must be 16-byte aligned
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       it.coords(tile, m_tile, n_tile);
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait_backoff<EPI_NS>(&tfull[acc], aph);
       tc_fence_after();
       const int64_t wrow = static_cast<int64_t>(m_tile) * BM + qd * 32 + lane;
       const bool row_ok = wrow < p.m_valid;
@@ -285,7 +285,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int k8 = MN ? (gtid & 15) : (gtid & 7);
       const int row0 = MN ? (gtid >> 4) : (gtid >> 3);
       constexpr int ROW_STEP = MN ? 8 : 16;
-      constexpr int QROW = 16 * BITS;  // bytes per Q row (128 codes)
       const int gshift = p.q_group_shift;  // log2(group) when group < 128, else -1
       const int gbox = p.q_grid_bytes / BM;  // grid bytes per Q row
       const uint32_t sQ32 = smem_u32(sQ), sW32 = smem_u32(sW);
@@ -311,13 +310,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int gsub = gshift >= 0 ? (code >> gshift)
                                            : (MN ? gpar_mn : (pair_group(kb >> 1, p) & 1));
               const int rbase = MN ? (row0 + 64 * kp) : row0;
-#pragma unroll
-              for (int i = 0; i < UPT; ++i) {
-                const int row = rbase + i * ROW_STEP;
-                const uint32_t v = q_unit<BITS>(qc + row * QROW, unit);
-                const float2 g = lds_f2(qg + row * gbox + gsub * 8);
-                sts128(st + soff[i], deq8_bf16_fast<BITS>(v, g));
-              }
+dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
               fence_proxy_async_smem();
             }
             __syncwarp();

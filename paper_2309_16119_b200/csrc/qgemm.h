@@ -34,6 +34,7 @@ struct GemmArgs {
   int q_grid_bytes;
   int q_group_shift; // log2(group) when group < 128, else -1
   int q_group_div128; // group / 128 when group >= 128
+  uint32_t q_group_magic; // ceil(2^32 / (group/128)) when group/128 > 1, else 0
   unsigned long long* trace;  // dev-only: per-CTA MMA-thread wait cycles (MLRA_TRACE), else null
 };
 

@@ -114,7 +114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int mp = tile % m_pairs, np = tile / m_pairs;
         const int cb = mp * 2 + static_cast<int>(rank);  // this CTA's 128-row block
         for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_backoff<PROD_NS>(&empty[s], ph ^ 1);
           const bool lora = kb >= n_kb_main;
           const bool w_tma = lora || W_TMA;
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * (T_TILE + (w_tma ? W_TILE : 0)));
@@ -211,7 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int mp = tile % m_pairs;
         const int cb = mp * 2 + static_cast<int>(rank);
         for (int pr = 0; pr < n_kb_main / 2; ++pr) {
-          mbar_wait(&qempty[qs], qph ^ 1);
+          mbar_wait_backoff<PROD_NS>(&qempty[qs], qph ^ 1);
           mbar_arrive_expect_tx(&qfull[qs], qbytes);
           uint8_t* dst = sQ + qs * p.q_stage_bytes;
           if (!MN) {
@@ -237,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int local = 0;
     for (int tile = cid; tile < n_tiles; tile += ncl, ++local) {
       const int mp = tile % m_pairs, np = tile / m_pairs;
-      mbar_wait(tfull, local & 1);
+      mbar_wait_backoff<EPI_NS>(tfull, local & 1);
       tc_fence_after();
       const int64_t wrow = static_cast<int64_t>(mp) * PAIR_ROWS + rank * BM + qd * 32 + lane;
       const bool row_ok = wrow < p.m_valid;
@@ -322,7 +322,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int k8 = MN ? (gtid & 15) : (gtid & 7);
       const int row0 = MN ? (gtid >> 4) : (gtid >> 3);
       constexpr int ROW_STEP = MN ? 8 : 16;
-      constexpr int QROW = 16 * BITS;
       const int gshift = p.q_group_shift;
       const int gbox = p.q_grid_bytes / BM;
       const uint32_t sQ32 = smem_u32(sQ), sW32 = smem_u32(sW);
@@ -347,13 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               const int gsub = gshift >= 0 ? (code >> gshift)
                                            : (MN ? gpar_mn : (pair_group(kb >> 1, p) & 1));
               const int rbase = MN ? (row0 + 64 * kp) : row0;
-#pragma unroll
-              for (int i = 0; i < UPT; ++i) {
-                const int row = rbase + i * ROW_STEP;
-                const uint32_t v = q_unit<BITS>(qc + row * QROW, unit);
-                const float2 g = lds_f2(qg + row * gbox + gsub * 8);
-                sts128(st + soff[i], deq8_bf16_fast<BITS>(v, g));
-              }
+dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
               fence_proxy_async_smem();
             }
             __syncwarp();

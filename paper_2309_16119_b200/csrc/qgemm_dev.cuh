@@ -13,10 +13,18 @@ namespace qg {
 constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 64;
+#ifndef MLRA_PROD_NS
+#define MLRA_PROD_NS 128  // backoff of the TMA producers' empty/qempty waits
+#endif
+#ifndef MLRA_EPI_NS
+#define MLRA_EPI_NS 64  // backoff of the epilogue's tfull wait
+#endif
 #ifndef MLRA_STAGES
 #define MLRA_STAGES 4
 #endif
 constexpr int STAGES = MLRA_STAGES;
+constexpr int PROD_NS = MLRA_PROD_NS;
+constexpr int EPI_NS = MLRA_EPI_NS;
 constexpr int MAX_QS = 4;
 constexpr int W_TILE = BM * BK * 2;  // 16 KB
 constexpr int T_TILE = BN * BK * 2;  // 32 KB
@@ -64,8 +72,43 @@ __device__ __forceinline__ uint32_t q_unit(uint32_t row, int j) {
 }
 
 // Group index of the first code of 128-code block `blk` along the code rows.
+// group >= 128: blk / (group/128) via the host's round-up reciprocal (exact for
+// blk < 2^32 / divisor; 0 encodes divisor 1) instead of a runtime-divisor
+// divide on every stage's critical path.
 __device__ __forceinline__ int pair_group(int blk, const GemmArgs& p) {
-  return p.q_group_shift >= 0 ? (blk << (7 - p.q_group_shift)) : blk / p.q_group_div128;
+  if (p.q_group_shift >= 0) return blk << (7 - p.q_group_shift);
+  return p.q_group_magic == 0u ? blk : static_cast<int>(__umulhi(static_cast<uint32_t>(blk),
+                                                                p.q_group_magic));
+}
+
+// One thread's share of a dequant stage: UPT units of 8 codes (rows rbase +
+// i*ROW_STEP of the Q stage) -> bf16 into the SW128 W tile. All code and grid
+// loads issue first; a single warp vote on the per-group certificates then
+// selects the branch-free FADD2/FFMA2 path for all units, so the units overlap
+// instead of serialising behind a per-unit branch.
+template <int BITS, int UPT, int ROW_STEP>
+__device__ __forceinline__ void dequant_units(uint32_t qc, uint32_t qg, uint32_t st,
+                                              const uint32_t (&soff)[UPT], int unit, int gsub,
+                                              int rbase, int gbox) {
+  constexpr int QROW = 16 * BITS;
+  uint32_t v[UPT];
+  float2 g[UPT];
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int row = rbase + i * ROW_STEP;
+    v[i] = q_unit<BITS>(qc + row * QROW, unit);
+    g[i] = lds_f2(qg + row * gbox + gsub * 8);
+  }
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) ok = ok && (g[i].x > 0.0f);
+  if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+    for (int i = 0; i < UPT; ++i) sts128(st + soff[i], deq8_bf16_cert<BITS>(v[i], g[i]));
+  } else {
+#pragma unroll
+    for (int i = 0; i < UPT; ++i) sts128(st + soff[i], deq8_bf16_fast<BITS>(v[i], g[i]));
+  }
 }
 
 struct TileIter {
