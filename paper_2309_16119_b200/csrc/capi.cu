@@ -196,6 +196,8 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
   a.out = gp.out;
   a.ldo = gp.ldo;
   a.bias = gp.bias;
+  a.out_pairs = !gp.out_f32 && gp.ldo % 2 == 0 &&
+                reinterpret_cast<uintptr_t>(gp.out) % 4 == 0 ? 1 : 0;
   // CTA-pair kernel (512 tokens per tile) once there are enough tokens to fill
   // it; MLRA_GEMM=1|2 forces the 1-CTA / pair kernel (tests cover both).
   bool pair = gp.tokens > 256;
@@ -250,8 +252,16 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
   }
   if (const char* tr = getenv("MLRA_TRACE"))  // dev-only: MMA-thread wait cycles per CTA pair
     a.trace = reinterpret_cast<unsigned long long*>(strtoull(tr, nullptr, 0));
-  if (pair)
+  if (pair) {
+    mlra::qgemm2_plan(a);
+    if (a.sk_pairs) {  // stream-K: fp32 partial slots + zeroed publish flags
+      a.sk_ws = sc.get<float>(static_cast<size_t>(a.sk_pairs * mlra::kSkSlotFloats));
+      a.sk_flags = sc.get<unsigned>(static_cast<size_t>(2 * a.sk_pairs));
+      if (!a.sk_ws || !a.sk_flags) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+      CUDA_TRY(cudaMemsetAsync(a.sk_flags, 0, 2 * a.sk_pairs * sizeof(unsigned), sc.st));
+    }
     CUDA_TRY(mlra::qgemm2_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
+  }
   else
     CUDA_TRY(mlra::qgemm_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
   return MLRA_OK;

@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int gsub = gshift >= 0 ? (code >> gshift)
                                            : (MN ? gpar_mn : (pair_group(kb >> 1, p) & 1));
               const int rbase = MN ? (row0 + 64 * kp) : row0;
-dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
+              dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
               fence_proxy_async_smem();
             }
             __syncwarp();

@@ -27,6 +27,7 @@ struct GemmArgs {
   void* out;         // [tokens x ldo], f32 or bf16
   int64_t ldo;
   const float* bias; // [m_valid] or nullptr
+  int out_pairs;     // bf16 out with even ldo and 4-byte aligned base: paired-row stores
   // Q ring (fused path with TMA-fed codes); q_stages == 0 selects the LDG path
   int q_stages;
   int q_stage_bytes;
@@ -36,6 +37,17 @@ struct GemmArgs {
   int q_group_div128; // group / 128 when group >= 128
   uint32_t q_group_magic; // ceil(2^32 / (group/128)) when group/128 > 1, else 0
   unsigned long long* trace;  // dev-only: per-CTA MMA-thread wait cycles (MLRA_TRACE), else null
+  // Stream-K (pair kernel only): 0 = whole tiles strided over the grid; else
+  // the tile x k-block space is cut into sk_pairs contiguous ranges. Split
+  // tiles are finished by their first segment's pair from fp32 partials.
+  // Pair q's range starts at k-block sk_off[q] of tile sk_tile[q] (q = 0..sk_pairs;
+  // entry sk_pairs is the end). Precomputed on the host so the device schedule
+  // needs no division and stays on the uniform datapath.
+  int sk_pairs;
+  float* sk_ws;          // [sk_pairs x 2 CTAs x 512 tokens x 128 rows] fp32 partials
+  unsigned* sk_flags;    // [sk_pairs x 2], zeroed before the launch
+  int sk_tile[129];
+  int sk_off[129];
 };
 
 // true when the fused path can stream codes/grids through the TMA Q ring
@@ -49,5 +61,10 @@ cudaError_t qgemm_launch(const GemmMaps& maps, const QWeightDev& q, const GemmAr
 // Same maps, except the activation boxes are 64 x 128 (each CTA stages half).
 cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                           bool w_tma, bool mn, bool out_f32, cudaStream_t stream);
+// Plans the pair kernel's schedule: sets p.sk_pairs (0 = whole tiles) and the
+// per-pair cut tables. The caller provides sk_ws / sk_flags when sk_pairs > 0.
+void qgemm2_plan(GemmArgs& p);
+constexpr int kMaxSkPairs = 128;
+constexpr int64_t kSkSlotFloats = 2LL * 512 * 128;  // per pair
 
 }  // namespace mlra

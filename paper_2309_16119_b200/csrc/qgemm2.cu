@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -36,11 +37,91 @@ namespace {
 
 using namespace qg;
 
+constexpr double kSkMinIdleBlocks = 50.0;  // stream-K only when it recovers more than this
+constexpr int64_t kSkMinBlocksPerPair = 8;
 constexpr int HB = 128;            // tokens per CTA per accumulator (MMA N=256 split in two)
 constexpr int HB_TILE = HB * BK * 2;  // 16 KB
 constexpr int PAIR_ROWS = 2 * BM;  // 256 weight-side rows per pair tile
 constexpr int PAIR_TOK = 2 * 2 * HB;  // 512 tokens per pair tile
 static_assert(2 * HB_TILE == T_TILE, "stage layout shared with the 1-CTA kernel");
+static_assert(kSkSlotFloats == 2LL * PAIR_TOK * BM, "stream-K slot = both CTAs' accumulators");
+
+// Work schedule shared by every warp role: a sequence of segments (tile,
+// k-blocks [kb0, kb1)) for this pair.
+//  * whole tiles (sk_pairs == 0): tiles cid, cid + ncl, ... each [0, n_kb);
+//  * stream-K: the tile-major space of n_tiles * n_kb k-blocks is cut into
+//    sk_pairs contiguous ranges, so every pair gets the same MMA work however
+//    the tile count divides the SM count. Cuts land on even k-block offsets
+//    inside a tile (a Q-ring stage holds two k-blocks). A segment that starts
+//    at k-block 0 but ends early OWNS its tile: it adds the fp32 partials of
+//    the following pairs' first segments (in pair order — deterministic) and
+//    stores the result. A pair's first segment may start mid-tile: it writes
+//    its accumulators as a partial and publishes a flag. Owners process their
+//    part last in their range, so the partials they need are normally ready.
+struct SegSched {
+  int t, kb, t_end, kb_end, n_kb, n_tiles, stride;
+  bool sk;
+  __device__ void init(const GemmArgs& p, int cid, int ncl, int tiles, int nkb) {
+    n_kb = nkb;
+    n_tiles = tiles;
+    sk = p.sk_pairs != 0;
+    if (sk) {
+      // called by full, converged warps: the REDUX broadcast puts the cuts in
+      // uniform registers, keeping the MMA issuer's loop (and its smem
+      // descriptors) on the uniform datapath instead of an R2UR waterfall
+      t = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_tile[cid])));
+      kb = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_off[cid])));
+      t_end = static_cast<int>(
+          __reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_tile[cid + 1])));
+      kb_end = static_cast<int>(
+          __reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_off[cid + 1])));
+    } else {
+      t = cid;
+      stride = ncl;
+    }
+  }
+  __device__ bool next(int& tile, int& kb0, int& kb1) {
+    if (!sk) {
+      if (t >= n_tiles) return false;
+      tile = t;
+      kb0 = 0;
+      kb1 = n_kb;
+      t += stride;
+      return true;
+    }
+    if (t > t_end || (t == t_end && kb >= kb_end)) return false;
+    tile = t;
+    kb0 = kb;
+    kb1 = t == t_end ? kb_end : n_kb;
+    ++t;
+    kb = 0;
+    return true;
+  }
+  // number of segments next() will yield
+  __device__ int count() const {
+    if (!sk) return t < n_tiles ? (n_tiles - 1 - t) / stride + 1 : 0;
+    if (t > t_end || (t == t_end && kb >= kb_end)) return 0;
+    return t_end - t + (kb_end > 0 ? 1 : 0);
+  }
+  // pairs (cid, q_end) whose ranges start inside `tile` (the owner's contributors)
+  __device__ static int contrib_end(const GemmArgs& p, int cid, int tile) {
+    int q = cid + 1;
+    while (q < p.sk_pairs && p.sk_tile[q] == tile) ++q;
+    return q;
+  }
+};
+
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void epi_bar_sync() {  // the 4 epilogue warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
 
 template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
@@ -75,6 +156,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int m_pairs = static_cast<int>(p.m_total / PAIR_ROWS);
   const int n_pairs = static_cast<int>((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
   const int n_tiles = m_pairs * n_pairs;
+  SegSched sched;
+  sched.init(p, cid, ncl, n_tiles, n_kb);
+  // warp-uniform schedule summary for the MMA issuer (REDUX -> uniform registers)
+  const int mma_nseg =
+      static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(sched.count())));
+  const int mma_kb_first = static_cast<int>(
+      __reduce_min_sync(0xffffffffu, static_cast<unsigned>(sched.sk ? sched.kb : 0)));
+  const int mma_kb_last = static_cast<int>(
+      __reduce_min_sync(0xffffffffu, static_cast<unsigned>(sched.sk ? sched.kb_end : 0)));
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_act);
@@ -110,10 +200,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
+      SegSched sc = sched;
+      int tile, kb0, kb1;
+      while (sc.next(tile, kb0, kb1)) {
         const int mp = tile % m_pairs, np = tile / m_pairs;
         const int cb = mp * 2 + static_cast<int>(rank);  // this CTA's 128-row block
-        for (int kb = 0; kb < n_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait_backoff<PROD_NS>(&empty[s], ph ^ 1);
           const bool lora = kb >= n_kb_main;
           const bool w_tma = lora || W_TMA;
@@ -147,20 +239,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
+    // Segment bounds come from values broadcast in the preamble (mma_nseg,
+    // mma_kb_first, mma_kb_last) and the segment index, so the loop, the stage
+    // counter and the smem descriptors stay on the uniform datapath.
     if (leader && lane == 0) {
       constexpr uint32_t idesc_main = idesc_bf16(2 * BM, 2 * HB, MN ? 1u : 0u, 0u);
       constexpr uint32_t idesc_kmaj = idesc_bf16(2 * BM, 2 * HB, 0u, 0u);
       int s = 0;
       uint32_t ph = 0;
-      int local = 0;
       unsigned long long t_full = 0, t_tempty = 0;
       const unsigned long long t_start = p.trace ? clock64() : 0;
-      for (int tile = cid; tile < n_tiles; tile += ncl, ++local) {
+      for (int sg = 0; sg < mma_nseg; ++sg) {
+        const int kb0 = sg == 0 ? mma_kb_first : 0;
+        const int kb1 = (sg == mma_nseg - 1 && mma_kb_last > 0) ? mma_kb_last : n_kb;
         const unsigned long long tw0 = p.trace ? clock64() : 0;
-        mbar_wait_acq_cluster(tempty, (local & 1) ^ 1);
+        mbar_wait_acq_cluster(tempty, (sg & 1) ^ 1);
         if (p.trace) t_tempty += clock64() - tw0;
         tc_fence_after();
-        for (int kb = 0; kb < n_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           const unsigned long long tf0 = p.trace ? clock64() : 0;
           mbar_wait_acq_cluster(&full[s], ph);
           if (p.trace) t_full += clock64() - tf0;
@@ -183,7 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             for (int a = 0; a < 2; ++a) {
               const uint64_t bdesc = sdesc_sw128(st + a * HB_TILE + k * 32, 16, 1024);
               tc_mma_f16_2sm(tmem_base + a * (2 * HB), adesc, bdesc, idesc,
-                             (kb | k) != 0 ? 1u : 0u);
+                             (kb == kb0 && k == 0) ? 0u : 1u);
             }
           }
           tc_commit_2sm_mc(&empty[s], 0x3);
@@ -198,7 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         p.trace[4 * cid + 0] = clock64() - t_start;
         p.trace[4 * cid + 1] = t_full;
         p.trace[4 * cid + 2] = t_tempty;
-        p.trace[4 * cid + 3] = static_cast<unsigned long long>(local);
+        p.trace[4 * cid + 3] = static_cast<unsigned long long>(mma_nseg);
       }
     }
   } else if (warp == 2) {
@@ -207,10 +303,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t qbytes = p.q_codes_bytes + p.q_grid_bytes;
       int qs = 0;
       uint32_t qph = 0;
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
+      SegSched sc = sched;
+      int tile, kb0, kb1;
+      while (sc.next(tile, kb0, kb1)) {
         const int mp = tile % m_pairs;
         const int cb = mp * 2 + static_cast<int>(rank);
-        for (int pr = 0; pr < n_kb_main / 2; ++pr) {
+        const int pr_end = (kb1 < n_kb_main ? kb1 : n_kb_main) / 2;
+        for (int pr = kb0 / 2; pr < pr_end; ++pr) {
           mbar_wait_backoff<PROD_NS>(&qempty[qs], qph ^ 1);
           mbar_arrive_expect_tx(&qfull[qs], qbytes);
           uint8_t* dst = sQ + qs * p.q_stage_bytes;
@@ -235,30 +334,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int qd = warp & 3;
     const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
     int local = 0;
-    for (int tile = cid; tile < n_tiles; tile += ncl, ++local) {
+    SegSched sc = sched;
+    int tile, kb0, kb1;
+    for (; sc.next(tile, kb0, kb1); ++local) {
       const int mp = tile % m_pairs, np = tile / m_pairs;
+      // stream-K roles: a segment starting mid-tile writes a partial; one that
+      // starts at k-block 0 but ends early adds pairs [cid+1, q_end)'s partials
+      const bool contrib = kb0 != 0;
+      const int q_end = (!contrib && kb1 != n_kb) ? SegSched::contrib_end(p, cid, tile) : cid + 1;
+      const int r_in = qd * 32 + lane;
       mbar_wait_backoff<EPI_NS>(tfull, local & 1);
       tc_fence_after();
-      const int64_t wrow = static_cast<int64_t>(mp) * PAIR_ROWS + rank * BM + qd * 32 + lane;
+      const int64_t wrow = static_cast<int64_t>(mp) * PAIR_ROWS + rank * BM + r_in;
       const bool row_ok = wrow < p.m_valid;
       const float bias = (p.bias != nullptr && row_ok) ? p.bias[wrow] : 0.0f;
-      // 16 chunks of 32 TMEM columns = tokens [np*512 + 32cc, +32) (acc0 then acc1).
-      // TMEM loads are double-buffered so their latency hides under the previous
-      // chunk's stores; TMEM is released right after the last load completes.
+      for (int q = cid + 1; q < q_end; ++q)
+        while (ld_acquire_gpu(&p.sk_flags[2 * q + rank]) == 0) __nanosleep(128);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
       const int64_t tbase = static_cast<int64_t>(np) * PAIR_TOK;
+      // bf16 output, paired rows: lanes 2i / 2i+1 swap half their tokens with one
+      // shfl.xor so each stores a 32-bit word (rows 2i, 2i+1) for one token; the
+      // pointer advances by ldo words. Needs even ldo and a 4-byte aligned output
+      // (p.out_pairs) and every row of the warp valid; otherwise the scalar path.
+      const float bias_nb = __shfl_xor_sync(0xffffffffu, bias, 1);
+      const bool odd = lane & 1;
+      const bool pairs = p.out_pairs && __all_sync(0xffffffffu, (wrow | 1) < p.m_valid);
       auto store_chunk = [&](const uint32_t(&r)[32], int cc) {
-        if (!row_ok) return;
         const int64_t t0 = tbase + cc * 32;
-        if (t0 + 32 <= p.tokens) {
+        if constexpr (!OUT_F32) {
+          if (pairs && t0 + 32 <= p.tokens) {
+            const float b_lo = odd ? bias_nb : bias, b_hi = odd ? bias : bias_nb;
+            uint32_t* o = reinterpret_cast<uint32_t*>(
+                reinterpret_cast<__nv_bfloat16*>(p.out) + (t0 + odd) * p.ldo + (wrow & ~1ll));
+            const int64_t step = p.ldo;  // two tokens = ldo 32-bit words
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float v = __uint_as_float(r[j]) + bias;
-            if constexpr (OUT_F32)
-              reinterpret_cast<float*>(p.out)[(t0 + j) * p.ldo + wrow] = v;
-            else
-              reinterpret_cast<__nv_bfloat16*>(p.out)[(t0 + j) * p.ldo + wrow] =
-                  __float2bfloat16_rn(v);
+            for (int k = 0; k < 16; ++k) {
+              const float ev = __uint_as_float(r[2 * k]), ov = __uint_as_float(r[2 * k + 1]);
+              const float mine = odd ? ov : ev;
+              const float other = __shfl_xor_sync(0xffffffffu, odd ? ev : ov, 1);
+              const float lo = odd ? other : mine, hi = odd ? mine : other;
+              *o = pack_bf16x2(lo + b_lo, hi + b_hi);
+              o += step;
+            }
+            return;
+          }
+        }
+        if (!row_ok) return;
+        if (t0 + 32 <= p.tokens) {
+          if constexpr (OUT_F32) {
+            float* o = reinterpret_cast<float*>(p.out) + t0 * p.ldo + wrow;
+#pragma unroll
+            for (int j = 0; j < 32; ++j, o += p.ldo) *o = __uint_as_float(r[j]) + bias;
+          } else {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + t0 * p.ldo + wrow;
+#pragma unroll
+            for (int j = 0; j < 32; ++j, o += p.ldo)
+              *o = __float2bfloat16_rn(__uint_as_float(r[j]) + bias);
           }
         } else {
 #pragma unroll
@@ -274,23 +405,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           }
         }
       };
-      uint32_t ra[32], rb[32];
-      tmem_ld_32x32b_x32(taddr, ra);
-      tc_wait_ld();
-#pragma unroll 1
-      for (int cc = 0; cc < 16; cc += 2) {
-        tmem_ld_32x32b_x32(taddr + (cc + 1) * 32, rb);
-        store_chunk(ra, cc);
+      // stream-K partial slots of this CTA's rows: [512 tokens][128 rows] fp32
+      auto slot_of = [&](int q, int cc) {
+        return p.sk_ws + (2 * static_cast<int64_t>(q) + rank) * (PAIR_TOK * BM) +
+               static_cast<int64_t>(cc * 32) * BM + r_in;
+      };
+      // Drains the 16 chunks of 32 TMEM columns = tokens [np*512 + 32cc, +32)
+      // (acc0 then acc1). TMEM loads are double-buffered so their latency hides
+      // under the previous chunk's stores; TMEM is released right after the last
+      // load completes.
+      auto drain = [&](auto&& handle) {
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32(taddr, ra);
         tc_wait_ld();
-        if (cc + 2 < 16) {
-          tmem_ld_32x32b_x32(taddr + (cc + 2) * 32, ra);
-        } else {
-          tc_fence_before();  // all TMEM reads of this tile are complete
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_leader);
+#pragma unroll 1
+        for (int cc = 0; cc < 16; cc += 2) {
+          tmem_ld_32x32b_x32(taddr + (cc + 1) * 32, rb);
+          handle(ra, cc);
+          tc_wait_ld();
+          if (cc + 2 < 16) {
+            tmem_ld_32x32b_x32(taddr + (cc + 2) * 32, ra);
+          } else {
+            tc_fence_before();  // all TMEM reads of this tile are complete
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader);
+          }
+          handle(rb, cc + 1);
+          if (cc + 2 < 16) tc_wait_ld();
         }
-        store_chunk(rb, cc + 1);
-        if (cc + 2 < 16) tc_wait_ld();
+      };
+      if (contrib) {
+        drain([&](uint32_t(&r)[32], int cc) {
+          if (!row_ok) return;
+          float* d = slot_of(cid, cc);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) d[j * BM] = __uint_as_float(r[j]);
+        });
+        __threadfence();  // publish this CTA's partial to the tile's owner
+        epi_bar_sync();
+        if (qd == 0 && lane == 0) st_release_gpu(&p.sk_flags[2 * cid + rank], 1u);
+      } else if (q_end > cid + 1) {
+        drain([&](uint32_t(&r)[32], int cc) {
+          if (!row_ok) return;
+          for (int q = cid + 1; q < q_end; ++q) {  // pair order: deterministic sums
+            const float* src = slot_of(q, cc);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              r[j] = __float_as_uint(__uint_as_float(r[j]) + src[j * BM]);
+          }
+          store_chunk(r, cc);
+        });
+      } else {
+        drain([&](uint32_t(&r)[32], int cc) { store_chunk(r, cc); });
       }
     }
   } else if (warp >= DQ_WARP0) {
@@ -301,8 +467,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int s = 0;
     uint32_t ph = 0;
     if constexpr (W_TMA) {
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
-        for (int kb = 0; kb < n_kb; ++kb) {
+      SegSched sc = sched;
+      int tile, kb0, kb1;
+      while (sc.next(tile, kb0, kb1)) {
+        (void)tile;
+        for (int kb = kb0; kb < kb1; ++kb) {
           if ((s & 1) == grp) {
             mbar_wait(&empty[s], ph ^ 1);
             __syncwarp();
@@ -327,11 +496,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t sQ32 = smem_u32(sQ), sW32 = smem_u32(sW);
       int qs = 0;
       uint32_t qph = 0;
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
+      SegSched sc = sched;
+      int tile, kb0, kb1;
+      while (sc.next(tile, kb0, kb1)) {
         const int mp = tile % m_pairs;
         const int cb = mp * 2 + static_cast<int>(rank);
         const int gpar_mn = pair_group(cb, p) & 1;
-        for (int kb = 0; kb < n_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           const bool main = kb < n_kb_main;
           const int kp = kb & 1;
           if ((s & 1) == grp) {
@@ -346,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               const int gsub = gshift >= 0 ? (code >> gshift)
                                            : (MN ? gpar_mn : (pair_group(kb >> 1, p) & 1));
               const int rbase = MN ? (row0 + 64 * kp) : row0;
-dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
+              dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
               fence_proxy_async_smem();
             }
             __syncwarp();
@@ -369,10 +540,12 @@ dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
       }
     } else {
       // generic LDG path (odd group sizes / 8-bit codes)
-      for (int tile = cid; tile < n_tiles; tile += ncl) {
+      SegSched sc = sched;
+      int tile, kb0, kb1;
+      while (sc.next(tile, kb0, kb1)) {
         const int mp = tile % m_pairs;
         const int cb = mp * 2 + static_cast<int>(rank);
-        for (int kb = 0; kb < n_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           if ((s & 1) == grp) {
             mbar_wait(&empty[s], ph ^ 1);
             if (kb < n_kb_main) {
@@ -429,7 +602,7 @@ cudaError_t launch2_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs&
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
-  const int64_t pairs = tiles < sm_total() / 2 ? tiles : sm_total() / 2;
+  const int64_t pairs = p.sk_pairs ? p.sk_pairs : (tiles < sm_total() / 2 ? tiles : sm_total() / 2);
   note_launch();
   kern<<<static_cast<unsigned>(2 * pairs), NUM_THREADS, smem, stream>>>(
       maps.act, maps.act_lora, maps.w, maps.w_lora, maps.codes, maps.grid, q, p);
@@ -446,6 +619,37 @@ cudaError_t launch2_mo(const GemmMaps& maps, const QWeightDev& q, const GemmArgs
 }
 
 }  // namespace
+
+void qgemm2_plan(GemmArgs& p) {
+  p.sk_pairs = 0;
+  const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
+  const int64_t n_kb = p.n_kb_main + p.n_kb_lora;
+  int64_t slots = sm_total() / 2;
+  if (slots > kMaxSkPairs) slots = kMaxSkPairs;
+  int mode = 2;  // MLRA_SK=0: whole tiles; 1: always stream-K; default: when waves quantize
+  if (const char* e = getenv("MLRA_SK")) mode = atoi(e);
+  if (mode == 0 || tiles <= 0) return;
+  // Whole tiles leave n_kb * (waves - tiles/slots) k-blocks of every pair's time
+  // idle in the last wave; stream-K pays a roughly fixed fix-up cost (owners
+  // read their contributors' partials chunk by chunk at the end). Measured
+  // break-even is ~45 k-blocks (m in {512..4096} at LLaMA-7B shapes).
+  const int64_t waves = (tiles + slots - 1) / slots;
+  const double idle_kb = static_cast<double>(n_kb) *
+                         (static_cast<double>(waves) - static_cast<double>(tiles) / slots);
+  if (mode == 2 && idle_kb < kSkMinIdleBlocks) return;
+  // every pair needs a few k-blocks of its own, so cuts never collide
+  const int64_t total = tiles * n_kb;
+  int64_t pairs = slots;
+  if (total / pairs < kSkMinBlocksPerPair) pairs = total / kSkMinBlocksPerPair;
+  if (pairs < 2) return;
+  for (int64_t q = 0; q <= pairs; ++q) {
+    int64_t b = total * q / pairs;
+    if ((b % n_kb) & 1) ++b;  // even offset: a Q-ring stage holds two k-blocks
+    p.sk_tile[q] = static_cast<int>(b / n_kb);
+    p.sk_off[q] = static_cast<int>(b % n_kb);
+  }
+  p.sk_pairs = static_cast<int>(pairs);
+}
 
 cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                           bool w_tma, bool mn, bool out_f32, cudaStream_t stream) {

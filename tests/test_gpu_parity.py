@@ -263,6 +263,7 @@ def test_pair_kernel_matches_single_cta(bits, mn, monkeypatch):
     ctx = M.LpLinearContext(dq, M.MaterializationStrategy.RowMaterialize)
     a = to_bf16_dev(orc.bf16_round(orc.gaussian(5, m, rows if mn else cols)))
     outs = []
+    monkeypatch.setenv("MLRA_SK", "0")  # whole tiles: same K order as the 1-CTA kernel
     for mode in ("1", "2"):
         monkeypatch.setenv("MLRA_GEMM", mode)
         f = M.lp_backward if mn else M.lp_forward
@@ -271,3 +272,58 @@ def test_pair_kernel_matches_single_cta(bits, mn, monkeypatch):
     wbf = deq_bf16_f64(words, rows, cols, bits, 128, sc, z)
     ref = f64(a) @ (wbf if mn else wbf.T)
     assert rel_fro(outs[1], ref) <= 1e-5
+
+
+@pytest.mark.parametrize("rows,cols,m,bits,mn", [
+    (768, 1024, 1100, 3, False),   # 9 tiles x 16 k-blocks over 18 pairs: 2-3 pairs per tile
+    (768, 1024, 1100, 4, True),
+    (4096, 4096, 1024, 3, False),  # 32 tiles over 74 pairs
+    (4096, 4096, 1024, 4, True),
+    (512, 4096, 512, 2, False),    # 2 tiles x 64 k-blocks: one tile cut among ~8 pairs
+])
+def test_stream_k_matches_whole_tiles(rows, cols, m, bits, mn, monkeypatch):
+    """Stream-K (tile x k-block ranges per CTA pair, split tiles finished from
+    fp32 partials) computes the same products as the whole-tile schedule; only
+    the fp32 summation order across the cut differs."""
+    q, words, sc, z = random_quantized(rows, cols, bits, 128, seed=rows + m + bits + 7 * mn)
+    dq = M.DeviceQuantizedMatrix(q)
+    ctx = M.LpLinearContext(dq, M.MaterializationStrategy.RowMaterialize)
+    a = to_bf16_dev(orc.bf16_round(orc.gaussian(9, m, rows if mn else cols)))
+    f = M.lp_backward if mn else M.lp_forward
+    monkeypatch.setenv("MLRA_GEMM", "2")
+    outs = {}
+    for sk in ("0", "1"):
+        monkeypatch.setenv("MLRA_SK", sk)
+        outs[sk] = f64(f(ctx, a, out_dtype=torch.float32))
+    assert rel_fro(outs["1"], outs["0"]) <= 1e-5  # fp32 order across the cut (~sqrt(K) ulp)
+    wbf = deq_bf16_f64(words, rows, cols, bits, 128, sc, z)
+    ref = f64(a) @ (wbf if mn else wbf.T)
+    assert rel_fro(outs["1"], ref) <= 1e-5
+    # repeatable: the owner adds partials in pair order
+    monkeypatch.setenv("MLRA_SK", "1")
+    assert np.array_equal(f64(f(ctx, a, out_dtype=torch.float32)), outs["1"])
+
+
+def test_stream_k_layer_with_lora_and_bias(monkeypatch):
+    """Split tiles whose cut falls next to the LoRA k-block, with bias."""
+    d_out, d_in, r, m, bits = 1024, 1536, 24, 900, 3
+    q, words, sc, z = random_quantized(d_out, d_in, bits, 128, seed=77)
+    dq = M.DeviceQuantizedMatrix(q)
+    a32 = orc.gaussian(78, d_out, r, 0.0, 0.02).astype(np.float32)
+    b32 = orc.gaussian(79, d_in, r, 0.0, 0.02).astype(np.float32)
+    bias = orc.gaussian(80, 1, d_out).astype(np.float32)[0]
+    x = to_bf16_dev(orc.bf16_round(orc.gaussian(81, m, d_in)))
+    g = to_bf16_dev(orc.bf16_round(orc.gaussian(82, m, d_out)))
+    monkeypatch.setenv("MLRA_GEMM", "2")
+    res = {}
+    for sk in ("0", "1"):
+        monkeypatch.setenv("MLRA_SK", sk)
+        ad = M.LoraAdapter(a=torch.from_numpy(a32).cuda(), b=torch.from_numpy(b32).cuda(), rank=r,
+                           alpha=32.0)
+        layer = M.ModuLoraLayer("k", dq, ad, bias=torch.from_numpy(bias).cuda(),
+                                strategy=M.MaterializationStrategy.RowMaterialize)
+        y, xb = M.layer_forward(layer, x, out_dtype=torch.float32)
+        dx = M.layer_backward(layer, x, xb, g, dx_dtype=torch.float32)
+        res[sk] = (f64(y), f64(dx))
+    assert rel_fro(res["1"][0], res["0"][0]) <= 1e-5
+    assert rel_fro(res["1"][1], res["0"][1]) <= 1e-5
