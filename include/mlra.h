@@ -58,14 +58,42 @@ typedef enum mlra_status {
  *                 hook is the same fused kernel */
 typedef enum mlra_strategy { MLRA_WEIGHT = 0, MLRA_ROW = 1, MLRA_MATVEC = 2 } mlra_strategy;
 
-typedef enum mlra_dtype { MLRA_F32 = 0, MLRA_BF16 = 1 } mlra_dtype;
+typedef enum mlra_dtype { MLRA_F32 = 0, MLRA_BF16 = 1, MLRA_F64 = 2 } mlra_dtype;
 
 /* Device-resident frozen QuantizedMatrix (quantize.hpp:29-48). Immutable and
  * shareable across streams once created. */
 typedef struct mlra_qweight mlra_qweight;
 
+/* Device form of the black-box Quantizer plugin (quantize.hpp:91-106).
+ *
+ * The reference's per-plugin override point is the virtual
+ * Quantizer::matvec / matvec_transposed pair (quantize.hpp:98-105), consulted
+ * by lp_forward / lp_backward under QuantizerMatvec (lowprec_linear.cpp:
+ * 174-182, 226-235) through LpLinearContext::matvec_hook
+ * (lowprec_linear.hpp:85-91). A per-token f64 matvec is the wrong shape for a
+ * GPU, so the device hook is the plugin's *dequantize* of one tile of Ŵ: the
+ * library materializes Ŵ through the hook in bounded slabs (rows for the
+ * forward, columns for dX) into a bf16 workspace and runs its TMA-fed tcgen05
+ * GEMM over each slab. The hook sees only (q, tile) — it may decode any packed
+ * format it owns (a non-affine codebook, a scaled copy of the affine codes…).
+ *
+ * materialize(): write Ŵ[row0:row0+nrows, col0:col0+ncols] (dtype, leading
+ * dimension ld, row-major) to device memory `out`, stream-ordered on `stream`
+ * (a cudaStream_t). col0 and ncols are multiples of 8 except at the last
+ * column. Return MLRA_OK or an error status (the message via the hook's own
+ * mlra_last_error-style channel is the plugin's business). */
+typedef struct mlra_hook {
+  const char* name; /* Quantizer::name() (quantize.hpp:94) */
+  void* state;
+  mlra_status (*materialize)(void* state, const mlra_qweight* q, int64_t row0, int64_t nrows,
+                             int64_t col0, int64_t ncols, void* out, mlra_dtype dtype,
+                             int64_t ld, void* stream);
+} mlra_hook;
+
 /* One ModuLoraLayer (lora.hpp:40-51) as seen by the kernels. scaling() = alpha/rank
- * (lora.hpp:30). bias may be NULL (zero bias). */
+ * (lora.hpp:30). bias may be NULL (zero bias). hook: the layer's optional
+ * Quantizer plugin (ModuLoraLayer::matvec_hook, lora.hpp:47; consulted only
+ * under MLRA_MATVEC, like lowprec_linear.cpp:174-182), NULL for none. */
 typedef struct mlra_lora {
   const mlra_qweight* q;
   mlra_strategy strategy;
@@ -74,6 +102,7 @@ typedef struct mlra_lora {
   const float* a;    /* device, [d_out x rank] */
   const float* b;    /* device, [d_in x rank]  */
   const float* bias; /* device, [d_out] or NULL */
+  const mlra_hook* hook; /* optional matvec hook (ABI >= 2) */
 } mlra_lora;
 
 /* Last error message of this thread ("" if none). */
@@ -103,6 +132,28 @@ MLRA_API mlra_status mlra_qweight_info(const mlra_qweight* q, int64_t* rows, int
                               int64_t* group_size, uint64_t* device_bytes,
                               int64_t* uncertified_groups);
 
+/* A quantized matrix whose packed format only its plugin understands (a
+ * non-affine codebook): rows x cols with nominal `bits` per
+ * entry, every dequantization (all strategies, mlra_materialize*) goes through
+ * hook->materialize. The hook struct is copied; hook->state must outlive q. */
+MLRA_API mlra_status mlra_qweight_create_opaque(int64_t rows, int64_t cols, int bits,
+                                                const mlra_hook* hook, mlra_qweight** out);
+
+/* Built-in non-affine plugin "cb2": a QuIP#-style 2-bit vector codebook.
+ * Every 8 consecutive entries of a row share one u16 code: bits 0-7 index a
+ * 256 x 8 f32 codebook of magnitudes, bit 8+j negates entry j. Per-(row,
+ * group) f32 scale s (group along cols, a multiple of 8 dividing cols):
+ *   Ŵ[i, 8u+j] = RN_f32(s[i, (8u+j)/g] · (±cb[idx][j]))
+ * codes: host u16 [rows x cols/8]; codebook: host f32 [256 x 8]; scales: host
+ * f32 [rows x cols/group] (> 0). Uploads everything and returns an opaque
+ * qweight whose hook is the library's cb2 materialize kernel. */
+MLRA_API mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group_size,
+                                     const uint16_t* codes, const float* codebook,
+                                     const float* scales, void* stream, mlra_qweight** out);
+
+/* The hook an opaque qweight carries (NULL for the affine built-in format). */
+MLRA_API const mlra_hook* mlra_qweight_hook(const mlra_qweight* q);
+
 /* dequantize_into (quantize.cpp:123-137): out[rows x cols] (leading dim ld) =
  * RN(double(s)·c + double(z)) as f32, or bf16 = RN(that f32). Bit-exact with
  * (float)modulora::dequantize(q). */
@@ -112,6 +163,13 @@ MLRA_API mlra_status mlra_materialize(const mlra_qweight* q, void* out, mlra_dty
  * RangeError when the range runs past q.rows. */
 MLRA_API mlra_status mlra_materialize_rows(const mlra_qweight* q, int64_t row0, int64_t nrows, void* out,
                                   mlra_dtype dtype, int64_t ld, void* stream);
+
+/* One tile Ŵ[row0:row0+nrows, col0:col0+ncols] (col0 a multiple of 8) —
+ * the device hook's unit of work. Affine qweights decode it with the K1
+ * kernel (bit-exact like mlra_materialize); opaque ones call their hook. */
+MLRA_API mlra_status mlra_materialize_tile(const mlra_qweight* q, int64_t row0, int64_t nrows,
+                                           int64_t col0, int64_t ncols, void* out,
+                                           mlra_dtype dtype, int64_t ld, void* stream);
 
 /* Bytes a strategy materializes in HBM per pass — what MemoryLedger::on_alloc
  * would be charged (lowprec_linear.cpp:17-37; bf16 = 2 B/entry on the GPU,
@@ -128,6 +186,19 @@ MLRA_API mlra_status mlra_lp_backward(const mlra_qweight* q, mlra_strategy strat
                              int64_t ldg, int64_t m, void* dx, mlra_dtype dx_dtype,
                              int64_t lddx, void* stream);
 
+/* lp_forward / lp_backward with LpLinearContext::matvec_hook
+ * (lowprec_linear.hpp:85-91): under MLRA_MATVEC a non-NULL hook replaces the
+ * built-in dequantization (slab materialization through the hook + GEMM);
+ * the other strategies ignore it, as the reference's do. */
+MLRA_API mlra_status mlra_lp_forward_ex(const mlra_qweight* q, mlra_strategy strategy,
+                                        const mlra_hook* hook, const void* x, int64_t ldx,
+                                        int64_t m, void* y, mlra_dtype y_dtype, int64_t ldy,
+                                        void* stream);
+MLRA_API mlra_status mlra_lp_backward_ex(const mlra_qweight* q, mlra_strategy strategy,
+                                         const mlra_hook* hook, const void* g, int64_t ldg,
+                                         int64_t m, void* dx, mlra_dtype dx_dtype, int64_t lddx,
+                                         void* stream);
+
 /* layer_forward (lora.cpp:52-72): y = x·Ŵᵀ + (alpha/r)·(x·B)·Aᵀ + bias.
  * xb: device f32 [m x rank], receives x·B (saved for the backward pass). */
 MLRA_API mlra_status mlra_lora_forward(const mlra_lora* layer, const void* x, int64_t ldx, int64_t m,
@@ -142,6 +213,32 @@ MLRA_API mlra_status mlra_lora_backward(const mlra_lora* layer, const void* x, i
                                const float* xb, const void* dy, int64_t lddy, int64_t m,
                                void* dx, mlra_dtype dx_dtype, int64_t lddx, float* da,
                                float* db, float* dbias, void* stream);
+
+/* AdamW with decoupled weight decay (train.hpp:51-70, AdamW::AdamW). */
+typedef struct mlra_adamw {
+  double beta1, beta2, eps, weight_decay;
+} mlra_adamw;
+
+/* AdamW::step (train.cpp:81-134) over n_params parameters stored back to back
+ * in one flat device bucket: parameter i is elements [offsets[i], offsets[i+1])
+ * (offsets: HOST array of n_params + 1, offsets[0] = 0, n_params <= 1024). params, m, v: device
+ * f64 (masters and moments; m, v zero before the first step — "allocated on
+ * first use"); grad: device, dtype MLRA_F32 (the layer kernels' gradients) or
+ * MLRA_F64; params_f32: optional device f32 working copy written with the new
+ * values (the factors the GEMMs read). step_index is the reference's
+ * zero-based step (t = step_index + 1). Bit-identical to the reference f64
+ * arithmetic given the same gradients.
+ * Non-finite gradients (train.cpp:113-117): parameters before the first one
+ * holding a non-finite gradient are updated, it and the rest are not. With
+ * first_bad == NULL the call synchronizes on `stream` and returns
+ * MLRA_ERR_NUMERIC naming that parameter; otherwise it stays asynchronous and
+ * writes the index (a value >= n_params when all are finite) to the device int
+ * *first_bad. Capturable in a CUDA graph in that form (no host copies). */
+MLRA_API mlra_status mlra_adamw_step(const mlra_adamw* opt, int64_t step_index, double lr,
+                                     int64_t n_params, const int64_t* offsets, double* params,
+                                     double* m, double* v, const void* grad,
+                                     mlra_dtype grad_dtype, float* params_f32, int* first_bad,
+                                     void* stream);
 
 #ifdef __cplusplus
 }

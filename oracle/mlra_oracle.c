@@ -276,6 +276,32 @@ ORC_EXPORT void orc_dequantize_f32(const uint32_t* words, uint64_t rows,
   }
 }
 
+/* The built-in non-affine plugin "cb2" (include/mlra.h mlra_cb2_create) —
+ * the device form of the black-box Quantizer hook (quantize.hpp:91-106). The
+ * reference hosts such plugins but ships none, so this
+ * decode law is pinned by the known-answer test in tests/test_cb2.py
+ * (hand-computed values) rather than by reference output. One u16 code per 8
+ * consecutive row entries: bits 0-7 index codebook[256][8], bit 8+j negates
+ * entry j; per-(row, group) f32 scale:
+ *   out[i, 8u+j] = RN_f32(s[i, (8u+j)/g] * (+-cb[idx][j]))   (one IEEE multiply) */
+ORC_EXPORT void orc_cb2_dequant_f32(const uint16_t* codes, uint64_t rows, uint64_t cols,
+                                    uint64_t group, const float* codebook,
+                                    const float* scales, float* out) {
+  const uint64_t ng = cols / group, cpr = cols / 8;
+  for (uint64_t i = 0; i < rows; ++i) {
+    for (uint64_t u = 0; u < cpr; ++u) {
+      const uint16_t code = codes[i * cpr + u];
+      const float* e = codebook + (uint64_t)(code & 0xFFu) * 8;
+      for (uint64_t j = 0; j < 8; ++j) {
+        const float s = scales[i * ng + (8 * u + j) / group];
+        float m = e[j];
+        if ((code >> (8 + j)) & 1u) m = -m;
+        out[i * cols + 8 * u + j] = s * m;
+      }
+    }
+  }
+}
+
 ORC_EXPORT uint16_t orc_f32_to_bf16(float f) {
   uint32_t u;
   memcpy(&u, &f, 4);
@@ -430,4 +456,29 @@ ORC_EXPORT void orc_layer_backward_dense(const double* w, uint64_t d_out,
   free(xbt);
   free(dat);
   free(xt);
+}
+
+/* ------------------------------------------------------------------------ */
+/* AdamW::step — train.cpp:81-134 (one parameter; the caller loops over the  */
+/* parameter list in order and stops at the first non-finite gradient, which */
+/* the reference reports with NumericError, train.cpp:113-117).              */
+/* ------------------------------------------------------------------------ */
+/* Returns 0, or 6 (NumericError) without touching p/m/v when g holds a
+ * non-finite value. */
+ORC_EXPORT int orc_adamw_step(double beta1, double beta2, double eps, double weight_decay,
+                              uint64_t step_index, double lr, uint64_t n, double* p,
+                              double* m, double* v, const double* g) {
+  for (uint64_t j = 0; j < n; ++j)
+    if (!isfinite(g[j])) return 6;                           /* :113-117 */
+  const double t = (double)step_index + 1.0;                 /* :99 */
+  const double bc1 = 1.0 - pow(beta1, t);                    /* :100 */
+  const double bc2 = 1.0 - pow(beta2, t);                    /* :101 */
+  for (uint64_t j = 0; j < n; ++j) {                         /* :122-129 */
+    m[j] = beta1 * m[j] + (1.0 - beta1) * g[j];
+    v[j] = beta2 * v[j] + (1.0 - beta2) * g[j] * g[j];
+    const double mhat = m[j] / bc1;
+    const double vhat = v[j] / bc2;
+    p[j] = p[j] * (1.0 - lr * weight_decay) - lr * mhat / (sqrt(vhat) + eps);
+  }
+  return 0;
 }

@@ -73,6 +73,12 @@ class _Lib:
             lib.orc_layer_backward_dense.argtypes = [
                 _f64p, _u64, _u64, _f64p, _f64p, _u64, C.c_double, _f64p, _f64p, _f64p,
                 _u64, vp, _f64p, _f64p, vp]
+            lib.orc_cb2_dequant_f32.argtypes = [
+                np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS"), _u64, _u64, _u64, _f32p,
+                _f32p, _f32p]
+            lib.orc_adamw_step.restype = _int
+            lib.orc_adamw_step.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, _u64,
+                                           C.c_double, _u64, _f64p, _f64p, _f64p, _f64p]
             cls._lib = lib
         return cls._lib
 
@@ -271,8 +277,23 @@ class Ref:
             lib.ref_bench_layer.argtypes = [
                 _u32p, _u64, _u64, _int, _u64, _f32p, _f32p, _int, _u64, C.c_double, _u64,
                 _int, _u64, C.POINTER(C.c_double)]
+            lib.ref_adamw_run.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, _u64,
+                                          np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS"),
+                                          _f64p, _f64p, _u64, _f64p, C.POINTER(_u64)]
+            lib.ref_adamw_run.restype = _int
             cls._lib = lib
         return cls._lib
+
+    @classmethod
+    def adamw_run(cls, sizes, values, grads, lrs, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0):
+        """The reference AdamW over len(lrs) steps; returns (rc, values, bad_step)."""
+        vals = np.ascontiguousarray(values, np.float64).copy()
+        bad = _u64(0)
+        rc = cls.get().ref_adamw_run(beta1, beta2, eps, wd, len(sizes),
+                                     np.asarray(sizes, np.uint64), vals,
+                                     np.ascontiguousarray(grads, np.float64).ravel(), len(lrs),
+                                     np.ascontiguousarray(lrs, np.float64), C.byref(bad))
+        return rc, vals, int(bad.value)
 
     @classmethod
     def _chk(cls, st):
@@ -346,3 +367,28 @@ class Ref:
             _c(zeros, np.float32), strategy, rank, float(alpha), m_per_thread, threads, seed,
             C.byref(secs)))
         return secs.value
+
+
+# --- cb2 plugin decode law (include/mlra.h mlra_cb2_create) ------------------
+def cb2_dequantize_f32(codes, rows: int, cols: int, group: int, codebook, scales) -> np.ndarray:
+    """orc_cb2_dequant_f32: the f32 image of the cb2 codebook plugin."""
+    out = np.empty(rows * cols, np.float32)
+    _Lib.get().orc_cb2_dequant_f32(_c(codes, np.uint16).ravel(), rows, cols, group,
+                                   _c(codebook, np.float32).ravel(),
+                                   _c(scales, np.float32).ravel(), out)
+    return out.reshape(rows, cols)
+
+
+# --- train.cpp AdamW ------------------------------------------------------------
+def adamw_step(params, ms, vs, grads, step_index: int, lr: float, beta1=0.9, beta2=0.999,
+               eps=1e-8, weight_decay=0.0) -> int:
+    """AdamW::step (train.cpp:81-134) over a list of f64 arrays, updated in
+    place in order. Returns the index of the first parameter whose gradient is
+    non-finite (it and the rest untouched), or len(params)."""
+    for i, (p, m, v, g) in enumerate(zip(params, ms, vs, grads)):
+        rc = _Lib.get().orc_adamw_step(beta1, beta2, eps, weight_decay, step_index, lr, p.size,
+                                       p.reshape(-1), m.reshape(-1), v.reshape(-1),
+                                       _c(g, np.float64).reshape(-1))
+        if rc:
+            return i
+    return len(params)

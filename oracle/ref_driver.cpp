@@ -24,6 +24,7 @@
 #include "modulora/lowprec_linear.hpp"
 #include "modulora/quantize.hpp"
 #include "modulora/rng.hpp"
+#include "modulora/train.hpp"
 
 using namespace modulora;
 
@@ -329,6 +330,52 @@ int ref_bench_layer(const uint32_t* words, uint64_t rows, uint64_t cols,
   } catch (...) {
     return map_exc();
   }
+}
+
+// AdamW::step (train.cpp:81-134) driven for `steps` steps over n_params
+// parameters (sizes[i] entries each, values concatenated, updated in place);
+// grads: steps x total f64, lrs: steps. On NumericError returns 6 with the
+// failing step in *bad_step (values hold the partial update of that step).
+int ref_adamw_run(double beta1, double beta2, double eps, double wd, uint64_t n_params,
+                  const uint64_t* sizes, double* values, const double* grads, uint64_t steps,
+                  const double* lrs, uint64_t* bad_step) {
+  uint64_t total = 0;
+  for (uint64_t i = 0; i < n_params; ++i) total += sizes[i];
+  AdamW opt(beta1, beta2, eps, wd);
+  std::vector<std::string> names;
+  for (uint64_t i = 0; i < n_params; ++i) names.push_back("p" + std::to_string(i));
+  std::vector<Variable> params;
+  uint64_t off = 0;
+  for (uint64_t i = 0; i < n_params; ++i) {
+    params.push_back(Variable::leaf(
+        DenseMatrix(1, sizes[i], std::vector<double>(values + off, values + off + sizes[i])),
+        true));
+    off += sizes[i];
+  }
+  for (uint64_t s = 0; s < steps; ++s) {
+    off = 0;
+    for (uint64_t i = 0; i < n_params; ++i) {
+      params[i].zero_grad();
+      const double* g = grads + s * total + off;
+      accumulate_grad(params[i], DenseMatrix(1, sizes[i], std::vector<double>(g, g + sizes[i])));
+      off += sizes[i];
+    }
+    int rc = 0;
+    try {
+      opt.step(params, names, s, lrs[s]);
+    } catch (...) {
+      rc = map_exc();
+      *bad_step = s;
+    }
+    off = 0;
+    for (uint64_t i = 0; i < n_params; ++i) {
+      const auto d = params[i].value().data();
+      std::memcpy(values + off, d.data(), sizes[i] * sizeof(double));
+      off += sizes[i];
+    }
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 }  // extern "C"

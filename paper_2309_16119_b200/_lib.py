@@ -15,15 +15,25 @@ STATUS_NAMES = {
     6: "NumericError", 7: "FormatError", 8: "CudaError", 9: "UnsupportedDevice",
 }
 WEIGHT, ROW, MATVEC = 0, 1, 2
-F32, BF16 = 0, 1
+F32, BF16, F64 = 0, 1, 2
 
 # Every symbol include/mlra.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = [
     "mlra_last_error", "mlra_abi_version", "mlra_kernel_launches", "mlra_device_check", "mlra_packed_word_count",
     "mlra_qweight_create", "mlra_qweight_destroy", "mlra_qweight_info", "mlra_materialize",
     "mlra_materialize_rows", "mlra_ledger_bytes", "mlra_lp_forward", "mlra_lp_backward",
-    "mlra_lora_forward", "mlra_lora_backward",
+    "mlra_lora_forward", "mlra_lora_backward", "mlra_qweight_create_opaque", "mlra_cb2_create",
+    "mlra_qweight_hook", "mlra_materialize_tile", "mlra_lp_forward_ex", "mlra_lp_backward_ex",
+    "mlra_adamw_step",
 ]
+
+# mlra_hook.materialize(state, q, row0, nrows, col0, ncols, out, dtype, ld, stream)
+HOOK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                      C.c_int64, C.c_void_p, C.c_int, C.c_int64, C.c_void_p)
+
+
+class MlraHook(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("state", C.c_void_p), ("materialize", HOOK_FN)]
 
 
 class MlraError(RuntimeError):
@@ -35,10 +45,16 @@ class MlraError(RuntimeError):
         super().__init__(f"{self.kind}: {msg}")
 
 
+class MlraAdamw(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double)]
+
+
 class MlraLora(C.Structure):
     _fields_ = [
         ("q", C.c_void_p), ("strategy", C.c_int), ("rank", C.c_int64), ("alpha", C.c_double),
         ("a", C.c_void_p), ("b", C.c_void_p), ("bias", C.c_void_p),
+        ("hook", C.POINTER(MlraHook)),
     ]
 
 
@@ -87,6 +103,24 @@ def lib() -> C.CDLL:
         L.mlra_lora_backward.restype = i32
         L.mlra_lora_backward.argtypes = [C.POINTER(MlraLora), vp, i64, vp, vp, i64, i64, vp, i32,
                                          i64, vp, vp, vp, vp]
+        L.mlra_qweight_create_opaque.restype = i32
+        L.mlra_qweight_create_opaque.argtypes = [i64, i64, i32, C.POINTER(MlraHook),
+                                                 C.POINTER(vp)]
+        L.mlra_cb2_create.restype = i32
+        L.mlra_cb2_create.argtypes = [i64, i64, i64, vp, vp, vp, vp, C.POINTER(vp)]
+        L.mlra_qweight_hook.restype = vp
+        L.mlra_qweight_hook.argtypes = [vp]
+        L.mlra_materialize_tile.restype = i32
+        L.mlra_materialize_tile.argtypes = [vp, i64, i64, i64, i64, vp, i32, i64, vp]
+        L.mlra_lp_forward_ex.restype = i32
+        L.mlra_lp_forward_ex.argtypes = [vp, i32, C.POINTER(MlraHook), vp, i64, i64, vp, i32,
+                                         i64, vp]
+        L.mlra_lp_backward_ex.restype = i32
+        L.mlra_lp_backward_ex.argtypes = [vp, i32, C.POINTER(MlraHook), vp, i64, i64, vp, i32,
+                                          i64, vp]
+        L.mlra_adamw_step.restype = i32
+        L.mlra_adamw_step.argtypes = [C.POINTER(MlraAdamw), i64, C.c_double, i64,
+                                      C.POINTER(i64), vp, vp, vp, vp, i32, vp, vp, vp]
         _lib = L
     return _lib
 

@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -33,6 +34,13 @@ struct mlra_qweight {
   float2* grid = nullptr;
   uint64_t device_bytes = 0;
   int64_t uncertified = 0;
+  // opaque (plugin-owned) formats: every dequantization goes through `hook`
+  bool opaque = false;
+  mlra_hook hook{};
+  std::string hook_name;
+  // built-in cb2 plugin state (owned when the qweight came from mlra_cb2_create)
+  mlra::Cb2Dev cb2{};
+  void* cb2_mem = nullptr;
 };
 
 namespace {
@@ -178,9 +186,11 @@ struct GemmPlan {
   const float* bias = nullptr;
 };
 
-mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPlan& gp,
-                     Scratch& sc) {
-  const QWeightDev& d = q->d;
+// One GEMM over the quantized operand described by d. w_mat != nullptr: Ŵ is
+// already materialized (bf16 [d.rows x w_ld]) and streamed by TMA; otherwise
+// the fused kernel dequantizes d's packed codes tile by tile.
+mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t w_ld,
+                       const GemmPlan& gp, Scratch& sc) {
   mlra::GemmMaps maps;
   std::memset(&maps, 0, sizeof(maps));
   mlra::GemmArgs a{};
@@ -212,13 +222,9 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
     maps.act_lora = maps.act;
     maps.w_lora = maps.act;
   }
-  const bool w_tma = strategy == MLRA_WEIGHT;
+  const bool w_tma = w_mat != nullptr;
   if (w_tma) {
-    // WeightMaterialize: the whole Ŵ in HBM for this pass (bf16), freed on return
-    auto* w = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows * d.cols_pad));
-    if (!w) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-    CUDA_TRY(mlra::launch_materialize(d, 0, d.rows, w, d.cols_pad, false, sc.st));
-    if ((st = make_map(&maps.w, w, d.cols, d.rows, d.cols_pad, 64, gp.mn ? 64 : 128))) return st;
+    if ((st = make_map(&maps.w, w_mat, d.cols, d.rows, w_ld, 64, gp.mn ? 64 : 128))) return st;
   } else {
     maps.w = maps.act;
   }
@@ -265,6 +271,102 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const GemmPl
   else
     CUDA_TRY(mlra::qgemm_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
   return MLRA_OK;
+}
+
+// Workspace budget of one hook slab (bytes of bf16 Ŵ); MLRA_SLAB_MB overrides.
+int64_t slab_budget() {
+  int64_t mb = 256;
+  if (const char* e = getenv("MLRA_SLAB_MB")) mb = atoll(e) > 0 ? atoll(e) : mb;
+  return mb << 20;
+}
+
+// Slab extent along one side of Ŵ: a multiple of 256 (one pair tile), at least
+// 256, covering `full` when `whole` (WeightMaterialize) or the budget allows.
+int64_t slab_extent(int64_t full_pad, int64_t other_pad, bool whole) {
+  if (whole) return full_pad;
+  int64_t e = slab_budget() / (2 * other_pad) / 256 * 256;
+  if (e < 256) e = 256;
+  return e < full_pad ? e : full_pad;
+}
+
+// One bf16 tile through a plugin hook; a failing hook's status is returned
+// with its name prepended to whatever message it left.
+mlra_status call_hook(const mlra_hook* hk, const mlra_qweight* q, int64_t row0, int64_t nrows,
+                      int64_t col0, int64_t ncols, void* out, int64_t ld, cudaStream_t st) {
+  g_last_error.clear();
+  const mlra_status rc = hk->materialize(hk->state, q, row0, nrows, col0, ncols, out, MLRA_BF16,
+                                         ld, st);
+  if (rc == MLRA_OK) return MLRA_OK;
+  const std::string prev = g_last_error;
+  return fail(rc, "quantizer hook '%s' failed (status %d)%s%s", hk->name ? hk->name : "?",
+              static_cast<int>(rc), prev.empty() ? "" : ": ", prev.c_str());
+}
+
+// The hook path (the device Quantizer::matvec, lowprec_linear.cpp:174-182 /
+// 226-235): Ŵ materialized through hk in slabs — rows for the forward (each
+// slab's GEMM writes its own output columns), columns for dX (each slab's GEMM
+// writes its own dX columns) — so no slab needs a cross-slab reduction.
+mlra_status run_gemm_hooked(const mlra_qweight* q, const mlra_hook* hk, bool whole,
+                            const GemmPlan& gp, Scratch& sc) {
+  const QWeightDev& d = q->d;
+  if (!hk->materialize) return fail(MLRA_ERR_CONTRACT, "quantizer hook without materialize()");
+  const int64_t esize = gp.out_f32 ? 4 : 2;
+  if (!gp.mn) {
+    const int64_t slab = slab_extent(d.rows_pad, d.cols_pad, whole);
+    auto* ws = sc.get<__nv_bfloat16>(static_cast<size_t>(slab * d.cols_pad));
+    if (!ws) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+    for (int64_t r0 = 0; r0 < d.rows; r0 += slab) {
+      const int64_t nr = d.rows - r0 < slab ? d.rows - r0 : slab;
+      if (mlra_status st = call_hook(hk, q, r0, nr, 0, d.cols, ws, d.cols_pad, sc.st)) return st;
+      QWeightDev v = d;
+      v.rows = nr;
+      v.rows_pad = round_up(nr, 256);
+      GemmPlan g2 = gp;
+      g2.out = static_cast<char*>(gp.out) + r0 * esize;
+      if (gp.bias) g2.bias = gp.bias + r0;
+      if (gp.w_lora) g2.w_lora = gp.w_lora + r0 * gp.rp;
+      if (mlra_status st = run_gemm_d(v, ws, d.cols_pad, g2, sc)) return st;
+    }
+  } else {
+    const int64_t slab = slab_extent(d.cols_pad, d.rows_pad, whole);
+    auto* ws = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows * slab));
+    if (!ws) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+    for (int64_t c0 = 0; c0 < d.cols; c0 += slab) {
+      const int64_t nc = d.cols - c0 < slab ? d.cols - c0 : slab;
+      if (mlra_status st = call_hook(hk, q, 0, d.rows, c0, nc, ws, slab, sc.st)) return st;
+      QWeightDev v = d;
+      v.cols = nc;
+      v.cols_pad = round_up(nc, 256);
+      GemmPlan g2 = gp;
+      g2.out = static_cast<char*>(gp.out) + c0 * esize;
+      if (gp.w_lora) g2.w_lora = gp.w_lora + c0 * gp.rp;
+      if (mlra_status st = run_gemm_d(v, ws, slab, g2, sc)) return st;
+    }
+  }
+  return MLRA_OK;
+}
+
+// Strategy dispatch (lowprec_linear.cpp:158-187): the hook is consulted under
+// QuantizerMatvec only; an opaque qweight has nothing but its own hook.
+const mlra_hook* pick_hook(const mlra_qweight* q, mlra_strategy strategy,
+                           const mlra_hook* ctx_hook) {
+  if (strategy == MLRA_MATVEC && ctx_hook) return ctx_hook;
+  return q->opaque ? &q->hook : nullptr;
+}
+
+mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const mlra_hook* ctx_hook,
+                     const GemmPlan& gp, Scratch& sc) {
+  if (const mlra_hook* hk = pick_hook(q, strategy, ctx_hook))
+    return run_gemm_hooked(q, hk, strategy == MLRA_WEIGHT, gp, sc);
+  const QWeightDev& d = q->d;
+  if (strategy == MLRA_WEIGHT) {
+    // WeightMaterialize: the whole Ŵ in HBM for this pass (bf16), freed on return
+    auto* w = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows * d.cols_pad));
+    if (!w) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+    CUDA_TRY(mlra::launch_materialize(d, 0, d.rows, w, d.cols_pad, false, sc.st));
+    return run_gemm_d(d, w, d.cols_pad, gp, sc);
+  }
+  return run_gemm_d(d, nullptr, 0, gp, sc);
 }
 
 mlra_status check_lora(const mlra_lora* L) {
@@ -355,7 +457,7 @@ mlra_status side_stream(SideStream** out) {
 extern "C" {
 
 const char* mlra_last_error(void) { return g_last_error.c_str(); }
-int mlra_abi_version(void) { return 1; }
+int mlra_abi_version(void) { return 2; }
 uint64_t mlra_kernel_launches(void) { return mlra::g_launches.load(); }
 mlra_status mlra_device_check(void) { return check_device(); }
 
@@ -470,9 +572,96 @@ mlra_status mlra_qweight_create(int64_t rows, int64_t cols, int bits, int64_t gr
 
 void mlra_qweight_destroy(mlra_qweight* q) {
   if (!q) return;
-  cudaFree(q->words);
-  cudaFree(q->grid);
+  if (q->words) cudaFree(q->words);
+  if (q->grid) cudaFree(q->grid);
+  if (q->cb2_mem) cudaFree(q->cb2_mem);
   delete q;
+}
+
+mlra_status mlra_qweight_create_opaque(int64_t rows, int64_t cols, int bits,
+                                       const mlra_hook* hook, mlra_qweight** out) {
+  if (!out) return fail(MLRA_ERR_CONTRACT, "null output handle");
+  *out = nullptr;
+  if (!hook || !hook->materialize)
+    return fail(MLRA_ERR_CONTRACT, "opaque qweight: hook with materialize() required");
+  if (rows <= 0 || cols <= 0)
+    return fail(MLRA_ERR_CONFIG, "QuantizedMatrix: empty shape %lld x %lld", (long long)rows,
+                (long long)cols);
+  if (bits < 1 || bits > 16) return fail(MLRA_ERR_CONFIG, "unsupported bit width %d", bits);
+  auto* q = new mlra_qweight();
+  q->opaque = true;
+  q->hook = *hook;
+  q->hook_name = hook->name ? hook->name : "";
+  q->hook.name = q->hook_name.c_str();
+  QWeightDev& d = q->d;
+  d.rows = rows;
+  d.cols = cols;
+  d.rows_pad = round_up(rows, 256);
+  d.cols_pad = round_up(cols, 256);
+  d.bits = bits;
+  d.group = cols;
+  *out = q;
+  return MLRA_OK;
+}
+
+mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group, const uint16_t* codes,
+                            const float* codebook, const float* scales, void* stream,
+                            mlra_qweight** out) {
+  if (!out) return fail(MLRA_ERR_CONTRACT, "null output handle");
+  *out = nullptr;
+  if (rows <= 0 || cols <= 0 || cols % 8 != 0)
+    return fail(MLRA_ERR_CONFIG, "cb2: cols %lld must be a positive multiple of 8",
+                (long long)cols);
+  if (group <= 0 || group % 8 != 0 || cols % group != 0)
+    return fail(MLRA_ERR_CONFIG, "cb2: group size %lld must be a multiple of 8 dividing cols %lld",
+                (long long)group, (long long)cols);
+  if (!codes || !codebook || !scales) return fail(MLRA_ERR_CONTRACT, "cb2: null buffers");
+  const int64_t ng = rows * (cols / group);
+  for (int64_t i = 0; i < ng; ++i)
+    if (!(scales[i] > 0.0f)) return fail(MLRA_ERR_NUMERIC, "cb2: non-positive scale");
+  for (int i = 0; i < 256 * 8; ++i)
+    if (!(codebook[i] >= 0.0f) || codebook[i] > 3.4e38f)
+      return fail(MLRA_ERR_NUMERIC, "cb2: codebook magnitudes must be finite and >= 0");
+  if (mlra_status st = check_device()) return st;
+  static const mlra_hook kCb2Hook = {
+      "cb2", nullptr,
+      [](void*, const mlra_qweight* q, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols,
+         void* o, mlra_dtype dtype, int64_t ld, void* st) -> mlra_status {
+        if (col0 % 8 != 0 || ncols % 8 != 0)
+          return fail(MLRA_ERR_RANGE, "cb2: tile columns must be 8-aligned");
+        CUDA_TRY(mlra::launch_cb2_materialize(q->cb2, row0, nrows, col0, ncols, o, ld,
+                                              dtype == MLRA_F32, static_cast<cudaStream_t>(st)));
+        return MLRA_OK;
+      }};
+  mlra_qweight* q = nullptr;
+  if (mlra_status st = mlra_qweight_create_opaque(rows, cols, 2, &kCb2Hook, &q)) return st;
+  const size_t cb_bytes = 256 * 8 * 4, code_bytes = static_cast<size_t>(rows * (cols / 8)) * 2,
+               sc_bytes = static_cast<size_t>(ng) * 4;
+  const size_t off_codes = cb_bytes, off_sc = round_up(off_codes + code_bytes, 16);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMalloc(&q->cb2_mem, off_sc + sc_bytes);
+  char* base = static_cast<char*>(q->cb2_mem);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(base, codebook, cb_bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(base + off_codes, codes, code_bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(base + off_sc, scales, sc_bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    mlra_qweight_destroy(q);
+    return fail(MLRA_ERR_CUDA, "cb2 upload: %s", cudaGetErrorString(e));
+  }
+  q->device_bytes = off_sc + sc_bytes;
+  q->d.group = group;
+  q->cb2 = mlra::Cb2Dev{rows, cols, group, cols / group,
+                        reinterpret_cast<const uint16_t*>(base + off_codes),
+                        reinterpret_cast<const float*>(base), reinterpret_cast<const float*>(base + off_sc)};
+  *out = q;
+  return MLRA_OK;
+}
+
+const mlra_hook* mlra_qweight_hook(const mlra_qweight* q) {
+  return q && q->opaque ? &q->hook : nullptr;
 }
 
 mlra_status mlra_qweight_info(const mlra_qweight* q, int64_t* rows, int64_t* cols, int* bits,
@@ -488,8 +677,15 @@ mlra_status mlra_qweight_info(const mlra_qweight* q, int64_t* rows, int64_t* col
 }
 
 uint64_t mlra_ledger_bytes(const mlra_qweight* q, mlra_strategy strategy) {
-  if (!q || strategy != MLRA_WEIGHT) return 0;
-  return static_cast<uint64_t>(q->d.rows) * static_cast<uint64_t>(q->d.cols) * 2u;
+  if (!q) return 0;
+  if (strategy == MLRA_WEIGHT)
+    return static_cast<uint64_t>(q->d.rows) * static_cast<uint64_t>(q->d.cols) * 2u;
+  if (!q->opaque) return 0;
+  // hook slabs: the larger of the forward (row) and dX (column) slab buffers
+  const QWeightDev& d = q->d;
+  const int64_t fwd = slab_extent(d.rows_pad, d.cols_pad, false) * d.cols_pad;
+  const int64_t bwd = slab_extent(d.cols_pad, d.rows_pad, false) * d.rows;
+  return static_cast<uint64_t>(fwd > bwd ? fwd : bwd) * 2u;
 }
 
 mlra_status mlra_materialize_rows(const mlra_qweight* q, int64_t row0, int64_t nrows, void* out,
@@ -501,10 +697,33 @@ mlra_status mlra_materialize_rows(const mlra_qweight* q, int64_t row0, int64_t n
   if (ld < q->d.cols)
     return fail(MLRA_ERR_DIMENSION, "dequantize_into: buffer size mismatch (ld %lld < cols %lld)",
                 (long long)ld, (long long)q->d.cols);
+  return mlra_materialize_tile(q, row0, nrows, 0, q->d.cols, out, dtype, ld, stream);
+}
+
+mlra_status mlra_materialize_tile(const mlra_qweight* q, int64_t row0, int64_t nrows,
+                                  int64_t col0, int64_t ncols, void* out, mlra_dtype dtype,
+                                  int64_t ld, void* stream) {
+  if (mlra_status st = check_q(q)) return st;
+  if (row0 < 0 || nrows < 0 || row0 + nrows > q->d.rows)
+    return fail(MLRA_ERR_RANGE, "dequantize_row: rows [%lld, %lld) out of range [0, %lld)",
+                (long long)row0, (long long)(row0 + nrows), (long long)q->d.rows);
+  if (col0 < 0 || ncols < 0 || col0 + ncols > q->d.cols || col0 % 8 != 0)
+    return fail(MLRA_ERR_RANGE, "materialize_tile: cols [%lld, %lld) out of range [0, %lld) "
+                "or not 8-aligned", (long long)col0, (long long)(col0 + ncols),
+                (long long)q->d.cols);
+  if (ld < ncols)
+    return fail(MLRA_ERR_DIMENSION, "dequantize_into: buffer size mismatch (ld %lld < cols %lld)",
+                (long long)ld, (long long)ncols);
   if (dtype != MLRA_F32 && dtype != MLRA_BF16) return fail(MLRA_ERR_CONFIG, "bad dtype");
   if (mlra_status st = check_device()) return st;
-  CUDA_TRY(mlra::launch_materialize(q->d, row0, nrows, out, ld, dtype == MLRA_F32,
-                                    static_cast<cudaStream_t>(stream)));
+  if (nrows == 0 || ncols == 0) return MLRA_OK;
+  if (q->opaque) {
+    if (!q->hook.materialize) return fail(MLRA_ERR_CONTRACT, "opaque qweight without a hook");
+    return q->hook.materialize(q->hook.state, q, row0, nrows, col0, ncols, out, dtype, ld,
+                               stream);
+  }
+  CUDA_TRY(mlra::launch_materialize_tile(q->d, row0, nrows, col0, ncols, out, ld,
+                                         dtype == MLRA_F32, static_cast<cudaStream_t>(stream)));
   return MLRA_OK;
 }
 
@@ -517,6 +736,12 @@ mlra_status mlra_materialize(const mlra_qweight* q, void* out, mlra_dtype dtype,
 mlra_status mlra_lp_forward(const mlra_qweight* q, mlra_strategy strategy, const void* x,
                             int64_t ldx, int64_t m, void* y, mlra_dtype y_dtype, int64_t ldy,
                             void* stream) {
+  return mlra_lp_forward_ex(q, strategy, nullptr, x, ldx, m, y, y_dtype, ldy, stream);
+}
+
+mlra_status mlra_lp_forward_ex(const mlra_qweight* q, mlra_strategy strategy,
+                               const mlra_hook* hook, const void* x, int64_t ldx, int64_t m,
+                               void* y, mlra_dtype y_dtype, int64_t ldy, void* stream) {
   if (mlra_status st = check_q(q)) return st;
   if (m < 0) return fail(MLRA_ERR_DIMENSION, "lp_forward: negative token count");
   if (ldx < q->d.cols)
@@ -536,12 +761,18 @@ mlra_status mlra_lp_forward(const mlra_qweight* q, mlra_strategy strategy, const
   gp.out = y;
   gp.ldo = ldy;
   gp.out_f32 = y_dtype == MLRA_F32;
-  return run_gemm(q, strategy, gp, sc);
+  return run_gemm(q, strategy, hook, gp, sc);
 }
 
 mlra_status mlra_lp_backward(const mlra_qweight* q, mlra_strategy strategy, const void* g,
                              int64_t ldg, int64_t m, void* dx, mlra_dtype dx_dtype,
                              int64_t lddx, void* stream) {
+  return mlra_lp_backward_ex(q, strategy, nullptr, g, ldg, m, dx, dx_dtype, lddx, stream);
+}
+
+mlra_status mlra_lp_backward_ex(const mlra_qweight* q, mlra_strategy strategy,
+                                const mlra_hook* hook, const void* g, int64_t ldg, int64_t m,
+                                void* dx, mlra_dtype dx_dtype, int64_t lddx, void* stream) {
   if (mlra_status st = check_q(q)) return st;
   if (m < 0) return fail(MLRA_ERR_DIMENSION, "lp_backward: negative token count");
   if (ldg < q->d.rows)
@@ -561,7 +792,7 @@ mlra_status mlra_lp_backward(const mlra_qweight* q, mlra_strategy strategy, cons
   gp.out = dx;
   gp.ldo = lddx;
   gp.out_f32 = dx_dtype == MLRA_F32;
-  return run_gemm(q, strategy, gp, sc);
+  return run_gemm(q, strategy, hook, gp, sc);
 }
 
 mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, int64_t m, void* y,
@@ -610,7 +841,7 @@ mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, in
   gp.out_f32 = y_dtype == MLRA_F32;
   gp.bias = L->bias;
   // K2: y = x·Ŵᵀ + (s·xb)·Aᵀ + bias
-  return run_gemm(L->q, L->strategy, gp, sc);
+  return run_gemm(L->q, L->strategy, L->hook, gp, sc);
 }
 
 mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, const float* xb,
@@ -692,11 +923,64 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   gp.ldo = lddx;
   gp.out_f32 = dx_dtype == MLRA_F32;
   // K3: dx = dy·Ŵ + (s·dyA)·Bᵀ   (lp_backward + matmul-bwd dx, lora.cpp:68)
-  const mlra_status gst = run_gemm(L->q, L->strategy, gp, sc);
+  const mlra_status gst = run_gemm(L->q, L->strategy, L->hook, gp, sc);
   // join: the caller's stream (and the scratch frees queued on it) waits for dA/dB
   CUDA_TRY(cudaEventRecord(side->join, cs));
   CUDA_TRY(cudaStreamWaitEvent(s, side->join, 0));
   return gst;
+}
+
+mlra_status mlra_adamw_step(const mlra_adamw* opt, int64_t step_index, double lr,
+                            int64_t n_params, const int64_t* offsets, double* params, double* m,
+                            double* v, const void* grad, mlra_dtype grad_dtype, float* params_f32,
+                            int* first_bad, void* stream) {
+  if (!opt) return fail(MLRA_ERR_CONTRACT, "adamw: null optimizer config");
+  if (n_params < 0 || (n_params > 0 && !offsets))
+    return fail(MLRA_ERR_CONTRACT, "adamw: params/names size mismatch");
+  if (step_index < 0) return fail(MLRA_ERR_CONTRACT, "adamw: negative step index");
+  if (grad_dtype != MLRA_F32 && grad_dtype != MLRA_F64)
+    return fail(MLRA_ERR_CONFIG, "adamw: gradients must be f32 or f64");
+  if (n_params == 0) return MLRA_OK;
+  if (offsets[0] != 0) return fail(MLRA_ERR_CONTRACT, "adamw: offsets[0] must be 0");
+  for (int64_t i = 0; i < n_params; ++i)
+    if (offsets[i + 1] < offsets[i])
+      return fail(MLRA_ERR_CONTRACT, "adamw: offsets must be non-decreasing");
+  const int64_t n = offsets[n_params];
+  if (n > 0 && (!params || !m || !v || !grad))
+    return fail(MLRA_ERR_CONTRACT, "adamw: gradient missing for parameter buffers");
+  if (n_params > mlra::kAdamwMaxSegs)
+    return fail(MLRA_ERR_CONFIG, "adamw: %lld parameters in one bucket (max %d)",
+                (long long)n_params, mlra::kAdamwMaxSegs);
+  if (mlra_status st = check_device()) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // train.cpp:99-101 and the per-element constants of :122-127, on the host
+  const double t = static_cast<double>(step_index) + 1.0;
+  mlra::AdamwConsts c{};
+  c.beta1 = opt->beta1;
+  c.one_m_beta1 = 1.0 - opt->beta1;
+  c.beta2 = opt->beta2;
+  c.one_m_beta2 = 1.0 - opt->beta2;
+  c.bc1 = 1.0 - std::pow(opt->beta1, t);
+  c.bc2 = 1.0 - std::pow(opt->beta2, t);
+  c.lr = lr;
+  c.eps = opt->eps;
+  c.decay = 1.0 - lr * opt->weight_decay;
+  Scratch sc(s);
+  int* bad = first_bad ? first_bad : sc.get<int>(1);
+  if (!bad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  const int nseg = static_cast<int>(n_params);
+  static thread_local mlra::AdamwSegs segs;
+  for (int64_t i = 0; i <= n_params; ++i) segs.off[i] = offsets[i];
+  CUDA_TRY(mlra::launch_adamw(grad, grad_dtype == MLRA_F64, n, segs, nseg, bad, params, m, v,
+                              params_f32, c, s));
+  if (first_bad) return MLRA_OK;
+  int host_bad = nseg;
+  CUDA_TRY(cudaMemcpyAsync(&host_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (host_bad >= 0 && host_bad < nseg)
+    return fail(MLRA_ERR_NUMERIC, "adamw: non-finite gradient for parameter #%d at step %lld",
+                host_bad, (long long)step_index);
+  return MLRA_OK;
 }
 
 }  // extern "C"

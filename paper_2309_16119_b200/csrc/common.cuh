@@ -34,6 +34,14 @@ struct QWeightDev {
   const float2* grid;          // rows_pad * ng_pad
 };
 
+// Device state of the built-in "cb2" codebook plugin (codebook.cu).
+struct Cb2Dev {
+  int64_t rows, cols, group, ng;  // ng = cols / group
+  const uint16_t* codes;          // [rows x cols/8]
+  const float* codebook;          // [256 x 8], 16-B aligned
+  const float* scales;            // [rows x ng]
+};
+
 // Bits of the 8 consecutive codes of unit `u` (codes 8u..8u+7) of a
 // word-aligned row, at the LSB of the result (bitpack.cpp:25-35 restated for
 // 8 codes at a time).

@@ -18,6 +18,28 @@ cudaError_t launch_grid(const float* scales, const float* zeros, int64_t rows, i
                         int* n_uncertified, cudaStream_t st);
 cudaError_t launch_materialize(const QWeightDev& q, int64_t row0, int64_t nrows, void* out,
                                int64_t ld, bool f32, cudaStream_t st);
+cudaError_t launch_materialize_tile(const QWeightDev& q, int64_t row0, int64_t nrows, int64_t col0,
+                                    int64_t ncols, void* out, int64_t ld, bool f32,
+                                    cudaStream_t st);
+cudaError_t launch_cb2_materialize(const Cb2Dev& c, int64_t row0, int64_t nrows, int64_t col0,
+                                   int64_t ncols, void* out, int64_t ld, bool f32,
+                                   cudaStream_t st);
+
+// AdamW (optim.cu): host-evaluated constants of AdamW::step (train.cpp:99-101, :122-127).
+struct AdamwConsts {
+  double beta1, one_m_beta1, beta2, one_m_beta2, bc1, bc2, lr, eps, decay;
+};
+// Parameter segment offsets passed by value (kernel parameter space), so a step
+// needs no host->device copy and can be captured in a CUDA graph.
+constexpr int kAdamwMaxSegs = 1024;
+struct AdamwSegs {
+  int64_t off[kAdamwMaxSegs + 1];
+};
+// first_bad: device int (set to the first parameter with a non-finite gradient,
+// any value >= nseg when none), or null for no check
+cudaError_t launch_adamw(const void* grad, bool grad_f64, int64_t n, const AdamwSegs& offs, int nseg,
+                         int* first_bad, double* p, double* m, double* v, float* p32,
+                         const AdamwConsts& c, cudaStream_t st);
 
 // Batched small jobs of one layer pass, one launch (thin_mma.cu k_prep).
 struct PrepTask {

@@ -84,24 +84,27 @@ __global__ void k_grid(const float* __restrict__ scales, const float* __restrict
 }
 
 // One thread per 8-entry unit of the (logical) matrix.
+// Tile form: columns [col0, col0 + ncols) of rows [row0, row0 + nrows), col0 % 8 == 0.
 template <int BITS, bool F32, bool VEC>
 __global__ void __launch_bounds__(256) k_materialize(const QWeightDev q, int64_t row0,
-                                                     int64_t nrows, void* __restrict__ out,
-                                                     int64_t ld) {
-  const int64_t upr = (q.cols + 7) / 8;  // units per logical row
+                                                     int64_t nrows, int64_t col0, int64_t ncols,
+                                                     void* __restrict__ out, int64_t ld) {
+  const int64_t upr = (ncols + 7) / 8;  // units per tile row
   const int64_t total = nrows * upr;
+  const int64_t col_end = ncols;  // valid extent of a tile row
   const bool fast_group = (q.group % 8) == 0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t rr = i / upr, u = i % upr;
     const int64_t r = row0 + rr;
-    const uint64_t v = load_unit<BITS>(q.words + r * q.row_words, u);
+    const int64_t ua = col0 / 8 + u;  // unit index within the row
+    const uint64_t v = load_unit<BITS>(q.words + r * q.row_words, ua);
     const float2* grow = q.grid + r * q.ng_pad;
     float f[8];
     if (fast_group)
-      deq8_f32<BITS>(v, __ldg(grow + (u * 8) / q.group), f);
+      deq8_f32<BITS>(v, __ldg(grow + (ua * 8) / q.group), f);
     else
-      deq8_f32_general<BITS>(v, grow, u * 8, q.group, f);
+      deq8_f32_general<BITS>(v, grow, ua * 8, q.group, f);
     const int64_t k0 = u * 8;
     if constexpr (VEC) {  // cols % 8 == 0 and ld % 8 == 0: aligned vector stores
       if constexpr (F32) {
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(256) k_materialize(const QWeightDev q, int64_t
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (k0 + j < q.cols) {
+        if (k0 + j < col_end) {
           if constexpr (F32)
             reinterpret_cast<float*>(out)[rr * ld + k0 + j] = f[j];
           else
@@ -192,6 +195,28 @@ int grid_for(int64_t work, int per_block) {
 }
 
 template <int BITS>
+cudaError_t materialize_tile_bits(const QWeightDev& q, int64_t row0, int64_t nrows, int64_t col0,
+                                  int64_t ncols, void* out, int64_t ld, bool f32, bool vec,
+                                  cudaStream_t st) {
+  const int64_t units = nrows * ((ncols + 7) / 8);
+  const int blocks = grid_for(units, 256);
+  note_launch();
+  if (f32) {
+    if (vec)
+      k_materialize<BITS, true, true><<<blocks, 256, 0, st>>>(q, row0, nrows, col0, ncols, out, ld);
+    else
+      k_materialize<BITS, true, false><<<blocks, 256, 0, st>>>(q, row0, nrows, col0, ncols, out, ld);
+  } else {
+    if (vec)
+      k_materialize<BITS, false, true><<<blocks, 256, 0, st>>>(q, row0, nrows, col0, ncols, out, ld);
+    else
+      k_materialize<BITS, false, false><<<blocks, 256, 0, st>>>(q, row0, nrows, col0, ncols, out,
+                                                                ld);
+  }
+  return cudaGetLastError();
+}
+
+template <int BITS>
 cudaError_t materialize_bits(const QWeightDev& q, int64_t row0, int64_t nrows, void* out,
                              int64_t ld, bool f32, cudaStream_t st) {
   const bool vec = (q.cols % 8 == 0) && (ld % 8 == 0) &&
@@ -209,21 +234,7 @@ cudaError_t materialize_bits(const QWeightDev& q, int64_t row0, int64_t nrows, v
       k_materialize_fast<BITS, false><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
     return cudaGetLastError();
   }
-  const int64_t units = nrows * ((q.cols + 7) / 8);
-  const int blocks = grid_for(units, 256);
-  note_launch();
-  if (f32) {
-    if (vec)
-      k_materialize<BITS, true, true><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
-    else
-      k_materialize<BITS, true, false><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
-  } else {
-    if (vec)
-      k_materialize<BITS, false, true><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
-    else
-      k_materialize<BITS, false, false><<<blocks, 256, 0, st>>>(q, row0, nrows, out, ld);
-  }
-  return cudaGetLastError();
+  return materialize_tile_bits<BITS>(q, row0, nrows, 0, q.cols, out, ld, f32, vec, st);
 }
 
 }  // namespace
@@ -254,6 +265,22 @@ cudaError_t launch_materialize(const QWeightDev& q, int64_t row0, int64_t nrows,
     case 3: return materialize_bits<3>(q, row0, nrows, out, ld, f32, st);
     case 4: return materialize_bits<4>(q, row0, nrows, out, ld, f32, st);
     case 8: return materialize_bits<8>(q, row0, nrows, out, ld, f32, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_materialize_tile(const QWeightDev& q, int64_t row0, int64_t nrows, int64_t col0,
+                                    int64_t ncols, void* out, int64_t ld, bool f32,
+                                    cudaStream_t st) {
+  if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+  if (col0 == 0 && ncols == q.cols) return launch_materialize(q, row0, nrows, out, ld, f32, st);
+  const bool vec = (ncols % 8 == 0) && (ld % 8 == 0) &&
+                   (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  switch (q.bits) {
+    case 2: return materialize_tile_bits<2>(q, row0, nrows, col0, ncols, out, ld, f32, vec, st);
+    case 3: return materialize_tile_bits<3>(q, row0, nrows, col0, ncols, out, ld, f32, vec, st);
+    case 4: return materialize_tile_bits<4>(q, row0, nrows, col0, ncols, out, ld, f32, vec, st);
+    case 8: return materialize_tile_bits<8>(q, row0, nrows, col0, ncols, out, ld, f32, vec, st);
     default: return cudaErrorInvalidValue;
   }
 }

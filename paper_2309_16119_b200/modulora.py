@@ -104,7 +104,25 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
 
 class DeviceQuantizedMatrix:
     """A frozen QuantizedMatrix resident in HBM (validated on upload exactly as
-    QuantizedMatrix::validate, quantize.cpp:82-115)."""
+    QuantizedMatrix::validate, quantize.cpp:82-115). Opaque (plugin-owned)
+    formats come from ``Codebook2Quantizer.upload`` / ``opaque``."""
+
+    @classmethod
+    def _wrap(cls, h: C.c_void_p, rows: int, cols: int, bits: int, group: int,
+              keepalive=None) -> "DeviceQuantizedMatrix":
+        self = cls.__new__(cls)
+        self._h = h
+        self.rows, self.cols, self.bits, self.group_size = rows, cols, bits, group
+        self._keepalive = keepalive
+        return self
+
+    @classmethod
+    def opaque(cls, rows: int, cols: int, bits: int, hook: "QuantizerHook") -> "DeviceQuantizedMatrix":
+        """mlra_qweight_create_opaque: a matrix only its plugin can dequantize;
+        every strategy materializes it through ``hook``."""
+        h = C.c_void_p()
+        check(lib().mlra_qweight_create_opaque(rows, cols, bits, C.byref(hook.c_hook()), C.byref(h)))
+        return cls._wrap(h, rows, cols, bits, cols, keepalive=hook)
 
     def __init__(self, q: QuantizedMatrix, stream: Optional[torch.cuda.Stream] = None):
         words = np.ascontiguousarray(q.codes.words, np.uint32)
@@ -155,6 +173,17 @@ def dequantize(q: DeviceQuantizedMatrix, dtype: torch.dtype = torch.float32,
     return out
 
 
+def dequantize_tile(q: DeviceQuantizedMatrix, row0: int, nrows: int, col0: int, ncols: int,
+                    dtype: torch.dtype = torch.float32, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """mlra_materialize_tile: Ŵ[row0:row0+nrows, col0:col0+ncols] (col0 % 8 == 0)
+    — the unit of work of the device dequant hook."""
+    if out is None:
+        out = torch.empty(nrows, ncols, dtype=dtype, device="cuda")
+    check(lib().mlra_materialize_tile(q.handle, row0, nrows, col0, ncols, out.data_ptr(),
+                                      _dtype_code(out.dtype), out.stride(0), _stream_ptr(None)))
+    return out
+
+
 def dequantize_row(q: DeviceQuantizedMatrix, row: int, dtype: torch.dtype = torch.float32) -> torch.Tensor:
     """dequantize_row (quantize.cpp:139-161); RangeError past the last row."""
     out = torch.empty(1, q.cols, dtype=dtype, device="cuda")
@@ -163,18 +192,162 @@ def dequantize_row(q: DeviceQuantizedMatrix, row: int, dtype: torch.dtype = torc
     return out[0]
 
 
+# --------------------------------------------------------------------------- plugins
+class _CudaArray:
+    """Zero-copy view of a raw device buffer (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, rows: int, cols: int, ld: int, esize: int):
+        self.__cuda_array_interface__ = {
+            "data": (ptr, False), "shape": (rows, cols), "strides": (ld * esize, esize),
+            "typestr": "<f4" if esize == 4 else "<i2", "version": 2}
+
+
+class QuantizerHook:
+    """The black-box Quantizer plugin (quantize.hpp:91-106) in device form.
+
+    The reference lets a plugin override ``Quantizer::matvec`` /
+    ``matvec_transposed`` (quantize.hpp:98-105); lp_forward / lp_backward call
+    them under QuantizerMatvec (lowprec_linear.cpp:174-182, 226-235). On the
+    GPU the override point is the plugin's dequantization of one tile of Ŵ:
+    subclasses implement :meth:`materialize`, writing the tile into ``out`` (a
+    bf16 or fp32 CUDA view with the caller's leading dimension) on ``stream``.
+    The library then runs its own tcgen05 GEMM over hook-materialized slabs.
+    """
+
+    def name(self) -> str:
+        return type(self).__name__
+
+    def materialize(self, q: int, row0: int, nrows: int, col0: int, ncols: int,
+                    out: torch.Tensor, stream: torch.cuda.Stream) -> None:
+        raise NotImplementedError
+
+    def _call(self, _state, q, row0, nrows, col0, ncols, out, dtype, ld, stream):
+        try:
+            esize = 4 if dtype == _lib.F32 else 2
+            view = torch.as_tensor(_CudaArray(out, nrows, ncols, ld, esize), device="cuda")
+            if esize == 2:
+                view = view.view(torch.bfloat16)
+            st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+            self.materialize(q, row0, nrows, col0, ncols, view, st)
+            return 0
+        except MlraError as e:
+            self._error = e
+            return e.status
+        except Exception as e:  # noqa: BLE001 — reported as a contract failure of the plugin
+            self._error = e
+            return 5
+
+    def c_hook(self) -> _lib.MlraHook:
+        if getattr(self, "_c", None) is None:
+            self._fn = _lib.HOOK_FN(self._call)
+            self._name = self.name().encode()
+            self._c = _lib.MlraHook(self._name, None, self._fn)
+        return self._c
+
+
+class DoublingQuantizer(QuantizerHook):
+    """The reference test plugin (test_lowprec.cpp:354-377): the hook returns
+    twice the default product, so outputs under QuantizerMatvec double."""
+
+    def materialize(self, q, row0, nrows, col0, ncols, out, stream):
+        check(lib().mlra_materialize_tile(q, row0, nrows, col0, ncols, out.data_ptr(),
+                                          _dtype_code(out.dtype), out.stride(0), stream.cuda_stream))
+        with torch.cuda.stream(stream):
+            out.mul_(2)
+
+
+def default_cb2_codebook() -> np.ndarray:
+    """The cb2 plugin's default 256 x 8 magnitude codebook: the 256 shortest
+    vectors of {1/2, 3/2, 5/2, 7/2}^8 (a shifted-lattice shell, as in QuIP#'s
+    E8-derived codebooks), ordered by squared norm then lexicographically."""
+    vals = np.array([0.5, 1.5, 2.5, 3.5])
+    idx = np.stack(np.meshgrid(*([np.arange(4)] * 8), indexing="ij"), -1).reshape(-1, 8)
+    vecs = vals[idx]
+    norm = (vecs ** 2).sum(1)
+    order = np.lexsort(tuple(idx[:, ::-1].T) + (norm,))
+    return np.ascontiguousarray(vecs[order[:256]], np.float32)
+
+
+@dataclass
+class Cb2Matrix:
+    """Host container of the cb2 format (include/mlra.h mlra_cb2_create)."""
+    rows: int
+    cols: int
+    group_size: int
+    codes: np.ndarray     # uint16 [rows x cols/8]
+    codebook: np.ndarray  # float32 [256 x 8]
+    scales: np.ndarray    # float32 [rows x cols/group]
+
+
+class Codebook2Quantizer:
+    """Quantizer plugin "cb2" (quantize.hpp:91-106 interface: name(), quantize()):
+    2 bits per weight as one u16 code per 8 entries (8-bit codebook index + 8
+    sign bits) with a per-(row, group) scale. ``quantize`` is the offline
+    nearest-codeword search on the host; ``upload`` moves the codes to HBM and
+    returns an opaque DeviceQuantizedMatrix whose hook is the library's cb2
+    materialize kernel."""
+
+    def __init__(self, codebook: Optional[np.ndarray] = None):
+        self.codebook = np.ascontiguousarray(
+            default_cb2_codebook() if codebook is None else codebook, np.float32).reshape(256, 8)
+
+    def name(self) -> str:
+        return "cb2"
+
+    def quantize(self, w: np.ndarray, calib=None, bits: int = 2, group_size: int = 128) -> Cb2Matrix:
+        if bits != 2:
+            raise MlraError(3, f"cb2: unsupported bit width {bits} (2 bits per weight)")
+        w = np.asarray(w, np.float64)
+        rows, cols = w.shape
+        if cols % 8 or group_size % 8 or cols % group_size:
+            raise MlraError(3, "cb2: cols and group size must be multiples of 8, group dividing cols")
+        cb = self.codebook.astype(np.float64)
+        ng = cols // group_size
+        # s = group RMS: minimises the codebook's relative error on Gaussian groups
+        rms = np.sqrt((w.reshape(rows, ng, group_size) ** 2).mean(-1))
+        scales = np.maximum(rms, np.finfo(np.float32).tiny).astype(np.float32)
+        v = w.reshape(rows, ng, group_size // 8, 8) / scales.astype(np.float64)[:, :, None, None]
+        v = v.reshape(-1, 8)
+        codes = np.empty(v.shape[0], np.uint16)
+        cn = (cb ** 2).sum(1)
+        for i in range(0, v.shape[0], 1 << 16):
+            a = np.abs(v[i:i + (1 << 16)])
+            d = cn[None, :] - 2.0 * a @ cb.T
+            best = d.argmin(1).astype(np.uint16)
+            sign = (v[i:i + (1 << 16)] < 0).astype(np.uint16)
+            codes[i:i + (1 << 16)] = best | (sign << np.arange(8, 16, dtype=np.uint16)).sum(1).astype(np.uint16)
+        return Cb2Matrix(rows, cols, group_size, codes.reshape(rows, cols // 8), self.codebook.copy(),
+                         scales.reshape(rows, ng))
+
+    def upload(self, m: Cb2Matrix, stream: Optional[torch.cuda.Stream] = None) -> DeviceQuantizedMatrix:
+        codes = np.ascontiguousarray(m.codes, np.uint16)
+        cb = np.ascontiguousarray(m.codebook, np.float32)
+        sc = np.ascontiguousarray(m.scales, np.float32)
+        if codes.size != m.rows * (m.cols // 8) or cb.size != 2048 or sc.size != m.rows * (m.cols // m.group_size):
+            raise MlraError(7, "cb2: buffer sizes do not match the shape")
+        h = C.c_void_p()
+        check(lib().mlra_cb2_create(m.rows, m.cols, m.group_size, codes.ctypes.data, cb.ctypes.data,
+                                    sc.ctypes.data, _stream_ptr(stream), C.byref(h)))
+        return DeviceQuantizedMatrix._wrap(h, m.rows, m.cols, 2, m.group_size)
+
+
 @dataclass
 class LpLinearContext:
     """lowprec_linear.hpp:85-91 (ledger replaced by ledger_bytes())."""
     q: Optional[DeviceQuantizedMatrix]
     strategy: MaterializationStrategy = MaterializationStrategy.RowMaterialize
     layer_name: str = ""
+    matvec_hook: Optional[QuantizerHook] = None  # consulted under QuantizerMatvec only
 
     def ledger_bytes(self) -> int:
         """Bytes this strategy materializes per pass (MemoryLedger semantics)."""
         if self.q is None:
             return 0
         return int(lib().mlra_ledger_bytes(self.q.handle, int(self.strategy)))
+
+
+def _hook_ptr(hook: Optional[QuantizerHook]):
+    return None if hook is None else C.pointer(hook.c_hook())
 
 
 def _need_q(ctx) -> DeviceQuantizedMatrix:
@@ -197,9 +370,9 @@ def lp_forward(ctx: LpLinearContext, x: torch.Tensor, out_dtype=torch.bfloat16) 
     q = _need_q(ctx)
     _check_act(x, q.cols, "lp_forward")
     y = torch.empty(x.shape[0], q.rows, dtype=out_dtype, device=x.device)
-    check(lib().mlra_lp_forward(q.handle, int(ctx.strategy), x.data_ptr(), x.stride(0),
-                                x.shape[0], y.data_ptr(), _dtype_code(out_dtype), q.rows,
-                                _stream_ptr(None)))
+    check(lib().mlra_lp_forward_ex(q.handle, int(ctx.strategy), _hook_ptr(ctx.matvec_hook),
+                                   x.data_ptr(), x.stride(0), x.shape[0], y.data_ptr(),
+                                   _dtype_code(out_dtype), q.rows, _stream_ptr(None)))
     return y
 
 
@@ -208,9 +381,10 @@ def lp_backward(ctx: LpLinearContext, grad_out: torch.Tensor, out_dtype=torch.bf
     q = _need_q(ctx)
     _check_act(grad_out, q.rows, "lp_backward")
     dx = torch.empty(grad_out.shape[0], q.cols, dtype=out_dtype, device=grad_out.device)
-    check(lib().mlra_lp_backward(q.handle, int(ctx.strategy), grad_out.data_ptr(),
-                                 grad_out.stride(0), grad_out.shape[0], dx.data_ptr(),
-                                 _dtype_code(out_dtype), q.cols, _stream_ptr(None)))
+    check(lib().mlra_lp_backward_ex(q.handle, int(ctx.strategy), _hook_ptr(ctx.matvec_hook),
+                                    grad_out.data_ptr(), grad_out.stride(0), grad_out.shape[0],
+                                    dx.data_ptr(), _dtype_code(out_dtype), q.cols,
+                                    _stream_ptr(None)))
     return dx
 
 
@@ -253,6 +427,7 @@ class ModuLoraLayer:
     bias: Optional[torch.Tensor] = None  # fp32 [d_out]
     bias_trainable: bool = False
     strategy: MaterializationStrategy = MaterializationStrategy.RowMaterialize
+    matvec_hook: Optional[QuantizerHook] = None  # lora.hpp:47
     grad_bias: Optional[torch.Tensor] = None
     _grads_ready: bool = field(default=False, repr=False)
 
@@ -267,7 +442,8 @@ class ModuLoraLayer:
         if a.a.dtype != torch.float32 or a.b.dtype != torch.float32:
             raise MlraError(3, "adapter factors must be fp32")
         return MlraLora(self.weights.handle, int(self.strategy), a.rank, float(a.alpha),
-                        a.a.data_ptr(), a.b.data_ptr(), _ptr(self.bias))
+                        a.a.data_ptr(), a.b.data_ptr(), _ptr(self.bias),
+                        _hook_ptr(self.matvec_hook))
 
 
 def make_layer(name: str, weights: DeviceQuantizedMatrix, rank: int, alpha: float, seed: int,
