@@ -47,7 +47,8 @@ typedef enum mlra_status {
   MLRA_ERR_NUMERIC = 6,     /* modulora::NumericError    errors.hpp:44 */
   MLRA_ERR_FORMAT = 7,      /* modulora::FormatError{BadField} errors.hpp:55-63 */
   MLRA_ERR_CUDA = 8,        /* CUDA runtime failure (no reference equivalent) */
-  MLRA_ERR_UNSUPPORTED = 9  /* not an sm_100 device / extension unavailable */
+  MLRA_ERR_UNSUPPORTED = 9, /* not an sm_100 device / extension unavailable */
+  MLRA_ERR_IO = 10          /* modulora::IoError         errors.hpp:50 */
 } mlra_status;
 
 /* MaterializationStrategy (lowprec_linear.hpp:29-30), GPU meaning:
@@ -108,6 +109,10 @@ typedef struct mlra_lora {
 /* Last error message of this thread ("" if none). */
 MLRA_API const char* mlra_last_error(void);
 MLRA_API int mlra_abi_version(void);
+/* FormatError::Kind of this thread's last MLRA_ERR_FORMAT (errors.hpp:55-63:
+ * 0 BadMagic, 1 BadVersion, 2 Truncated, 3 BadField) and its byte offset;
+ * -1 when the last error carried no kind. */
+MLRA_API int mlra_last_format_error(uint64_t* offset);
 /* Number of CUDA kernels this library has launched in this process. */
 MLRA_API uint64_t mlra_kernel_launches(void);
 
@@ -239,6 +244,60 @@ MLRA_API mlra_status mlra_adamw_step(const mlra_adamw* opt, int64_t step_index, 
                                      double* m, double* v, const void* grad,
                                      mlra_dtype grad_dtype, float* params_f32, int* first_bad,
                                      void* stream);
+
+/* ------------------------------------------------------------------------
+ * On-disk checkpoint -> device. The reference's binary .mlra
+ * format (checkpoint.hpp:4-24, little-endian): parsed and validated with the
+ * reference's rules and error taxonomy (checkpoint.cpp:141-306: FormatError
+ * BadMagic / BadVersion / Truncated / BadField with the byte offset, IoError),
+ * each layer's packed words then uploaded verbatim to HBM (they are already
+ * the device layout at LLaMA shapes). The config JSON is carried as opaque
+ * bytes (model assembly from it is outside the hot path). Saving re-encodes
+ * byte-identically (checkpoint.cpp:93-130), with adapters optionally replaced
+ * (the finetune flow rewrites only the adapter section). */
+typedef struct mlra_checkpoint mlra_checkpoint;
+
+/* One layer record + its adapter (pointers into the checkpoint, valid until it
+ * is freed or the adapter is replaced). */
+typedef struct mlra_ckpt_layer {
+  const char* name;
+  int64_t rows, cols;
+  int bits;
+  int64_t group_size;
+  const uint32_t* words;
+  uint64_t word_count;
+  const float* scales; /* rows * (cols/group) */
+  const float* zeros;
+  const float* bias;   /* rows */
+  int64_t rank;        /* 0 when the layer has no adapter record */
+  float alpha;
+  const double* a;     /* rows x rank */
+  const double* b;     /* cols x rank */
+  uint64_t record_offset, record_size;   /* layer record bytes (inspect_layout) */
+  uint64_t adapter_offset, adapter_size; /* adapter record bytes */
+} mlra_ckpt_layer;
+
+/* load_model's parse (checkpoint.cpp:141-306) of `path`. */
+MLRA_API mlra_status mlra_checkpoint_load(const char* path, mlra_checkpoint** out);
+MLRA_API void mlra_checkpoint_free(mlra_checkpoint* c);
+MLRA_API int64_t mlra_checkpoint_layer_count(const mlra_checkpoint* c);
+MLRA_API mlra_status mlra_checkpoint_layer(const mlra_checkpoint* c, int64_t i,
+                                           mlra_ckpt_layer* out);
+/* The ModelConfig JSON bytes (NUL-terminated copy) and format version. */
+MLRA_API const char* mlra_checkpoint_config_json(const mlra_checkpoint* c, int* version);
+/* ToyModel::frozen_state_hash (model.cpp:203-211; hash_quantized
+ * quantize.cpp:383-391) over the layer records, and fnv1a64_file
+ * (hash.cpp:11-20) of the bytes save() would write. */
+MLRA_API uint64_t mlra_checkpoint_frozen_hash(const mlra_checkpoint* c);
+MLRA_API uint64_t mlra_checkpoint_file_hash(const mlra_checkpoint* c);
+/* Device upload of layer i's QuantizedMatrix (mlra_qweight_create, verbatim). */
+MLRA_API mlra_status mlra_checkpoint_upload(const mlra_checkpoint* c, int64_t i, void* stream,
+                                            mlra_qweight** out);
+/* Replace layer i's adapter factors (host f64, rows x rank and cols x rank). */
+MLRA_API mlra_status mlra_checkpoint_set_adapter(mlra_checkpoint* c, int64_t i, const double* a,
+                                                 const double* b);
+/* save_model's encoding (checkpoint.cpp:93-130, 307-314) to `path`. */
+MLRA_API mlra_status mlra_checkpoint_save(const mlra_checkpoint* c, const char* path);
 
 #ifdef __cplusplus
 }

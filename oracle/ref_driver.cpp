@@ -25,6 +25,10 @@
 #include "modulora/quantize.hpp"
 #include "modulora/rng.hpp"
 #include "modulora/train.hpp"
+#include "modulora/checkpoint.hpp"
+#include "modulora/hash.hpp"
+#include "modulora/model.hpp"
+#include "modulora/tasks.hpp"
 
 using namespace modulora;
 
@@ -327,6 +331,57 @@ int ref_bench_layer(const uint32_t* words, uint64_t rows, uint64_t cols,
     for (double s : secs) mx = s > mx ? s : mx;
     *seconds = mx;
     return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// The CLI's `quantize` command (modulora_main.cpp:93-110, QuantizeOpts
+// defaults :78-87): the recipe of the reference's golden.mlra fixture
+// (test_checkpoint.cpp:28: --task regression --bits 3 --seed 11). `task`
+// "regression" or "parity".
+int ref_make_checkpoint(const char* path, const char* task, int bits, uint64_t seed,
+                        uint64_t group_size) {
+  try {
+    ModelConfig mc;
+    mc.task = parse_task(task);
+    mc.kind = mc.task == TaskKind::TeacherResidualRegression ? ModelKind::Mlp
+                                                             : ModelKind::ParityTransformer;
+    mc.bits = bits;
+    mc.quantizer = "rtn";
+    mc.group_size = group_size;
+    mc.calib_samples = 0;
+    mc.rank = 8;
+    mc.alpha = 32.0;
+    mc.strategy = parse_strategy("weight");
+    mc.base_seed = seed;
+    mc.adapter_seed = mix_seed(seed, 0xADA9);
+    BuiltModel built = build_model(mc);
+    save_model(built.model, path);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// fnv1a64_file (hash.cpp:11-20) and load_model(path).frozen_state_hash();
+// on a load failure returns the status with FormatError kind/offset.
+int ref_checkpoint_probe(const char* path, uint64_t* file_hash, uint64_t* frozen_hash,
+                         int* fmt_kind, uint64_t* fmt_offset) {
+  *fmt_kind = -1;
+  *fmt_offset = 0;
+  try {
+    *file_hash = fnv1a64_file(path);
+    *frozen_hash = load_model(path).frozen_state_hash();
+    return 0;
+  } catch (const FormatError& e) {
+    *fmt_kind = static_cast<int>(e.kind);
+    *fmt_offset = e.offset;
+    g_err = e.what();
+    return 7;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return 10;
   } catch (...) {
     return map_exc();
   }

@@ -12,8 +12,9 @@ LIB_PATH = os.environ.get("MLRA_LIB") or os.path.join(HERE, "libmlra.so")
 MLRA_OK = 0
 STATUS_NAMES = {
     2: "DimensionError", 3: "ConfigError", 4: "RangeError", 5: "ContractError",
-    6: "NumericError", 7: "FormatError", 8: "CudaError", 9: "UnsupportedDevice",
+    6: "NumericError", 7: "FormatError", 8: "CudaError", 9: "UnsupportedDevice", 10: "IoError",
 }
+FORMAT_KINDS = {0: "BadMagic", 1: "BadVersion", 2: "Truncated", 3: "BadField"}
 WEIGHT, ROW, MATVEC = 0, 1, 2
 F32, BF16, F64 = 0, 1, 2
 
@@ -24,7 +25,10 @@ EXPORTS = [
     "mlra_materialize_rows", "mlra_ledger_bytes", "mlra_lp_forward", "mlra_lp_backward",
     "mlra_lora_forward", "mlra_lora_backward", "mlra_qweight_create_opaque", "mlra_cb2_create",
     "mlra_qweight_hook", "mlra_materialize_tile", "mlra_lp_forward_ex", "mlra_lp_backward_ex",
-    "mlra_adamw_step",
+    "mlra_adamw_step", "mlra_last_format_error", "mlra_checkpoint_load", "mlra_checkpoint_free",
+    "mlra_checkpoint_layer_count", "mlra_checkpoint_layer", "mlra_checkpoint_config_json",
+    "mlra_checkpoint_frozen_hash", "mlra_checkpoint_file_hash", "mlra_checkpoint_upload",
+    "mlra_checkpoint_set_adapter", "mlra_checkpoint_save",
 ]
 
 # mlra_hook.materialize(state, q, row0, nrows, col0, ncols, out, dtype, ld, stream)
@@ -37,12 +41,27 @@ class MlraHook(C.Structure):
 
 
 class MlraError(RuntimeError):
-    """Mirrors the reference exception taxonomy (errors.hpp:15-63)."""
+    """Mirrors the reference exception taxonomy (errors.hpp:15-63). A
+    FormatError also carries ``format_kind`` (BadMagic / BadVersion / Truncated /
+    BadField) and the byte ``offset`` when the library reported them."""
 
-    def __init__(self, status: int, msg: str):
+    def __init__(self, status: int, msg: str, format_kind: str = None, offset: int = 0):
         self.status = status
         self.kind = STATUS_NAMES.get(status, f"status{status}")
+        self.format_kind = format_kind
+        self.offset = offset
         super().__init__(f"{self.kind}: {msg}")
+
+
+class MlraCkptLayer(C.Structure):
+    _fields_ = [
+        ("name", C.c_char_p), ("rows", C.c_int64), ("cols", C.c_int64), ("bits", C.c_int),
+        ("group_size", C.c_int64), ("words", C.c_void_p), ("word_count", C.c_uint64),
+        ("scales", C.c_void_p), ("zeros", C.c_void_p), ("bias", C.c_void_p), ("rank", C.c_int64),
+        ("alpha", C.c_float), ("a", C.c_void_p), ("b", C.c_void_p),
+        ("record_offset", C.c_uint64), ("record_size", C.c_uint64),
+        ("adapter_offset", C.c_uint64), ("adapter_size", C.c_uint64),
+    ]
 
 
 class MlraAdamw(C.Structure):
@@ -121,10 +140,39 @@ def lib() -> C.CDLL:
         L.mlra_adamw_step.restype = i32
         L.mlra_adamw_step.argtypes = [C.POINTER(MlraAdamw), i64, C.c_double, i64,
                                       C.POINTER(i64), vp, vp, vp, vp, i32, vp, vp, vp]
+        L.mlra_last_format_error.restype = i32
+        L.mlra_last_format_error.argtypes = [C.POINTER(u64)]
+        L.mlra_checkpoint_load.restype = i32
+        L.mlra_checkpoint_load.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.mlra_checkpoint_free.restype = None
+        L.mlra_checkpoint_free.argtypes = [vp]
+        L.mlra_checkpoint_layer_count.restype = i64
+        L.mlra_checkpoint_layer_count.argtypes = [vp]
+        L.mlra_checkpoint_layer.restype = i32
+        L.mlra_checkpoint_layer.argtypes = [vp, i64, C.POINTER(MlraCkptLayer)]
+        L.mlra_checkpoint_config_json.restype = C.c_char_p
+        L.mlra_checkpoint_config_json.argtypes = [vp, C.POINTER(i32)]
+        L.mlra_checkpoint_frozen_hash.restype = u64
+        L.mlra_checkpoint_frozen_hash.argtypes = [vp]
+        L.mlra_checkpoint_file_hash.restype = u64
+        L.mlra_checkpoint_file_hash.argtypes = [vp]
+        L.mlra_checkpoint_upload.restype = i32
+        L.mlra_checkpoint_upload.argtypes = [vp, i64, vp, C.POINTER(vp)]
+        L.mlra_checkpoint_set_adapter.restype = i32
+        L.mlra_checkpoint_set_adapter.argtypes = [vp, i64, vp, vp]
+        L.mlra_checkpoint_save.restype = i32
+        L.mlra_checkpoint_save.argtypes = [vp, C.c_char_p]
         _lib = L
     return _lib
 
 
 def check(status: int) -> None:
     if status != MLRA_OK:
-        raise MlraError(status, lib().mlra_last_error().decode())
+        msg = lib().mlra_last_error().decode()
+        fk, off = None, 0
+        if status == 7:
+            o = C.c_uint64()
+            k = lib().mlra_last_format_error(C.byref(o))
+            if k >= 0:
+                fk, off = FORMAT_KINDS.get(k), o.value
+        raise MlraError(status, msg, fk, off)

@@ -1,0 +1,158 @@
+"""The reference's .mlra checkpoint -> device.
+
+  reference (checkpoint.hpp)                  here (libmlra C ABI, host C++)
+  -----------------------------------------   ------------------------------------------------
+  load_model(path) parse + validation         Checkpoint.load: same checks, same FormatError
+  (checkpoint.cpp:141-306)                    kinds and byte offsets, IoError
+  save_model(model, path) (:93-130, :307-314) Checkpoint.save: byte-identical re-encoding
+  inspect_layout(path) (:320-322)             Checkpoint.layout()
+  ToyModel::frozen_state_hash (model.cpp:203) Checkpoint.frozen_hash(); fnv1a64 file digest
+  (assemble_model from the config JSON)       not on the hot path: config JSON kept verbatim
+
+Each layer's packed words go to HBM verbatim (``upload``): at LLaMA shapes the
+reference bitstream already is the device layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import MlraError, check, lib
+from .modulora import (DeviceQuantizedMatrix, LoraAdapter, MaterializationStrategy, ModuLoraLayer,
+                       _stream_ptr)
+
+
+def _arr(ptr, n, dt):
+    if n == 0:
+        return np.zeros(0, dt)
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dt))),
+                                 shape=(n,)).copy()
+
+
+@dataclass
+class LayerRecord:
+    """One layer record with its adapter (checkpoint.hpp:11-24)."""
+    name: str
+    rows: int
+    cols: int
+    bits: int
+    group_size: int
+    words: np.ndarray
+    scales: np.ndarray
+    zeros: np.ndarray
+    bias: np.ndarray
+    rank: int
+    alpha: float
+    a: np.ndarray  # f64 [rows x rank]
+    b: np.ndarray  # f64 [cols x rank]
+    offset: int
+    size: int
+    adapter_offset: int
+    adapter_size: int
+
+
+class Checkpoint:
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+
+    @classmethod
+    def load(cls, path: str) -> "Checkpoint":
+        h = C.c_void_p()
+        check(lib().mlra_checkpoint_load(path.encode(), C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None and self._h.value and _lib._lib is not None:
+                lib().mlra_checkpoint_free(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
+
+    def __len__(self) -> int:
+        return int(lib().mlra_checkpoint_layer_count(self._h))
+
+    def config_json(self) -> str:
+        v = C.c_int()
+        return lib().mlra_checkpoint_config_json(self._h, C.byref(v)).decode()
+
+    def version(self) -> int:
+        v = C.c_int()
+        lib().mlra_checkpoint_config_json(self._h, C.byref(v))
+        return v.value
+
+    def layer(self, i: int) -> LayerRecord:
+        o = _lib.MlraCkptLayer()
+        check(lib().mlra_checkpoint_layer(self._h, i, C.byref(o)))
+        ng = o.rows * (o.cols // o.group_size)
+        return LayerRecord(
+            o.name.decode(), o.rows, o.cols, o.bits, o.group_size,
+            _arr(o.words, o.word_count, np.uint32), _arr(o.scales, ng, np.float32),
+            _arr(o.zeros, ng, np.float32), _arr(o.bias, o.rows, np.float32), o.rank, o.alpha,
+            _arr(o.a, o.rows * o.rank, np.float64).reshape(o.rows, o.rank),
+            _arr(o.b, o.cols * o.rank, np.float64).reshape(o.cols, o.rank),
+            o.record_offset, o.record_size, o.adapter_offset, o.adapter_size)
+
+    def layers(self) -> List[LayerRecord]:
+        return [self.layer(i) for i in range(len(self))]
+
+    def layout(self) -> dict:
+        """inspect_layout (checkpoint.cpp:320-322): record offsets and sizes."""
+        recs = self.layers()
+        return {"version": self.version(),
+                "layers": [(r.name, r.offset, r.size) for r in recs],
+                "adapters": [(r.name, r.adapter_offset, r.adapter_size) for r in recs if r.rank]}
+
+    def frozen_hash(self) -> int:
+        return int(lib().mlra_checkpoint_frozen_hash(self._h))
+
+    def file_hash(self) -> int:
+        return int(lib().mlra_checkpoint_file_hash(self._h))
+
+    def upload(self, i: int, stream: Optional[torch.cuda.Stream] = None) -> DeviceQuantizedMatrix:
+        """Layer i's packed words + grids to HBM, verbatim (mlra_checkpoint_upload)."""
+        rec = self.layer(i)
+        h = C.c_void_p()
+        check(lib().mlra_checkpoint_upload(self._h, i, _stream_ptr(stream), C.byref(h)))
+        return DeviceQuantizedMatrix._wrap(h, rec.rows, rec.cols, rec.bits, rec.group_size)
+
+    def to_layers(self, strategy=MaterializationStrategy.RowMaterialize) -> List[ModuLoraLayer]:
+        """Device ModuLoraLayers: frozen weights uploaded, bias and adapter
+        factors as fp32 device tensors (the f64 values stay available through
+        layer(i).a / .b for an exact AdamW master copy)."""
+        out = []
+        for i in range(len(self)):
+            r = self.layer(i)
+            if not r.rank:
+                raise MlraError(5, f"checkpoint: layer '{r.name}' has no adapter")
+            ad = LoraAdapter(torch.from_numpy(r.a.astype(np.float32)).cuda(),
+                             torch.from_numpy(r.b.astype(np.float32)).cuda(), r.rank, float(r.alpha))
+            out.append(ModuLoraLayer(r.name, self.upload(i), ad,
+                                     bias=torch.from_numpy(r.bias).cuda(),
+                                     strategy=MaterializationStrategy(strategy)))
+        return out
+
+    def set_adapter(self, i: int, a: np.ndarray, b: np.ndarray) -> None:
+        rec = self.layer(i)
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        if a.shape != (rec.rows, rec.rank) or b.shape != (rec.cols, rec.rank):
+            raise MlraError(2, "checkpoint: adapter shape mismatch")
+        check(lib().mlra_checkpoint_set_adapter(self._h, i, a.ctypes.data, b.ctypes.data))
+
+    def save(self, path: str) -> None:
+        check(lib().mlra_checkpoint_save(self._h, path.encode()))
+
+
+def load_model(path: str) -> Checkpoint:
+    """load_model (checkpoint.hpp:43) — parse + validate; see Checkpoint."""
+    return Checkpoint.load(path)
+
+
+def inspect_layout(path: str) -> dict:
+    return Checkpoint.load(path).layout()

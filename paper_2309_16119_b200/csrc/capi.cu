@@ -44,8 +44,28 @@ struct mlra_qweight {
 };
 
 namespace {
-
 thread_local std::string g_last_error;
+thread_local int g_format_kind = -1;
+thread_local uint64_t g_format_offset = 0;
+}  // namespace
+
+namespace mlra {
+// Error channel shared with the host-side translation units (checkpoint.cpp).
+mlra_status set_error(mlra_status st, const std::string& msg) {
+  g_last_error = msg;
+  g_format_kind = -1;
+  g_format_offset = 0;
+  return st;
+}
+mlra_status set_format_error(int kind, uint64_t offset, const std::string& msg) {
+  g_last_error = msg;
+  g_format_kind = kind;
+  g_format_offset = offset;
+  return MLRA_ERR_FORMAT;
+}
+}  // namespace mlra
+
+namespace {
 
 mlra_status fail(mlra_status st, const char* fmt, ...) {
   char buf[512];
@@ -457,6 +477,10 @@ mlra_status side_stream(SideStream** out) {
 extern "C" {
 
 const char* mlra_last_error(void) { return g_last_error.c_str(); }
+int mlra_last_format_error(uint64_t* offset) {
+  if (offset) *offset = g_format_offset;
+  return g_format_kind;
+}
 int mlra_abi_version(void) { return 2; }
 uint64_t mlra_kernel_launches(void) { return mlra::g_launches.load(); }
 mlra_status mlra_device_check(void) { return check_device(); }

@@ -123,6 +123,112 @@ def layer_cases():
     return out
 
 
+# --------------------------------------------------------------------------- checkpoints
+CKPTS = [  # (file, task, bits, seed, group): the first is the reference's own golden.mlra
+    ("golden.mlra", "regression", 3, 11, 0),   # test_checkpoint.cpp:28 recipe
+    ("parity_b4.mlra", "parity", 4, 5, 0),
+    ("regression_b2_g4.mlra", "regression", 2, 7, 4),
+    ("regression_b8.mlra", "regression", 8, 9, 0),
+]
+
+
+def field_offsets(buf: bytes) -> dict:
+    """Byte offsets of the first layer's fields in a checkpoint (checkpoint.hpp:4-24)."""
+    import struct
+    o = 6
+    (clen,) = struct.unpack_from("<I", buf, o)
+    o += 4 + clen
+    f = {"n_layers": o}
+    o += 4
+    f["layer0"] = o
+    (nlen,) = struct.unpack_from("<I", buf, o)
+    o += 4 + nlen
+    rows, cols = struct.unpack_from("<II", buf, o)
+    f["rows"], f["cols"] = o, o + 4
+    o += 8
+    bits = buf[o]
+    f["bits"] = o
+    o += 1
+    (group,) = struct.unpack_from("<I", buf, o)
+    f["group"] = o
+    o += 4
+    f["n_words"] = o
+    (nw,) = struct.unpack_from("<I", buf, o)
+    o += 4
+    f["words"] = o
+    f["last_word"] = o + 4 * (nw - 1)
+    o += 4 * nw
+    ng = rows * (cols // group)
+    f["scales"] = o
+    o += 8 * ng
+    f["bias_len"] = o
+    return f
+
+
+def corruptions(buf: bytes):
+    """Deterministic corrupt variants of a checkpoint: name -> bytes."""
+    import struct
+    f = field_offsets(buf)
+    out = {}
+
+    def put(name, off, data):
+        b = bytearray(buf)
+        b[off:off + len(data)] = data
+        out[name] = bytes(b)
+
+    put("bad_magic", 0, b"MLRB")
+    put("bad_version", 4, struct.pack("<H", 2))
+    put("bits5", f["bits"], bytes([5]))
+    put("group7", f["group"], struct.pack("<I", 7))
+    put("zero_rows", f["rows"], struct.pack("<I", 0))
+    put("word_count", f["n_words"], struct.pack("<I", struct.unpack_from("<I", buf, f["n_words"])[0] + 1))
+    put("neg_scale", f["scales"], struct.pack("<f", -1.0))
+    put("bias_len", f["bias_len"], struct.pack("<I", 1))
+    put("n_layers_big", f["n_layers"], struct.pack("<I", 7))
+    out["trailing"] = buf + b"\0"
+    for cut in (3, 5, 9, f["layer0"] + 2, f["words"] + 6, f["scales"] + 3, len(buf) - 1):
+        out[f"trunc{cut}"] = buf[:cut]
+    # nonzero trailing bits: set the top bit of the last packed word when it is padding
+    lw = struct.unpack_from("<I", buf, f["last_word"])[0]
+    put("trailing_bits", f["last_word"], struct.pack("<I", lw | 0x80000000))
+    return out
+
+
+def checkpoint_cases():
+    import ctypes as C
+    import json
+    L = Ref.get()
+    L.ref_make_checkpoint.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64, C.c_uint64]
+    L.ref_checkpoint_probe.argtypes = [C.c_char_p] + [C.POINTER(C.c_uint64)] * 2 + [
+        C.POINTER(C.c_int), C.POINTER(C.c_uint64)]
+
+    def probe(path):
+        fh, zh, k, o = C.c_uint64(), C.c_uint64(), C.c_int(), C.c_uint64()
+        rc = L.ref_checkpoint_probe(path.encode(), fh, zh, k, o)
+        return {"status": rc, "file_hash": fh.value if rc == 0 else None,
+                "frozen_hash": zh.value if rc == 0 else None, "format_kind": k.value,
+                "offset": o.value if rc else None}
+
+    expect = {}
+    tmp = os.path.join(HERE, "_tmp.mlra")
+    for name, task, bits, seed, group in CKPTS:
+        path = os.path.join(HERE, name)
+        rc = L.ref_make_checkpoint(path.encode(), task.encode(), bits, seed, group)
+        assert rc == 0, L.ref_last_error()
+        expect[name] = probe(path)
+        buf = open(path, "rb").read()
+        for cname, data in corruptions(buf).items():
+            with open(tmp, "wb") as fh:
+                fh.write(data)
+            expect[f"{name}:{cname}"] = probe(tmp)
+    os.remove(tmp)
+    with open(os.path.join(HERE, "checkpoints.json"), "w") as fh:
+        json.dump(expect, fh, indent=1, sort_keys=True)
+    # the reference's pinned digests (acceptance.cpp:462-463, test_checkpoint.cpp:31-32)
+    assert expect["golden.mlra"]["file_hash"] == 0xb48207d130703ee4
+    assert expect["golden.mlra"]["frozen_hash"] == 0xa3d66a9e729158ff
+
+
 def main():
     if not Ref.available():
         raise SystemExit("oracle/_ref/libmlra_ref.so missing: run `make -C oracle` with /root/reference present")
@@ -134,8 +240,9 @@ def main():
                         gaussian_seed7=Ref.gaussian(7, 3, 5),
                         gaussian_seed8_scaled=Ref.gaussian(8, 4, 4, 0.5, 0.02),
                         mix_seed_11_ada9=np.array([meta["mix_seed_11_ada9"]], np.uint64))
+    checkpoint_cases()
     for f in sorted(os.listdir(HERE)):
-        if f.endswith(".npz"):
+        if f.endswith((".npz", ".mlra", ".json")):
             print(f, os.path.getsize(os.path.join(HERE, f)))
 
 
