@@ -64,6 +64,9 @@ struct FormatError : Error {
 struct CudaError : Error {
   using Error::Error;
 };
+struct IoError : Error {
+  using Error::Error;
+};
 
 inline void check(mlra_status st) {
   if (st == MLRA_OK) return;
@@ -74,7 +77,13 @@ inline void check(mlra_status st) {
     case MLRA_ERR_RANGE: throw RangeError(m);
     case MLRA_ERR_CONTRACT: throw ContractError(m);
     case MLRA_ERR_NUMERIC: throw NumericError(m);
-    case MLRA_ERR_FORMAT: throw FormatError(FormatError::Kind::BadField, 0, m);
+    case MLRA_ERR_FORMAT: {
+      uint64_t off = 0;
+      const int k = mlra_last_format_error(&off);
+      throw FormatError(k >= 0 ? static_cast<FormatError::Kind>(k) : FormatError::Kind::BadField,
+                        static_cast<std::size_t>(off), m);
+    }
+    case MLRA_ERR_IO: throw IoError(m);
     default: throw CudaError(m);
   }
 }
@@ -165,6 +174,10 @@ class DeviceQuantizedMatrix {
                               q.scales.empty() ? &kZeroF : q.scales.data(),
                               q.zeros.empty() ? &kZeroF : q.zeros.data(), q.scales.size(), st, &h_));
   }
+  // Adopts a handle from another constructor of the C ABI (mlra_cb2_create,
+  // mlra_qweight_create_opaque, mlra_checkpoint_upload).
+  DeviceQuantizedMatrix(mlra_qweight* h, std::size_t rows, std::size_t cols)
+      : h_(h), rows_(rows), cols_(cols) {}
   ~DeviceQuantizedMatrix() { mlra_qweight_destroy(h_); }
   DeviceQuantizedMatrix(const DeviceQuantizedMatrix&) = delete;
   DeviceQuantizedMatrix& operator=(const DeviceQuantizedMatrix&) = delete;
@@ -198,6 +211,67 @@ inline std::vector<double> dequantize_row(const DeviceQuantizedMatrix& q, std::s
   return std::vector<double>(h.begin(), h.end());
 }
 
+// ----------------------------------------------------------------- quantize.hpp:91-106
+// The black-box Quantizer plugin in device form (include/mlra.h mlra_hook):
+// the reference's override point is Quantizer::matvec / matvec_transposed;
+// here a plugin overrides materialize_tile(), the dequantization of one tile
+// of Ŵ into device memory on a stream, and the library runs its own tcgen05
+// GEMM over hook-materialized slabs under QuantizerMatvec.
+class Quantizer {
+ public:
+  virtual ~Quantizer() = default;
+  virtual std::string_view name() const = 0;
+  virtual mlra_status materialize_tile(const mlra_qweight* q, int64_t row0, int64_t nrows,
+                                       int64_t col0, int64_t ncols, void* out, mlra_dtype dtype,
+                                       int64_t ld, cudaStream_t stream) const = 0;
+  // The C-ABI hook (valid while this object lives).
+  const mlra_hook* hook() const {
+    name_ = std::string(name());
+    hook_.name = name_.c_str();
+    hook_.state = const_cast<Quantizer*>(this);
+    hook_.materialize = [](void* st, const mlra_qweight* q, int64_t r0, int64_t nr, int64_t c0,
+                           int64_t nc, void* out, mlra_dtype dt, int64_t ld,
+                           void* stream) -> mlra_status {
+      try {
+        return static_cast<const Quantizer*>(st)->materialize_tile(
+            q, r0, nr, c0, nc, out, dt, ld, static_cast<cudaStream_t>(stream));
+      } catch (...) {
+        return MLRA_ERR_CONTRACT;  // exceptions do not cross the C ABI
+      }
+    };
+    return &hook_;
+  }
+
+ private:
+  mutable mlra_hook hook_{};
+  mutable std::string name_;
+};
+
+// The reference test plugin (test_lowprec.cpp:354-377): twice the default product.
+class DoublingQuantizer final : public Quantizer {
+ public:
+  std::string_view name() const override { return "doubling"; }
+  mlra_status materialize_tile(const mlra_qweight* q, int64_t r0, int64_t nr, int64_t c0,
+                               int64_t nc, void* out, mlra_dtype dt, int64_t ld,
+                               cudaStream_t st) const override;
+};
+
+// Built-in non-affine plugin "cb2" (mlra_cb2_create): 2 bits per weight as one
+// u16 code per 8 entries (8-bit codebook index + 8 sign bits), f32 scale per
+// (row, group). Returns the frozen matrix, dequantized only through its hook.
+inline std::shared_ptr<const DeviceQuantizedMatrix> upload_cb2(
+    std::size_t rows, std::size_t cols, std::size_t group, const std::vector<std::uint16_t>& codes,
+    const std::vector<float>& codebook, const std::vector<float>& scales, cudaStream_t st = nullptr) {
+  if (codes.size() != rows * (cols / 8) || codebook.size() != 256 * 8 ||
+      (group && scales.size() != rows * (cols / group)))
+    throw FormatError(FormatError::Kind::BadField, 0, "cb2: buffer sizes do not match the shape");
+  mlra_qweight* h = nullptr;
+  check(mlra_cb2_create(static_cast<int64_t>(rows), static_cast<int64_t>(cols),
+                        static_cast<int64_t>(group), codes.data(), codebook.data(), scales.data(),
+                        st, &h));
+  return std::make_shared<const DeviceQuantizedMatrix>(h, rows, cols);
+}
+
 // ----------------------------------------------------------------- lowprec_linear.hpp:29-112
 enum class MaterializationStrategy { WeightMaterialize = MLRA_WEIGHT, RowMaterialize = MLRA_ROW,
                                      QuantizerMatvec = MLRA_MATVEC };
@@ -222,6 +296,7 @@ struct LpLinearContext {
   std::shared_ptr<const DeviceQuantizedMatrix> q;
   MaterializationStrategy strategy = MaterializationStrategy::RowMaterialize;
   std::string layer_name;
+  std::shared_ptr<const Quantizer> matvec_hook;  // optional, QuantizerMatvec only
   // bytes the strategy materializes per pass (MemoryLedger charge)
   std::size_t ledger_bytes() const {
     return q ? static_cast<std::size_t>(mlra_ledger_bytes(q->handle(), static_cast<mlra_strategy>(strategy)))
@@ -252,7 +327,8 @@ inline HostMatrix lp_forward(const LpLinearContext& ctx, const HostMatrix& x) {
   DeviceBuffer<__nv_bfloat16> dx(x.rows * x.cols);
   DeviceBuffer<float> dy(x.rows * ctx.q->rows());
   if (x.rows) dx.upload(to_bf16(x.data).data());
-  check(mlra_lp_forward(q, static_cast<mlra_strategy>(ctx.strategy), dx.get(),
+  check(mlra_lp_forward_ex(q, static_cast<mlra_strategy>(ctx.strategy),
+                           ctx.matvec_hook ? ctx.matvec_hook->hook() : nullptr, dx.get(),
                         static_cast<int64_t>(x.cols), static_cast<int64_t>(x.rows), dy.get(), MLRA_F32,
                         static_cast<int64_t>(ctx.q->rows()), nullptr));
   return detail::download_f32(dy, x.rows, ctx.q->rows());
@@ -267,7 +343,8 @@ inline HostMatrix lp_backward(const LpLinearContext& ctx, const HostMatrix& g) {
   DeviceBuffer<__nv_bfloat16> dg(g.rows * g.cols);
   DeviceBuffer<float> dx(g.rows * ctx.q->cols());
   if (g.rows) dg.upload(to_bf16(g.data).data());
-  check(mlra_lp_backward(q, static_cast<mlra_strategy>(ctx.strategy), dg.get(),
+  check(mlra_lp_backward_ex(q, static_cast<mlra_strategy>(ctx.strategy),
+                            ctx.matvec_hook ? ctx.matvec_hook->hook() : nullptr, dg.get(),
                          static_cast<int64_t>(g.cols), static_cast<int64_t>(g.rows), dx.get(), MLRA_F32,
                          static_cast<int64_t>(ctx.q->cols()), nullptr));
   return detail::download_f32(dx, g.rows, ctx.q->cols());
@@ -294,6 +371,7 @@ struct ModuLoraLayer {
   bool bias_trainable = false;
   HostMatrix grad_bias;
   MaterializationStrategy strategy = MaterializationStrategy::RowMaterialize;
+  std::shared_ptr<const Quantizer> matvec_hook;  // lora.hpp:47
   std::size_t d_in() const { return weights->cols(); }
   std::size_t d_out() const { return weights->rows(); }
 };
@@ -349,6 +427,7 @@ inline mlra_lora c_layer(const ModuLoraLayer& L) {
   c.a = L.adapter.a.get();
   c.b = L.adapter.b.get();
   c.bias = L.bias.get();
+  c.hook = L.matvec_hook ? L.matvec_hook->hook() : nullptr;
   return c;
 }
 
@@ -400,5 +479,118 @@ inline std::pair<HostMatrix, HostMatrix> grads_of_adapter(const ModuLoraLayer& L
   if (!L.adapter.has_grad) throw ContractError("grads_of_adapter: called before backward()");
   return {L.adapter.grad_a, L.adapter.grad_b};
 }
+
+inline mlra_status DoublingQuantizer::materialize_tile(const mlra_qweight* q, int64_t r0,
+                                                     int64_t nr, int64_t c0, int64_t nc, void* out,
+                                                     mlra_dtype dt, int64_t ld,
+                                                     cudaStream_t st) const {
+  // default dequantization, then x2 on the host side of a round trip: a plugin
+  // may do anything; this one stays simple (exact: x2 is exact in bf16 / f32)
+  if (mlra_status s = mlra_materialize_tile(q, r0, nr, c0, nc, out, dt, ld, st)) return s;
+  const std::size_t es = dt == MLRA_F32 ? 4 : 2;
+  std::vector<unsigned char> h(static_cast<std::size_t>(nr * ld) * es);
+  if (cudaMemcpyAsync(h.data(), out, h.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return MLRA_ERR_CUDA;
+  for (int64_t i = 0; i < nr; ++i)
+    for (int64_t j = 0; j < nc; ++j) {
+      const std::size_t k = static_cast<std::size_t>(i * ld + j);
+      if (dt == MLRA_F32) {
+        float* f = reinterpret_cast<float*>(h.data()) + k;
+        *f *= 2.0f;
+      } else {
+        __nv_bfloat16* b = reinterpret_cast<__nv_bfloat16*>(h.data()) + k;
+        *b = __float2bfloat16_rn(2.0f * __bfloat162float(*b));
+      }
+    }
+  if (cudaMemcpyAsync(out, h.data(), h.size(), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return MLRA_ERR_CUDA;
+  return MLRA_OK;
+}
+
+// ----------------------------------------------------------------- train.hpp:51-70
+// AdamW (train.cpp:75-134) over device f64 parameters: masters and moments stay
+// in HBM, one fused launch per step, bit-identical to the reference's f64
+// arithmetic given the same gradients. NumericError (naming the parameter)
+// on a non-finite gradient, with the earlier parameters updated.
+class AdamW {
+ public:
+  AdamW(double beta1, double beta2, double eps, double weight_decay)
+      : cfg_{beta1, beta2, eps, weight_decay} {}
+  // params: device f64 [n] (flat bucket, updated in place); grads: device f32 or
+  // f64 [n]; sizes/names: the parameter list laid out back to back.
+  void step(double* params, const void* grads, mlra_dtype grad_dtype,
+            const std::vector<std::size_t>& sizes, const std::vector<std::string>& names,
+            std::size_t step_index, double lr, float* params_f32 = nullptr,
+            cudaStream_t st = nullptr) {
+    if (sizes.size() != names.size()) throw ContractError("adamw: params/names size mismatch");
+    std::size_t n = 0;
+    std::vector<int64_t> offs{0};
+    for (std::size_t s : sizes) offs.push_back(static_cast<int64_t>(n += s));
+    if (m_.size() == 0) {
+      sizes_ = sizes;
+      m_ = DeviceBuffer<double>(n);
+      v_ = DeviceBuffer<double>(n);
+      cuda_check(cudaMemsetAsync(m_.get(), 0, n * 8, st), "cudaMemsetAsync");
+      cuda_check(cudaMemsetAsync(v_.get(), 0, n * 8, st), "cudaMemsetAsync");
+    } else if (sizes != sizes_) {
+      throw ContractError("adamw: parameter list changed between steps");
+    }
+    const mlra_status s = mlra_adamw_step(&cfg_, static_cast<int64_t>(step_index), lr,
+                                          static_cast<int64_t>(sizes.size()), offs.data(), params,
+                                          m_.get(), v_.get(), grads, grad_dtype, params_f32,
+                                          nullptr, st);
+    if (s == MLRA_ERR_NUMERIC) {
+      const std::string m = mlra_last_error();
+      const std::size_t i = std::stoul(m.substr(m.find('#') + 1));
+      throw NumericError("adamw: non-finite gradient for parameter '" + names[i] + "' at step " +
+                         std::to_string(step_index));
+    }
+    check(s);
+  }
+
+ private:
+  mlra_adamw cfg_;
+  DeviceBuffer<double> m_, v_;
+  std::vector<std::size_t> sizes_;
+};
+
+// ----------------------------------------------------------------- checkpoint.hpp:36-67
+// The .mlra format -> device: parse + validate like load_model (FormatError
+// kinds/offsets, IoError), upload layers verbatim, save byte-identically.
+class Checkpoint {
+ public:
+  explicit Checkpoint(const std::string& path) { check(mlra_checkpoint_load(path.c_str(), &h_)); }
+  ~Checkpoint() { mlra_checkpoint_free(h_); }
+  Checkpoint(const Checkpoint&) = delete;
+  Checkpoint& operator=(const Checkpoint&) = delete;
+  std::size_t size() const { return static_cast<std::size_t>(mlra_checkpoint_layer_count(h_)); }
+  mlra_ckpt_layer layer(std::size_t i) const {
+    mlra_ckpt_layer o{};
+    check(mlra_checkpoint_layer(h_, static_cast<int64_t>(i), &o));
+    return o;
+  }
+  std::uint64_t frozen_state_hash() const { return mlra_checkpoint_frozen_hash(h_); }
+  std::uint64_t file_hash() const { return mlra_checkpoint_file_hash(h_); }
+  std::shared_ptr<const DeviceQuantizedMatrix> upload(std::size_t i, cudaStream_t st = nullptr) const {
+    const mlra_ckpt_layer L = layer(i);
+    mlra_qweight* q = nullptr;
+    check(mlra_checkpoint_upload(h_, static_cast<int64_t>(i), st, &q));
+    return std::make_shared<const DeviceQuantizedMatrix>(q, static_cast<std::size_t>(L.rows),
+                                                         static_cast<std::size_t>(L.cols));
+  }
+  void set_adapter(std::size_t i, const HostMatrix& a, const HostMatrix& b) {
+    const mlra_ckpt_layer L = layer(i);
+    if (a.rows != static_cast<std::size_t>(L.rows) || a.cols != static_cast<std::size_t>(L.rank) ||
+        b.rows != static_cast<std::size_t>(L.cols) || b.cols != static_cast<std::size_t>(L.rank))
+      throw DimensionError("checkpoint: adapter shape mismatch");
+    check(mlra_checkpoint_set_adapter(h_, static_cast<int64_t>(i), a.data.data(), b.data.data()));
+  }
+  void save(const std::string& path) const { check(mlra_checkpoint_save(h_, path.c_str())); }
+
+ private:
+  mlra_checkpoint* h_ = nullptr;
+};
 
 }  // namespace modulora_b200

@@ -8,41 +8,27 @@
 //     dB = s·Xᵀ·dYA   — dB = xᵀ·d(xb)                  autodiff.cpp:153-155
 //     dbias = Σ_t dY  — bias_add backward (a ones column of V)  autodiff.cpp:183-191
 //
-// These are HBM-bound (r flop/B): each CTA streams 64-row activation tiles
-// through a cp.async double buffer and runs bf16 mma.sync m16n8k16 against the
-// rank-r factor. The fp32 factor is split into bf16 hi + lo parts (two MMAs),
+// These are HBM-bound (r flop/B): each CTA streams 64 x 64 activation chunks
+// through a TMA ring and runs bf16 mma.sync m16n8k16 against the rank-r factor. The fp32 factor is split into bf16 hi + lo parts (two MMAs),
 // so the product keeps ~16 mantissa bits (fp32-grade
 // intermediates); activations are exact bf16. Split-K / split-token CTAs
 // combine with fp32 atomics.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace mlra {
 
 namespace {
 
-constexpr int TILE = 64;      // rows (tokens or n) per CTA tile, and K chunk
-constexpr int PADW = 72;      // padded smem row (bf16): conflict-free ldmatrix
-constexpr int NS = 4;         // cp.async pipeline depth (chunks in flight per CTA)
-constexpr int thin_smem_bytes(int nt) { return (NS * TILE * PADW + NS * 2 * 8 * nt * PADW) * 2; }
-
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-               "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
+constexpr int TILE = 64;      // rows (tokens or n) per unit, and reduction chunk
 __device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -62,178 +48,197 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// Load a 64-row x 64-col bf16 tile (rows r0.., cols c0..) of a row-major
-// matrix [rows x cols] (leading dim ld) into padded smem; zero-fill outside.
-__device__ __forceinline__ void load_tile(uint32_t dst, const __nv_bfloat16* src, int64_t ld,
-                                          int64_t rows, int64_t cols, int64_t r0, int64_t c0) {
-  for (int i = threadIdx.x; i < TILE * 8; i += blockDim.x) {
-    const int rr = i >> 3, cc = (i & 7) * 8;
-    const int64_t r = r0 + rr, c = c0 + cc;
-    int bytes = 0;
-    const __nv_bfloat16* p = src;
-    if (r < rows && c < cols) {
-      const int64_t rem = cols - c;
-      bytes = rem >= 8 ? 16 : static_cast<int>(rem) * 2;
-      p = src + r * ld + c;
-    }
-    cp_async16(dst + (rr * PADW + cc) * 2, p, bytes);
-  }
-}
+// Work decomposition (both kernels): the (output tile x reduction chunk) space
+// is flattened tile-major into U units of 64 x 64 activations and cut into
+// gridDim.x equal contiguous ranges — one resident wave, every CTA streaming
+// the same number of chunks through one continuous pipeline. A CTA flushes its
+// fp32 partials (atomics) whenever its range leaves an output tile.
+//
+// Operand staging is TMA (cp.async.bulk.tensor, SWIZZLE_128B): one elected
+// thread issues the activation chunk and the hi+lo factor chunk per unit into
+// an NS-deep ring signalled by mbarrier complete_tx, so the warps spend their
+// issue slots on ldmatrix + mma only. Reads use the 128-B swizzle: 16-B chunk
+// c of row r sits at r*128 + ((c ^ (r & 7)) << 4).
 
-// Load factor rows [0, 8*NT) x cols [c0, c0+64) of a [8*NT x ld] bf16 matrix
-// (hi and lo planes) into padded smem.
+constexpr int TNS = 6;  // TMA ring depth (units in flight per CTA)
+
 template <int NT>
-__device__ __forceinline__ void load_factor(uint32_t dst, const __nv_bfloat16* hi,
-                                            const __nv_bfloat16* lo, int64_t ld, int64_t c0) {
-  constexpr int ROWS = 8 * NT;
-  for (int i = threadIdx.x; i < 2 * ROWS * 8; i += blockDim.x) {
-    const int plane = i / (ROWS * 8), j = i % (ROWS * 8);
-    const int rr = j >> 3, cc = (j & 7) * 8;
-    const __nv_bfloat16* p = (plane ? lo : hi) + rr * ld + c0 + cc;
-    cp_async16(dst + ((plane * ROWS + rr) * PADW + cc) * 2, p, 16);
-  }
+struct ThinSmem {
+  static constexpr int ROWS = 8 * NT;
+  static constexpr int ACT = TILE * 128;        // 64 x 64 bf16
+  static constexpr int FAC = 2 * ROWS * 128;    // hi + lo planes, 64 columns
+  static constexpr int STAGE = ACT + FAC;       // multiple of 1024 when NT is even
+  static constexpr int STAGE_AL = (STAGE + 1023) / 1024 * 1024;
+  static constexpr int BYTES = 1024 + TNS * STAGE_AL + 64;  // + alignment slack + barriers
+};
+
+__device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
+  return base + row * 128 + ((chunk ^ (row & 7)) << 4);
 }
 
-// out[t, j] (+)= Σ_k act[t, k] · Wt[j, k]   (Wt = W transposed, hi/lo bf16, [8NT x kpad])
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// out[t, j] (+)= Σ_k act[t, k] · Wt[j, k]   (Wt = W transposed, hi/lo bf16 planes)
 template <int NT>
 __global__ void __launch_bounds__(128)
-    k_rowmma(const __nv_bfloat16* __restrict__ act, int64_t lda, int64_t m, int64_t kd,
-             const __nv_bfloat16* __restrict__ wt_hi, const __nv_bfloat16* __restrict__ wt_lo,
-             int64_t ldw, int64_t k_per_split, float* __restrict__ out, int64_t ldo, int rc) {
-  constexpr int ROWS = 8 * NT;
-  extern __shared__ __align__(16) __nv_bfloat16 thin_smem[];
-  __nv_bfloat16* const sa0 = thin_smem;                      // NS act tiles
-  __nv_bfloat16* const sw0 = thin_smem + NS * TILE * PADW;   // NS factor tiles (hi+lo)
+    k_rowmma(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap fac_map,
+             int64_t m, int kchunks, int units, float* __restrict__ out, int64_t ldo, int rc) {
+  using L = ThinSmem<NT>;
+  constexpr int ROWS = L::ROWS;
+  extern __shared__ __align__(16) unsigned char thin_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(thin_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + TNS * L::STAGE_AL);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * TILE;
-  const int64_t ks = static_cast<int64_t>(blockIdx.y) * k_per_split;
-  const int64_t ke = ks + k_per_split < kd ? ks + k_per_split : kd;
-  const int nch = static_cast<int>((ke - ks + TILE - 1) / TILE);
+  const int u0 = static_cast<int>(static_cast<int64_t>(blockIdx.x) * units / gridDim.x);
+  const int u1 = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * units / gridDim.x);
+  auto issue = [&](int u, int slot) {
+    const int tile = u / kchunks, ch = u - tile * kchunks;
+    unsigned char* st = sm + slot * L::STAGE_AL;
+    mbar_arrive_expect_tx(&full[slot], L::STAGE);
+    tma_load_2d(st, &act_map, &full[slot], ch * TILE, tile * TILE);
+    tma_load_2d(st + L::ACT, &fac_map, &full[slot], ch * TILE, 0);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TNS; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int c = 0; c < TNS - 1; ++c)
+      if (u0 + c < u1) issue(u0 + c, c);
+  }
+  __syncthreads();
   float acc[NT][4];
 #pragma unroll
   for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
-  for (int c = 0; c < NS - 1; ++c) {
-    if (c < nch) {
-      load_tile(su32(sa0 + c * TILE * PADW), act, lda, m, ke, t0, ks + c * TILE);
-      load_factor<NT>(su32(sw0 + c * 2 * ROWS * PADW), wt_hi, wt_lo, ldw, ks + c * TILE);
+  const int arow = warp * 16 + (lane & 15);
+  for (int u = u0; u < u1; ++u) {
+    const int i = u - u0, b = i % TNS;
+    if (threadIdx.x == 0 && u + TNS - 1 < u1) {
+      fence_proxy_async_smem();  // the slot's last generic reads (iteration i-1) before TMA
+      issue(u + TNS - 1, (i + TNS - 1) % TNS);
     }
-    cp_commit();
-  }
-  for (int c = 0; c < nch; ++c) {
-    const int pf = c + NS - 1, b = c % NS;
-    if (pf < nch) {
-      load_tile(su32(sa0 + (pf % NS) * TILE * PADW), act, lda, m, ke, t0, ks + pf * TILE);
-      load_factor<NT>(su32(sw0 + (pf % NS) * 2 * ROWS * PADW), wt_hi, wt_lo, ldw, ks + pf * TILE);
-    }
-    cp_commit();
-    cp_wait<NS - 1>();
-    __syncthreads();
-    const uint32_t abase =
-        su32(sa0 + b * TILE * PADW) + ((warp * 16 + (lane & 15)) * PADW + (lane >> 4) * 8) * 2;
-    const __nv_bfloat16* wsm = sw0 + b * 2 * ROWS * PADW;
+    mbar_wait(&full[b], static_cast<uint32_t>((i / TNS) & 1));
+    const uint32_t abase = smem_u32(sm + b * L::STAGE_AL);
+    const uint32_t fbase = abase + L::ACT;
 #pragma unroll
     for (int k16 = 0; k16 < 4; ++k16) {
       uint32_t a[4];
-      ldsm_x4(abase + k16 * 32, a);
+      ldsm_x4(swz(abase, arow, k16 * 2 + (lane >> 4)), a);
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
-        const __nv_bfloat16* wh = wsm + (n * 8 + g) * PADW + k16 * 16 + 2 * tq;
-        const __nv_bfloat16* wl = wh + ROWS * PADW;
-        mma_bf16(acc[n], a, *reinterpret_cast<const uint32_t*>(wh),
-                 *reinterpret_cast<const uint32_t*>(wh + 8));
-        mma_bf16(acc[n], a, *reinterpret_cast<const uint32_t*>(wl),
-                 *reinterpret_cast<const uint32_t*>(wl + 8));
+        const int rh = n * 8 + g, rl = rh + ROWS;
+        const uint32_t h0 = lds_u32(swz(fbase, rh, k16 * 2) + 4 * tq);
+        const uint32_t h1 = lds_u32(swz(fbase, rh, k16 * 2 + 1) + 4 * tq);
+        const uint32_t l0 = lds_u32(swz(fbase, rl, k16 * 2) + 4 * tq);
+        const uint32_t l1 = lds_u32(swz(fbase, rl, k16 * 2 + 1) + 4 * tq);
+        mma_bf16(acc[n], a, h0, h1);
+        mma_bf16(acc[n], a, l0, l1);
       }
     }
     __syncthreads();
-  }
-  const int64_t ta = t0 + warp * 16 + g, tb = ta + 8;
+    const int tile = u / kchunks;
+    if (u + 1 == u1 || (u + 1) / kchunks != tile) {  // leaving this token tile: flush
+      const int64_t ta = static_cast<int64_t>(tile) * TILE + warp * 16 + g, tb = ta + 8;
 #pragma unroll
-  for (int n = 0; n < NT; ++n) {
-    const int j = n * 8 + 2 * tq;
-    if (ta < m) {
-      if (j < rc) atomicAdd(out + ta * ldo + j, acc[n][0]);
-      if (j + 1 < rc) atomicAdd(out + ta * ldo + j + 1, acc[n][1]);
-    }
-    if (tb < m) {
-      if (j < rc) atomicAdd(out + tb * ldo + j, acc[n][2]);
-      if (j + 1 < rc) atomicAdd(out + tb * ldo + j + 1, acc[n][3]);
+      for (int n = 0; n < NT; ++n) {
+        const int j = n * 8 + 2 * tq;
+        if (ta < m) {
+          if (j < rc) atomicAdd(out + ta * ldo + j, acc[n][0]);
+          if (j + 1 < rc) atomicAdd(out + ta * ldo + j + 1, acc[n][1]);
+        }
+        if (tb < m) {
+          if (j < rc) atomicAdd(out + tb * ldo + j, acc[n][2]);
+          if (j + 1 < rc) atomicAdd(out + tb * ldo + j + 1, acc[n][3]);
+        }
+        acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
+      }
     }
   }
 }
 
-// out[n, j] += scale · Σ_t act[t, n] · Vt[j, t]   (Vt = V transposed, hi/lo bf16, [8NT x ldv])
+// out[n, j] += scale · Σ_t act[t, n] · Vt[j, t]   (Vt = V transposed, hi/lo bf16 planes)
 // Columns j >= rc of the product go to colsum (the ones column) when j == rc.
 template <int NT>
 __global__ void __launch_bounds__(128)
-    k_colmma(const __nv_bfloat16* __restrict__ act, int64_t lda, int64_t m, int64_t nd,
-             const __nv_bfloat16* __restrict__ vt_hi, const __nv_bfloat16* __restrict__ vt_lo,
-             int64_t ldv, int64_t t_per_split, float scale, float* __restrict__ out, int64_t ldo,
-             int rc, float* __restrict__ colsum) {
-  constexpr int ROWS = 8 * NT;
-  extern __shared__ __align__(16) __nv_bfloat16 thin_smem[];
-  __nv_bfloat16* const sa0 = thin_smem;
-  __nv_bfloat16* const sv0 = thin_smem + NS * TILE * PADW;
+    k_colmma(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap fac_map,
+             int64_t nd, int tchunks, int units, float scale, float* __restrict__ out,
+             int64_t ldo, int rc, float* __restrict__ colsum) {
+  using L = ThinSmem<NT>;
+  constexpr int ROWS = L::ROWS;
+  extern __shared__ __align__(16) unsigned char thin_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(thin_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + TNS * L::STAGE_AL);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
-  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * TILE;
-  const int64_t ts = static_cast<int64_t>(blockIdx.y) * t_per_split;
-  const int64_t te = ts + t_per_split < m ? ts + t_per_split : m;
-  const int nch = static_cast<int>((te - ts + TILE - 1) / TILE);
+  const int u0 = static_cast<int>(static_cast<int64_t>(blockIdx.x) * units / gridDim.x);
+  const int u1 = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * units / gridDim.x);
+  auto issue = [&](int u, int slot) {
+    const int nt = u / tchunks, ch = u - nt * tchunks;
+    unsigned char* st = sm + slot * L::STAGE_AL;
+    mbar_arrive_expect_tx(&full[slot], L::STAGE);
+    tma_load_2d(st, &act_map, &full[slot], nt * TILE, ch * TILE);
+    tma_load_2d(st + L::ACT, &fac_map, &full[slot], ch * TILE, 0);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TNS; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int c = 0; c < TNS - 1; ++c)
+      if (u0 + c < u1) issue(u0 + c, c);
+  }
+  __syncthreads();
   float acc[NT][4];
 #pragma unroll
   for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
-  for (int c = 0; c < NS - 1; ++c) {
-    if (c < nch) {
-      load_tile(su32(sa0 + c * TILE * PADW), act, lda, te, nd, ts + c * TILE, n0);
-      load_factor<NT>(su32(sv0 + c * 2 * ROWS * PADW), vt_hi, vt_lo, ldv, ts + c * TILE);
+  // A fragment (M = n, K = t) from the [t][n] tile via transposed ldmatrix:
+  // lane l addresses row t = (l & 7) + 8*(l >> 4) (+16 per k16), n chunk warp*2 + ((l >> 3) & 1)
+  const int trow = (lane & 7) + ((lane >> 4) << 3), nchunk = warp * 2 + ((lane >> 3) & 1);
+  for (int u = u0; u < u1; ++u) {
+    const int i = u - u0, b = i % TNS;
+    if (threadIdx.x == 0 && u + TNS - 1 < u1) {
+      fence_proxy_async_smem();
+      issue(u + TNS - 1, (i + TNS - 1) % TNS);
     }
-    cp_commit();
-  }
-  for (int c = 0; c < nch; ++c) {
-    const int pf = c + NS - 1, b = c % NS;
-    if (pf < nch) {
-      load_tile(su32(sa0 + (pf % NS) * TILE * PADW), act, lda, te, nd, ts + pf * TILE, n0);
-      load_factor<NT>(su32(sv0 + (pf % NS) * 2 * ROWS * PADW), vt_hi, vt_lo, ldv, ts + pf * TILE);
-    }
-    cp_commit();
-    cp_wait<NS - 1>();
-    __syncthreads();
-    // A fragment (M = n, K = t) from the [t][n] tile via transposed ldmatrix:
-    // lane l addresses row t = (l & 7) + 8*(l >> 4), col n = warp*16 + 8*((l >> 3) & 1)
-    const uint32_t abase = su32(sa0 + b * TILE * PADW) +
-                           (((lane & 7) + ((lane >> 4) << 3)) * PADW + warp * 16 +
-                            ((lane >> 3) & 1) * 8) * 2;
-    const __nv_bfloat16* vsm = sv0 + b * 2 * ROWS * PADW;
+    mbar_wait(&full[b], static_cast<uint32_t>((i / TNS) & 1));
+    const uint32_t abase = smem_u32(sm + b * L::STAGE_AL);
+    const uint32_t fbase = abase + L::ACT;
 #pragma unroll
     for (int k16 = 0; k16 < 4; ++k16) {
       uint32_t a[4];
-      ldsm_x4_t(abase + k16 * 16 * PADW * 2, a);
+      ldsm_x4_t(swz(abase, trow + 16 * k16, nchunk), a);
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
-        const __nv_bfloat16* vh = vsm + (n * 8 + g) * PADW + k16 * 16 + 2 * tq;
-        const __nv_bfloat16* vl = vh + ROWS * PADW;
-        mma_bf16(acc[n], a, *reinterpret_cast<const uint32_t*>(vh),
-                 *reinterpret_cast<const uint32_t*>(vh + 8));
-        mma_bf16(acc[n], a, *reinterpret_cast<const uint32_t*>(vl),
-                 *reinterpret_cast<const uint32_t*>(vl + 8));
+        const int rh = n * 8 + g, rl = rh + ROWS;
+        const uint32_t h0 = lds_u32(swz(fbase, rh, k16 * 2) + 4 * tq);
+        const uint32_t h1 = lds_u32(swz(fbase, rh, k16 * 2 + 1) + 4 * tq);
+        const uint32_t l0 = lds_u32(swz(fbase, rl, k16 * 2) + 4 * tq);
+        const uint32_t l1 = lds_u32(swz(fbase, rl, k16 * 2 + 1) + 4 * tq);
+        mma_bf16(acc[n], a, h0, h1);
+        mma_bf16(acc[n], a, l0, l1);
       }
     }
     __syncthreads();
-  }
-  const int64_t na = n0 + warp * 16 + g, nb = na + 8;
+    const int nt = u / tchunks;
+    if (u + 1 == u1 || (u + 1) / tchunks != nt) {  // leaving this n tile: flush
+      const int64_t na = static_cast<int64_t>(nt) * TILE + warp * 16 + g, nb = na + 8;
 #pragma unroll
-  for (int n = 0; n < NT; ++n) {
+      for (int n = 0; n < NT; ++n) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = n * 8 + 2 * tq + h;
-      if (j < rc) {
-        if (na < nd) atomicAdd(out + na * ldo + j, scale * acc[n][h]);
-        if (nb < nd) atomicAdd(out + nb * ldo + j, scale * acc[n][2 + h]);
-      } else if (j == rc && colsum != nullptr) {
-        if (na < nd) atomicAdd(colsum + na, acc[n][h]);
-        if (nb < nd) atomicAdd(colsum + nb, acc[n][2 + h]);
+        for (int h = 0; h < 2; ++h) {
+          const int j = n * 8 + 2 * tq + h;
+          if (j < rc) {
+            if (na < nd) atomicAdd(out + na * ldo + j, scale * acc[n][h]);
+            if (nb < nd) atomicAdd(out + nb * ldo + j, scale * acc[n][2 + h]);
+          } else if (j == rc && colsum != nullptr) {
+            if (na < nd) atomicAdd(colsum + na, acc[n][h]);
+            if (nb < nd) atomicAdd(colsum + nb, acc[n][2 + h]);
+          }
+        }
+        acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
       }
     }
   }
@@ -296,24 +301,71 @@ int blocks_for(int64_t work) {
   return static_cast<int>(b < 1 ? 1 : b);
 }
 
+// One resident wave: CTAs = min(units, resident CTAs per SM x SMs).
+template <typename K>
+int wave_ctas(K kernel, int smem, int64_t units) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t cap = static_cast<int64_t>(per_sm) * sms();
+  return static_cast<int>(units < cap ? units : cap);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// bf16 [outer x inner] (row stride ld elements), box 64 x box_outer, SWIZZLE_128B
+cudaError_t thin_map(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ld,
+                     int box_outer) {
+  auto enc = encoder();
+  if (!enc || ld % 8 || reinterpret_cast<uintptr_t>(base) % 16) return cudaErrorInvalidValue;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int NT>
 cudaError_t rowmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
                       const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t ldw, float* out,
                       int64_t ldo, int64_t r, cudaStream_t st) {
+  constexpr int ROWS = 8 * NT;
   const int64_t tb = (m + TILE - 1) / TILE;
   const int64_t kchunks = (kd + TILE - 1) / TILE;
-  int64_t splits = (4 * sms() + tb - 1) / tb;
-  if (splits > kchunks) splits = kchunks;
-  if (splits < 1) splits = 1;
-  const int64_t kps = (kchunks + splits - 1) / splits * TILE;
-  splits = (kd + kps - 1) / kps;
-  dim3 grid(static_cast<unsigned>(tb), static_cast<unsigned>(splits));
-  const int smem = thin_smem_bytes(NT);
-  cudaError_t e = cudaFuncSetAttribute(k_rowmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int64_t units = tb * kchunks;
+  if (units <= 0) return cudaSuccess;
+  if (units > INT32_MAX || lo != hi + ROWS * ldw) return cudaErrorInvalidValue;
+  CUtensorMap am, fm;
+  cudaError_t e = thin_map(&am, act, kd, m, lda, TILE);
+  if (e == cudaSuccess) e = thin_map(&fm, hi, ldw, 2 * ROWS, ldw, 2 * ROWS);
   if (e != cudaSuccess) return e;
+  const int smem = ThinSmem<NT>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_rowmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ctas = wave_ctas(k_rowmma<NT>, smem, units);
   note_launch();
-  k_rowmma<NT><<<grid, 128, smem, st>>>(act, lda, m, kd, hi, lo, ldw, kps, out, ldo,
-                                        static_cast<int>(r));
+  k_rowmma<NT><<<ctas, 128, smem, st>>>(am, fm, m, static_cast<int>(kchunks),
+                                        static_cast<int>(units), out, ldo, static_cast<int>(r));
   return cudaGetLastError();
 }
 
@@ -321,19 +373,27 @@ template <int NT>
 cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t nd,
                       const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t ldv, float scale,
                       float* out, int64_t ldo, int64_t r, float* colsum, cudaStream_t st) {
+  constexpr int ROWS = 8 * NT;
   const int64_t nb = (nd + TILE - 1) / TILE;
   const int64_t tchunks = (m + TILE - 1) / TILE;
-  int64_t splits = (4 * sms() + nb - 1) / nb;
-  if (splits > tchunks) splits = tchunks;
-  if (splits < 1) splits = 1;
-  const int64_t tps = (tchunks + splits - 1) / splits * TILE;
-  splits = (m + tps - 1) / tps;
-  dim3 grid(static_cast<unsigned>(nb), static_cast<unsigned>(splits));
-  const int smem = thin_smem_bytes(NT);
-  cudaError_t e = cudaFuncSetAttribute(k_colmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int64_t units = nb * tchunks;
+  if (units <= 0) return cudaSuccess;
+  if (units > INT32_MAX || lo != hi + ROWS * ldv) return cudaErrorInvalidValue;
+  CUtensorMap am, fm;
+  cudaError_t e = thin_map(&am, act, nd, m, lda, TILE);
+  if (e == cudaSuccess) e = thin_map(&fm, hi, ldv, 2 * ROWS, ldv, 2 * ROWS);
   if (e != cudaSuccess) return e;
+  const int smem = ThinSmem<NT>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_colmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ctas = wave_ctas(k_colmma<NT>, smem, units);
   note_launch();
-  k_colmma<NT><<<grid, 128, smem, st>>>(act, lda, m, nd, hi, lo, ldv, tps, scale, out, ldo,
+  k_colmma<NT><<<ctas, 128, smem, st>>>(am, fm, nd, static_cast<int>(tchunks),
+                                        static_cast<int>(units), scale, out, ldo,
                                         static_cast<int>(r), colsum);
   return cudaGetLastError();
 }

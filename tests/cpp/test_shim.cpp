@@ -104,7 +104,8 @@ static double rel_fro(const HostMatrix& a, const HostMatrix& b) {
   return std::sqrt(num / (den > 0 ? den : 1.0));
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const std::string golden = argc > 1 ? argv[1] : "tests/golden";
   if (mlra_device_check() != MLRA_OK) {
     std::printf("SKIP: %s\n", mlra_last_error());
     return 0;
@@ -237,6 +238,78 @@ int main() {
     CHECK(throws<ContractError>([&] { lp_forward(empty, HostMatrix(2, 16)); }));
     CHECK(throws<ConfigError>([&] { init_adapter(16, 8, 0, 16.0, 1); }));
     CHECK(throws<ConfigError>([&] { init_adapter(16, 8, 2, 0.0, 1); }));
+  }
+  // --- the matvec hook is consulted under QuantizerMatvec only (test_lowprec.cpp:354-377)
+  {
+    auto dq = std::make_shared<const DeviceQuantizedMatrix>(random_q(40, 64, 4, 16, 33));
+    const HostMatrix x = randn(3, 64, 34), g = randn(3, 40, 35);
+    LpLinearContext plain{dq, MaterializationStrategy::QuantizerMatvec, "p"};
+    LpLinearContext hooked = plain;
+    hooked.matvec_hook = std::make_shared<DoublingQuantizer>();
+    const HostMatrix y0 = lp_forward(plain, x), y1 = lp_forward(hooked, x);
+    HostMatrix y2 = y0;
+    for (double& v : y2.data) v *= 2.0;
+    CHECK(rel_fro(y1, y2) <= 1e-6);
+    const HostMatrix d0 = lp_backward(plain, g), d1 = lp_backward(hooked, g);
+    HostMatrix d2 = d0;
+    for (double& v : d2.data) v *= 2.0;
+    CHECK(rel_fro(d1, d2) <= 1e-6);
+    LpLinearContext w0{dq, MaterializationStrategy::WeightMaterialize, "w"};
+    LpLinearContext w1 = w0;
+    w1.matvec_hook = hooked.matvec_hook;
+    CHECK(lp_forward(w0, x).data == lp_forward(w1, x).data);
+  }
+  // --- cb2 plugin: decode law known answer (tests/test_cb2.py::test_cb2_known_answer)
+  {
+    std::vector<float> cb(256 * 8, 0.0f);
+    const float e3[8] = {0.5f, 1.5f, 2.5f, 3.5f, 0.25f, 0.0f, 1.0f, 2.0f};
+    for (int j = 0; j < 8; ++j) cb[3 * 8 + j] = e3[j];
+    const std::vector<std::uint16_t> codes = {static_cast<std::uint16_t>(3 | (1 << 9) | (1 << 15)), 3};
+    auto q = upload_cb2(1, 16, 8, codes, cb, {2.0f, 0.5f});
+    const HostMatrix w = dequantize(*q);
+    const double want[16] = {1, -3, 5, 7, 0.5, 0, 2, -4, 0.25, 0.75, 1.25, 1.75, 0.125, 0, 0.5, 1};
+    bool ok = true;
+    for (int j = 0; j < 16; ++j) ok = ok && w(0, j) == want[j];
+    CHECK(ok);
+    CHECK(throws<NumericError>([&] { upload_cb2(1, 16, 8, codes, cb, {2.0f, -1.0f}); }));
+  }
+  // --- AdamW first step replicates the update arithmetic (test_train.cpp:145-167)
+  {
+    const double p0[3] = {1.0, -2.0, 3.0}, g0[3] = {0.1, -0.2, 0.3};
+    DeviceBuffer<double> p(3), gr(3);
+    p.upload(p0);
+    gr.upload(g0);
+    AdamW opt(0.9, 0.999, 1e-8, 0.0);
+    opt.step(p.get(), gr.get(), MLRA_F64, {3}, {"p"}, 0, 0.01);
+    double got[3];
+    p.download(got);
+    bool ok = true;
+    for (int j = 0; j < 3; ++j) {
+      const double m = (1.0 - 0.9) * g0[j], v = (1.0 - 0.999) * g0[j] * g0[j];
+      const double mhat = m / (1.0 - std::pow(0.9, 1.0)), vhat = v / (1.0 - std::pow(0.999, 1.0));
+      ok = ok && got[j] == p0[j] * (1.0 - 0.01 * 0.0) - 0.01 * mhat / (std::sqrt(vhat) + 1e-8);
+    }
+    CHECK(ok);
+    const double bad[3] = {0.1, NAN, 0.3};
+    gr.upload(bad);
+    CHECK(throws<NumericError>([&] { opt.step(p.get(), gr.get(), MLRA_F64, {3}, {"p"}, 1, 0.01); }));
+  }
+  // --- checkpoint: the reference's golden.mlra digests (acceptance.cpp:462-463)
+  {
+    Checkpoint c(golden + "/golden.mlra");
+    CHECK(c.file_hash() == 0xb48207d130703ee4ull);
+    CHECK(c.frozen_state_hash() == 0xa3d66a9e729158ffull);
+    CHECK(c.size() == 2);
+    auto q = c.upload(0);
+    CHECK(q->rows() == static_cast<std::size_t>(c.layer(0).rows));
+    CHECK(throws<IoError>([&] { Checkpoint bad(golden + "/missing.mlra"); }));
+    bool kind_ok = false;
+    try {
+      Checkpoint bad(golden + "/layer.npz");
+    } catch (const FormatError& e) {
+      kind_ok = e.kind == FormatError::Kind::BadMagic && e.offset == 0;
+    }
+    CHECK(kind_ok);
   }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail;

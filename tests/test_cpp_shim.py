@@ -28,7 +28,8 @@ def test_cpp_shim_compiles_with_gxx_cxx20():
 @pytest.mark.gpu
 def test_cpp_shim_on_device():
     exe = _build()
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([exe, os.path.join(ROOT, "tests", "golden")], capture_output=True, text=True,
+                       timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "0 failed" in r.stdout
