@@ -215,10 +215,18 @@ def main():
     from paper_2309_16119_b200 import modulora as M
     from paper_2309_16119_b200._lib import lib
 
+    # One rank per GPU. Functional multi-rank runs on a box with fewer GPUs (the
+    # 1-GPU dev box) may share devices and use gloo: MLRA_DIST_BACKEND=gloo.
+    ndev = torch.cuda.device_count()
+    local = local % ndev if ndev else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("MLRA_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     strat = M.parse_strategy(args.strategy)
     m, r = CFG["m"], CFG["rank"]
 
@@ -245,8 +253,13 @@ def main():
         y1, xb1 = M.layer_forward(up, xin)
         y2, xb2 = M.layer_forward(down, y1)
         dx2 = M.layer_backward(down, y1, xb2, dyin, da=da_dn, db=db_dn)
+        # the down layer's gradients all-reduce (NCCL) while the up layer's backward runs
+        w_dn = grads.allreduce_async(["l1.dA", "l1.dB"])
         M.layer_backward(up, xin, xb1, dx2, da=da_up, db=db_up)
-        grads.allreduce()
+        w_up = grads.allreduce_async(["l0.dA", "l0.dB"])
+        for w in (w_dn, w_up):
+            if w is not None:
+                w.wait()
         return y2
 
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -336,19 +349,28 @@ def main():
     step_flops = 2 * (4.0 * m * CFG["d_ff"] * CFG["d_model"] + 6.0 * m * r * (CFG["d_ff"] + CFG["d_model"]))
 
     # ---- e2e through the public API with host buffers. Every step copies its own
-    # X and dY from pinned host memory and reads its gradient bucket back; the
-    # device input buffers are double-buffered so step i+1's host->device copy
-    # (copy stream) overlaps step i's compute. The first step's copy is inside
-    # the timed region; the final synchronize covers the last D2H.
+    # X and dY from pinned host memory and reads its gradient bucket back. The
+    # device input buffers are double-buffered and each input has its own event:
+    # a step's forward waits only for its X, its backward for its dY, so dY's
+    # copy (and the next step's copies) overlap compute on the copy engine. The
+    # gradient D2H runs on a third stream (the other copy direction) after the
+    # step's last kernel, and the next step's backward waits for it before
+    # rewriting the bucket. The first step's copies are inside the timed region;
+    # the final synchronize covers the last D2H.
     n_e2e = args.steps
     xh = [x.cpu().pin_memory() for _ in range(2)]
     dyh = [dy2.cpu().pin_memory() for _ in range(2)]
     gh = torch.empty(bucket.numel(), dtype=torch.float32).pin_memory()
     copy_stream = torch.cuda.Stream(dev)
+    d2h_stream = torch.cuda.Stream(dev)
     xd = [torch.empty_like(x) for _ in range(2)]
     dyd = [torch.empty_like(dy2) for _ in range(2)]
-    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_x = [torch.cuda.Event() for _ in range(2)]
+    ev_dy = [torch.cuda.Event() for _ in range(2)]
     ev_free = [torch.cuda.Event() for _ in range(2)]
+    ev_done, ev_read = torch.cuda.Event(), torch.cuda.Event()
+
+    AB_OLD = bool(os.environ.get("MLRA_E2E_OLD"))  # dev A/B toggle
 
     def issue_copy(i):
         sl = i % 2
@@ -356,8 +378,9 @@ def main():
             if i >= 2:
                 copy_stream.wait_event(ev_free[sl])  # step i-2 finished with this slot
             xd[sl].copy_(xh[sl], non_blocking=True)
+            ev_x[sl].record(copy_stream)
             dyd[sl].copy_(dyh[sl], non_blocking=True)
-            ev_in[sl].record(copy_stream)
+            ev_dy[sl].record(copy_stream)
 
     def e2e_run(n):
         issue_copy(0)
@@ -365,14 +388,30 @@ def main():
             sl = i % 2
             if i + 1 < n:
                 issue_copy(i + 1)
-            stream.wait_event(ev_in[sl])
+            stream.wait_event(ev_x[sl])
+            if AB_OLD:
+                stream.wait_event(ev_dy[sl])
             y1, xb1 = M.layer_forward(up, xd[sl])
             y2, xb2 = M.layer_forward(down, y1)
+            stream.wait_event(ev_dy[sl])
+            if i > 0 and not AB_OLD:
+                stream.wait_event(ev_read)  # previous step's gradients read back
             dx2 = M.layer_backward(down, y1, xb2, dyd[sl], da=da_dn, db=db_dn)
+            w_dn = grads.allreduce_async(["l1.dA", "l1.dB"])
             M.layer_backward(up, xd[sl], xb1, dx2, da=da_up, db=db_up)
-            grads.allreduce()
+            w_up = grads.allreduce_async(["l0.dA", "l0.dB"])
+            for w in (w_dn, w_up):
+                if w is not None:
+                    w.wait()
             ev_free[sl].record(stream)
-            gh.copy_(bucket, non_blocking=True)
+            if AB_OLD:
+                gh.copy_(bucket, non_blocking=True)
+                continue
+            ev_done.record(stream)
+            with torch.cuda.stream(d2h_stream):
+                d2h_stream.wait_event(ev_done)
+                gh.copy_(bucket, non_blocking=True)
+                ev_read.record(d2h_stream)
 
     e2e_run(3)
     torch.cuda.synchronize(dev)
@@ -381,6 +420,8 @@ def main():
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(stream)
     e2e_run(n_e2e)
+    if not AB_OLD:
+        stream.wait_event(ev_read)  # the last step's gradient read-back is inside the region
     e.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = s.elapsed_time(e) / n_e2e
@@ -423,8 +464,10 @@ def main():
             "e2e": {"value": e2e_val, "unit": "tokens/s",
                     "h2d_bytes_per_step": int(xh[0].numel() * 2 + dyh[0].numel() * 2),
                     "d2h_bytes_per_step": int(gh.numel() * 4), "ms_per_step": e2e_ms,
-                    "note": "pinned host X/dY copied H2D every step (double-buffered: step i+1's "
-                            "copy overlaps step i); LoRA gradient bucket copied D2H every step"},
+                    "note": "pinned host X/dY copied H2D every step (double-buffered; the forward "
+                            "waits for X only, the backward for dY, so copies overlap compute); "
+                            "LoRA gradient bucket copied D2H every step on its own stream; the "
+                            "region ends after the last D2H"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

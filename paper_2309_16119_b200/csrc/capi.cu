@@ -228,9 +228,9 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
   a.bias = gp.bias;
   a.out_pairs = !gp.out_f32 && gp.ldo % 2 == 0 &&
                 reinterpret_cast<uintptr_t>(gp.out) % 4 == 0 ? 1 : 0;
-  // CTA-pair kernel (512 tokens per tile) once there are enough tokens to fill
-  // it; MLRA_GEMM=1|2 forces the 1-CTA / pair kernel (tests cover both).
-  bool pair = gp.tokens > 256;
+  // CTA-pair kernel (512 tokens per tile) or the 1-CTA kernel (256), by the
+  // cost model; MLRA_GEMM=1|2 forces the 1-CTA / pair kernel (tests cover both).
+  bool pair = mlra::qgemm_prefer_pair(a);
   if (const char* force = getenv("MLRA_GEMM")) pair = atoi(force) == 2;
   const uint32_t tbox = pair ? 128 : 256;
   mlra_status st = make_map(&maps.act, gp.act, gp.k_red_valid, gp.tokens, gp.ld_act, 64, tbox);

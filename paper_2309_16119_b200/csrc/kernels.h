@@ -85,6 +85,10 @@ struct PrepBatch {
         rows_out * ldd);
   }
 };
+// First block of each task in a k_prep launch (host-computed partition).
+struct PrepBlocks {
+  int first[kMaxPrep + 1];
+};
 cudaError_t launch_prep(const PrepBatch& b, cudaStream_t st);
 
 // Skinny rank-r products on tensor cores (thin_mma.cu); r <= 64 per call. Factors are passed

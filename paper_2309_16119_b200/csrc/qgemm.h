@@ -64,6 +64,9 @@ cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmA
 // Plans the pair kernel's schedule: sets p.sk_pairs (0 = whole tiles) and the
 // per-pair cut tables. The caller provides sk_ws / sk_flags when sk_pairs > 0.
 void qgemm2_plan(GemmArgs& p);
+// true: the pair kernel (with its planned schedule) is expected to beat the
+// 1-CTA kernel for this GEMM (cost model in qgemm2.cu).
+bool qgemm_prefer_pair(const GemmArgs& p);
 constexpr int kMaxSkPairs = 128;
 constexpr int64_t kSkSlotFloats = 2LL * 512 * 128;  // per pair
 

@@ -651,6 +651,25 @@ void qgemm2_plan(GemmArgs& p) {
   p.sk_pairs = static_cast<int>(pairs);
 }
 
+// Kernel choice for a GEMM of p.tokens tokens (p's tile extents set, schedule
+// not yet planned). Costs in k-block-waves of the pair kernel, fitted to
+// graph-timed sweeps over m in {512..2048} at the LLaMA-7B shapes
+// (scripts/sk_probe.py): a pair k-block wave ~0.8 us, a 1-CTA k-block wave
+// ~0.6 us (0.75 units), stream-K's partial write + in-order fix-up ~56 units.
+bool qgemm_prefer_pair(const GemmArgs& p0) {
+  if (p0.tokens <= 256) return false;
+  GemmArgs p = p0;
+  qgemm2_plan(p);
+  const int64_t sms = sm_total(), slots = sms / 2;
+  const double n_kb = static_cast<double>(p.n_kb_main + p.n_kb_lora);
+  const int64_t tiles2 = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
+  const int64_t tiles1 = (p.m_total / BM) * ((p.tokens + 255) / 256);
+  const double pair = p.sk_pairs ? static_cast<double>(tiles2) * n_kb / p.sk_pairs + 56.0
+                                 : static_cast<double>((tiles2 + slots - 1) / slots) * n_kb;
+  const double cta1 = static_cast<double>((tiles1 + sms - 1) / sms) * n_kb * 0.75;
+  return cta1 >= 0.95 * pair;
+}
+
 cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                           bool w_tma, bool mn, bool out_f32, cudaStream_t stream) {
   if (p.tokens <= 0 || p.m_total <= 0) return cudaSuccess;

@@ -245,15 +245,17 @@ __global__ void __launch_bounds__(128)
 }
 
 // One launch for a layer pass's small conversion / zeroing jobs (PrepBatch):
-// grid-stride over the concatenated index spaces of up to kMaxPrep tasks.
-__global__ void k_prep(const PrepBatch b) {
-  const int64_t total = b.offs[b.n];
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int t = 0;
-    while (i >= b.offs[t + 1]) ++t;
-    const PrepTask& k = b.t[t];
-    const int64_t j = i - b.offs[t];
+// blocks are partitioned among the tasks in proportion to their sizes (host
+// computed), so each block resolves its task once and runs a 32-bit
+// grid-stride loop over that task's index space.
+__global__ void __launch_bounds__(256) k_prep(const PrepBatch b, const PrepBlocks pbk) {
+  int t = 0;
+  while (static_cast<int>(blockIdx.x) >= pbk.first[t + 1]) ++t;
+  const PrepTask& k = b.t[t];
+  const uint32_t count = static_cast<uint32_t>(b.offs[t + 1] - b.offs[t]);
+  const uint32_t stride = static_cast<uint32_t>(pbk.first[t + 1] - pbk.first[t]) * blockDim.x;
+  const uint32_t ldd = static_cast<uint32_t>(k.ldd);
+  for (uint32_t j = (blockIdx.x - pbk.first[t]) * blockDim.x + threadIdx.x; j < count; j += stride) {
     switch (k.kind) {
       case PrepTask::kZeroF32:
         reinterpret_cast<float*>(k.dst)[j] = 0.0f;
@@ -262,11 +264,11 @@ __global__ void k_prep(const PrepBatch b) {
         reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = __float2bfloat16_rn(0.0f);
         break;
       case PrepTask::kSplitT: {  // hi/lo planes [rows_out x ldd] of src^T (cols = r)
-        const int64_t row = j / k.ldd, col = j % k.ldd;
+        const uint32_t row = j / ldd, col = j - row * ldd;
         float v = 0.0f;
         if (col < k.rows) {
           if (row < k.cols)
-            v = k.src[col * k.lds + row];
+            v = k.src[static_cast<int64_t>(col) * k.lds + row];
           else if (row == k.cols && k.ones)
             v = 1.0f;
         }
@@ -276,8 +278,10 @@ __global__ void k_prep(const PrepBatch b) {
         break;
       }
       case PrepTask::kPadBf16: {  // dst [rows_out x ldd] = bf16(scale * src) zero-padded
-        const int64_t row = j / k.ldd, col = j % k.ldd;
-        const float v = (row < k.rows && col < k.cols) ? k.scale * k.src[row * k.lds + col] : 0.0f;
+        const uint32_t row = j / ldd, col = j - row * ldd;
+        const float v = (row < k.rows && col < k.cols)
+                            ? k.scale * k.src[static_cast<int64_t>(row) * k.lds + col]
+                            : 0.0f;
         reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = __float2bfloat16_rn(v);
         break;
       }
@@ -402,8 +406,22 @@ cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
 
 cudaError_t launch_prep(const PrepBatch& b, cudaStream_t st) {
   if (b.n == 0 || b.offs[b.n] == 0) return cudaSuccess;
+  PrepBlocks pbk{};
+  int nb = 0;
+  for (int t = 0; t < b.n; ++t) {
+    const int64_t count = b.offs[t + 1] - b.offs[t];
+    if (count >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+    // ~1 element per thread: the tasks are latency-bound (a dependent global
+    // load per element), so parallelism, not per-thread work, sets the time
+    int64_t want = (count + 255) / 256;
+    if (want > 32 * sms()) want = 32 * sms();
+    pbk.first[t] = nb;
+    nb += static_cast<int>(want);  // zero-size tasks get no block
+  }
+  pbk.first[b.n] = nb;
+  if (nb == 0) return cudaSuccess;
   note_launch();
-  k_prep<<<blocks_for(b.offs[b.n]), 256, 0, st>>>(b);
+  k_prep<<<nb, 256, 0, st>>>(b, pbk);
   return cudaGetLastError();
 }
 

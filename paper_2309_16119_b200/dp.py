@@ -55,6 +55,24 @@ class GradBucket:
                 shapes.append((f"{L.name}.dbias", (L.d_out(),)))
         return GradBucket.create(shapes, device)
 
+    def slice_of(self, names: Sequence[str]) -> torch.Tensor:
+        """The contiguous span of the flat buffer covering the named views."""
+        base = self.flat.data_ptr()
+        es = self.flat.element_size()
+        lo = min((self.views[n].data_ptr() - base) // es for n in names)
+        hi = max((self.views[n].data_ptr() - base) // es + self.views[n].numel() for n in names)
+        return self.flat[lo:hi]
+
+    def allreduce_async(self, names: Sequence[str], group=None):
+        """Start the sum all-reduce of one layer's gradients (their span of the
+        bucket) as soon as they exist, so it overlaps the remaining backward;
+        returns the work handle (None when not distributed)."""
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            return dist.all_reduce(self.slice_of(names), op=dist.ReduceOp.SUM, group=group,
+                                   async_op=True)
+        return None
+
     def allreduce(self, group=None) -> None:
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:

@@ -234,7 +234,6 @@ class LinearStackTrainer:
 
     def backward(self, xs, xbs, dys, need_dx: bool = False):
         """Reverse order; returns the dX list (None entries when not needed)."""
-        import torch.distributed as dist
         world = self._world()
         works, dxs = [], [None] * len(self.layers)
         for i in reversed(range(len(self.layers))):
@@ -245,20 +244,13 @@ class LinearStackTrainer:
             if L.bias_trainable and L.grad_bias is not None:
                 self.grads.views[f"{L.name}.dbias"].copy_(L.grad_bias)
             if world > 1:
-                lo, hi = self._slice(L)
-                works.append(dist.all_reduce(self.grads.flat[lo:hi], op=dist.ReduceOp.SUM,
-                                             group=self.group, async_op=True))
+                names = [f"{L.name}.dA", f"{L.name}.dB"] + (
+                    [f"{L.name}.dbias"] if L.bias_trainable else [])
+                works.append(self.grads.allreduce_async(names, group=self.group))
         for w in works:
-            w.wait()
+            if w is not None:
+                w.wait()
         return dxs
-
-    def _slice(self, L):
-        names = [f"{L.name}.dA", f"{L.name}.dB"] + ([f"{L.name}.dbias"] if L.bias_trainable else [])
-        base = self.grads.flat.data_ptr()
-        lo = min((self.grads.views[n].data_ptr() - base) // 4 for n in names)
-        hi = max((self.grads.views[n].data_ptr() - base) // 4 + self.grads.views[n].numel()
-                 for n in names)
-        return lo, hi
 
     def optimizer_step(self, check_finite: bool = True):
         lr = lr_at(self.config, self.step_index)

@@ -5,9 +5,14 @@ headline bench; writes one JSON line per config).
   cfg2  LLaMA-7B MLP up+down, 3-bit, r=16, m=4096 (the bench.py headline)
   cfg3  LLaMA-7B decoder linear stack Q,K,V,O,gate,up,down, 3-bit, r=8, m=8192
   cfg4  LLaMA-65B up 22016x8192 + down 8192x22016, b in {3,4}, r=64, m=2048 (per GPU of 8)
-  cfg5  2-bit 6656x17920 materialize() bandwidth sweep (bf16 and f32 out)
+  cfg5  2-bit 6656x17920 materialize() bandwidth sweep (bf16 and f32 out): the affine
+        2-bit format and the black-box "cb2" codebook plugin (hook), plus the cb2 layer
+        fwd+bwd through the hook (slabbed hook materialization + tcgen05 GEMM), m=4096
+  cfg3_train  the cfg3 stack as a training step (LinearStackTrainer: fwd, bwd, AdamW)
 
-Timing: CUDA events, 3 warm-up + 10 timed steps, L2 flushed between steps.
+Timing: CUDA events, 3 warm-up + 10 timed steps, L2 flushed between steps. Each
+layer config is timed eager and as a replayed CUDA graph ("launch" key): small
+configs (cfg1) are host-launch bound when eager.
 """
 import json
 import os
@@ -60,10 +65,26 @@ def independent_layers_step(layers, m):
     return step
 
 
+def graphed(fn):
+    """Capture fn once (after a warm-up call) and return a replay closure."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    torch.cuda.synchronize()
+    return g.replay
+
+
 def main():
     strat = M.parse_strategy(os.environ.get("STRATEGY", "row"))
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    pk = 1646.4
+    try:
+        peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                            "MEASURED_PEAKS.json")))
+        pk, hbm = float(peaks["bf16_tflops"]), float(peaks["hbm_gbs"])
+    except Exception:
+        pk, hbm = 1646.4, 6544.3
     cfgs = {
         "cfg1": ([(4096, 4096)], 4, 8, 512),
         "cfg2": ([(11008, 4096), (4096, 11008)], 3, 16, 4096),
@@ -76,14 +97,33 @@ def main():
         if only and name not in only:
             continue
         layers = layers_for(shapes, bits, r, strat)
-        ms = time_steps(independent_layers_step(layers, m), flush)
+        fn = independent_layers_step(layers, m)
         flops = sum(4.0 * m * a * b + 6.0 * m * r * (a + b) for a, b in shapes)
-        print(json.dumps({"config": name, "shapes": shapes, "bits": bits, "rank": r, "tokens": m,
-                          "strategy": M.strategy_name(strat), "ms_per_step": ms,
-                          "tokens_per_s": m / (ms / 1e3), "tflops": flops / (ms / 1e3) / 1e12,
-                          "pct_measured_bf16_peak": 100 * flops / (ms / 1e3) / 1e12 / pk}),
+        for launch, f in (("eager", fn), ("cuda-graph", graphed(fn))):
+            ms = time_steps(f, flush)
+            print(json.dumps({"config": name, "shapes": shapes, "bits": bits, "rank": r,
+                              "tokens": m, "strategy": M.strategy_name(strat), "launch": launch,
+                              "ms_per_step": ms, "tokens_per_s": m / (ms / 1e3),
+                              "tflops": flops / (ms / 1e3) / 1e12,
+                              "pct_measured_bf16_peak": 100 * flops / (ms / 1e3) / 1e12 / pk}),
+                  flush=True)
+        del layers, fn
+        torch.cuda.empty_cache()
+    if not only or "cfg3_train" in only:
+        from paper_2309_16119_b200 import train as T
+        shapes, m, r = [(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)], 8192, 8
+        layers = layers_for(shapes, 3, r, strat)
+        tr = T.LinearStackTrainer(layers, T.TrainConfig(lr=1e-4))
+        xs = [torch.randn(m, L.d_in(), device="cuda").to(torch.bfloat16) for L in layers]
+        dys = [torch.randn(m, L.d_out(), device="cuda").to(torch.bfloat16) for L in layers]
+        ms = time_steps(lambda: tr.step(xs, dys, need_dx=True, check_finite=False), flush)
+        flops = sum(4.0 * m * a * b + 6.0 * m * r * (a + b) for a, b in shapes)
+        print(json.dumps({"config": "cfg3_train", "shapes": shapes, "bits": 3, "rank": r,
+                          "tokens": m, "step": "fwd + bwd (with dX) + AdamW over the adapter bucket",
+                          "adapter_params": int(tr.params.flat.numel()), "ms_per_step": ms,
+                          "tokens_per_s": m / (ms / 1e3), "tflops": flops / (ms / 1e3) / 1e12}),
               flush=True)
-        del layers
+        del layers, tr
         torch.cuda.empty_cache()
     if not only or "cfg5" in only:
         q, *_ = synthetic_qmatrix(6656, 17920, 2, 128, 500)
@@ -92,10 +132,42 @@ def main():
             out = torch.empty(6656, 17920, dtype=dt, device="cuda")
             ms = time_steps(lambda: M.dequantize(dq, dt, out=out), flush)
             nbytes = 6656 * 17920 * (2 / 8 + eb) + 6656 * (17920 // 128) * 8
-            print(json.dumps({"config": "cfg5_materialize", "shape": [6656, 17920], "bits": 2,
-                              "out": str(dt), "us": ms * 1e3,
+            print(json.dumps({"config": "cfg5_materialize", "format": "affine", "shape": [6656, 17920],
+                              "bits": 2, "out": str(dt), "us": ms * 1e3,
                               "gbs": nbytes / (ms / 1e3) / 1e9,
-                              "frac_measured_hbm": nbytes / (ms / 1e3) / 1e9 / 6544.3}),
+                              "frac_measured_hbm": nbytes / (ms / 1e3) / 1e9 / hbm}),
+                  flush=True)
+        # the black-box cb2 plugin (QuIP#-style vector codebook) through its hook
+        import numpy as np
+        rng = np.random.default_rng(501)
+        rows, cols = 6656, 17920
+        cbm = M.Cb2Matrix(rows, cols, 128,
+                          rng.integers(0, 1 << 16, (rows, cols // 8), dtype=np.uint32).astype(np.uint16),
+                          M.default_cb2_codebook(),
+                          (0.01 * (0.5 + rng.random((rows, cols // 128)))).astype(np.float32))
+        cq = M.Codebook2Quantizer().upload(cbm)
+        for dt, eb in ((torch.bfloat16, 2), (torch.float32, 4)):
+            out = torch.empty(rows, cols, dtype=dt, device="cuda")
+            ms = time_steps(lambda: M.dequantize(cq, dt, out=out), flush)
+            nbytes = rows * cols * (2 / 8 + eb) + rows * (cols // 128) * 4 + 8192
+            print(json.dumps({"config": "cfg5_materialize", "format": "cb2 plugin (hook)",
+                              "shape": [rows, cols], "bits": 2, "out": str(dt), "us": ms * 1e3,
+                              "gbs": nbytes / (ms / 1e3) / 1e9,
+                              "frac_measured_hbm": nbytes / (ms / 1e3) / 1e9 / hbm}),
+                  flush=True)
+        del out
+        m, r = 4096, 8
+        a = torch.randn(rows, r, device="cuda") * 0.02
+        b = torch.randn(cols, r, device="cuda") * 0.02
+        for sname in ("row", "weight"):
+            L = M.ModuLoraLayer("cb2", cq, M.LoraAdapter(a, b, r, 16.0),
+                                strategy=M.parse_strategy(sname))
+            ms = time_steps(independent_layers_step([L], m), flush)
+            flops = 4.0 * m * rows * cols + 6.0 * m * r * (rows + cols)
+            print(json.dumps({"config": "cfg5_cb2_layer", "shape": [rows, cols], "rank": r,
+                              "tokens": m, "strategy": sname,
+                              "ledger_bytes": M.LpLinearContext(cq, L.strategy).ledger_bytes(),
+                              "ms_per_step": ms, "tflops": flops / (ms / 1e3) / 1e12}),
                   flush=True)
 
 

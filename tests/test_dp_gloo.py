@@ -50,7 +50,14 @@ def _worker(rank, world, port, out):
     bucket.views["l.dA"].copy_(torch.from_numpy(da))
     bucket.views["l.dB"].copy_(torch.from_numpy(db))
     bucket.views["l.dbias"].copy_(torch.from_numpy(dbias))
-    bucket.allreduce()
+    if os.environ.get("MLRA_TEST_ASYNC"):
+        # per-layer form used by bench.py / LinearStackTrainer: slices all-reduced
+        # asynchronously as they become ready, then waited on
+        works = [bucket.allreduce_async(["l.dbias"]), bucket.allreduce_async(["l.dA", "l.dB"])]
+        for wk in works:
+            wk.wait()
+    else:
+        bucket.allreduce()
     if rank == 0:
         out.put({k: v.numpy().copy() for k, v in bucket.views.items()})
     dist.barrier()
@@ -68,8 +75,11 @@ def test_shard_tokens_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
-def test_gloo_allreduce_matches_full_batch():
+@pytest.mark.parametrize("mode", ["flat", "async_slices"])
+def test_gloo_allreduce_matches_full_batch(mode, monkeypatch):
     from oracle import oracle as orc
+    if mode == "async_slices":
+        monkeypatch.setenv("MLRA_TEST_ASYNC", "1")  # inherited by the spawned workers
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
