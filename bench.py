@@ -370,8 +370,6 @@ def main():
     ev_free = [torch.cuda.Event() for _ in range(2)]
     ev_done, ev_read = torch.cuda.Event(), torch.cuda.Event()
 
-    AB_OLD = bool(os.environ.get("MLRA_E2E_OLD"))  # dev A/B toggle
-
     def issue_copy(i):
         sl = i % 2
         with torch.cuda.stream(copy_stream):
@@ -389,12 +387,10 @@ def main():
             if i + 1 < n:
                 issue_copy(i + 1)
             stream.wait_event(ev_x[sl])
-            if AB_OLD:
-                stream.wait_event(ev_dy[sl])
             y1, xb1 = M.layer_forward(up, xd[sl])
             y2, xb2 = M.layer_forward(down, y1)
             stream.wait_event(ev_dy[sl])
-            if i > 0 and not AB_OLD:
+            if i > 0:
                 stream.wait_event(ev_read)  # previous step's gradients read back
             dx2 = M.layer_backward(down, y1, xb2, dyd[sl], da=da_dn, db=db_dn)
             w_dn = grads.allreduce_async(["l1.dA", "l1.dB"])
@@ -404,9 +400,6 @@ def main():
                 if w is not None:
                     w.wait()
             ev_free[sl].record(stream)
-            if AB_OLD:
-                gh.copy_(bucket, non_blocking=True)
-                continue
             ev_done.record(stream)
             with torch.cuda.stream(d2h_stream):
                 d2h_stream.wait_event(ev_done)
@@ -420,8 +413,7 @@ def main():
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(stream)
     e2e_run(n_e2e)
-    if not AB_OLD:
-        stream.wait_event(ev_read)  # the last step's gradient read-back is inside the region
+    stream.wait_event(ev_read)  # the last step's gradient read-back is inside the region
     e.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = s.elapsed_time(e) / n_e2e

@@ -156,6 +156,18 @@ MLRA_API mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group_s
                                      const uint16_t* codes, const float* codebook,
                                      const float* scales, void* stream, mlra_qweight** out);
 
+/* RtnQuantizer::quantize (quantize.hpp:108-113; quantize.cpp:24-44, 163-184)
+ * on the device: w is a DEVICE matrix [rows x cols] of dtype MLRA_F64 or
+ * MLRA_F32 (widened exactly); group_size 0 selects per-row grids
+ * (quantize.cpp:78-80). Writes, on `stream`, the reference's QuantizedMatrix
+ * layout to device buffers: words [mlra_packed_word_count(rows*cols, bits)]
+ * (LSB-first bitstream over the whole row-major matrix), scales / zeros
+ * [rows x cols/group]. Bit-identical to quantize_rtn((double)w).
+ * Errors: DimensionError (empty), ConfigError (bits / group). */
+MLRA_API mlra_status mlra_quantize_rtn(const void* w, mlra_dtype dtype, int64_t rows, int64_t cols,
+                                       int bits, int64_t group_size, uint32_t* words,
+                                       float* scales, float* zeros, void* stream);
+
 /* The hook an opaque qweight carries (NULL for the affine built-in format). */
 MLRA_API const mlra_hook* mlra_qweight_hook(const mlra_qweight* q);
 

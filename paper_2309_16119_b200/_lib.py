@@ -28,7 +28,7 @@ EXPORTS = [
     "mlra_adamw_step", "mlra_last_format_error", "mlra_checkpoint_load", "mlra_checkpoint_free",
     "mlra_checkpoint_layer_count", "mlra_checkpoint_layer", "mlra_checkpoint_config_json",
     "mlra_checkpoint_frozen_hash", "mlra_checkpoint_file_hash", "mlra_checkpoint_upload",
-    "mlra_checkpoint_set_adapter", "mlra_checkpoint_save",
+    "mlra_checkpoint_set_adapter", "mlra_checkpoint_save", "mlra_quantize_rtn",
 ]
 
 # mlra_hook.materialize(state, q, row0, nrows, col0, ncols, out, dtype, ld, stream)
@@ -162,6 +162,8 @@ def lib() -> C.CDLL:
         L.mlra_checkpoint_set_adapter.argtypes = [vp, i64, vp, vp]
         L.mlra_checkpoint_save.restype = i32
         L.mlra_checkpoint_save.argtypes = [vp, C.c_char_p]
+        L.mlra_quantize_rtn.restype = i32
+        L.mlra_quantize_rtn.argtypes = [vp, i32, i64, i64, i32, i64, vp, vp, vp, vp]
         _lib = L
     return _lib
 

@@ -684,6 +684,27 @@ mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group, const uin
   return MLRA_OK;
 }
 
+mlra_status mlra_quantize_rtn(const void* w, mlra_dtype dtype, int64_t rows, int64_t cols,
+                              int bits, int64_t group, uint32_t* words, float* scales,
+                              float* zeros, void* stream) {
+  // validate_quantize_args (quantize.cpp:46-59), group 0 = per row (:78-80)
+  if (group == 0) group = cols;
+  if (rows <= 0 || cols <= 0) return fail(MLRA_ERR_DIMENSION, "quantize: matrix must be non-empty");
+  if (!supported_bits(bits))
+    return fail(MLRA_ERR_CONFIG, "quantize: unsupported bit width %d", bits);
+  if (group <= 0 || cols % group != 0)
+    return fail(MLRA_ERR_CONFIG, "quantize: group size %lld does not divide cols %lld",
+                (long long)group, (long long)cols);
+  if (dtype != MLRA_F64 && dtype != MLRA_F32)
+    return fail(MLRA_ERR_CONFIG, "quantize: weights must be f64 or f32");
+  if (!w || !words || !scales || !zeros) return fail(MLRA_ERR_CONTRACT, "quantize: null buffers");
+  if (mlra_status st = check_device()) return st;
+  const uint64_t nwords = mlra_packed_word_count(static_cast<uint64_t>(rows * cols), bits);
+  CUDA_TRY(mlra::launch_quantize_rtn(w, dtype == MLRA_F64, rows, cols, group, bits, words, nwords,
+                                     scales, zeros, static_cast<cudaStream_t>(stream)));
+  return MLRA_OK;
+}
+
 const mlra_hook* mlra_qweight_hook(const mlra_qweight* q) {
   return q && q->opaque ? &q->hook : nullptr;
 }

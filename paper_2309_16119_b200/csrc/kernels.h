@@ -25,6 +25,12 @@ cudaError_t launch_cb2_materialize(const Cb2Dev& c, int64_t row0, int64_t nrows,
                                    int64_t ncols, void* out, int64_t ld, bool f32,
                                    cudaStream_t st);
 
+// RTN quantize (quantize.cu): w device f64/f32 [rows x cols] -> reference bitstream words
+// [nwords] + f32 scales / zeros [rows x cols/group]
+cudaError_t launch_quantize_rtn(const void* w, bool f64, int64_t rows, int64_t cols, int64_t group,
+                                int bits, uint32_t* words, uint64_t nwords, float* scales,
+                                float* zeros, cudaStream_t st);
+
 // AdamW (optim.cu): host-evaluated constants of AdamW::step (train.cpp:99-101, :122-127).
 struct AdamwConsts {
   double beta1, one_m_beta1, beta2, one_m_beta2, bc1, bc2, lr, eps, decay;

@@ -256,6 +256,37 @@ class DoublingQuantizer(QuantizerHook):
             out.mul_(2)
 
 
+class RtnQuantizer:
+    """The reference's built-in plugin RtnQuantizer (quantize.hpp:108-113):
+    round-to-nearest per-(row, group) affine grids. ``quantize`` runs on the
+    device (mlra_quantize_rtn) and returns the reference's host QuantizedMatrix
+    layout, bit-identical to quantize_rtn((double)w)."""
+
+    def name(self) -> str:
+        return "rtn"
+
+    def quantize(self, w, calib=None, bits: int = 4, group_size: int = 0) -> QuantizedMatrix:
+        t = torch.as_tensor(w)
+        if t.dim() != 2:
+            raise MlraError(2, "quantize: expected a 2-D weight matrix")
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.double()
+        t = t.contiguous().cuda()
+        rows, cols = t.shape
+        g = cols if group_size == 0 else group_size
+        nw = packed_word_count(rows * cols, bits) if rows and cols else 0
+        words = torch.empty(max(nw, 1), dtype=torch.int32, device="cuda")
+        ng = rows * (cols // g) if g and cols % g == 0 else 0
+        scales = torch.empty(max(ng, 1), dtype=torch.float32, device="cuda")
+        zeros = torch.empty(max(ng, 1), dtype=torch.float32, device="cuda")
+        check(lib().mlra_quantize_rtn(t.data_ptr(), _lib.F64 if t.dtype == torch.float64 else _lib.F32,
+                                      rows, cols, bits, group_size, words.data_ptr(),
+                                      scales.data_ptr(), zeros.data_ptr(), _stream_ptr(None)))
+        wh = words[:nw].cpu().numpy().view(np.uint32).copy()
+        return QuantizedMatrix(rows, cols, bits, g, PackedCodes(bits, rows * cols, wh),
+                               scales[:ng].cpu().numpy(), zeros[:ng].cpu().numpy())
+
+
 def default_cb2_codebook() -> np.ndarray:
     """The cb2 plugin's default 256 x 8 magnitude codebook: the 256 shortest
     vectors of {1/2, 3/2, 5/2, 7/2}^8 (a shifted-lattice shell, as in QuIP#'s

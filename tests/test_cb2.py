@@ -224,3 +224,46 @@ def test_python_plugin_on_opaque_matrix():
     with pytest.raises(MlraError) as e:
         M.lp_forward(M.LpLinearContext(bq, S.RowMaterialize), x[:, :256], torch.float32)
     assert e.value.kind == "ContractError"
+
+
+# ----------------------------------------------------------------------------- RTN
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols,bits,group", [(7, 9, 3, 0), (7, 9, 3, 3), (64, 96, 2, 32),
+                                                  (300, 1000, 4, 40), (512, 4096, 3, 128),
+                                                  (256, 4096, 8, 0), (1024, 11008, 3, 128)])
+def test_device_rtn_quantizer_bit_exact(rows, cols, bits, group):
+    # the oracle's quantize_rtn is pinned to the reference (test_oracle_golden.py)
+    w = orc.gaussian(rows + cols + bits, rows, cols, 0.0, 0.02)
+    words, sc, z = orc.quantize_rtn(w, bits, group)
+    q = M.RtnQuantizer().quantize(torch.from_numpy(w), None, bits, group)
+    assert np.array_equal(q.codes.words, words)
+    assert np.array_equal(q.scales.view(np.uint32), np.asarray(sc, np.float32).view(np.uint32))
+    assert np.array_equal(q.zeros.view(np.uint32), np.asarray(z, np.float32).view(np.uint32))
+    # f32 weights = the reference on the widened values
+    w32 = w.astype(np.float32)
+    words32, sc32, z32 = orc.quantize_rtn(w32.astype(np.float64), bits, group)
+    q32 = M.RtnQuantizer().quantize(torch.from_numpy(w32), None, bits, group)
+    assert np.array_equal(q32.codes.words, words32)
+    assert np.array_equal(q32.scales, np.asarray(sc32, np.float32))
+
+
+@pytest.mark.gpu
+def test_device_rtn_edge_grids():
+    # flat groups (scale 1), signed zeros, ties at the extremes
+    w = np.zeros((4, 16))
+    w[1, 3] = -0.0
+    w[1, 0] = 0.0
+    w[2] = np.linspace(-1, 1, 16)
+    w[3, ::2] = 0.5
+    w[3, 1::2] = -0.5
+    words, sc, z = orc.quantize_rtn(w, 4, 8)
+    q = M.RtnQuantizer().quantize(torch.from_numpy(w), None, 4, 8)
+    assert np.array_equal(q.codes.words, words)
+    assert np.array_equal(q.scales.view(np.uint32), np.asarray(sc, np.float32).view(np.uint32))
+    assert np.array_equal(q.zeros.view(np.uint32), np.asarray(z, np.float32).view(np.uint32))
+    with pytest.raises(MlraError) as e:
+        M.RtnQuantizer().quantize(torch.from_numpy(w), None, 5, 8)
+    assert e.value.kind == "ConfigError"
+    with pytest.raises(MlraError) as e:
+        M.RtnQuantizer().quantize(torch.from_numpy(w), None, 4, 5)
+    assert e.value.kind == "ConfigError"
