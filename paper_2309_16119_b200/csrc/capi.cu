@@ -659,13 +659,31 @@ mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group, const uin
       }};
   mlra_qweight* q = nullptr;
   if (mlra_status st = mlra_qweight_create_opaque(rows, cols, 2, &kCb2Hook, &q)) return st;
-  const size_t cb_bytes = 256 * 8 * 4, code_bytes = static_cast<size_t>(rows * (cols / 8)) * 2,
+  // device codebook layout (common.cuh Cb2Dev): bf16-exact magnitudes -> 8 bf16
+  // per code, else the two float4 halves in separate arrays
+  bool cb16 = true;
+  for (int i = 0; i < 256 * 8 && cb16; ++i) {
+    uint32_t u;
+    std::memcpy(&u, &codebook[i], 4);
+    cb16 = (u & 0xFFFFu) == 0;
+  }
+  std::vector<uint32_t> cbdev(cb16 ? 256 * 4 : 256 * 8);
+  for (int i = 0; i < 256; ++i)
+    for (int e = 0; e < 8; ++e) {
+      uint32_t u;
+      std::memcpy(&u, &codebook[i * 8 + e], 4);
+      if (cb16)
+        cbdev[i * 4 + e / 2] |= (u >> 16) << (16 * (e & 1));
+      else
+        cbdev[(e / 4) * 1024 + i * 4 + (e & 3)] = u;
+    }
+  const size_t cb_bytes = cbdev.size() * 4, code_bytes = static_cast<size_t>(rows * (cols / 8)) * 2,
                sc_bytes = static_cast<size_t>(ng) * 4;
   const size_t off_codes = cb_bytes, off_sc = round_up(off_codes + code_bytes, 16);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMalloc(&q->cb2_mem, off_sc + sc_bytes);
   char* base = static_cast<char*>(q->cb2_mem);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(base, codebook, cb_bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(base, cbdev.data(), cb_bytes, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(base + off_codes, codes, code_bytes, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
@@ -678,8 +696,8 @@ mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group, const uin
   q->device_bytes = off_sc + sc_bytes;
   q->d.group = group;
   q->cb2 = mlra::Cb2Dev{rows, cols, group, cols / group,
-                        reinterpret_cast<const uint16_t*>(base + off_codes),
-                        reinterpret_cast<const float*>(base), reinterpret_cast<const float*>(base + off_sc)};
+                        reinterpret_cast<const uint16_t*>(base + off_codes), base, cb16 ? 1 : 0,
+                        reinterpret_cast<const float*>(base + off_sc)};
   *out = q;
   return MLRA_OK;
 }

@@ -25,61 +25,103 @@ namespace {
 constexpr int kCbThreads = 256;
 constexpr int kCbPerThread = 4;
 
+// One code -> 8 outputs. Products RN_f32(s·mag) (scalar IEEE multiplies); the
+// sign is applied after rounding (RN commutes with negation): for bf16, the
+// mask of entries (2p, 2p+1) is ((code >> (8+2p)) & 3) * 0x40008000 &
+// 0x80008000 — bit 15 and bit 31 of the packed pair — 3 ops per pair.
+// Magnitudes of a code's 8 entries from the shared codebook.
+template <bool CB16>
+__device__ __forceinline__ void cb2_mags(uint32_t code, const uint4* cbh, const float4* cb0,
+                                         const float4* cb1, float (&m)[8]) {
+  const uint32_t i = code & 0xFFu;
+  if constexpr (CB16) {
+    const uint4 q = cbh[i];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      m[2 * p] = __uint_as_float(w[p] << 16);
+      m[2 * p + 1] = __uint_as_float(w[p] & 0xFFFF0000u);
+    }
+  } else {
+    const float4 a = cb0[i], b = cb1[i];
+    m[0] = a.x, m[1] = a.y, m[2] = a.z, m[3] = a.w;
+    m[4] = b.x, m[5] = b.y, m[6] = b.z, m[7] = b.w;
+  }
+}
+
+// One code -> 8 outputs. Products RN_f32(s·mag) (scalar IEEE multiplies); the
+// sign is applied after rounding (RN commutes with negation): for bf16, the
+// mask of entries (2p, 2p+1) is ((code >> (8+2p)) & 3) * 0x40008000 &
+// 0x80008000 — bit 15 and bit 31 of the packed pair — 3 ops per pair.
 template <bool F32, bool VEC>
-__device__ __forceinline__ void cb2_store(void* __restrict__ out, int64_t o, const float (&f)[8]) {
-  if constexpr (VEC) {
-    if constexpr (F32) {
-      float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + o);
-      p[0] = make_float4(f[0], f[1], f[2], f[3]);
-      p[1] = make_float4(f[4], f[5], f[6], f[7]);
-    } else {
-      uint4 v;
-      v.x = pack_bf16x2(f[0], f[1]);
-      v.y = pack_bf16x2(f[2], f[3]);
-      v.z = pack_bf16x2(f[4], f[5]);
-      v.w = pack_bf16x2(f[6], f[7]);
+__device__ __forceinline__ void cb2_emit(void* __restrict__ out, int64_t o, uint32_t code, float s,
+                                         const float (&m)[8]) {
+  float f[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) f[e] = __fmul_rn(s, m[e]);
+  if constexpr (!F32) {
+    uint4 v;
+    v.x = pack_bf16x2(f[0], f[1]) ^ ((((code >> 8) & 3u) * 0x40008000u) & 0x80008000u);
+    v.y = pack_bf16x2(f[2], f[3]) ^ ((((code >> 10) & 3u) * 0x40008000u) & 0x80008000u);
+    v.z = pack_bf16x2(f[4], f[5]) ^ ((((code >> 12) & 3u) * 0x40008000u) & 0x80008000u);
+    v.w = pack_bf16x2(f[6], f[7]) ^ ((((code >> 14) & 3u) * 0x40008000u) & 0x80008000u);
+    if constexpr (VEC) {
       *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + o) = v;
+    } else {
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        reinterpret_cast<uint16_t*>(out)[o + e] =
+            static_cast<uint16_t>(w[e >> 1] >> (16 * (e & 1)));
     }
   } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      if constexpr (F32)
-        reinterpret_cast<float*>(out)[o + e] = f[e];
-      else
-        reinterpret_cast<__nv_bfloat16*>(out)[o + e] = __float2bfloat16_rn(f[e]);
+    for (int e = 0; e < 8; ++e)
+      f[e] = __uint_as_float(__float_as_uint(f[e]) ^ (((code >> (8 + e)) & 1u) << 31));
+    if constexpr (VEC) {
+      float4* q = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + o);
+      q[0] = make_float4(f[0], f[1], f[2], f[3]);
+      q[1] = make_float4(f[4], f[5], f[6], f[7]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) reinterpret_cast<float*>(out)[o + e] = f[e];
     }
   }
 }
 
 // Work items = (row, pass of kCbThreads * kCbPerThread codes) strided over a
 // resident-size grid (the 8 KB codebook is staged into shared memory once per
-// CTA). Software-pipelined: the codes and scales of the next item are loaded
-// before the current item is decoded, so a load latency is exposed once per
-// CTA, not once per pass (ncu: the one-pass-at-a-time form was long-scoreboard
-// bound at 32% of DRAM bandwidth). Within a pass a thread owns kCbPerThread
-// codes strided by the block size, so each warp store covers a contiguous
-// 512 B (bf16).
-template <bool F32, bool VEC>
+// CTA); the (row, pass) of a thread's next item advances incrementally (no
+// per-item division). Software-pipelined: the codes and scales of the next item
+// are loaded before the current item is decoded (ncu: the one-pass-at-a-time
+// form was long-scoreboard bound at 32% of DRAM bandwidth). Within a pass a
+// thread owns kCbPerThread codes strided by the block size, so each warp store
+// covers a contiguous 512 B (bf16).
+template <bool F32, bool VEC, bool CB16>
 __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
     const Cb2Dev c, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols,
     void* __restrict__ out, int64_t ld, int gshift) {
-  __shared__ float4 cb[256 * 2];
-  for (int i = threadIdx.x; i < 512; i += kCbThreads)
-    cb[i] = __ldg(reinterpret_cast<const float4*>(c.codebook) + i);
+  __shared__ float4 cbs[CB16 ? 256 : 512];
+  const uint4* cbh = reinterpret_cast<const uint4*>(cbs);
+  const float4* cb0 = cbs;
+  const float4* cb1 = cbs + 256;
+  for (int i = threadIdx.x; i < (CB16 ? 256 : 512); i += kCbThreads)
+    cbs[i] = __ldg(reinterpret_cast<const float4*>(c.codebook) + i);
   const int ncodes = static_cast<int>(ncols >> 3);
   const int ucol0 = static_cast<int>(col0 >> 3);
   const int64_t cpr = c.cols >> 3;  // codes per full row
   const int gdiv = static_cast<int>(c.group);
   constexpr int CH = kCbThreads * kCbPerThread;
   const int ipr = (ncodes + CH - 1) / CH;  // passes per row
-  const int64_t items = nrows * ipr;
+  const int drow = static_cast<int>(gridDim.x) / ipr, dpass = static_cast<int>(gridDim.x) % ipr;
+  int64_t rr = static_cast<int64_t>(blockIdx.x) / ipr;
+  int pass = static_cast<int>(blockIdx.x) % ipr;
   uint32_t code[kCbPerThread];
   float scl[kCbPerThread];
-  auto fetch = [&](int64_t item) {
-    const int64_t rr = item / ipr;
-    const int base = static_cast<int>(item - rr * ipr) * CH + threadIdx.x;
-    const uint16_t* crow = c.codes + (row0 + rr) * cpr + ucol0;
-    const float* srow = c.scales + (row0 + rr) * c.ng;
+  auto fetch = [&](int64_t r, int ps) {
+    const int base = ps * CH + static_cast<int>(threadIdx.x);
+    const uint16_t* crow = c.codes + (row0 + r) * cpr + ucol0;
+    const float* srow = c.scales + (row0 + r) * c.ng;
 #pragma unroll
     for (int j = 0; j < kCbPerThread; ++j) {
       const int it = base + j * kCbThreads;
@@ -88,10 +130,9 @@ __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
       scl[j] = it < ncodes ? __ldg(srow + (gshift >= 0 ? (k >> gshift) : k / gdiv)) : 0.0f;
     }
   };
-  int64_t item = blockIdx.x;
-  if (item < items) fetch(item);
+  if (rr < nrows) fetch(rr, pass);
   __syncthreads();
-  for (; item < items; item += gridDim.x) {
+  while (rr < nrows) {
     uint32_t cur[kCbPerThread];
     float cs[kCbPerThread];
 #pragma unroll
@@ -99,22 +140,25 @@ __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
       cur[j] = code[j];
       cs[j] = scl[j];
     }
-    if (item + gridDim.x < items) fetch(item + gridDim.x);  // next item in flight
-    const int64_t rr = item / ipr;
-    const int base = static_cast<int>(item - rr * ipr) * CH + threadIdx.x;
+    const int64_t r_cur = rr;
+    const int p_cur = pass;
+    pass += dpass;
+    rr += drow;
+    if (pass >= ipr) {
+      pass -= ipr;
+      ++rr;
+    }
+    if (rr < nrows) fetch(rr, pass);  // next item in flight
+    const int base = p_cur * CH + static_cast<int>(threadIdx.x);
+    void* orow = F32 ? static_cast<void*>(reinterpret_cast<float*>(out) + r_cur * ld)
+                     : static_cast<void*>(reinterpret_cast<__nv_bfloat16*>(out) + r_cur * ld);
 #pragma unroll
     for (int j = 0; j < kCbPerThread; ++j) {
       const int it = base + j * kCbThreads;
       if (it >= ncodes) break;
-      const float4 m0 = cb[(cur[j] & 0xFFu) * 2], m1 = cb[(cur[j] & 0xFFu) * 2 + 1];
-      const float mag[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-      float f[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const uint32_t neg = (cur[j] >> (8 + e)) & 1u;
-        f[e] = __uint_as_float(__float_as_uint(__fmul_rn(cs[j], mag[e])) ^ (neg << 31));
-      }
-      cb2_store<F32, VEC>(out, rr * ld + (static_cast<int64_t>(it) << 3), f);
+      float m[8];
+      cb2_mags<CB16>(cur[j], cbh, cb0, cb1, m);
+      cb2_emit<F32, VEC>(orow, static_cast<int64_t>(it) << 3, cur[j], cs[j], m);
     }
   }
 }
@@ -133,7 +177,7 @@ cudaError_t launch_cb2_materialize(const Cb2Dev& c, int64_t row0, int64_t nrows,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 0;  // one resident wave
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cb2_materialize<true, true>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cb2_materialize<false, true, false>,
                                                     kCbThreads, 0) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   const int64_t cap = static_cast<int64_t>(sms) * per_sm;
@@ -141,21 +185,23 @@ cudaError_t launch_cb2_materialize(const Cb2Dev& c, int64_t row0, int64_t nrows,
   const int64_t items = nrows * ((ncodes + kCbThreads * kCbPerThread - 1) / (kCbThreads * kCbPerThread));
   const dim3 grid(static_cast<unsigned>(items < cap ? items : cap));
   note_launch();
-  if (f32) {
-    if (vec)
-      k_cb2_materialize<true, true><<<grid, kCbThreads, 0, st>>>(c, row0, nrows, col0, ncols, out,
-                                                                 ld, gshift);
-    else
-      k_cb2_materialize<true, false><<<grid, kCbThreads, 0, st>>>(c, row0, nrows, col0, ncols,
-                                                                  out, ld, gshift);
+#define MLRA_CB2_LAUNCH(F, V, H)                                                          \
+  k_cb2_materialize<F, V, H><<<grid, kCbThreads, 0, st>>>(c, row0, nrows, col0, ncols, out, \
+                                                          ld, gshift)
+  if (c.bf16) {
+    if (f32) {
+      if (vec) MLRA_CB2_LAUNCH(true, true, true); else MLRA_CB2_LAUNCH(true, false, true);
+    } else {
+      if (vec) MLRA_CB2_LAUNCH(false, true, true); else MLRA_CB2_LAUNCH(false, false, true);
+    }
   } else {
-    if (vec)
-      k_cb2_materialize<false, true><<<grid, kCbThreads, 0, st>>>(c, row0, nrows, col0, ncols,
-                                                                  out, ld, gshift);
-    else
-      k_cb2_materialize<false, false><<<grid, kCbThreads, 0, st>>>(c, row0, nrows, col0, ncols,
-                                                                   out, ld, gshift);
+    if (f32) {
+      if (vec) MLRA_CB2_LAUNCH(true, true, false); else MLRA_CB2_LAUNCH(true, false, false);
+    } else {
+      if (vec) MLRA_CB2_LAUNCH(false, true, false); else MLRA_CB2_LAUNCH(false, false, false);
+    }
   }
+#undef MLRA_CB2_LAUNCH
   return cudaGetLastError();
 }
 

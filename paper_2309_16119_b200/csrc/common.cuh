@@ -38,7 +38,14 @@ struct QWeightDev {
 struct Cb2Dev {
   int64_t rows, cols, group, ng;  // ng = cols / group
   const uint16_t* codes;          // [rows x cols/8]
-  const float* codebook;          // [256 x 8], 16-B aligned
+  // Device codebook layout (host-converted at upload; shared-memory gathers are
+  // random, so the layout sets the bank-conflict cost):
+  //  bf16 != 0: every magnitude is exactly a bf16 -> uint4[256], entry i = 8 bf16
+  //             (one 16-B gather per code; products stay exact in f32);
+  //  bf16 == 0: float4[2][256]: entries 0-3 of code i at [0][i], 4-7 at [1][i]
+  //             (each gather's 16-B slot spans all 8 bank groups).
+  const void* codebook;           // 16-B aligned
+  int bf16;
   const float* scales;            // [rows x ng]
 };
 

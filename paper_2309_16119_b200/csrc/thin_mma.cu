@@ -60,7 +60,10 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], 
 // issue slots on ldmatrix + mma only. Reads use the 128-B swizzle: 16-B chunk
 // c of row r sits at r*128 + ((c ^ (r & 7)) << 4).
 
-constexpr int TNS = 6;  // TMA ring depth (units in flight per CTA)
+#ifndef MLRA_THIN_NS
+#define MLRA_THIN_NS 6
+#endif
+constexpr int TNS = MLRA_THIN_NS;  // TMA ring depth (units in flight per CTA)
 
 template <int NT>
 struct ThinSmem {
@@ -411,10 +414,8 @@ cudaError_t launch_prep(const PrepBatch& b, cudaStream_t st) {
   for (int t = 0; t < b.n; ++t) {
     const int64_t count = b.offs[t + 1] - b.offs[t];
     if (count >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
-    // ~1 element per thread: the tasks are latency-bound (a dependent global
-    // load per element), so parallelism, not per-thread work, sets the time
-    int64_t want = (count + 255) / 256;
-    if (want > 32 * sms()) want = 32 * sms();
+    int64_t want = (count + 4 * 256 - 1) / (4 * 256);  // ~4 elements per thread
+    if (want > 4 * sms()) want = 4 * sms();
     pbk.first[t] = nb;
     nb += static_cast<int>(want);  // zero-size tasks get no block
   }

@@ -267,3 +267,18 @@ def test_device_rtn_edge_grids():
     with pytest.raises(MlraError) as e:
         M.RtnQuantizer().quantize(torch.from_numpy(w), None, 4, 5)
     assert e.value.kind == "ConfigError"
+
+
+@pytest.mark.gpu
+def test_cb2_materialize_non_bf16_codebook():
+    # magnitudes that are not bf16-exact take the f32 codebook layout
+    rng = np.random.default_rng(9)
+    cb = (rng.random((256, 8)) * 3.0 + 0.1).astype(np.float32)
+    m = _random_cb2(130, 512, 64, seed=4)
+    m = M.Cb2Matrix(m.rows, m.cols, m.group_size, m.codes, cb, m.scales)
+    dq = M.Codebook2Quantizer(cb).upload(m)
+    want = orc.cb2_dequantize_f32(m.codes, m.rows, m.cols, m.group_size, cb, m.scales)
+    got = M.dequantize(dq, torch.float32).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    got16 = M.dequantize(dq, torch.bfloat16).view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(got16, orc.f32_to_bf16_bits(want))
