@@ -9,9 +9,9 @@
 // RN to bf16 for the GEMM operand.
 //
 // k_cb2_materialize is HBM-bound: 0.25 B of code + 4/g B of scale read and
-// 2 (bf16) or 4 (f32) B written per entry. The 8 KB codebook lives in shared
-// memory (one float4 pair per code lookup); each thread owns 4 codes strided
-// by the block size so a warp's 16-B stores cover a contiguous 512 B (bf16).
+// 2 (bf16) or 4 (f32) B written per entry. The codebook lives in shared memory
+// in a bank-conflict-aware layout (Cb2Dev); every warp store covers a
+// contiguous 512 B.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -25,10 +25,6 @@ namespace {
 constexpr int kCbThreads = 256;
 constexpr int kCbPerThread = 4;
 
-// One code -> 8 outputs. Products RN_f32(s·mag) (scalar IEEE multiplies); the
-// sign is applied after rounding (RN commutes with negation): for bf16, the
-// mask of entries (2p, 2p+1) is ((code >> (8+2p)) & 3) * 0x40008000 &
-// 0x80008000 — bit 15 and bit 31 of the packed pair — 3 ops per pair.
 // Magnitudes of a code's 8 entries from the shared codebook.
 template <bool CB16>
 __device__ __forceinline__ void cb2_mags(uint32_t code, const uint4* cbh, const float4* cb0,
@@ -49,43 +45,59 @@ __device__ __forceinline__ void cb2_mags(uint32_t code, const uint4* cbh, const 
   }
 }
 
-// One code -> 8 outputs. Products RN_f32(s·mag) (scalar IEEE multiplies); the
-// sign is applied after rounding (RN commutes with negation): for bf16, the
-// mask of entries (2p, 2p+1) is ((code >> (8+2p)) & 3) * 0x40008000 &
+// One code -> 8 bf16 outputs. Products RN_f32(s·mag) (scalar IEEE
+// multiplies); the sign is applied after rounding (RN commutes with negation):
+// the mask of entries (2p, 2p+1) is ((code >> (8+2p)) & 3) * 0x40008000 &
 // 0x80008000 — bit 15 and bit 31 of the packed pair — 3 ops per pair.
-template <bool F32, bool VEC>
+template <bool VEC>
 __device__ __forceinline__ void cb2_emit(void* __restrict__ out, int64_t o, uint32_t code, float s,
                                          const float (&m)[8]) {
   float f[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) f[e] = __fmul_rn(s, m[e]);
-  if constexpr (!F32) {
-    uint4 v;
-    v.x = pack_bf16x2(f[0], f[1]) ^ ((((code >> 8) & 3u) * 0x40008000u) & 0x80008000u);
-    v.y = pack_bf16x2(f[2], f[3]) ^ ((((code >> 10) & 3u) * 0x40008000u) & 0x80008000u);
-    v.z = pack_bf16x2(f[4], f[5]) ^ ((((code >> 12) & 3u) * 0x40008000u) & 0x80008000u);
-    v.w = pack_bf16x2(f[6], f[7]) ^ ((((code >> 14) & 3u) * 0x40008000u) & 0x80008000u);
-    if constexpr (VEC) {
-      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + o) = v;
-    } else {
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        reinterpret_cast<uint16_t*>(out)[o + e] =
-            static_cast<uint16_t>(w[e >> 1] >> (16 * (e & 1)));
-    }
+  uint4 v;
+  v.x = pack_bf16x2(f[0], f[1]) ^ ((((code >> 8) & 3u) * 0x40008000u) & 0x80008000u);
+  v.y = pack_bf16x2(f[2], f[3]) ^ ((((code >> 10) & 3u) * 0x40008000u) & 0x80008000u);
+  v.z = pack_bf16x2(f[4], f[5]) ^ ((((code >> 12) & 3u) * 0x40008000u) & 0x80008000u);
+  v.w = pack_bf16x2(f[6], f[7]) ^ ((((code >> 14) & 3u) * 0x40008000u) & 0x80008000u);
+  if constexpr (VEC) {
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + o) = v;
   } else {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      f[e] = __uint_as_float(__float_as_uint(f[e]) ^ (((code >> (8 + e)) & 1u) << 31));
-    if constexpr (VEC) {
-      float4* q = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + o);
-      q[0] = make_float4(f[0], f[1], f[2], f[3]);
-      q[1] = make_float4(f[4], f[5], f[6], f[7]);
-    } else {
+      reinterpret_cast<uint16_t*>(out)[o + e] = static_cast<uint16_t>(w[e >> 1] >> (16 * (e & 1)));
+  }
+}
+
+// f32 output, half a code per thread: entries 4h..4h+3 of the code, one
+// 16-B store — adjacent lanes write adjacent 16 B, so each warp store covers
+// a contiguous 512 B (a whole code per lane would leave 32-B gaps per store).
+template <bool VEC, bool CB16>
+__device__ __forceinline__ void cb2_emit_half(float* __restrict__ out, int64_t o, uint32_t code,
+                                              float s, int h, const uint4* cbh, const float4* cb0,
+                                              const float4* cb1) {
+  const uint32_t i = code & 0xFFu;
+  float m[4];
+  if constexpr (CB16) {
+    const uint4 q = cbh[i];
+    const uint32_t a = h ? q.z : q.x, b = h ? q.w : q.y;
+    m[0] = __uint_as_float(a << 16), m[1] = __uint_as_float(a & 0xFFFF0000u);
+    m[2] = __uint_as_float(b << 16), m[3] = __uint_as_float(b & 0xFFFF0000u);
+  } else {
+    const float4 v = h ? cb1[i] : cb0[i];
+    m[0] = v.x, m[1] = v.y, m[2] = v.z, m[3] = v.w;
+  }
+  const uint32_t sg = code >> (8 + 4 * h);
+  float f[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) reinterpret_cast<float*>(out)[o + e] = f[e];
-    }
+  for (int e = 0; e < 4; ++e)
+    f[e] = __uint_as_float(__float_as_uint(__fmul_rn(s, m[e])) ^ (((sg >> e) & 1u) << 31));
+  if constexpr (VEC) {
+    *reinterpret_cast<float4*>(out + o) = make_float4(f[0], f[1], f[2], f[3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) out[o + e] = f[e];
   }
 }
 
@@ -107,12 +119,14 @@ __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
   const float4* cb1 = cbs + 256;
   for (int i = threadIdx.x; i < (CB16 ? 256 : 512); i += kCbThreads)
     cbs[i] = __ldg(reinterpret_cast<const float4*>(c.codebook) + i);
+  constexpr int SH = F32 ? 1 : 0;  // work unit: a code (bf16) or half a code (f32)
   const int ncodes = static_cast<int>(ncols >> 3);
+  const int nunits = ncodes << SH;
   const int ucol0 = static_cast<int>(col0 >> 3);
   const int64_t cpr = c.cols >> 3;  // codes per full row
   const int gdiv = static_cast<int>(c.group);
   constexpr int CH = kCbThreads * kCbPerThread;
-  const int ipr = (ncodes + CH - 1) / CH;  // passes per row
+  const int ipr = (nunits + CH - 1) / CH;  // passes per row
   const int drow = static_cast<int>(gridDim.x) / ipr, dpass = static_cast<int>(gridDim.x) % ipr;
   int64_t rr = static_cast<int64_t>(blockIdx.x) / ipr;
   int pass = static_cast<int>(blockIdx.x) % ipr;
@@ -125,9 +139,10 @@ __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
 #pragma unroll
     for (int j = 0; j < kCbPerThread; ++j) {
       const int it = base + j * kCbThreads;
-      const int k = (ucol0 + it) << 3;
-      code[j] = it < ncodes ? __ldg(crow + it) : 0u;
-      scl[j] = it < ncodes ? __ldg(srow + (gshift >= 0 ? (k >> gshift) : k / gdiv)) : 0.0f;
+      const int ci = it >> SH;
+      const int k = (ucol0 + ci) << 3;
+      code[j] = it < nunits ? __ldg(crow + ci) : 0u;
+      scl[j] = it < nunits ? __ldg(srow + (gshift >= 0 ? (k >> gshift) : k / gdiv)) : 0.0f;
     }
   };
   if (rr < nrows) fetch(rr, pass);
@@ -155,10 +170,15 @@ __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
 #pragma unroll
     for (int j = 0; j < kCbPerThread; ++j) {
       const int it = base + j * kCbThreads;
-      if (it >= ncodes) break;
-      float m[8];
-      cb2_mags<CB16>(cur[j], cbh, cb0, cb1, m);
-      cb2_emit<F32, VEC>(orow, static_cast<int64_t>(it) << 3, cur[j], cs[j], m);
+      if (it >= nunits) break;
+      if constexpr (F32) {
+        cb2_emit_half<VEC, CB16>(static_cast<float*>(orow), static_cast<int64_t>(it) << 2, cur[j],
+                                 cs[j], it & 1, cbh, cb0, cb1);
+      } else {
+        float m[8];
+        cb2_mags<CB16>(cur[j], cbh, cb0, cb1, m);
+        cb2_emit<VEC>(orow, static_cast<int64_t>(it) << 3, cur[j], cs[j], m);
+      }
     }
   }
 }
@@ -181,8 +201,8 @@ cudaError_t launch_cb2_materialize(const Cb2Dev& c, int64_t row0, int64_t nrows,
                                                     kCbThreads, 0) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   const int64_t cap = static_cast<int64_t>(sms) * per_sm;
-  const int64_t ncodes = ncols >> 3;
-  const int64_t items = nrows * ((ncodes + kCbThreads * kCbPerThread - 1) / (kCbThreads * kCbPerThread));
+  const int64_t nunits = (ncols >> 3) << (f32 ? 1 : 0);
+  const int64_t items = nrows * ((nunits + kCbThreads * kCbPerThread - 1) / (kCbThreads * kCbPerThread));
   const dim3 grid(static_cast<unsigned>(items < cap ? items : cap));
   note_launch();
 #define MLRA_CB2_LAUNCH(F, V, H)                                                          \

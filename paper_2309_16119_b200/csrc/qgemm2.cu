@@ -143,8 +143,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* qfull = empty + STAGES;
   uint64_t* qempty = qfull + MAX_QS;
   uint64_t* tfull = qempty + MAX_QS;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tempty = tfull + 1;    // accumulator 0 (tokens 0..255 of the pair tile) drained
+  uint64_t* tempty1 = tempty + 1;  // accumulator 1 drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty1 + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -187,6 +188,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 2 * 4);
+    mbar_init(tempty1, 2 * 4);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc2(tmem_slot, TMEM_COLS);
@@ -249,39 +251,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t ph = 0;
       unsigned long long t_full = 0, t_tempty = 0;
       const unsigned long long t_start = p.trace ? clock64() : 0;
+      // k16 MMAs of stage s (k-block kb) into accumulators [a0, a1]; per k16 the
+      // accumulators are issued back to back so they share the A (weight) read
+      auto issue = [&](int s_, int kb, int kb0, int a0, int a1) {
+        const bool lora = kb >= n_kb_main;
+        const int nk16 = (lora && kb == n_kb - 1) ? p.lora_k16_last : BK / 16;
+        const uint32_t sw = smem_u32(sW + s_ * W_TILE);
+        const uint32_t st = smem_u32(sT + s_ * T_TILE);
+        for (int k = 0; k < nk16; ++k) {
+          uint64_t adesc;
+          uint32_t idesc;
+          if (MN && !lora) {
+            adesc = sdesc_sw128(sw + k * 2048, 8192, 1024);
+            idesc = idesc_main;
+          } else {
+            adesc = sdesc_sw128(sw + k * 32, 16, 1024);
+            idesc = idesc_kmaj;
+          }
+          for (int a = a0; a <= a1; ++a) {
+            const uint64_t bdesc = sdesc_sw128(st + a * HB_TILE + k * 32, 16, 1024);
+            tc_mma_f16_2sm(tmem_base + a * (2 * HB), adesc, bdesc, idesc,
+                           (kb == kb0 && k == 0) ? 0u : 1u);
+          }
+        }
+      };
       for (int sg = 0; sg < mma_nseg; ++sg) {
         const int kb0 = sg == 0 ? mma_kb_first : 0;
         const int kb1 = (sg == mma_nseg - 1 && mma_kb_last > 0) ? mma_kb_last : n_kb;
+        // The epilogue drains accumulator 0 first and releases it early
+        // (tempty): the first `pre` k-blocks' accumulator-0 MMAs of this tile
+        // run while accumulator 1 is still being drained; their stages are
+        // released once accumulator 1's MMAs for them follow (tempty1).
+        const int pre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
         const unsigned long long tw0 = p.trace ? clock64() : 0;
         mbar_wait_acq_cluster(tempty, (sg & 1) ^ 1);
         if (p.trace) t_tempty += clock64() - tw0;
         tc_fence_after();
-        for (int kb = kb0; kb < kb1; ++kb) {
+        int s0 = s;
+        uint32_t ph0 = ph;
+        for (int i = 0; i < pre; ++i) {
           const unsigned long long tf0 = p.trace ? clock64() : 0;
           mbar_wait_acq_cluster(&full[s], ph);
           if (p.trace) t_full += clock64() - tf0;
           tc_fence_after();
-          const bool lora = kb >= n_kb_main;
-          const int nk16 = (lora && kb == n_kb - 1) ? p.lora_k16_last : BK / 16;
-          const uint32_t sw = smem_u32(sW + s * W_TILE);
-          const uint32_t st = smem_u32(sT + s * T_TILE);
-          for (int k = 0; k < nk16; ++k) {
-            uint64_t adesc;
-            uint32_t idesc;
-            if (MN && !lora) {
-              adesc = sdesc_sw128(sw + k * 2048, 8192, 1024);
-              idesc = idesc_main;
-            } else {
-              adesc = sdesc_sw128(sw + k * 32, 16, 1024);
-              idesc = idesc_kmaj;
-            }
-#pragma unroll
-            for (int a = 0; a < 2; ++a) {
-              const uint64_t bdesc = sdesc_sw128(st + a * HB_TILE + k * 32, 16, 1024);
-              tc_mma_f16_2sm(tmem_base + a * (2 * HB), adesc, bdesc, idesc,
-                             (kb == kb0 && k == 0) ? 0u : 1u);
-            }
+          issue(s, kb0 + i, kb0, 0, 0);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
           }
+        }
+        const unsigned long long tw1 = p.trace ? clock64() : 0;
+        mbar_wait_acq_cluster(tempty1, (sg & 1) ^ 1);
+        if (p.trace) t_tempty += clock64() - tw1;
+        tc_fence_after();
+        for (int i = 0; i < pre; ++i) {
+          issue(s0, kb0 + i, kb0, 1, 1);
+          tc_commit_2sm_mc(&empty[s0], 0x3);
+          if (++s0 == STAGES) {
+            s0 = 0;
+            ph0 ^= 1;
+          }
+        }
+        (void)ph0;
+        for (int kb = kb0 + pre; kb < kb1; ++kb) {
+          const unsigned long long tf0 = p.trace ? clock64() : 0;
+          mbar_wait_acq_cluster(&full[s], ph);
+          if (p.trace) t_full += clock64() - tf0;
+          tc_fence_after();
+          issue(s, kb, kb0, 0, 1);
           tc_commit_2sm_mc(&empty[s], 0x3);
           if (++s == STAGES) {
             s = 0;
@@ -333,6 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int qd = warp & 3;
     const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
+    const uint32_t tempty1_leader = mapa(smem_u32(tempty1), 0);
     int local = 0;
     SegSched sc = sched;
     int tile, kb0, kb1;
@@ -423,12 +461,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           tmem_ld_32x32b_x32(taddr + (cc + 1) * 32, rb);
           handle(ra, cc);
           tc_wait_ld();
+          if (cc + 1 == 7) {
+            tc_fence_before();  // accumulator 0 (chunks 0..7) fully read
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader);
+          }
           if (cc + 2 < 16) {
             tmem_ld_32x32b_x32(taddr + (cc + 2) * 32, ra);
           } else {
             tc_fence_before();  // all TMEM reads of this tile are complete
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty_leader);
+            if (lane == 0) mbar_arrive_cluster(tempty1_leader);
           }
           handle(rb, cc + 1);
           if (cc + 2 < 16) tc_wait_ld();

@@ -61,7 +61,7 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], 
 // c of row r sits at r*128 + ((c ^ (r & 7)) << 4).
 
 #ifndef MLRA_THIN_NS
-#define MLRA_THIN_NS 6
+#define MLRA_THIN_NS 3
 #endif
 constexpr int TNS = MLRA_THIN_NS;  // TMA ring depth (units in flight per CTA)
 
