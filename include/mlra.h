@@ -258,6 +258,24 @@ MLRA_API mlra_status mlra_adamw_step(const mlra_adamw* opt, int64_t step_index, 
                                      void* stream);
 
 /* ------------------------------------------------------------------------
+ * Data-parallel exchange: tokens sharded across ranks, frozen
+ * weights replicated; the only per-step exchange is a sum all-reduce of the
+ * flat fp32 LoRA-gradient bucket ({dA, dB[, dbias]} per layer, the parameter
+ * order of ToyModel::trainable_params, model.cpp:170-184), NCCL over NVLink /
+ * NVSwitch. NCCL is loaded at run time (dlopen libnccl.so.2); without it these
+ * return MLRA_ERR_UNSUPPORTED. The reference itself has no distribution
+ * (SPEC.md:453). */
+typedef struct mlra_dp mlra_dp;
+/* Rank 0 creates the 128-byte id and shares it out of band (file, socket). */
+MLRA_API mlra_status mlra_dp_unique_id(void* id_out);
+/* One communicator per process (one process per GPU; the current device). */
+MLRA_API mlra_status mlra_dp_init(int rank, int world, const void* id, mlra_dp** out);
+/* In-place sum all-reduce of `count` fp32 gradients on `stream`. */
+MLRA_API mlra_status mlra_allreduce_lora_grads(mlra_dp* dp, float* bucket, uint64_t count,
+                                               void* stream);
+MLRA_API void mlra_dp_destroy(mlra_dp* dp);
+
+/* ------------------------------------------------------------------------
  * On-disk checkpoint -> device. The reference's binary .mlra
  * format (checkpoint.hpp:4-24, little-endian): parsed and validated with the
  * reference's rules and error taxonomy (checkpoint.cpp:141-306: FormatError

@@ -556,6 +556,31 @@ class AdamW {
   std::vector<std::size_t> sizes_;
 };
 
+// ----------------------------------------------------------------- data parallelism
+// One sum all-reduce of the flat fp32 LoRA-gradient bucket per step (NCCL, loaded
+// by libmlra at run time). Rank 0 calls unique_id() and shares the bytes.
+class GradExchange {
+ public:
+  static std::vector<unsigned char> unique_id() {
+    std::vector<unsigned char> id(128);
+    check(mlra_dp_unique_id(id.data()));
+    return id;
+  }
+  GradExchange(int rank, int world, const std::vector<unsigned char>& id) {
+    if (id.size() != 128) throw ContractError("dp: unique id must be 128 bytes");
+    check(mlra_dp_init(rank, world, id.data(), &h_));
+  }
+  ~GradExchange() { mlra_dp_destroy(h_); }
+  GradExchange(const GradExchange&) = delete;
+  GradExchange& operator=(const GradExchange&) = delete;
+  void allreduce(float* bucket, std::size_t count, cudaStream_t st = nullptr) {
+    check(mlra_allreduce_lora_grads(h_, bucket, count, st));
+  }
+
+ private:
+  mlra_dp* h_ = nullptr;
+};
+
 // ----------------------------------------------------------------- checkpoint.hpp:36-67
 // The .mlra format -> device: parse + validate like load_model (FormatError
 // kinds/offsets, IoError), upload layers verbatim, save byte-identically.

@@ -29,6 +29,7 @@ EXPORTS = [
     "mlra_checkpoint_layer_count", "mlra_checkpoint_layer", "mlra_checkpoint_config_json",
     "mlra_checkpoint_frozen_hash", "mlra_checkpoint_file_hash", "mlra_checkpoint_upload",
     "mlra_checkpoint_set_adapter", "mlra_checkpoint_save", "mlra_quantize_rtn",
+    "mlra_dp_unique_id", "mlra_dp_init", "mlra_allreduce_lora_grads", "mlra_dp_destroy",
 ]
 
 # mlra_hook.materialize(state, q, row0, nrows, col0, ncols, out, dtype, ld, stream)
@@ -164,6 +165,14 @@ def lib() -> C.CDLL:
         L.mlra_checkpoint_save.argtypes = [vp, C.c_char_p]
         L.mlra_quantize_rtn.restype = i32
         L.mlra_quantize_rtn.argtypes = [vp, i32, i64, i64, i32, i64, vp, vp, vp, vp]
+        L.mlra_dp_unique_id.restype = i32
+        L.mlra_dp_unique_id.argtypes = [vp]
+        L.mlra_dp_init.restype = i32
+        L.mlra_dp_init.argtypes = [i32, i32, vp, C.POINTER(vp)]
+        L.mlra_allreduce_lora_grads.restype = i32
+        L.mlra_allreduce_lora_grads.argtypes = [vp, vp, u64, vp]
+        L.mlra_dp_destroy.restype = None
+        L.mlra_dp_destroy.argtypes = [vp]
         _lib = L
     return _lib
 

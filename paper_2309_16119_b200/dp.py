@@ -77,3 +77,43 @@ class GradBucket:
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
             dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=group)
+
+
+class NcclGradExchange:
+    """The same exchange through libmlra's own C ABI (mlra_dp_* /
+    mlra_allreduce_lora_grads: NCCL loaded by the library) for processes that
+    do not run torch.distributed — the path a C++ caller of include/mlra.h
+    uses. Rank 0 makes the id (``unique_id()``) and shares it out of band."""
+
+    def __init__(self, rank: int, world: int, uid: bytes):
+        import ctypes as C
+        from ._lib import check, lib
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self._buf = C.create_string_buffer(uid, 128)
+        h = C.c_void_p()
+        check(lib().mlra_dp_init(rank, world, self._buf, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        from ._lib import check, lib
+        b = C.create_string_buffer(128)
+        check(lib().mlra_dp_unique_id(b))
+        return b.raw
+
+    def allreduce(self, bucket: GradBucket, stream=None) -> None:
+        from ._lib import check, lib
+        s = stream if stream is not None else torch.cuda.current_stream()
+        check(lib().mlra_allreduce_lora_grads(self._h, bucket.flat.data_ptr(), bucket.flat.numel(),
+                                              s.cuda_stream))
+
+    def __del__(self):
+        try:
+            from . import _lib
+            if getattr(self, "_h", None) is not None and self._h.value and _lib._lib is not None:
+                _lib.lib().mlra_dp_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
