@@ -5,7 +5,8 @@ The compute lives in libmlra.so (include/mlra.h); this package is the host-side
 mirror of the reference interface (see modulora.py)."""
 from ._lib import MlraError, build, lib  # noqa: F401
 from .modulora import (  # noqa: F401
-    DeviceQuantizedMatrix, LoraAdapter, LpLinearContext, MaterializationStrategy,
-    ModuLoraLayer, ModuLoraLinearFunction, PackedCodes, QuantizedMatrix, dequantize,
-    dequantize_row, grads_of_adapter, init_adapter, layer_backward, layer_forward, lp_backward,
-    lp_forward, make_layer, packed_word_count, parse_strategy, strategy_name)
+    Cb2Matrix, Codebook2Quantizer, DeviceQuantizedMatrix, DoublingQuantizer, LoraAdapter,
+    LpLinearContext, MaterializationStrategy, ModuLoraLayer, ModuLoraLinearFunction, PackedCodes,
+    QuantizedMatrix, QuantizerHook, RtnQuantizer, default_cb2_codebook, dequantize,
+    dequantize_row, dequantize_tile, grads_of_adapter, init_adapter, layer_backward, layer_forward,
+    lp_backward, lp_forward, make_layer, packed_word_count, parse_strategy, strategy_name)

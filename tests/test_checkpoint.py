@@ -8,7 +8,6 @@ are the constants pinned in acceptance.cpp:462-463 / test_checkpoint.cpp:31-32.
 """
 import json
 import os
-import shutil
 
 import numpy as np
 import pytest
