@@ -327,3 +327,51 @@ def test_stream_k_layer_with_lora_and_bias(monkeypatch):
         res[sk] = (f64(y), f64(dx))
     assert rel_fro(res["1"][0], res["0"][0]) <= 1e-5
     assert rel_fro(res["1"][1], res["0"][1]) <= 1e-5
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_identity_and_one_hot_exact(strategy):
+    # test_lowprec.cpp:73-96: identity weights pass x and g through exactly; a one-hot
+    # input reads out one column of the dequantized weights exactly
+    n = 256
+    codes = np.zeros((n, n), np.uint32)
+    codes[np.arange(n), np.arange(n)] = 1
+    words = orc.pack(codes.ravel(), 8)
+    dq = M.DeviceQuantizedMatrix(qmatrix(words, n, n, 8, n, np.ones(n, np.float32),
+                                         np.zeros(n, np.float32)))
+    ctx = M.LpLinearContext(dq, strategy)
+    x64 = orc.bf16_round(orc.gaussian(3, 40, n))
+    x = to_bf16_dev(x64)
+    assert np.array_equal(f64(M.lp_forward(ctx, x, torch.float32)), x64)
+    assert np.array_equal(f64(M.lp_backward(ctx, x, torch.float32)), x64)
+    q, words, sc, z = random_quantized(384, 512, 3, 128, seed=12)
+    dq = M.DeviceQuantizedMatrix(q)
+    wb = deq_bf16_f64(words, 384, 512, 3, 128, sc, z)
+    k = 137
+    e = np.zeros((3, 512))
+    e[:, k] = 1.0
+    y = f64(M.lp_forward(M.LpLinearContext(dq, strategy), to_bf16_dev(e), torch.float32))
+    assert np.array_equal(y[0], wb[:, k])
+
+
+def test_fresh_adapter_equals_base_and_zero_base():
+    # test_lora.cpp:91-150: with A = 0 (the init) the layer is the base linear; a
+    # zero base leaves only the adapter term
+    d_out, d_in, r, m = 512, 768, 8, 100
+    q, words, sc, z = random_quantized(d_out, d_in, 4, 128, seed=21)
+    dq = M.DeviceQuantizedMatrix(q)
+    layer = M.make_layer("fresh", dq, r, 16.0, seed=3)
+    x = to_bf16_dev(orc.bf16_round(orc.gaussian(22, m, d_in)))
+    y, _ = M.layer_forward(layer, x, out_dtype=torch.float32)
+    base = M.lp_forward(M.LpLinearContext(dq, M.MaterializationStrategy.RowMaterialize), x,
+                        torch.float32)
+    assert torch.equal(y, base)
+    zq = qmatrix(orc.pack(np.zeros(d_out * d_in, np.uint32), 2), d_out, d_in, 2, 128,
+                 np.ones(d_out * d_in // 128, np.float32), np.zeros(d_out * d_in // 128, np.float32))
+    zl = M.ModuLoraLayer("zero", M.DeviceQuantizedMatrix(zq),
+                         M.LoraAdapter((torch.randn(d_out, r) * 0.1).cuda(),
+                                       (torch.randn(d_in, r) * 0.1).cuda(), r, 16.0))
+    yz, xb = M.layer_forward(zl, x, out_dtype=torch.float32)
+    s = 16.0 / r
+    ref = orc.bf16_round(s * f64(xb)) @ orc.bf16_round(f64(zl.adapter.a)).T
+    assert rel_fro(f64(yz), ref) <= 1e-5

@@ -170,3 +170,32 @@ def test_stack_trainer_step_matches_oracle():
         assert np.array_equal(tr.params.flat.cpu().numpy(), ps[0].astype(np.float32))
     # the layers read the updated factors (views into the flat parameter bucket)
     assert layers[0].adapter.a.data_ptr() == tr.params.flat.data_ptr()
+
+
+@pytest.mark.gpu
+def test_stack_trainer_fits_a_planted_adapter():
+    # finetune efficacy (the reference's C7, acceptance.cpp): a target made by a
+    # planted rank-r update of the frozen layer is fitted by training the adapter
+    # with the device step (fwd, bwd, AdamW); the loss must fall by 10x
+    from paper_2309_16119_b200 import modulora as M
+    from tests.gpu_util import random_quantized
+    d_out, d_in, r, m = 256, 512, 8, 512
+    q, *_ = random_quantized(d_out, d_in, 4, 128, seed=90)
+    L = M.make_layer("l", M.DeviceQuantizedMatrix(q), r, 16.0, seed=91)
+    g = torch.Generator(device="cpu").manual_seed(92)
+    x = torch.randn(m, d_in, generator=g).cuda().to(torch.bfloat16)
+    with torch.no_grad():
+        base, _ = M.layer_forward(L, x, out_dtype=torch.float32)
+        bp = (torch.randn(d_in, r, generator=g) * 0.05).cuda()
+        ap = (torch.randn(d_out, r, generator=g) * 0.05).cuda()
+        planted = (x.float() @ bp) @ ap.T  # representable by the adapter: s·(x·B)·Aᵀ
+        target = base + planted
+    tr = T.LinearStackTrainer([L], T.TrainConfig(steps=200, lr=3e-3))
+    losses = []
+    for _ in range(200):
+        (y, xb), = tr.forward([x])
+        diff = y.float() - target
+        losses.append(float((diff ** 2).mean()))
+        tr.backward([x], [xb], [diff.to(torch.bfloat16)])  # ∝ d(mean sq. error)/dy
+        tr.optimizer_step(check_finite=False)
+    assert losses[-1] < 0.1 * losses[0], (losses[0], losses[-1])
