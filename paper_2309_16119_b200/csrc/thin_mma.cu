@@ -65,10 +65,17 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], 
 #endif
 constexpr int TNS = MLRA_THIN_NS;  // TMA ring depth (units in flight per CTA)
 
+#ifndef MLRA_THIN_WARPS
+#define MLRA_THIN_WARPS 8
+#endif
+constexpr int TW = MLRA_THIN_WARPS;   // warps per CTA; each owns 16 output rows of a unit
+constexpr int TM = 16 * TW;           // output-tile rows per unit (tokens or n)
+constexpr int TTHREADS = 32 * TW;
+
 template <int NT>
 struct ThinSmem {
   static constexpr int ROWS = 8 * NT;
-  static constexpr int ACT = TILE * 128;        // 64 x 64 bf16
+  static constexpr int ACT = TM * 128;          // TM x 64 bf16
   static constexpr int FAC = 2 * ROWS * 128;    // hi + lo planes, 64 columns
   static constexpr int STAGE = ACT + FAC;       // multiple of 1024 when NT is even
   static constexpr int STAGE_AL = (STAGE + 1023) / 1024 * 1024;
@@ -87,7 +94,7 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 
 // out[t, j] (+)= Σ_k act[t, k] · Wt[j, k]   (Wt = W transposed, hi/lo bf16 planes)
 template <int NT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(TTHREADS)
     k_rowmma(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap fac_map,
              int64_t m, int kchunks, int units, float* __restrict__ out, int64_t ldo, int rc) {
   using L = ThinSmem<NT>;
@@ -104,7 +111,7 @@ __global__ void __launch_bounds__(128)
     const int tile = u / kchunks, ch = u - tile * kchunks;
     unsigned char* st = sm + slot * L::STAGE_AL;
     mbar_arrive_expect_tx(&full[slot], L::STAGE);
-    tma_load_2d(st, &act_map, &full[slot], ch * TILE, tile * TILE);
+    tma_load_2d(st, &act_map, &full[slot], ch * TILE, tile * TM);
     tma_load_2d(st + L::ACT, &fac_map, &full[slot], ch * TILE, 0);
   };
   if (threadIdx.x == 0) {
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
     const int tile = u / kchunks;
     if (u + 1 == u1 || (u + 1) / kchunks != tile) {  // leaving this token tile: flush
-      const int64_t ta = static_cast<int64_t>(tile) * TILE + warp * 16 + g, tb = ta + 8;
+      const int64_t ta = static_cast<int64_t>(tile) * TM + warp * 16 + g, tb = ta + 8;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         const int j = n * 8 + 2 * tq;
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(128)
 // out[n, j] += scale · Σ_t act[t, n] · Vt[j, t]   (Vt = V transposed, hi/lo bf16 planes)
 // Columns j >= rc of the product go to colsum (the ones column) when j == rc.
 template <int NT>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(TTHREADS)
     k_colmma(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap fac_map,
              int64_t nd, int tchunks, int units, float scale, float* __restrict__ out,
              int64_t ldo, int rc, float* __restrict__ colsum) {
@@ -184,7 +191,9 @@ __global__ void __launch_bounds__(128)
     const int nt = u / tchunks, ch = u - nt * tchunks;
     unsigned char* st = sm + slot * L::STAGE_AL;
     mbar_arrive_expect_tx(&full[slot], L::STAGE);
-    tma_load_2d(st, &act_map, &full[slot], nt * TILE, ch * TILE);
+#pragma unroll
+    for (int h = 0; h < TM / 64; ++h)  // [64 tokens x TM n] as 64-n boxes, 8 KB apart
+      tma_load_2d(st + h * 8192, &act_map, &full[slot], nt * TM + h * 64, ch * TILE);
     tma_load_2d(st + L::ACT, &fac_map, &full[slot], ch * TILE, 0);
   };
   if (threadIdx.x == 0) {
@@ -200,6 +209,7 @@ __global__ void __launch_bounds__(128)
   // A fragment (M = n, K = t) from the [t][n] tile via transposed ldmatrix:
   // lane l addresses row t = (l & 7) + 8*(l >> 4) (+16 per k16), n chunk warp*2 + ((l >> 3) & 1)
   const int trow = (lane & 7) + ((lane >> 4) << 3), nchunk = warp * 2 + ((lane >> 3) & 1);
+  const uint32_t nhalf = static_cast<uint32_t>(nchunk >> 3) * 8192u;  // which 64-n box
   for (int u = u0; u < u1; ++u) {
     const int i = u - u0, b = i % TNS;
     if (threadIdx.x == 0 && u + TNS - 1 < u1) {
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int k16 = 0; k16 < 4; ++k16) {
       uint32_t a[4];
-      ldsm_x4_t(swz(abase, trow + 16 * k16, nchunk), a);
+      ldsm_x4_t(swz(abase + nhalf, trow + 16 * k16, nchunk & 7), a);
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         const int rh = n * 8 + g, rl = rh + ROWS;
@@ -227,7 +237,7 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
     const int nt = u / tchunks;
     if (u + 1 == u1 || (u + 1) / tchunks != nt) {  // leaving this n tile: flush
-      const int64_t na = static_cast<int64_t>(nt) * TILE + warp * 16 + g, nb = na + 8;
+      const int64_t na = static_cast<int64_t>(nt) * TM + warp * 16 + g, nb = na + 8;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
 #pragma unroll
@@ -312,7 +322,7 @@ int blocks_for(int64_t work) {
 template <typename K>
 int wave_ctas(K kernel, int smem, int64_t units) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TTHREADS, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
   const int64_t cap = static_cast<int64_t>(per_sm) * sms();
@@ -353,13 +363,13 @@ cudaError_t rowmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
                       const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t ldw, float* out,
                       int64_t ldo, int64_t r, cudaStream_t st) {
   constexpr int ROWS = 8 * NT;
-  const int64_t tb = (m + TILE - 1) / TILE;
+  const int64_t tb = (m + TM - 1) / TM;
   const int64_t kchunks = (kd + TILE - 1) / TILE;
   const int64_t units = tb * kchunks;
   if (units <= 0) return cudaSuccess;
   if (units > INT32_MAX || lo != hi + ROWS * ldw) return cudaErrorInvalidValue;
   CUtensorMap am, fm;
-  cudaError_t e = thin_map(&am, act, kd, m, lda, TILE);
+  cudaError_t e = thin_map(&am, act, kd, m, lda, TM);
   if (e == cudaSuccess) e = thin_map(&fm, hi, ldw, 2 * ROWS, ldw, 2 * ROWS);
   if (e != cudaSuccess) return e;
   const int smem = ThinSmem<NT>::BYTES;
@@ -371,7 +381,7 @@ cudaError_t rowmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   }
   const int ctas = wave_ctas(k_rowmma<NT>, smem, units);
   note_launch();
-  k_rowmma<NT><<<ctas, 128, smem, st>>>(am, fm, m, static_cast<int>(kchunks),
+  k_rowmma<NT><<<ctas, TTHREADS, smem, st>>>(am, fm, m, static_cast<int>(kchunks),
                                         static_cast<int>(units), out, ldo, static_cast<int>(r));
   return cudaGetLastError();
 }
@@ -381,7 +391,7 @@ cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
                       const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t ldv, float scale,
                       float* out, int64_t ldo, int64_t r, float* colsum, cudaStream_t st) {
   constexpr int ROWS = 8 * NT;
-  const int64_t nb = (nd + TILE - 1) / TILE;
+  const int64_t nb = (nd + TM - 1) / TM;
   const int64_t tchunks = (m + TILE - 1) / TILE;
   const int64_t units = nb * tchunks;
   if (units <= 0) return cudaSuccess;
@@ -399,7 +409,7 @@ cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   }
   const int ctas = wave_ctas(k_colmma<NT>, smem, units);
   note_launch();
-  k_colmma<NT><<<ctas, 128, smem, st>>>(am, fm, nd, static_cast<int>(tchunks),
+  k_colmma<NT><<<ctas, TTHREADS, smem, st>>>(am, fm, nd, static_cast<int>(tchunks),
                                         static_cast<int>(units), scale, out, ldo,
                                         static_cast<int>(r), colsum);
   return cudaGetLastError();
