@@ -41,6 +41,10 @@ struct mlra_qweight {
   // built-in cb2 plugin state (owned when the qweight came from mlra_cb2_create)
   mlra::Cb2Dev cb2{};
   void* cb2_mem = nullptr;
+  // fused cb2 path: the u16 code stream seen as a 2-bit packed matrix + {s, 0} grid
+  bool cb2_fused = false;
+  QWeightDev cb2_d{};
+  float2* cb2_grid = nullptr;
 };
 
 namespace {
@@ -204,6 +208,7 @@ struct GemmPlan {
   int64_t ldo;
   bool out_f32;
   const float* bias = nullptr;
+  const void* cb2_codebook = nullptr;  // fused cb2 plugin decode (pair kernel, Q ring)
 };
 
 // One GEMM over the quantized operand described by d. w_mat != nullptr: Ŵ is
@@ -230,8 +235,10 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
                 reinterpret_cast<uintptr_t>(gp.out) % 4 == 0 ? 1 : 0;
   // CTA-pair kernel (512 tokens per tile) or the 1-CTA kernel (256), by the
   // cost model; MLRA_GEMM=1|2 forces the 1-CTA / pair kernel (tests cover both).
+  a.cb2_codebook = gp.cb2_codebook;
   bool pair = mlra::qgemm_prefer_pair(a);
   if (const char* force = getenv("MLRA_GEMM")) pair = atoi(force) == 2;
+  if (gp.cb2_codebook) pair = true;  // the fused cb2 decode lives in the pair kernel
   const uint32_t tbox = pair ? 128 : 256;
   mlra_status st = make_map(&maps.act, gp.act, gp.k_red_valid, gp.tokens, gp.ld_act, 64, tbox);
   if (st) return st;
@@ -257,7 +264,8 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
     a.q_codes_bytes = 128 * 16 * d.bits;
     a.q_grid_bytes = 128 * gfl * 4;
     a.q_stage_bytes = static_cast<int>(round_up(a.q_codes_bytes + a.q_grid_bytes, 128));
-    a.q_stages = mlra::qgemm_max_q_stages(a.q_stage_bytes);
+    a.q_stages = mlra::qgemm_max_q_stages(a.q_stage_bytes,
+                                          gp.cb2_codebook ? mlra::kCb2SmemBytes : 0);
     a.q_group_shift = g < 128 ? (g == 32 ? 5 : 6) : -1;
     a.q_group_div128 = g >= 128 ? static_cast<int>(g / 128) : 1;
     {
@@ -376,6 +384,14 @@ const mlra_hook* pick_hook(const mlra_qweight* q, mlra_strategy strategy,
 
 mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const mlra_hook* ctx_hook,
                      const GemmPlan& gp, Scratch& sc) {
+  // the built-in cb2 plugin decodes inside the fused GEMM (Ŵ never in HBM) for
+  // the tile-materializing strategies unless a context hook overrides it
+  if (q->opaque && q->cb2_fused && strategy != MLRA_WEIGHT &&
+      !(strategy == MLRA_MATVEC && ctx_hook) && getenv("MLRA_CB2_HOOK") == nullptr) {
+    GemmPlan g2 = gp;
+    g2.cb2_codebook = q->cb2.codebook;
+    return run_gemm_d(q->cb2_d, nullptr, 0, g2, sc);
+  }
   if (const mlra_hook* hk = pick_hook(q, strategy, ctx_hook))
     return run_gemm_hooked(q, hk, strategy == MLRA_WEIGHT, gp, sc);
   const QWeightDev& d = q->d;
@@ -599,6 +615,7 @@ void mlra_qweight_destroy(mlra_qweight* q) {
   if (q->words) cudaFree(q->words);
   if (q->grid) cudaFree(q->grid);
   if (q->cb2_mem) cudaFree(q->cb2_mem);
+  if (q->cb2_grid) cudaFree(q->cb2_grid);
   delete q;
 }
 
@@ -695,6 +712,33 @@ mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group, const uin
   }
   q->device_bytes = off_sc + sc_bytes;
   q->d.group = group;
+  // fused path: whole 256-multiples (the u16 codes are then the row-aligned 2-bit
+  // stream the Q ring tiles), a bf16-exact codebook, a group the Q ring supports
+  const bool g_ok = group == 32 || group == 64 || group % 128 == 0;
+  if (cb16 && g_ok && rows % 256 == 0 && cols % 256 == 0) {
+    QWeightDev& fd = q->cb2_d;
+    fd.rows = fd.rows_pad = rows;
+    fd.cols = fd.cols_pad = cols;
+    fd.bits = 2;
+    fd.group = group;
+    fd.ng_pad = round_up(cols / group, 2);
+    fd.row_words = cols / 16;
+    fd.words = reinterpret_cast<const uint32_t*>(base + off_codes);
+    std::vector<float2> g(static_cast<size_t>(rows * fd.ng_pad), make_float2(1.0f, 0.0f));
+    for (int64_t i = 0; i < rows; ++i)
+      for (int64_t j = 0; j < cols / group; ++j)
+        g[static_cast<size_t>(i * fd.ng_pad + j)] = make_float2(scales[i * (cols / group) + j], 0.0f);
+    e = cudaMalloc(&q->cb2_grid, g.size() * sizeof(float2));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(q->cb2_grid, g.data(), g.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      mlra_qweight_destroy(q);
+      return fail(MLRA_ERR_CUDA, "cb2 grid upload: %s", cudaGetErrorString(e));
+    }
+    fd.grid = q->cb2_grid;
+    q->device_bytes += g.size() * sizeof(float2);
+    q->cb2_fused = true;
+  }
   q->cb2 = mlra::Cb2Dev{rows, cols, group, cols / group,
                         reinterpret_cast<const uint16_t*>(base + off_codes), base, cb16 ? 1 : 0,
                         reinterpret_cast<const float*>(base + off_sc)};
@@ -743,7 +787,7 @@ uint64_t mlra_ledger_bytes(const mlra_qweight* q, mlra_strategy strategy) {
   if (!q) return 0;
   if (strategy == MLRA_WEIGHT)
     return static_cast<uint64_t>(q->d.rows) * static_cast<uint64_t>(q->d.cols) * 2u;
-  if (!q->opaque) return 0;
+  if (!q->opaque || q->cb2_fused) return 0;
   // hook slabs: the larger of the forward (row) and dX (column) slab buffers
   const QWeightDev& d = q->d;
   const int64_t fwd = slab_extent(d.rows_pad, d.cols_pad, false) * d.cols_pad;

@@ -417,8 +417,8 @@ bool qgemm_q_tma_ok(const QWeightDev& q) {
   return (q.bits == 2 || q.bits == 3 || q.bits == 4) && g_ok;
 }
 
-int qgemm_max_q_stages(int q_stage_bytes) {
-  int qs = (SMEM_LIMIT - SMEM_FIXED) / q_stage_bytes;
+int qgemm_max_q_stages(int q_stage_bytes, int extra_smem) {
+  int qs = (SMEM_LIMIT - SMEM_FIXED - extra_smem) / q_stage_bytes;
   return qs > MAX_QS ? MAX_QS : qs;
 }
 

@@ -28,6 +28,7 @@ struct GemmArgs {
   int64_t ldo;
   const float* bias; // [m_valid] or nullptr
   int out_pairs;     // bf16 out with even ldo and 4-byte aligned base: paired-row stores
+  const void* cb2_codebook;  // non-null: fused cb2 plugin decode (bf16 codebook, uint4[256])
   // Q ring (fused path with TMA-fed codes); q_stages == 0 selects the LDG path
   int q_stages;
   int q_stage_bytes;
@@ -52,7 +53,7 @@ struct GemmArgs {
 
 // true when the fused path can stream codes/grids through the TMA Q ring
 bool qgemm_q_tma_ok(const QWeightDev& q);
-int qgemm_max_q_stages(int q_stage_bytes);
+int qgemm_max_q_stages(int q_stage_bytes, int extra_smem = 0);
 
 // mn = false: forward (Ŵ K-major on the weight side); true: dX (Ŵᵀ, MN-major).
 cudaError_t qgemm_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
@@ -68,6 +69,7 @@ void qgemm2_plan(GemmArgs& p);
 // 1-CTA kernel for this GEMM (cost model in qgemm2.cu).
 bool qgemm_prefer_pair(const GemmArgs& p);
 constexpr int kMaxSkPairs = 128;
+constexpr int kCb2SmemBytes = 256 * 16;  // the cb2 codebook staged in shared memory
 constexpr int64_t kSkSlotFloats = 2LL * 512 * 128;  // per pair
 
 }  // namespace mlra

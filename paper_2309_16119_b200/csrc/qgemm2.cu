@@ -138,7 +138,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sW = smem;
   uint8_t* sT = sW + STAGES * W_TILE;
   uint8_t* sQ = sT + STAGES * T_TILE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sQ + p.q_stages * p.q_stage_bytes);
+  constexpr bool CB2 = BITS == kCb2Bits;
+  constexpr int QB = q_geom_bits<BITS>();  // packed-stream geometry
+  uint8_t* sCb = sQ + p.q_stages * p.q_stage_bytes;  // cb2 codebook (CB2 only)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sCb + (CB2 ? kCb2SmemBytes : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* qfull = empty + STAGES;
   uint64_t* qempty = qfull + MAX_QS;
@@ -192,6 +195,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc2(tmem_slot, TMEM_COLS);
+  if constexpr (CB2) {  // stage the 4 KB codebook (read by this CTA's dequant warps)
+    if (threadIdx.x < kCb2SmemBytes / 16)
+      reinterpret_cast<uint4*>(sCb)[threadIdx.x] =
+          __ldg(reinterpret_cast<const uint4*>(p.cb2_codebook) + threadIdx.x);
+  }
   tc_fence_before();
   cluster_sync();  // barrier inits visible to the peer before any remote arrive
   tc_fence_after();
@@ -351,11 +359,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           mbar_arrive_expect_tx(&qfull[qs], qbytes);
           uint8_t* dst = sQ + qs * p.q_stage_bytes;
           if (!MN) {
-            tma_load_2d(dst, &tm_codes, &qfull[qs], pr * 16 * BITS, cb * BM);
+            tma_load_2d(dst, &tm_codes, &qfull[qs], pr * 16 * QB, cb * BM);
             tma_load_2d(dst + p.q_codes_bytes, &tm_grid, &qfull[qs],
                         2 * (pair_group(pr, p) & ~1), cb * BM);
           } else {
-            tma_load_2d(dst, &tm_codes, &qfull[qs], cb * 16 * BITS, pr * 128);
+            tma_load_2d(dst, &tm_codes, &qfull[qs], cb * 16 * QB, pr * 128);
             tma_load_2d(dst + p.q_codes_bytes, &tm_grid, &qfull[qs],
                         2 * (pair_group(cb, p) & ~1), pr * 128);
           }
@@ -560,7 +568,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               const int gsub = gshift >= 0 ? (code >> gshift)
                                            : (MN ? gpar_mn : (pair_group(kb >> 1, p) & 1));
               const int rbase = MN ? (row0 + 64 * kp) : row0;
-              dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
+              if constexpr (CB2)
+                dequant_units_cb2<UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox,
+                                                 smem_u32(sCb));
+              else
+                dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
               fence_proxy_async_smem();
             }
             __syncwarp();
@@ -604,9 +616,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                   wrow = static_cast<int64_t>(kb) * BK + (u >> 4);
                   wunit = static_cast<int64_t>(cb) * (BM / 8) + (u & 15);
                 }
-                const uint64_t v = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
-                *reinterpret_cast<uint4*>(stile + unit_soff<MN>(u)) =
-                    deq8_bf16_general<BITS>(v, q.grid + wrow * q.ng_pad, wunit * 8, q.group);
+                if constexpr (!CB2) {  // (the fused cb2 path always runs on the Q ring)
+                  const uint64_t v = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
+                  *reinterpret_cast<uint4*>(stile + unit_soff<MN>(u)) =
+                      deq8_bf16_general<BITS>(v, q.grid + wrow * q.ng_pad, wunit * 8, q.group);
+                }
               }
               fence_proxy_async_smem();
             }
@@ -641,7 +655,8 @@ template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA>
 cudaError_t launch2_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                       cudaStream_t stream) {
   auto kern = qgemm2_kernel<BITS, W_TMA, MN, OUT_F32, QTMA>;
-  const int smem = SMEM_FIXED + p.q_stages * p.q_stage_bytes;
+  const int smem = SMEM_FIXED + p.q_stages * p.q_stage_bytes +
+                   (BITS == kCb2Bits ? kCb2SmemBytes : 0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
@@ -718,6 +733,10 @@ cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmA
   if (p.tokens <= 0 || p.m_total <= 0) return cudaSuccess;
   if (w_tma) return launch2_mo<4, true, false>(maps, q, p, mn, out_f32, stream);
   const bool qtma = p.q_stages > 0;
+  if (p.cb2_codebook != nullptr) {
+    if (!qtma) return cudaErrorInvalidValue;  // the fused cb2 decode needs the Q ring
+    return launch2_mo<kCb2Bits, false, true>(maps, q, p, mn, out_f32, stream);
+  }
   switch (q.bits) {
     case 2: return qtma ? launch2_mo<2, false, true>(maps, q, p, mn, out_f32, stream)
                         : launch2_mo<2, false, false>(maps, q, p, mn, out_f32, stream);

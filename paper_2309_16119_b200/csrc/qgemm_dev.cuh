@@ -111,6 +111,51 @@ __device__ __forceinline__ void dequant_units(uint32_t qc, uint32_t qg, uint32_t
   }
 }
 
+// The cb2 codebook plugin's tile decode (codebook.cu, fused path): BITS tag
+// kCb2Bits selects it; its packed stream has the 2-bit geometry (one u16 code
+// per 8 weights), so the Q ring is loaded exactly as for BITS = 2 and only the
+// decode differs. `cbs` = shared address of the bf16-exact codebook, uint4[256].
+constexpr int kCb2Bits = 18;
+template <int BITS>
+constexpr int q_geom_bits() { return BITS == kCb2Bits ? 2 : BITS; }
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+
+template <int UPT, int ROW_STEP>
+__device__ __forceinline__ void dequant_units_cb2(uint32_t qc, uint32_t qg, uint32_t st,
+                                                  const uint32_t (&soff)[UPT], int unit, int gsub,
+                                                  int rbase, int gbox, uint32_t cbs) {
+  constexpr int QROW = 32;  // 128 weights x 2 bits
+  uint32_t v[UPT];
+  float sc[UPT];
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int row = rbase + i * ROW_STEP;
+    v[i] = lds16(qc + row * QROW + unit * 2);
+    sc[i] = lds_f2(qg + row * gbox + gsub * 8).x;
+  }
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const uint4 q = lds128(cbs + ((v[i] & 0xFFu) << 4));
+    const float s = fabsf(sc[i]);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const float a = __fmul_rn(s, __uint_as_float(w[p] << 16));
+      const float b = __fmul_rn(s, __uint_as_float(w[p] & 0xFFFF0000u));
+      o[p] = pack_bf16x2(a, b) ^ ((((v[i] >> (8 + 2 * p)) & 3u) * 0x40008000u) & 0x80008000u);
+    }
+    sts128(st + soff[i], make_uint4(o[0], o[1], o[2], o[3]));
+  }
+}
+
 struct TileIter {
   int m_tiles;
   int n_tiles;

@@ -282,3 +282,28 @@ def test_cb2_materialize_non_bf16_codebook():
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     got16 = M.dequantize(dq, torch.bfloat16).view(torch.int16).cpu().numpy().view(np.uint16)
     assert np.array_equal(got16, orc.f32_to_bf16_bits(want))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d_out,d_in,group,m", [(1024, 2048, 128, 700), (512, 768, 64, 1100)])
+def test_cb2_fused_decode_matches_materialized(d_out, d_in, group, m, monkeypatch):
+    # the fused path (codes decoded into the GEMM's smem tiles, Ŵ never in HBM)
+    # feeds the tensor cores exactly the bf16 operands the hook materializes:
+    # same MMA sequence -> bit-identical outputs; and nothing is charged to HBM
+    monkeypatch.setenv("MLRA_GEMM", "2")
+    w = orc.gaussian(31 + d_out, d_out, d_in, 0.0, 0.02)
+    qz = M.Codebook2Quantizer()
+    dq = qz.upload(qz.quantize(w, None, 2, group))
+    x = to_bf16_dev(orc.bf16_round(orc.gaussian(32, m, d_in)))
+    g = to_bf16_dev(orc.bf16_round(orc.gaussian(33, m, d_out)))
+    fused = M.LpLinearContext(dq, S.RowMaterialize)
+    assert fused.ledger_bytes() == 0
+    y_f = M.lp_forward(fused, x, torch.float32)
+    dx_f = M.lp_backward(fused, g, torch.float32)
+    wctx = M.LpLinearContext(dq, S.WeightMaterialize)
+    assert torch.equal(y_f, M.lp_forward(wctx, x, torch.float32))
+    assert torch.equal(dx_f, M.lp_backward(wctx, g, torch.float32))
+    monkeypatch.setenv("MLRA_CB2_HOOK", "1")  # the slabbed hook path, same numbers
+    assert torch.equal(y_f, M.lp_forward(fused, x, torch.float32))
+    wb = _deq_bf16(dq)
+    assert rel_fro(f64(y_f), orc.bf16_round(orc.gaussian(32, m, d_in)) @ wb.T) < 1e-5
