@@ -119,6 +119,15 @@ MLRA_API uint64_t mlra_kernel_launches(void);
 /* MLRA_OK iff the current CUDA device is sm_100 (B200). */
 MLRA_API mlra_status mlra_device_check(void);
 
+/* The reference's seeded generator (rng.hpp:15-57) on the host: mix_seed, and
+ * DenseMatrix::gaussian's row-major fill out[i] = mean + stddev·g_i
+ * (matrix.cpp:62-67) from Rng(seed) — bit-identical to the reference, so
+ * init_adapter (lora.cpp:14-32: B = gaussian(d_in x r, Rng(seed), 0, 0.02))
+ * and seeded inputs match it exactly. */
+MLRA_API uint64_t mlra_mix_seed(uint64_t seed, uint64_t salt);
+MLRA_API void mlra_gaussian_fill(uint64_t seed, double* out, uint64_t n, double mean,
+                                 double stddev);
+
 /* packed_word_count (bitpack.cpp:64-66). */
 MLRA_API uint64_t mlra_packed_word_count(uint64_t count, int bits);
 

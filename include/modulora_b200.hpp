@@ -376,8 +376,9 @@ struct ModuLoraLayer {
   std::size_t d_out() const { return weights->rows(); }
 };
 
-// init_adapter semantics (lora.cpp:14-32): A = 0, B ~ N(0, 0.02^2) (std::mt19937_64
-// stream, not the reference's hand-written Box-Muller), ConfigError on rank 0 / alpha <= 0.
+// init_adapter (lora.cpp:14-32): A = 0, B = gaussian(d_in x r, Rng(seed), 0, 0.02) from the
+// reference's own stream (mlra_gaussian_fill: bit-identical f64 values, stored as fp32);
+// ConfigError on rank 0 / alpha <= 0.
 inline LoraAdapter init_adapter(std::size_t d_in, std::size_t d_out, std::size_t rank, double alpha,
                                 std::uint64_t seed) {
   if (rank == 0) throw ConfigError("adapter rank must be >= 1");
@@ -388,9 +389,9 @@ inline LoraAdapter init_adapter(std::size_t d_in, std::size_t d_out, std::size_t
   ad.a = DeviceBuffer<float>(d_out * rank);
   ad.b = DeviceBuffer<float>(d_in * rank);
   std::vector<float> za(d_out * rank, 0.0f), hb(d_in * rank);
-  std::mt19937_64 gen(seed);
-  std::normal_distribution<double> nd(0.0, kAdapterInitStd);
-  for (float& v : hb) v = static_cast<float>(nd(gen));
+  std::vector<double> b64(d_in * rank);
+  mlra_gaussian_fill(seed, b64.data(), b64.size(), 0.0, kAdapterInitStd);
+  for (std::size_t i = 0; i < hb.size(); ++i) hb[i] = static_cast<float>(b64[i]);
   ad.a.upload(za.data());
   ad.b.upload(hb.data());
   return ad;

@@ -30,6 +30,7 @@ EXPORTS = [
     "mlra_checkpoint_frozen_hash", "mlra_checkpoint_file_hash", "mlra_checkpoint_upload",
     "mlra_checkpoint_set_adapter", "mlra_checkpoint_save", "mlra_quantize_rtn",
     "mlra_dp_unique_id", "mlra_dp_init", "mlra_allreduce_lora_grads", "mlra_dp_destroy",
+    "mlra_mix_seed", "mlra_gaussian_fill",
 ]
 
 # mlra_hook.materialize(state, q, row0, nrows, col0, ncols, out, dtype, ld, stream)
@@ -173,6 +174,10 @@ def lib() -> C.CDLL:
         L.mlra_allreduce_lora_grads.argtypes = [vp, vp, u64, vp]
         L.mlra_dp_destroy.restype = None
         L.mlra_dp_destroy.argtypes = [vp]
+        L.mlra_mix_seed.restype = u64
+        L.mlra_mix_seed.argtypes = [u64, u64]
+        L.mlra_gaussian_fill.restype = None
+        L.mlra_gaussian_fill.argtypes = [u64, vp, u64, C.c_double, C.c_double]
         _lib = L
     return _lib
 

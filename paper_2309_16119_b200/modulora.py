@@ -436,17 +436,35 @@ class LoraAdapter:
         return self.alpha / float(self.rank)
 
 
+def mix_seed(seed: int, salt: int) -> int:
+    """mix_seed (rng.hpp:52-57)."""
+    return int(lib().mlra_mix_seed(seed, salt))
+
+
+def gaussian(seed: int, rows: int, cols: int, mean: float = 0.0, std: float = 1.0) -> np.ndarray:
+    """DenseMatrix::gaussian(rows, cols, Rng(seed), mean, std) (matrix.cpp:62-67), f64 host,
+    bit-identical to the reference's stream."""
+    out = np.empty(rows * cols, np.float64)
+    if out.size:
+        lib().mlra_gaussian_fill(seed, out.ctypes.data, out.size, mean, std)
+    return out.reshape(rows, cols)
+
+
 def init_adapter(d_in: int, d_out: int, rank: int, alpha: float, seed: int) -> LoraAdapter:
-    """init_adapter (lora.cpp:14-32): same shapes, init law and errors. The
-    Gaussian stream comes from torch (not the reference mt19937_64 stream)."""
+    """init_adapter (lora.cpp:14-32): A = 0, B = gaussian(d_in x r, Rng(seed), 0, 0.02) —
+    the reference's own stream (B's f64 values are bit-identical; the device copy is
+    their fp32 rounding). Same errors and the same low-rank warning."""
     if rank == 0:
         raise MlraError(3, "adapter rank must be >= 1")
     if not alpha > 0.0:
         raise MlraError(3, "adapter alpha must be positive")
-    g = torch.Generator(device="cpu").manual_seed(seed)
-    b = (torch.randn(d_in, rank, generator=g, dtype=torch.float64) * kAdapterInitStd).float()
-    return LoraAdapter(a=torch.zeros(d_out, rank, device="cuda"), b=b.cuda(), rank=rank,
-                       alpha=alpha)
+    if rank > min(d_in, d_out) // 2:
+        import warnings
+        warnings.warn(f"adapter rank {rank} exceeds half of min({d_in}, {d_out}); "
+                      "the low-rank assumption is weak")
+    b = gaussian(seed, d_in, rank, 0.0, kAdapterInitStd)
+    return LoraAdapter(a=torch.zeros(d_out, rank, device="cuda"),
+                       b=torch.from_numpy(b.astype(np.float32)).cuda(), rank=rank, alpha=alpha)
 
 
 @dataclass

@@ -79,3 +79,28 @@ def test_no_cpu_fallback():
     st, msg = _create(4, 8, 4, 4, w, 32, s, z)
     assert st == 9, msg  # MLRA_ERR_UNSUPPORTED: valid input, but no sm_100 device
     assert _lib.lib().mlra_device_check() == 9
+
+
+def test_host_rng_matches_reference_stream():
+    # rng.hpp:15-57 restated in libmlra (init_adapter's stream): bit-identical to the
+    # golden fixtures made by the reference and to the oracle
+    import ctypes as C
+    from tests.conftest import load_golden
+    L = _lib.lib()
+    g = load_golden("rng.npz")
+    out = np.empty(15, np.float64)
+    L.mlra_gaussian_fill(7, out.ctypes.data_as(C.c_void_p), 15, 0.0, 1.0)
+    assert np.array_equal(out.view(np.uint64), g["gaussian_seed7"].ravel().view(np.uint64))
+    out = np.empty(16, np.float64)
+    L.mlra_gaussian_fill(8, out.ctypes.data_as(C.c_void_p), 16, 0.5, 0.02)
+    assert np.array_equal(out.view(np.uint64), g["gaussian_seed8_scaled"].ravel().view(np.uint64))
+    assert L.mlra_mix_seed(11, 0xADA9) == int(g["mix_seed_11_ada9"][0])
+    big = np.empty(4096 * 16, np.float64)
+    L.mlra_gaussian_fill(123, big.ctypes.data_as(C.c_void_p), big.size, 0.0, 0.02)
+    assert np.array_equal(big.view(np.uint64), orc.gaussian(123, 4096, 16, 0.0, 0.02).ravel().view(np.uint64))
+    if orc.Ref.available():
+        b = np.empty(300 * 8, np.float64)
+        assert orc.Ref.get().ref_init_adapter_b(300, 200, 8, 16.0, 99, b) == 0
+        mine = np.empty(300 * 8, np.float64)
+        L.mlra_gaussian_fill(99, mine.ctypes.data_as(C.c_void_p), mine.size, 0.0, 0.02)
+        assert np.array_equal(mine.view(np.uint64), b.view(np.uint64))
