@@ -40,6 +40,7 @@ __global__ void k_rtn_grid(const T* __restrict__ w, int64_t rows, int64_t cols, 
     // the sign of a zero extreme: carry the index and break ties by it.
     double lo = ld_w(p, lane < group ? lane : 0), hi = lo;
     int64_t li = lane < group ? lane : 0, hix = li;
+#pragma unroll 4
     for (int64_t j = lane; j < group; j += 32) {
       const double v = ld_w(p, j);
       if (v < lo) lo = v, li = j;
@@ -78,10 +79,13 @@ __global__ void k_rtn_pack(const T* __restrict__ w, int64_t rows, int64_t cols, 
     const uint64_t c_first = b0 / bits;
     uint64_t c_last = (b0 + 31) / bits;
     if (c_last >= count) c_last = count - 1;
+    // (row, col, group) of the first code once; the rest advance incrementally
+    // (64-bit divides per code dominated this kernel)
+    int64_t r = static_cast<int64_t>(c_first / cols), j = static_cast<int64_t>(c_first % cols);
+    int64_t gcol = j / group, jg = j - gcol * group;
     uint32_t out = 0;
     for (uint64_t c = c_first; c <= c_last; ++c) {
-      const int64_t r = static_cast<int64_t>(c / cols), j = static_cast<int64_t>(c % cols);
-      const int64_t gi = r * ng + j / group;
+      const int64_t gi = r * ng + gcol;
       const double z = static_cast<double>(__ldg(zeros + gi));
       const double s = static_cast<double>(__ldg(scales + gi));
       double q = round(__ddiv_rn(__dsub_rn(ld_w(w, static_cast<int64_t>(c)), z), s));
@@ -89,6 +93,16 @@ __global__ void k_rtn_pack(const T* __restrict__ w, int64_t rows, int64_t cols, 
       const uint32_t code = static_cast<uint32_t>(q);
       const int64_t sh = static_cast<int64_t>(c * bits) - static_cast<int64_t>(b0);
       out |= sh >= 0 ? code << sh : code >> (-sh);
+      if (++jg == group) {
+        jg = 0;
+        ++gcol;
+      }
+      if (++j == cols) {
+        j = 0;
+        jg = 0;
+        gcol = 0;
+        ++r;
+      }
     }
     words[wi] = out;
   }
