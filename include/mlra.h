@@ -165,6 +165,20 @@ MLRA_API mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group_s
                                      const uint16_t* codes, const float* codebook,
                                      const float* scales, void* stream, mlra_qweight** out);
 
+/* Built-in "lut" plugin (non-uniform levels, e.g. QLoRA's NF4; a plugin behind
+ * the reference's Quantizer interface, quantize.hpp:91-106, like cb2): codes
+ * in the reference's b-bit bitstream (bitpack.cpp:25-35; words / word_count as
+ * mlra_qweight_create), a table of 2^bits finite f32 levels and one f32 scale
+ * (> 0) per (row, group):  Ŵ[i, j] = RN_f32(s[i, j/g] · levels[c[i, j]]).
+ * bits in {2, 3, 4}; group_size % 8 == 0. The result is an ordinary
+ * (non-opaque) qweight: materialize() runs the lut kernel, and the fused GEMM
+ * decodes the table in its dequant warps when the group tiles the Q ring
+ * (32, 64 or a multiple of 128), else Ŵ goes through HBM. */
+MLRA_API mlra_status mlra_lut_create(int64_t rows, int64_t cols, int bits, int64_t group_size,
+                                     const uint32_t* words, uint64_t word_count,
+                                     const float* levels, const float* scales, void* stream,
+                                     mlra_qweight** out);
+
 /* RtnQuantizer::quantize (quantize.hpp:108-113; quantize.cpp:24-44, 163-184)
  * on the device: w is a DEVICE matrix [rows x cols] of dtype MLRA_F64 or
  * MLRA_F32 (widened exactly); group_size 0 selects per-row grids

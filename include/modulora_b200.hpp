@@ -149,6 +149,25 @@ struct PackedCodes {
   std::size_t packed_bytes() const { return words.size() * 4; }
 };
 
+// bitpack.hpp:31 pack(): LSB-first bitstream, code i at bit i*bits (host side,
+// for building plugin formats; RangeError on a code wider than `bits`).
+inline PackedCodes pack(const std::vector<std::uint32_t>& codes, int bits) {
+  if (bits < 1 || bits > 16) throw ConfigError("bitpack: unsupported bit width " + std::to_string(bits));
+  PackedCodes p;
+  p.bits = bits;
+  p.count = codes.size();
+  p.words.assign(mlra_packed_word_count(codes.size(), bits), 0u);
+  for (std::size_t i = 0; i < codes.size(); ++i) {
+    const std::uint32_t c = codes[i];
+    if (c >> bits) throw RangeError("bitpack: code " + std::to_string(c) + " out of range");
+    const std::uint64_t bit = static_cast<std::uint64_t>(i) * bits;
+    const std::uint64_t v = static_cast<std::uint64_t>(c) << (bit & 31);
+    p.words[bit >> 5] |= static_cast<std::uint32_t>(v);
+    if ((bit & 31) + bits > 32) p.words[(bit >> 5) + 1] |= static_cast<std::uint32_t>(v >> 32);
+  }
+  return p;
+}
+
 struct QuantizedMatrix {
   std::size_t rows = 0, cols = 0;
   int bits = 0;
@@ -269,6 +288,23 @@ inline std::shared_ptr<const DeviceQuantizedMatrix> upload_cb2(
   check(mlra_cb2_create(static_cast<int64_t>(rows), static_cast<int64_t>(cols),
                         static_cast<int64_t>(group), codes.data(), codebook.data(), scales.data(),
                         st, &h));
+  return std::make_shared<const DeviceQuantizedMatrix>(h, rows, cols);
+}
+
+// Built-in plugin "lut" (mlra_lut_create): the reference's b-bit bitstream of
+// level indices (b in {2, 3, 4}), a table of 2^b f32 levels (e.g. NF4) and an
+// f32 scale per (row, group); Ŵ = RN_f32(s · levels[c]). An ordinary frozen
+// matrix: materialize() and the fused GEMM decode the table on the device.
+inline std::shared_ptr<const DeviceQuantizedMatrix> upload_lut(
+    std::size_t rows, std::size_t cols, std::size_t group, const PackedCodes& codes,
+    const std::vector<float>& levels, const std::vector<float>& scales, cudaStream_t st = nullptr) {
+  if (codes.bits < 1 || codes.bits > 4 || levels.size() != (std::size_t{1} << codes.bits) ||
+      !group || scales.size() != rows * (cols / group) || codes.count != rows * cols)
+    throw FormatError(FormatError::Kind::BadField, 0, "lut: buffer sizes do not match the shape");
+  mlra_qweight* h = nullptr;
+  check(mlra_lut_create(static_cast<int64_t>(rows), static_cast<int64_t>(cols), codes.bits,
+                        static_cast<int64_t>(group), codes.words.data(), codes.words.size(),
+                        levels.data(), scales.data(), st, &h));
   return std::make_shared<const DeviceQuantizedMatrix>(h, rows, cols);
 }
 

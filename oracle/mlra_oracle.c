@@ -302,6 +302,21 @@ ORC_EXPORT void orc_cb2_dequant_f32(const uint16_t* codes, uint64_t rows, uint64
   }
 }
 
+/* The built-in "lut" plugin (include/mlra.h mlra_lut_create; e.g. QLoRA's NF4):
+ * codes in the reference's bitstream (bitpack.cpp:25-35), a per-matrix table of
+ * 2^bits f32 levels and a per-(row, group) f32 scale:
+ *   out[i, j] = RN_f32(s[i, j/g] * lut[c[i, j]])   (one IEEE multiply) */
+ORC_EXPORT void orc_lut_dequant_f32(const uint32_t* words, uint64_t rows, uint64_t cols,
+                                    int bits, uint64_t group, const float* lut,
+                                    const float* scales, float* out) {
+  const uint64_t ng = cols / group;
+  for (uint64_t i = 0; i < rows; ++i)
+    for (uint64_t j = 0; j < cols; ++j) {
+      const uint32_t c = orc_read_code(words, bits, i * cols + j);
+      out[i * cols + j] = scales[i * ng + j / group] * lut[c];
+    }
+}
+
 ORC_EXPORT uint16_t orc_f32_to_bf16(float f) {
   uint32_t u;
   memcpy(&u, &f, 4);

@@ -79,6 +79,7 @@ class _Lib:
             lib.orc_adamw_step.restype = _int
             lib.orc_adamw_step.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, _u64,
                                            C.c_double, _u64, _f64p, _f64p, _f64p, _f64p]
+            lib.orc_lut_dequant_f32.argtypes = [_u32p, _u64, _u64, _int, _u64, _f32p, _f32p, _f32p]
             cls._lib = lib
         return cls._lib
 
@@ -392,3 +393,12 @@ def adamw_step(params, ms, vs, grads, step_index: int, lr: float, beta1=0.9, bet
         if rc:
             return i
     return len(params)
+
+
+# --- lut plugin decode law (include/mlra.h mlra_lut_create) -------------------
+def lut_dequantize_f32(words, rows: int, cols: int, bits: int, group: int, lut, scales) -> np.ndarray:
+    """orc_lut_dequant_f32: RN_f32(s * lut[c]) per entry."""
+    out = np.empty(rows * cols, np.float32)
+    _Lib.get().orc_lut_dequant_f32(_c(words, np.uint32).ravel(), rows, cols, bits, group,
+                                   _c(lut, np.float32).ravel(), _c(scales, np.float32).ravel(), out)
+    return out.reshape(rows, cols)

@@ -30,7 +30,7 @@ EXPORTS = [
     "mlra_checkpoint_frozen_hash", "mlra_checkpoint_file_hash", "mlra_checkpoint_upload",
     "mlra_checkpoint_set_adapter", "mlra_checkpoint_save", "mlra_quantize_rtn",
     "mlra_dp_unique_id", "mlra_dp_init", "mlra_allreduce_lora_grads", "mlra_dp_destroy",
-    "mlra_mix_seed", "mlra_gaussian_fill",
+    "mlra_mix_seed", "mlra_gaussian_fill", "mlra_lut_create",
 ]
 
 # mlra_hook.materialize(state, q, row0, nrows, col0, ncols, out, dtype, ld, stream)
@@ -129,6 +129,9 @@ def lib() -> C.CDLL:
                                                  C.POINTER(vp)]
         L.mlra_cb2_create.restype = i32
         L.mlra_cb2_create.argtypes = [i64, i64, i64, vp, vp, vp, vp, C.POINTER(vp)]
+        L.mlra_lut_create.restype = i32
+        L.mlra_lut_create.argtypes = [i64, i64, C.c_int, i64, vp, C.c_uint64, vp, vp, vp,
+                                      C.POINTER(vp)]
         L.mlra_qweight_hook.restype = vp
         L.mlra_qweight_hook.argtypes = [vp]
         L.mlra_materialize_tile.restype = i32

@@ -45,6 +45,8 @@ struct mlra_qweight {
   bool cb2_fused = false;
   QWeightDev cb2_d{};
   float2* cb2_grid = nullptr;
+  // built-in lut plugin: the 16-float level table (d.lut points here)
+  float* lut_mem = nullptr;
 };
 
 namespace {
@@ -209,6 +211,7 @@ struct GemmPlan {
   bool out_f32;
   const float* bias = nullptr;
   const void* cb2_codebook = nullptr;  // fused cb2 plugin decode (pair kernel, Q ring)
+  const float* lut = nullptr;          // fused lut plugin decode (pair kernel, Q ring)
 };
 
 // One GEMM over the quantized operand described by d. w_mat != nullptr: Ŵ is
@@ -236,9 +239,10 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
   // CTA-pair kernel (512 tokens per tile) or the 1-CTA kernel (256), by the
   // cost model; MLRA_GEMM=1|2 forces the 1-CTA / pair kernel (tests cover both).
   a.cb2_codebook = gp.cb2_codebook;
+  a.lut = gp.lut;
   bool pair = mlra::qgemm_prefer_pair(a);
   if (const char* force = getenv("MLRA_GEMM")) pair = atoi(force) == 2;
-  if (gp.cb2_codebook) pair = true;  // the fused cb2 decode lives in the pair kernel
+  if (gp.cb2_codebook || gp.lut) pair = true;  // the plugin decodes live in the pair kernel
   const uint32_t tbox = pair ? 128 : 256;
   mlra_status st = make_map(&maps.act, gp.act, gp.k_red_valid, gp.tokens, gp.ld_act, 64, tbox);
   if (st) return st;
@@ -264,8 +268,9 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
     a.q_codes_bytes = 128 * 16 * d.bits;
     a.q_grid_bytes = 128 * gfl * 4;
     a.q_stage_bytes = static_cast<int>(round_up(a.q_codes_bytes + a.q_grid_bytes, 128));
-    a.q_stages = mlra::qgemm_max_q_stages(a.q_stage_bytes,
-                                          gp.cb2_codebook ? mlra::kCb2SmemBytes : 0);
+    a.q_stages = mlra::qgemm_max_q_stages(
+        a.q_stage_bytes,
+        gp.cb2_codebook ? mlra::kCb2SmemBytes : (gp.lut ? mlra::kLutSmemBytes : 0));
     a.q_group_shift = g < 128 ? (g == 32 ? 5 : 6) : -1;
     a.q_group_div128 = g >= 128 ? static_cast<int>(g / 128) : 1;
     {
@@ -395,7 +400,13 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const mlra_h
   if (const mlra_hook* hk = pick_hook(q, strategy, ctx_hook))
     return run_gemm_hooked(q, hk, strategy == MLRA_WEIGHT, gp, sc);
   const QWeightDev& d = q->d;
-  if (strategy == MLRA_WEIGHT) {
+  if (d.lut && strategy != MLRA_WEIGHT && mlra::qgemm_q_tma_ok(d)) {
+    // the built-in lut plugin decodes inside the fused GEMM on the Q ring
+    GemmPlan g2 = gp;
+    g2.lut = d.lut;
+    return run_gemm_d(d, nullptr, 0, g2, sc);
+  }
+  if (strategy == MLRA_WEIGHT || d.lut) {  // (lut groups the Q ring cannot tile: via HBM)
     // WeightMaterialize: the whole Ŵ in HBM for this pass (bf16), freed on return
     auto* w = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows * d.cols_pad));
     if (!w) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
@@ -616,6 +627,7 @@ void mlra_qweight_destroy(mlra_qweight* q) {
   if (q->grid) cudaFree(q->grid);
   if (q->cb2_mem) cudaFree(q->cb2_mem);
   if (q->cb2_grid) cudaFree(q->cb2_grid);
+  if (q->lut_mem) cudaFree(q->lut_mem);
   delete q;
 }
 
@@ -746,6 +758,47 @@ mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group, const uin
   return MLRA_OK;
 }
 
+mlra_status mlra_lut_create(int64_t rows, int64_t cols, int bits, int64_t group,
+                            const uint32_t* words, uint64_t word_count, const float* levels,
+                            const float* scales, void* stream, mlra_qweight** out) {
+  if (!out) return fail(MLRA_ERR_CONTRACT, "null output handle");
+  *out = nullptr;
+  if (bits != 2 && bits != 3 && bits != 4)
+    return fail(MLRA_ERR_CONFIG, "lut: unsupported bit width %d (2, 3 or 4)", bits);
+  if (rows <= 0 || cols <= 0 || group <= 0 || group % 8 != 0 || cols % group != 0)
+    return fail(MLRA_ERR_CONFIG, "lut: group size %lld must be a multiple of 8 dividing cols %lld",
+                (long long)group, (long long)cols);
+  if (!words || !levels || !scales) return fail(MLRA_ERR_CONTRACT, "lut: null buffers");
+  const int nl = 1 << bits;
+  for (int i = 0; i < nl; ++i)
+    if (!std::isfinite(levels[i])) return fail(MLRA_ERR_NUMERIC, "lut: level %d is not finite", i);
+  const uint64_t ng = static_cast<uint64_t>(rows * (cols / group));
+  for (uint64_t i = 0; i < ng; ++i)
+    if (!(scales[i] > 0.0f) || !std::isfinite(scales[i]))
+      return fail(MLRA_ERR_NUMERIC, "lut: scales must be positive and finite");
+  // the codes and scales go through the affine upload with zero = 0 (its grid
+  // is then {s, 0}, every group certified: s·c is exact in f64); the table
+  // replaces the affine decode
+  std::vector<float> zeros(ng, 0.0f);
+  mlra_qweight* q = nullptr;
+  if (mlra_status st = mlra_qweight_create(rows, cols, bits, group, words, word_count,
+                                           static_cast<uint64_t>(rows * cols), scales,
+                                           zeros.data(), ng, stream, &q))
+    return st;
+  float table[16] = {};
+  std::memcpy(table, levels, nl * sizeof(float));
+  cudaError_t e = cudaMalloc(&q->lut_mem, sizeof(table));
+  if (e == cudaSuccess) e = cudaMemcpy(q->lut_mem, table, sizeof(table), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    mlra_qweight_destroy(q);
+    return fail(MLRA_ERR_CUDA, "lut upload: %s", cudaGetErrorString(e));
+  }
+  q->d.lut = q->lut_mem;
+  q->device_bytes += sizeof(table);
+  *out = q;
+  return MLRA_OK;
+}
+
 mlra_status mlra_quantize_rtn(const void* w, mlra_dtype dtype, int64_t rows, int64_t cols,
                               int bits, int64_t group, uint32_t* words, float* scales,
                               float* zeros, void* stream) {
@@ -786,6 +839,8 @@ mlra_status mlra_qweight_info(const mlra_qweight* q, int64_t* rows, int64_t* col
 uint64_t mlra_ledger_bytes(const mlra_qweight* q, mlra_strategy strategy) {
   if (!q) return 0;
   if (strategy == MLRA_WEIGHT)
+    return static_cast<uint64_t>(q->d.rows) * static_cast<uint64_t>(q->d.cols) * 2u;
+  if (q->d.lut && !mlra::qgemm_q_tma_ok(q->d))  // lut groups off the Q ring: whole Ŵ
     return static_cast<uint64_t>(q->d.rows) * static_cast<uint64_t>(q->d.cols) * 2u;
   if (!q->opaque || q->cb2_fused) return 0;
   // hook slabs: the larger of the forward (row) and dX (column) slab buffers
@@ -829,6 +884,8 @@ mlra_status mlra_materialize_tile(const mlra_qweight* q, int64_t row0, int64_t n
     return q->hook.materialize(q->hook.state, q, row0, nrows, col0, ncols, out, dtype, ld,
                                stream);
   }
+  if (q->d.lut && ncols % 8 != 0)
+    return fail(MLRA_ERR_RANGE, "lut: tile columns must be 8-aligned");
   CUDA_TRY(mlra::launch_materialize_tile(q->d, row0, nrows, col0, ncols, out, ld,
                                          dtype == MLRA_F32, static_cast<cudaStream_t>(stream)));
   return MLRA_OK;

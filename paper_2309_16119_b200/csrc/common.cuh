@@ -32,6 +32,7 @@ struct QWeightDev {
   int64_t row_words;           // 32-bit words per padded row = cols_pad*bits/32
   const uint32_t* words;       // rows_pad * row_words (+ 4 words slack)
   const float2* grid;          // rows_pad * ng_pad
+  const float* lut = nullptr;  // lut plugin: 16 f32 levels (grid = {s, 0}); null = affine
 };
 
 // Device state of the built-in "cb2" codebook plugin (codebook.cu).

@@ -8,6 +8,7 @@
 //  * k_materialize: Ŵ = RN(double(s)·c + double(z)) (quantize.cpp:123-137,
 //    139-155) into f32 or bf16, bit-exact with (float)dequantize().
 //    HBM-bound: reads b/8 + 8/g bytes and writes 2 or 4 bytes per entry.
+//  * k_materialize_lut: the lut plugin's Ŵ = RN_f32(s · lut[c]).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -184,6 +185,123 @@ __global__ void __launch_bounds__(128) k_materialize_fast(const QWeightDev q, in
   }
 }
 
+// The lut plugin's materialize (mlra_lut_create): Ŵ[i, j] = RN_f32(s · lut[c]),
+// s = the {s, 0} grid entry of (i, j/g). group % 8 == 0 (checked at upload), so
+// every 8-code unit shares one scale. Block rows over blockIdx.y, 128 units per
+// block along x (contiguous 16-B stores per warp); the table sits in 16
+// conflict-free shared words.
+template <int BITS, bool F32, bool VEC>
+__global__ void __launch_bounds__(128) k_materialize_lut(const QWeightDev q, int64_t row0,
+                                                         int64_t nrows, int64_t u0, int64_t units,
+                                                         void* __restrict__ out, int64_t ld,
+                                                         int gshift) {
+  constexpr int UPT = 4;  // units per thread, strided by the block: 4 loads in flight
+  __shared__ float lut[16];
+  if (threadIdx.x < 16) lut[threadIdx.x] = __ldg(q.lut + threadIdx.x);
+  __syncthreads();
+  constexpr uint32_t mask = (1u << BITS) - 1u;
+  for (int64_t rr = blockIdx.y; rr < nrows; rr += gridDim.y) {
+    const int64_t r = row0 + rr;
+    const uint32_t* rw = q.words + r * q.row_words;
+    const float2* grow = q.grid + r * q.ng_pad;
+    for (int64_t it0 = static_cast<int64_t>(blockIdx.x) * (128 * UPT) + threadIdx.x; it0 < units;
+         it0 += static_cast<int64_t>(gridDim.x) * (128 * UPT)) {
+      uint32_t v[UPT];
+      float s[UPT];
+#pragma unroll
+      for (int j = 0; j < UPT; ++j) {
+        const int64_t it = it0 + j * 128;
+        if (it < units) {
+          const int64_t ua = u0 + it;
+          v[j] = static_cast<uint32_t>(load_unit<BITS>(rw, ua));
+          const int64_t k = ua * 8;
+          s[j] = __ldg(grow + (gshift >= 0 ? (k >> gshift) : k / q.group)).x;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < UPT; ++j) {
+        const int64_t it = it0 + j * 128;
+        if (it >= units) break;
+        float f[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = __fmul_rn(s[j], lut[(v[j] >> (BITS * i)) & mask]);
+        const int64_t o = rr * ld + it * 8;
+        if constexpr (F32) {
+          float* op = reinterpret_cast<float*>(out) + o;
+          if constexpr (VEC) {
+            reinterpret_cast<float4*>(op)[0] = make_float4(f[0], f[1], f[2], f[3]);
+            reinterpret_cast<float4*>(op)[1] = make_float4(f[4], f[5], f[6], f[7]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) op[i] = f[i];
+          }
+        } else {
+          const uint4 w = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                                     pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+          __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(out) + o;
+          if constexpr (VEC) {
+            *reinterpret_cast<uint4*>(op) = w;
+          } else {
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              op[2 * i] = __ushort_as_bfloat16(static_cast<unsigned short>(ws[i] & 0xFFFFu));
+              op[2 * i + 1] = __ushort_as_bfloat16(static_cast<unsigned short>(ws[i] >> 16));
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+int grid_for(int64_t work, int per_block);
+
+template <int BITS>
+cudaError_t materialize_lut_bits(const QWeightDev& q, int64_t row0, int64_t nrows, int64_t col0,
+                                 int64_t ncols, void* out, int64_t ld, bool f32,
+                                 cudaStream_t st) {
+  const int64_t units = ncols / 8;
+  const bool vec = ld % (f32 ? 4 : 8) == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  int gshift = -1;
+  for (int sft = 3; sft < 31; ++sft)
+    if ((int64_t{1} << sft) == q.group) gshift = sft;
+  const int64_t bx = (units + 511) / 512;
+  int64_t by = static_cast<int64_t>(grid_for(nrows * bx, 1)) / bx;
+  if (by < 1) by = 1;
+  if (by > nrows) by = nrows;
+  if (by > 65535) by = 65535;
+  const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(by));
+  note_launch();
+  if (f32) {
+    if (vec)
+      k_materialize_lut<BITS, true, true><<<grid, 128, 0, st>>>(q, row0, nrows, col0 / 8, units,
+                                                                 out, ld, gshift);
+    else
+      k_materialize_lut<BITS, true, false><<<grid, 128, 0, st>>>(q, row0, nrows, col0 / 8, units,
+                                                                  out, ld, gshift);
+  } else {
+    if (vec)
+      k_materialize_lut<BITS, false, true><<<grid, 128, 0, st>>>(q, row0, nrows, col0 / 8, units,
+                                                                  out, ld, gshift);
+    else
+      k_materialize_lut<BITS, false, false><<<grid, 128, 0, st>>>(q, row0, nrows, col0 / 8,
+                                                                   units, out, ld, gshift);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t materialize_lut(const QWeightDev& q, int64_t row0, int64_t nrows, int64_t col0,
+                            int64_t ncols, void* out, int64_t ld, bool f32, cudaStream_t st) {
+  if (col0 % 8 != 0 || ncols % 8 != 0) return cudaErrorInvalidValue;
+  switch (q.bits) {
+    case 2: return materialize_lut_bits<2>(q, row0, nrows, col0, ncols, out, ld, f32, st);
+    case 3: return materialize_lut_bits<3>(q, row0, nrows, col0, ncols, out, ld, f32, st);
+    case 4: return materialize_lut_bits<4>(q, row0, nrows, col0, ncols, out, ld, f32, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 int grid_for(int64_t work, int per_block) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -260,6 +378,7 @@ cudaError_t launch_grid(const float* scales, const float* zeros, int64_t rows, i
 cudaError_t launch_materialize(const QWeightDev& q, int64_t row0, int64_t nrows, void* out,
                                int64_t ld, bool f32, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
+  if (q.lut) return materialize_lut(q, row0, nrows, 0, q.cols, out, ld, f32, st);
   switch (q.bits) {
     case 2: return materialize_bits<2>(q, row0, nrows, out, ld, f32, st);
     case 3: return materialize_bits<3>(q, row0, nrows, out, ld, f32, st);
@@ -273,6 +392,7 @@ cudaError_t launch_materialize_tile(const QWeightDev& q, int64_t row0, int64_t n
                                     int64_t ncols, void* out, int64_t ld, bool f32,
                                     cudaStream_t st) {
   if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+  if (q.lut) return materialize_lut(q, row0, nrows, col0, ncols, out, ld, f32, st);
   if (col0 == 0 && ncols == q.cols) return launch_materialize(q, row0, nrows, out, ld, f32, st);
   const bool vec = (ncols % 8 == 0) && (ld % 8 == 0) &&
                    (reinterpret_cast<uintptr_t>(out) % 16 == 0);

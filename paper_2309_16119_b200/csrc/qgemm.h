@@ -29,6 +29,7 @@ struct GemmArgs {
   const float* bias; // [m_valid] or nullptr
   int out_pairs;     // bf16 out with even ldo and 4-byte aligned base: paired-row stores
   const void* cb2_codebook;  // non-null: fused cb2 plugin decode (bf16 codebook, uint4[256])
+  const float* lut;          // non-null: fused lut plugin decode (16 f32 levels)
   // Q ring (fused path with TMA-fed codes); q_stages == 0 selects the LDG path
   int q_stages;
   int q_stage_bytes;
@@ -70,6 +71,7 @@ void qgemm2_plan(GemmArgs& p);
 bool qgemm_prefer_pair(const GemmArgs& p);
 constexpr int kMaxSkPairs = 128;
 constexpr int kCb2SmemBytes = 256 * 16;  // the cb2 codebook staged in shared memory
+constexpr int kLutSmemBytes = 64;         // the lut plugin's 16 levels in shared memory
 constexpr int64_t kSkSlotFloats = 2LL * 512 * 128;  // per pair
 
 }  // namespace mlra

@@ -139,9 +139,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sT = sW + STAGES * W_TILE;
   uint8_t* sQ = sT + STAGES * T_TILE;
   constexpr bool CB2 = BITS == kCb2Bits;
+  constexpr bool LUT = is_lut<BITS>();
   constexpr int QB = q_geom_bits<BITS>();  // packed-stream geometry
-  uint8_t* sCb = sQ + p.q_stages * p.q_stage_bytes;  // cb2 codebook (CB2 only)
-  uint64_t* full = reinterpret_cast<uint64_t*>(sCb + (CB2 ? kCb2SmemBytes : 0));
+  uint8_t* sCb = sQ + p.q_stages * p.q_stage_bytes;  // cb2 codebook / lut levels
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      sCb + (CB2 ? kCb2SmemBytes : (LUT ? kLutSmemBytes : 0)));
   uint64_t* empty = full + STAGES;
   uint64_t* qfull = empty + STAGES;
   uint64_t* qempty = qfull + MAX_QS;
@@ -199,6 +201,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (threadIdx.x < kCb2SmemBytes / 16)
       reinterpret_cast<uint4*>(sCb)[threadIdx.x] =
           __ldg(reinterpret_cast<const uint4*>(p.cb2_codebook) + threadIdx.x);
+  }
+  if constexpr (LUT) {
+    if (threadIdx.x < kLutSmemBytes / 4)
+      reinterpret_cast<float*>(sCb)[threadIdx.x] = __ldg(p.lut + threadIdx.x);
   }
   tc_fence_before();
   cluster_sync();  // barrier inits visible to the peer before any remote arrive
@@ -571,6 +577,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               if constexpr (CB2)
                 dequant_units_cb2<UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox,
                                                  smem_u32(sCb));
+              else if constexpr (LUT)
+                dequant_units_lut<QB, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox,
+                                                     smem_u32(sCb));
               else
                 dequant_units<BITS, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox);
               fence_proxy_async_smem();
@@ -616,7 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                   wrow = static_cast<int64_t>(kb) * BK + (u >> 4);
                   wunit = static_cast<int64_t>(cb) * (BM / 8) + (u & 15);
                 }
-                if constexpr (!CB2) {  // (the fused cb2 path always runs on the Q ring)
+                if constexpr (!CB2 && !LUT) {  // (the plugin decodes always run on the Q ring)
                   const uint64_t v = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
                   *reinterpret_cast<uint4*>(stile + unit_soff<MN>(u)) =
                       deq8_bf16_general<BITS>(v, q.grid + wrow * q.ng_pad, wunit * 8, q.group);
@@ -656,7 +665,7 @@ cudaError_t launch2_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs&
                       cudaStream_t stream) {
   auto kern = qgemm2_kernel<BITS, W_TMA, MN, OUT_F32, QTMA>;
   const int smem = SMEM_FIXED + p.q_stages * p.q_stage_bytes +
-                   (BITS == kCb2Bits ? kCb2SmemBytes : 0);
+                   (BITS == kCb2Bits ? kCb2SmemBytes : (is_lut<BITS>() ? kLutSmemBytes : 0));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
@@ -736,6 +745,15 @@ cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmA
   if (p.cb2_codebook != nullptr) {
     if (!qtma) return cudaErrorInvalidValue;  // the fused cb2 decode needs the Q ring
     return launch2_mo<kCb2Bits, false, true>(maps, q, p, mn, out_f32, stream);
+  }
+  if (p.lut != nullptr) {
+    if (!qtma) return cudaErrorInvalidValue;  // so does the lut decode
+    switch (q.bits) {
+      case 2: return launch2_mo<kLutTag + 2, false, true>(maps, q, p, mn, out_f32, stream);
+      case 3: return launch2_mo<kLutTag + 3, false, true>(maps, q, p, mn, out_f32, stream);
+      case 4: return launch2_mo<kLutTag + 4, false, true>(maps, q, p, mn, out_f32, stream);
+      default: return cudaErrorInvalidValue;
+    }
   }
   switch (q.bits) {
     case 2: return qtma ? launch2_mo<2, false, true>(maps, q, p, mn, out_f32, stream)

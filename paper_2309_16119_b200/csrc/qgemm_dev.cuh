@@ -116,8 +116,15 @@ __device__ __forceinline__ void dequant_units(uint32_t qc, uint32_t qg, uint32_t
 // per 8 weights), so the Q ring is loaded exactly as for BITS = 2 and only the
 // decode differs. `cbs` = shared address of the bf16-exact codebook, uint4[256].
 constexpr int kCb2Bits = 18;
+// The lut plugin (a per-matrix table of 2^b f32 levels, e.g. NF4): BITS tag
+// kLutTag + b; its codes are the plain b-bit stream, so only the decode differs.
+constexpr int kLutTag = 32;
 template <int BITS>
-constexpr int q_geom_bits() { return BITS == kCb2Bits ? 2 : BITS; }
+constexpr bool is_lut() { return BITS > kLutTag; }
+template <int BITS>
+constexpr int q_geom_bits() {
+  return BITS == kCb2Bits ? 2 : (BITS > kLutTag ? BITS - kLutTag : BITS);
+}
 
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
@@ -151,6 +158,38 @@ __device__ __forceinline__ void dequant_units_cb2(uint32_t qc, uint32_t qg, uint
       const float a = __fmul_rn(s, __uint_as_float(w[p] << 16));
       const float b = __fmul_rn(s, __uint_as_float(w[p] & 0xFFFF0000u));
       o[p] = pack_bf16x2(a, b) ^ ((((v[i] >> (8 + 2 * p)) & 3u) * 0x40008000u) & 0x80008000u);
+    }
+    sts128(st + soff[i], make_uint4(o[0], o[1], o[2], o[3]));
+  }
+}
+
+// The lut plugin's tile decode: w = RN_f32(s · lut[c]) -> bf16, the same
+// law as k_materialize_lut (materialize.cu), so fused == materialized bit for
+// bit. `lut` = shared address of the 16-float table: 16 consecutive words sit
+// in 16 distinct banks, so the per-code gathers never conflict.
+template <int B, int UPT, int ROW_STEP>
+__device__ __forceinline__ void dequant_units_lut(uint32_t qc, uint32_t qg, uint32_t st,
+                                                  const uint32_t (&soff)[UPT], int unit, int gsub,
+                                                  int rbase, int gbox, uint32_t lut) {
+  constexpr int QROW = 16 * B;
+  constexpr uint32_t mask = (1u << B) - 1u;
+  uint32_t v[UPT];
+  float sc[UPT];
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int row = rbase + i * ROW_STEP;
+    v[i] = q_unit<B>(qc + row * QROW, unit);
+    sc[i] = lds_f2(qg + row * gbox + gsub * 8).x;
+  }
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    uint32_t o[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const float a = __fmul_rn(sc[i], __uint_as_float(lds32(lut + (((v[i] >> (B * 2 * p)) & mask) << 2))));
+      const float b =
+          __fmul_rn(sc[i], __uint_as_float(lds32(lut + (((v[i] >> (B * (2 * p + 1))) & mask) << 2))));
+      o[p] = pack_bf16x2(a, b);
     }
     sts128(st + soff[i], make_uint4(o[0], o[1], o[2], o[3]));
   }

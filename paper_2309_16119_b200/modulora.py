@@ -362,6 +362,119 @@ class Codebook2Quantizer:
         return DeviceQuantizedMatrix._wrap(h, m.rows, m.cols, 2, m.group_size)
 
 
+# The QLoRA NF4 levels (Dettmers et al. 2023, "normal float 4"): the
+# published f32 table, sorted, normalised to [-1, 1] with an exact 0.
+NF4_LEVELS = np.array([
+    -1.0, -0.6961928009986877, -0.5250730514526367, -0.39491748809814453,
+    -0.28444138169288635, -0.18477343022823334, -0.09105003625154495, 0.0,
+    0.07958029955625534, 0.16093020141124725, 0.24611230194568634, 0.33791524171829224,
+    0.44070982933044434, 0.5626170039176941, 0.7229568362236023, 1.0], np.float32)
+
+
+def normal_float_levels(bits: int) -> np.ndarray:
+    """2^bits "normal float" levels: NF4 for 4 bits; for 2 / 3 bits the same
+    construction (quantiles of N(0, 1) at evenly spaced probabilities from
+    0.9677 to 1/2 on each side, 2^(b-1) positive, 2^(b-1) - 1 negative, plus an
+    exact 0), normalised by the largest magnitude."""
+    if bits == 4:
+        return NF4_LEVELS.copy()
+    if bits not in (2, 3):
+        raise MlraError(3, f"lut: unsupported bit width {bits} (2, 3 or 4)")
+    from statistics import NormalDist
+    inv = NormalDist().inv_cdf
+    hp, hn, off = 1 << (bits - 1), (1 << (bits - 1)) - 1, 0.9677083
+    pos = [inv(off + (0.5 - off) * i / hp) for i in range(hp)]
+    neg = [-inv(off + (0.5 - off) * i / hn) for i in range(hn)] if hn else []
+    v = np.sort(np.array(pos + neg + [0.0]))
+    return (v / np.abs(v).max()).astype(np.float32)
+
+
+def pack_codes(codes: np.ndarray, bits: int) -> np.ndarray:
+    """The reference's LSB-first bitstream (bitpack.cpp:68-91: code i at bit
+    i*bits of a u32 word array, ceil(n*bits/32) words), vectorised on the host."""
+    c = np.ascontiguousarray(codes, np.uint32).ravel()
+    if c.size and int(c.max()) >> bits:
+        raise MlraError(4, f"bitpack: code out of range for {bits} bits")
+    nw = (c.size * bits + 31) // 32
+    out = np.zeros(nw, np.uint32)
+    chunk = 1 << 20  # codes per pass, a multiple of 32 (so passes start on word boundaries)
+    for i in range(0, c.size, chunk):
+        bitv = ((c[i:i + chunk, None] >> np.arange(bits, dtype=np.uint32)) & 1).astype(np.uint8)
+        by = np.packbits(bitv.ravel(), bitorder="little")
+        by = np.pad(by, (0, (-by.size) % 4))
+        w = by.view("<u4")
+        w0 = i * bits // 32
+        out[w0:w0 + w.size] = w[:nw - w0]
+    return out
+
+
+@dataclass
+class LutMatrix:
+    """Host container of the lut format (include/mlra.h mlra_lut_create)."""
+    rows: int
+    cols: int
+    bits: int
+    group_size: int
+    codes: PackedCodes    # the reference bitstream of the b-bit level indices
+    levels: np.ndarray    # float32 [2^bits]
+    scales: np.ndarray    # float32 [rows x cols/group], > 0
+
+
+class LutQuantizer:
+    """Quantizer plugin "lut" (quantize.hpp:91-106 interface: name(), quantize()):
+    non-uniform levels (NF4 by default) with a per-(row, group) absmax scale,
+    Ŵ = RN_f32(s · levels[c]). ``quantize`` is the offline nearest-level search
+    on the host; ``upload`` returns an ordinary DeviceQuantizedMatrix whose
+    materialize() and fused GEMM decode run the library's lut kernels."""
+
+    def __init__(self, levels: Optional[np.ndarray] = None):
+        self.levels = None if levels is None else np.ascontiguousarray(levels, np.float32).ravel()
+
+    def name(self) -> str:
+        return "lut"
+
+    def levels_for(self, bits: int) -> np.ndarray:
+        if self.levels is None:
+            return normal_float_levels(bits)
+        if self.levels.size != 1 << bits:
+            raise MlraError(3, f"lut: {self.levels.size} levels for {bits} bits")
+        return self.levels
+
+    def quantize(self, w, calib=None, bits: int = 4, group_size: int = 64) -> LutMatrix:
+        w = np.asarray(w, np.float64)
+        if w.ndim != 2 or w.size == 0:
+            raise MlraError(2, "quantize: expected a non-empty 2-D weight matrix")
+        rows, cols = w.shape
+        g = cols if group_size == 0 else group_size
+        if g % 8 or cols % g:
+            raise MlraError(3, f"lut: group size {g} must be a multiple of 8 dividing cols {cols}")
+        lv = self.levels_for(bits).astype(np.float64)
+        ng = cols // g
+        amax = np.abs(w.reshape(rows, ng, g)).max(-1)
+        scales = np.where(amax > 0, amax, 1.0).astype(np.float32)
+        scales = np.maximum(scales, np.finfo(np.float32).tiny)
+        x = (w.reshape(rows, ng, g) / scales.astype(np.float64)[:, :, None]).reshape(-1)
+        # nearest level (levels sorted: compare against the midpoints; ties -> lower index)
+        order = np.argsort(lv, kind="stable")
+        srt = lv[order]
+        mid = (srt[1:] + srt[:-1]) / 2
+        codes = order[np.searchsorted(mid, x, side="left")].astype(np.uint32)
+        return LutMatrix(rows, cols, bits, g, PackedCodes(bits, rows * cols, pack_codes(codes, bits)),
+                         lv.astype(np.float32), scales.reshape(rows, ng))
+
+    def upload(self, m: LutMatrix, stream: Optional[torch.cuda.Stream] = None) -> DeviceQuantizedMatrix:
+        words = np.ascontiguousarray(m.codes.words, np.uint32)
+        lv = np.ascontiguousarray(m.levels, np.float32)
+        sc = np.ascontiguousarray(m.scales, np.float32)
+        if lv.size != 1 << m.bits or sc.size != m.rows * (m.cols // m.group_size):
+            raise MlraError(7, "lut: buffer sizes do not match the shape")
+        h = C.c_void_p()
+        check(lib().mlra_lut_create(m.rows, m.cols, m.bits, m.group_size, words.ctypes.data,
+                                    words.size, lv.ctypes.data, sc.ctypes.data,
+                                    _stream_ptr(stream), C.byref(h)))
+        return DeviceQuantizedMatrix._wrap(h, m.rows, m.cols, m.bits, m.group_size)
+
+
 @dataclass
 class LpLinearContext:
     """lowprec_linear.hpp:85-91 (ledger replaced by ledger_bytes())."""

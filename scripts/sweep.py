@@ -9,6 +9,8 @@ headline bench; writes one JSON line per config).
         2-bit format and the black-box "cb2" codebook plugin (hook), plus the cb2 layer
         fwd+bwd through the hook (slabbed hook materialization + tcgen05 GEMM), m=4096
   cfg3_train  the cfg3 stack as a training step (LinearStackTrainer: fwd, bwd, AdamW)
+  nf4   the lut plugin (NF4, g64) vs the affine 4-bit format at the cfg2 shapes, and
+        its materialize() bandwidth at the cfg5 matrix
 
 Timing: CUDA events, 3 warm-up + 10 timed steps, L2 flushed between steps. Each
 layer config is timed eager and as a replayed CUDA graph ("launch" key): small
@@ -169,6 +171,59 @@ def main():
                               "ledger_bytes": M.LpLinearContext(cq, L.strategy).ledger_bytes(),
                               "ms_per_step": ms, "tflops": flops / (ms / 1e3) / 1e12}),
                   flush=True)
+
+    if not only or "nf4" in only:
+        # the lut plugin (NF4 levels, absmax scale, g64) against the affine 4-bit
+        # format at the cfg2 shapes (LLaMA-7B MLP up + down, r=16, m=4096), and its
+        # materialize() bandwidth at the cfg5 matrix
+        import numpy as np
+        rng = np.random.default_rng(700)
+        shapes, m, r = [(11008, 4096), (4096, 11008)], 4096, 16
+
+        def lut_dq(rows, cols, bits, group, seed):
+            g = np.random.default_rng(seed)
+            codes = g.integers(0, 1 << bits, rows * cols, dtype=np.uint32)
+            lm = M.LutMatrix(rows, cols, bits, group,
+                             M.PackedCodes(bits, rows * cols, M.pack_codes(codes, bits)),
+                             M.normal_float_levels(bits),
+                             (0.02 * (0.5 + g.random((rows, cols // group)))).astype(np.float32))
+            return M.LutQuantizer().upload(lm)
+
+        for fmt in ("nf4", "affine4"):
+            layers = []
+            for i, (rows, cols) in enumerate(shapes):
+                if fmt == "nf4":
+                    dq = lut_dq(rows, cols, 4, 64, 710 + i)
+                else:
+                    q, *_ = synthetic_qmatrix(rows, cols, 4, 64, 720 + i)
+                    dq = M.DeviceQuantizedMatrix(q)
+                a = torch.randn(rows, r, device="cuda") * 0.02
+                b = torch.randn(cols, r, device="cuda") * 0.02
+                layers.append(M.ModuLoraLayer(f"{fmt}{i}", dq, M.LoraAdapter(a, b, r, 32.0),
+                                              strategy=strat))
+            fn = graphed(independent_layers_step(layers, m))
+            ms = time_steps(fn, flush)
+            flops = sum(4.0 * m * a_ * b_ + 6.0 * m * r * (a_ + b_) for a_, b_ in shapes)
+            print(json.dumps({"config": "nf4_mlp", "format": fmt, "shapes": shapes, "bits": 4,
+                              "group": 64, "rank": r, "tokens": m, "launch": "cuda-graph",
+                              "ms_per_step": ms, "tokens_per_s": m / (ms / 1e3),
+                              "tflops": flops / (ms / 1e3) / 1e12,
+                              "pct_measured_bf16_peak": 100 * flops / (ms / 1e3) / 1e12 / pk}),
+                  flush=True)
+            del layers, fn
+            torch.cuda.empty_cache()
+        rows, cols = 6656, 17920
+        dq = lut_dq(rows, cols, 4, 64, 730)
+        for dt, eb in ((torch.bfloat16, 2), (torch.float32, 4)):
+            out = torch.empty(rows, cols, dtype=dt, device="cuda")
+            ms = time_steps(lambda: M.dequantize(dq, dt, out=out), flush)
+            nbytes = rows * cols * (4 / 8 + eb) + rows * (cols // 64) * 8
+            print(json.dumps({"config": "nf4_materialize", "shape": [rows, cols], "bits": 4,
+                              "group": 64, "out": str(dt), "us": ms * 1e3,
+                              "gbs": nbytes / (ms / 1e3) / 1e9,
+                              "frac_measured_hbm": nbytes / (ms / 1e3) / 1e9 / hbm}),
+                  flush=True)
+            del out
 
 
 if __name__ == "__main__":

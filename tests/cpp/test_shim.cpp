@@ -36,7 +36,7 @@ static bool throws(const std::function<void()>& f) {
 }
 
 // LSB-first bitstream (bitpack.cpp:68-91), test-side restatement.
-static PackedCodes pack(const std::vector<uint32_t>& codes, int bits) {
+static PackedCodes ref_pack(const std::vector<uint32_t>& codes, int bits) {
   PackedCodes p;
   p.bits = bits;
   p.count = codes.size();
@@ -59,7 +59,7 @@ static QuantizedMatrix random_q(std::size_t rows, std::size_t cols, int bits, st
   q.cols = cols;
   q.bits = bits;
   q.group_size = group;
-  q.codes = pack(codes, bits);
+  q.codes = ref_pack(codes, bits);
   std::uniform_real_distribution<double> u(0.0, 1.0);
   for (std::size_t i = 0; i < rows * (cols / group); ++i) {
     q.scales.push_back(static_cast<float>(0.002 + 0.01 * u(g)));
@@ -117,7 +117,7 @@ int main(int argc, char** argv) {
     q.cols = 2;
     q.bits = 2;
     q.group_size = 2;
-    q.codes = pack({0, 1, 2, 3}, 2);
+    q.codes = ref_pack({0, 1, 2, 3}, 2);
     q.scales = {0.5f, 1.0f};
     q.zeros = {-1.0f, 0.0f};
     DeviceQuantizedMatrix dq(q);
@@ -143,7 +143,7 @@ int main(int argc, char** argv) {
     q.rows = q.cols = n;
     q.bits = 8;
     q.group_size = n;
-    q.codes = pack(codes, 8);
+    q.codes = ref_pack(codes, 8);
     q.scales.assign(n, 1.0f);
     q.zeros.assign(n, 0.0f);
     auto dq = std::make_shared<const DeviceQuantizedMatrix>(q);
@@ -272,6 +272,29 @@ int main(int argc, char** argv) {
     for (int j = 0; j < 16; ++j) ok = ok && w(0, j) == want[j];
     CHECK(ok);
     CHECK(throws<NumericError>([&] { upload_cb2(1, 16, 8, codes, cb, {2.0f, -1.0f}); }));
+  }
+  // --- lut plugin: decode law known answer (tests/test_lut.py::test_lut_known_answer)
+  {
+    // the header's pack() against the test-side restatement, all widths
+    bool same = true;
+    for (int b : {2, 3, 4, 8}) {
+      std::vector<std::uint32_t> cs(1000);
+      for (std::size_t i = 0; i < cs.size(); ++i) cs[i] = static_cast<std::uint32_t>(i * 2654435761u >> 7) & ((1u << b) - 1u);
+      same = same && pack(cs, b).words == ref_pack(cs, b).words;
+    }
+    CHECK(same);
+    CHECK(throws<RangeError>([] { pack(std::vector<std::uint32_t>{4}, 2); }));
+    PackedCodes pc = pack(std::vector<std::uint32_t>{0, 1, 2, 3, 3, 2, 1, 0, 0, 1, 2, 3, 3, 2, 1, 0}, 2);
+    auto q = upload_lut(2, 8, 8, pc, {-1.0f, -0.25f, 0.5f, 3.0f}, {2.0f, 0.5f});
+    const HostMatrix w = dequantize(*q);
+    const double want[2][8] = {{-2, -0.5, 1, 6, 6, 1, -0.5, -2},
+                               {-0.5, -0.125, 0.25, 1.5, 1.5, 0.25, -0.125, -0.5}};
+    bool ok = true;
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 8; ++j) ok = ok && w(i, j) == want[i][j];
+    CHECK(ok);
+    CHECK(throws<NumericError>([&] { upload_lut(2, 8, 8, pc, {-1.0f, NAN, 0.5f, 3.0f}, {2.0f, 0.5f}); }));
+    CHECK(throws<ConfigError>([&] { upload_lut(2, 8, 4, pc, {-1.0f, 0.0f, 0.5f, 3.0f}, {1, 1, 1, 1}); }));
   }
   // --- AdamW first step replicates the update arithmetic (test_train.cpp:145-167)
   {
