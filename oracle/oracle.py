@@ -282,6 +282,10 @@ class Ref:
                                           np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS"),
                                           _f64p, _f64p, _u64, _f64p, C.POINTER(_u64)]
             lib.ref_adamw_run.restype = _int
+            lib.ref_parity_loss_grads.argtypes = [C.c_char_p, _f64p,
+                                                  np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"),
+                                                  _u64, _u64, _u64, C.POINTER(C.c_double), _f64p, _u64]
+            lib.ref_parity_loss_grads.restype = _int
             cls._lib = lib
         return cls._lib
 
@@ -295,6 +299,19 @@ class Ref:
                                      np.ascontiguousarray(grads, np.float64).ravel(), len(lrs),
                                      np.ascontiguousarray(lrs, np.float64), C.byref(bad))
         return rc, vals, int(bad.value)
+
+    @classmethod
+    def parity_loss_grads(cls, path: str, xs, labels, n_grads: int):
+        """The reference's parity-transformer model_loss + tape backward on the
+        checkpoint at ``path``: (loss, flat trainable-param grads)."""
+        xs = np.ascontiguousarray(xs, np.float64)
+        n, seq, d = xs.shape
+        g = np.empty(n_grads, np.float64)
+        loss = C.c_double()
+        cls._chk(cls.get().ref_parity_loss_grads(path.encode(), xs.ravel(),
+                                                 np.ascontiguousarray(labels, np.int32), n, seq, d,
+                                                 C.byref(loss), g, n_grads))
+        return loss.value, g
 
     @classmethod
     def _chk(cls, st):

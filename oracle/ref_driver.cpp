@@ -9,6 +9,7 @@
 //   * bench.py --impl reference / cpu_baseline — the reference's own CPU
 //     hot path timed on the host cores (token-sharded replicas, one Tape per
 //     thread as SPEC.md:310 allows).
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -431,6 +432,52 @@ int ref_adamw_run(double beta1, double beta2, double eps, double wd, uint64_t n_
     if (rc) return rc;
   }
   return 0;
+}
+
+// model_loss of the parity transformer (model.cpp:226-292: transformer_forward
+// per sequence, cross_entropy, mean) on the model saved at `path`, for caller
+// sequences xs [n x seq x d] (row-major f64) and labels [n]; then the tape
+// backward (autodiff.cpp:101-139). Writes the loss and every trainable
+// parameter's gradient, trainable_params order (model.cpp:186-197), flat.
+int ref_parity_loss_grads(const char* path, const double* xs, const int* labels, uint64_t n,
+                          uint64_t seq, uint64_t d, double* loss, double* grads,
+                          uint64_t grads_len) {
+  try {
+    ToyModel m = load_model(path);
+    Tape t;
+    Variable total;
+    for (uint64_t i = 0; i < n; ++i) {
+      DenseMatrix x(seq, d);
+      for (uint64_t r = 0; r < seq; ++r)
+        for (uint64_t c = 0; c < d; ++c) x(r, c) = xs[(i * seq + r) * d + c];
+      Variable logits = transformer_forward(t, m, Variable::leaf(std::move(x)), nullptr);
+      const int lab[] = {labels[i]};
+      Variable ce = cross_entropy(t, logits, lab);
+      total = total.defined() ? add(t, total, ce) : ce;
+    }
+    Variable L = scalar_mul(t, total, 1.0 / static_cast<double>(n));
+    std::vector<Variable> params = m.trainable_params();
+    for (Variable& p : params) p.zero_grad();
+    backward(t, L);
+    *loss = L.value()(0, 0);
+    uint64_t off = 0;
+    for (Variable& p : params) {
+      const std::size_t cnt = p.value().rows() * p.value().cols();
+      if (off + cnt > grads_len) throw ContractError("ref_parity_loss_grads: grads buffer too small");
+      if (p.has_grad()) {
+        const DenseMatrix& g = p.grad();
+        for (std::size_t r = 0; r < g.rows(); ++r)
+          for (std::size_t c = 0; c < g.cols(); ++c) grads[off + r * g.cols() + c] = g(r, c);
+      } else {
+        std::fill(grads + off, grads + off + cnt, 0.0);
+      }
+      off += cnt;
+    }
+    if (off != grads_len) throw ContractError("ref_parity_loss_grads: grads buffer size mismatch");
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
 }
 
 }  // extern "C"

@@ -9,6 +9,8 @@ headline bench; writes one JSON line per config).
         2-bit format and the black-box "cb2" codebook plugin (hook), plus the cb2 layer
         fwd+bwd through the hook (slabbed hook materialization + tcgen05 GEMM), m=4096
   cfg3_train  the cfg3 stack as a training step (LinearStackTrainer: fwd, bwd, AdamW)
+  decoder  the reference's parity-transformer block at LLaMA-7B widths as a device
+        training step (model.py: fwd, bwd, AdamW)
   nf4   the lut plugin (NF4, g64) vs the affine 4-bit format at the cfg2 shapes, and
         its materialize() bandwidth at the cfg5 matrix
 
@@ -224,6 +226,36 @@ def main():
                               "frac_measured_hbm": nbytes / (ms / 1e3) / 1e9 / hbm}),
                   flush=True)
             del out
+
+    if not only or "decoder" in only:
+        # the reference's parity-transformer block (model.cpp:226-257) at LLaMA-7B
+        # widths as a full training step on the device: 7 quantized linears (3-bit
+        # g128, r=16; head to 2 classes) + fp32 glue, backward, AdamW over the
+        # adapter bucket. 8 sequences x 512 tokens.
+        from paper_2309_16119_b200 import model as Mdl
+        from paper_2309_16119_b200 import train as T
+        d, dff, B, seq, r = 4096, 11008, 8, 512, 16
+        shapes = [(d, d)] * 4 + [(dff, d), (d, dff), (2, d)]
+        layers = []
+        for i, ((rows, cols), nm) in enumerate(zip(shapes, Mdl.LAYER_NAMES)):
+            q, *_ = synthetic_qmatrix(rows, cols, 3, 128, 800 + i)
+            a = torch.randn(rows, r, device="cuda") * 0.02
+            b = torch.randn(cols, r, device="cuda") * 0.02
+            layers.append(M.ModuLoraLayer(nm, M.DeviceQuantizedMatrix(q), M.LoraAdapter(a, b, r, 32.0),
+                                          bias=torch.zeros(rows, device="cuda"), strategy=strat))
+        tr = Mdl.TransformerTrainer(Mdl.ParityTransformer(layers), T.TrainConfig(lr=1e-4))
+        x = torch.randn(B, seq, d, device="cuda")
+        y = torch.randint(0, 2, (B,), device="cuda")
+        ms = time_steps(lambda: tr.step(x, y, check_finite=False), flush)
+        m = B * seq
+        lin_flops = sum(4.0 * (m if nm != "head" else B) * a_ * b_ for (a_, b_), nm in zip(shapes, Mdl.LAYER_NAMES))
+        print(json.dumps({"config": "decoder_train", "model": "parity_transformer block",
+                          "d_model": d, "d_ff": dff, "sequences": B, "seq_len": seq, "bits": 3,
+                          "rank": r, "step": "fwd + bwd (dX) + AdamW", "ms_per_step": ms,
+                          "tokens_per_s": m / (ms / 1e3),
+                          "linear_tflops": lin_flops / (ms / 1e3) / 1e12}), flush=True)
+        del layers, tr
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":

@@ -3,7 +3,8 @@
 Run in the build container (needs /root/reference, via oracle/_ref built by
 ``make -C oracle``):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py          # everything
+    python tests/golden/make_golden.py model    # only parity_model.npz (+ its checkpoint)
 
 Every array is produced by the unmodified reference library
 (oracle/_ref/libmlra_ref.so: /root/reference/proj/src + oracle/ref_driver.cpp).
@@ -229,9 +230,38 @@ def checkpoint_cases():
     assert expect["golden.mlra"]["frozen_hash"] == 0xa3d66a9e729158ff
 
 
+def model_cases():
+    """The parity transformer (model.cpp:226-292) pinned by the reference: the
+    reference-made parity_b4.mlra with seeded non-zero adapters (so every dA /
+    dB is live), then the reference's own model_loss + tape backward on seeded
+    sequences -> loss and the flat trainable-parameter gradients."""
+    import json
+    from paper_2309_16119_b200.checkpoint import Checkpoint
+    ck = Checkpoint.load(os.path.join(HERE, "parity_b4.mlra"))
+    rng = np.random.default_rng(2309)
+    n_grads = 0
+    for i in range(len(ck)):
+        r = ck.layer(i)
+        ck.set_adapter(i, rng.normal(0.0, 0.15, (r.rows, r.rank)), rng.normal(0.0, 0.15, (r.cols, r.rank)))
+        n_grads += r.rank * (r.rows + r.cols)
+    path = os.path.join(HERE, "parity_b4_adapted.mlra")
+    ck.save(path)
+    cfg = json.loads(ck.config_json())
+    dims = cfg.get("task_dims", {})
+    seq, d = int(dims.get("seq_len", 8)), int(dims.get("d_model", 16))
+    n = 6
+    xs = rng.normal(0.0, 1.0, (n, seq, d))
+    labels = rng.integers(0, 2, n).astype(np.int32)
+    loss, grads = Ref.parity_loss_grads(path, xs, labels, n_grads)
+    return dict(xs=xs, labels=labels, loss=np.array([loss]), grads=grads)
+
+
 def main():
     if not Ref.available():
         raise SystemExit("oracle/_ref/libmlra_ref.so missing: run `make -C oracle` with /root/reference present")
+    if sys.argv[1:] == ["model"]:
+        np.savez_compressed(os.path.join(HERE, "parity_model.npz"), **model_cases())
+        return
     np.savez_compressed(os.path.join(HERE, "bitpack.npz"), **bitpack_cases())
     np.savez_compressed(os.path.join(HERE, "quantize.npz"), **quant_cases())
     np.savez_compressed(os.path.join(HERE, "layer.npz"), **layer_cases())
@@ -241,6 +271,7 @@ def main():
                         gaussian_seed8_scaled=Ref.gaussian(8, 4, 4, 0.5, 0.02),
                         mix_seed_11_ada9=np.array([meta["mix_seed_11_ada9"]], np.uint64))
     checkpoint_cases()
+    np.savez_compressed(os.path.join(HERE, "parity_model.npz"), **model_cases())
     for f in sorted(os.listdir(HERE)):
         if f.endswith((".npz", ".mlra", ".json")):
             print(f, os.path.getsize(os.path.join(HERE, f)))
