@@ -191,6 +191,28 @@ MLRA_API mlra_status mlra_quantize_rtn(const void* w, mlra_dtype dtype, int64_t 
                                        int bits, int64_t group_size, uint32_t* words,
                                        float* scales, float* zeros, void* stream);
 
+/* build_optq_workspace (quantize.hpp:65-71; quantize.cpp:186-211) on the
+ * device: calib DEVICE f64 [m x dim] -> hessian = XᵀX + damping·mean(diag)·I
+ * and upper = the upper Cholesky factor of its inverse (linalg.cpp:68-71),
+ * both DEVICE f64 [dim x dim], bit-identical to the reference. Synchronous.
+ * Errors: DimensionError (empty calibration), ConfigError (damping < 0 or
+ * NaN), NumericError ("Hessian not invertible after damping"). */
+MLRA_API mlra_status mlra_optq_workspace(const double* calib, int64_t m, int64_t dim,
+                                         double damping, double* hessian, double* upper,
+                                         void* stream);
+
+/* OptqQuantizer::quantize (quantize.hpp:73-75, 115-125; quantize.cpp:213-255)
+ * on the device: w DEVICE f64 [rows x cols], calib DEVICE f64 [m x cols];
+ * writes the reference's QuantizedMatrix layout to DEVICE words / scales /
+ * zeros exactly as mlra_quantize_rtn (same grids: computed from the original
+ * weights), with the calibration-aware column sweep's codes. Bit-identical to
+ * quantize_optq. Synchronous. Errors as quantize_rtn, then as
+ * mlra_optq_workspace. */
+MLRA_API mlra_status mlra_quantize_optq(const double* w, const double* calib, int64_t rows,
+                                        int64_t cols, int64_t m, int bits, int64_t group_size,
+                                        double damping, uint32_t* words, float* scales,
+                                        float* zeros, void* stream);
+
 /* The hook an opaque qweight carries (NULL for the affine built-in format). */
 MLRA_API const mlra_hook* mlra_qweight_hook(const mlra_qweight* q);
 

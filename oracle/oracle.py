@@ -266,6 +266,9 @@ class Ref:
             lib.ref_pack.argtypes = [_u32p, _u64, _int, _u32p]
             lib.ref_unpack.argtypes = [_u32p, _u64, _u64, _int, _u32p]
             lib.ref_quantize_rtn.argtypes = [_f64p, _u64, _u64, _int, _u64, _u32p, _f32p, _f32p]
+            lib.ref_quantize_optq.argtypes = [_f64p, _f64p, _u64, _u64, _u64, _int, _u64, C.c_double,
+                                              _u32p, _f32p, _f32p]
+            lib.ref_optq_workspace.argtypes = [_f64p, _u64, _u64, C.c_double, _f64p, _f64p]
             lib.ref_validate.argtypes = [_u32p, _u64, _u64, _int, _u64, _f32p, _f32p]
             lib.ref_dequantize.argtypes = [_u32p, _u64, _u64, _int, _u64, _f32p, _f32p, _f64p]
             lib.ref_lp_forward.argtypes = [_u32p, _u64, _u64, _int, _u64, _f32p, _f32p, _int,
@@ -350,6 +353,29 @@ class Ref:
         zeros = np.zeros(rows * (cols // g), np.float32)
         cls._chk(cls.get().ref_quantize_rtn(w, rows, cols, bits, group, words, scales, zeros))
         return words[:nw], scales, zeros
+
+    @classmethod
+    def quantize_optq(cls, w, calib, bits, group=0, damping=0.01):
+        w = _c(w, np.float64)
+        calib = _c(calib, np.float64)
+        rows, cols = w.shape
+        g = cols if group == 0 else group
+        nw = int(cls.get().ref_packed_word_count(rows * cols, bits))
+        words = np.zeros(max(nw, 1), np.uint32)
+        scales = np.zeros(rows * (cols // g), np.float32)
+        zeros = np.zeros(rows * (cols // g), np.float32)
+        cls._chk(cls.get().ref_quantize_optq(w, calib, rows, cols, calib.shape[0], bits, group,
+                                             damping, words, scales, zeros))
+        return words[:nw], scales, zeros
+
+    @classmethod
+    def optq_workspace(cls, calib, damping=0.01):
+        calib = _c(calib, np.float64)
+        m, n = calib.shape
+        h = np.zeros((n, n), np.float64)
+        u = np.zeros((n, n), np.float64)
+        cls._chk(cls.get().ref_optq_workspace(calib, m, n, damping, h, u))
+        return h, u
 
     @classmethod
     def dequantize(cls, words, rows, cols, bits, group, scales, zeros):

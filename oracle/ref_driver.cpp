@@ -180,6 +180,36 @@ int ref_quantize_rtn(const double* w, uint64_t rows, uint64_t cols, int bits,
   }
 }
 
+// quantize_optq (quantize.cpp:213-255) and build_optq_workspace (:186-211).
+int ref_quantize_optq(const double* w, const double* calib, uint64_t rows, uint64_t cols,
+                      uint64_t m, int bits, uint64_t group, double damping, uint32_t* words,
+                      float* scales, float* zeros) {
+  try {
+    QuantizedMatrix q = quantize_optq(dm(w, rows, cols), dm(calib, m, cols), bits, group, damping);
+    std::memcpy(words, q.codes.words.data(), q.codes.words.size() * 4);
+    std::memcpy(scales, q.scales.data(), q.scales.size() * 4);
+    std::memcpy(zeros, q.zeros.data(), q.zeros.size() * 4);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+int ref_optq_workspace(const double* calib, uint64_t m, uint64_t dim, double damping,
+                       double* hessian, double* upper) {
+  try {
+    OptqWorkspace ws = build_optq_workspace(dm(calib, m, dim), dim, damping);
+    for (uint64_t i = 0; i < dim; ++i)
+      for (uint64_t j = 0; j < dim; ++j) {
+        hessian[i * dim + j] = ws.hessian(i, j);
+        upper[i * dim + j] = ws.inv_chol_upper(i, j);
+      }
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
 int ref_validate(const uint32_t* words, uint64_t rows, uint64_t cols, int bits,
                  uint64_t group, const float* scales, const float* zeros) {
   try {

@@ -6,7 +6,7 @@ mirror of the reference interface (see modulora.py)."""
 from ._lib import MlraError, build, lib  # noqa: F401
 from .modulora import (  # noqa: F401
     Cb2Matrix, Codebook2Quantizer, DeviceQuantizedMatrix, DoublingQuantizer, LoraAdapter,
-    LpLinearContext, LutMatrix, LutQuantizer, MaterializationStrategy, NF4_LEVELS, ModuLoraLayer, ModuLoraLinearFunction, PackedCodes,
+    LpLinearContext, LutMatrix, LutQuantizer, MaterializationStrategy, NF4_LEVELS, OptqQuantizer, ModuLoraLayer, ModuLoraLinearFunction, PackedCodes,
     QuantizedMatrix, QuantizerHook, RtnQuantizer, default_cb2_codebook, dequantize,
     dequantize_row, dequantize_tile, grads_of_adapter, init_adapter, layer_backward, layer_forward,
-    lp_backward, lp_forward, make_layer, normal_float_levels, pack_codes, packed_word_count, parse_strategy, strategy_name)
+    lp_backward, lp_forward, make_layer, normal_float_levels, optq_workspace, pack_codes, packed_word_count, parse_strategy, strategy_name)

@@ -30,7 +30,8 @@ EXPORTS = [
     "mlra_checkpoint_frozen_hash", "mlra_checkpoint_file_hash", "mlra_checkpoint_upload",
     "mlra_checkpoint_set_adapter", "mlra_checkpoint_save", "mlra_quantize_rtn",
     "mlra_dp_unique_id", "mlra_dp_init", "mlra_allreduce_lora_grads", "mlra_dp_destroy",
-    "mlra_mix_seed", "mlra_gaussian_fill", "mlra_lut_create",
+    "mlra_mix_seed", "mlra_gaussian_fill", "mlra_lut_create", "mlra_optq_workspace",
+    "mlra_quantize_optq",
 ]
 
 # mlra_hook.materialize(state, q, row0, nrows, col0, ncols, out, dtype, ld, stream)
@@ -129,6 +130,11 @@ def lib() -> C.CDLL:
                                                  C.POINTER(vp)]
         L.mlra_cb2_create.restype = i32
         L.mlra_cb2_create.argtypes = [i64, i64, i64, vp, vp, vp, vp, C.POINTER(vp)]
+        L.mlra_optq_workspace.restype = i32
+        L.mlra_optq_workspace.argtypes = [vp, i64, i64, C.c_double, vp, vp, vp]
+        L.mlra_quantize_optq.restype = i32
+        L.mlra_quantize_optq.argtypes = [vp, vp, i64, i64, i64, C.c_int, i64, C.c_double, vp, vp,
+                                         vp, vp]
         L.mlra_lut_create.restype = i32
         L.mlra_lut_create.argtypes = [i64, i64, C.c_int, i64, vp, C.c_uint64, vp, vp, vp,
                                       C.POINTER(vp)]

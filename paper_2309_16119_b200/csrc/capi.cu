@@ -820,6 +820,79 @@ mlra_status mlra_quantize_rtn(const void* w, mlra_dtype dtype, int64_t rows, int
   return MLRA_OK;
 }
 
+mlra_status mlra_optq_workspace(const double* calib, int64_t m, int64_t dim, double damping,
+                                double* hessian, double* upper, void* stream) {
+  // build_optq_workspace (quantize.cpp:186-211)
+  if (m <= 0 || dim <= 0)
+    return fail(MLRA_ERR_DIMENSION, "optq: calibration must be [m x %lld], got %lldx%lld",
+                (long long)dim, (long long)m, (long long)dim);
+  if (!(damping >= 0.0)) return fail(MLRA_ERR_CONFIG, "optq: damping must be non-negative");
+  if (!calib || !hessian || !upper) return fail(MLRA_ERR_CONTRACT, "optq: null buffers");
+  if (mlra_status st = check_device()) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* scratch = nullptr;
+  int* bad = nullptr;
+  CUDA_TRY(cudaMallocAsync(&scratch, 2 * dim * dim * sizeof(double), s));
+  cudaError_t e = cudaMallocAsync(&bad, 2 * sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0x7f, 2 * sizeof(int), s);
+  if (e == cudaSuccess)
+    e = mlra::launch_optq_workspace(calib, m, dim, damping, hessian, upper, scratch, bad, s);
+  int hb[2] = {0x7f7f7f7f, 0x7f7f7f7f};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(scratch, s);
+  if (bad) cudaFreeAsync(bad, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(MLRA_ERR_CUDA, "optq workspace: %s", cudaGetErrorString(e));
+  if (hb[0] < dim || hb[1] < dim)
+    return fail(MLRA_ERR_NUMERIC, "optq: calibration Hessian not invertible after damping");
+  return MLRA_OK;
+}
+
+mlra_status mlra_quantize_optq(const double* w, const double* calib, int64_t rows, int64_t cols,
+                               int64_t m, int bits, int64_t group, double damping, uint32_t* words,
+                               float* scales, float* zeros, void* stream) {
+  // quantize_optq (quantize.cpp:213-255): normalize_group_size, validate_quantize_args,
+  // build_optq_workspace, grids from the original weights, the column sweep
+  if (group == 0) group = cols;
+  if (rows <= 0 || cols <= 0) return fail(MLRA_ERR_DIMENSION, "quantize: matrix must be non-empty");
+  if (!supported_bits(bits))
+    return fail(MLRA_ERR_CONFIG, "quantize: unsupported bit width %d", bits);
+  if (group <= 0 || cols % group != 0)
+    return fail(MLRA_ERR_CONFIG, "quantize: group size %lld does not divide cols %lld",
+                (long long)group, (long long)cols);
+  if (!w || !words || !scales || !zeros) return fail(MLRA_ERR_CONTRACT, "optq: null buffers");
+  if (mlra_status st = check_device()) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double *h = nullptr, *u = nullptr, *es = nullptr;
+  uint32_t* codes = nullptr;
+  auto release = [&]() {
+    if (h) cudaFreeAsync(h, s);
+    if (u) cudaFreeAsync(u, s);
+    if (es) cudaFreeAsync(es, s);
+    if (codes) cudaFreeAsync(codes, s);
+  };
+  if (cudaMallocAsync(&h, cols * cols * sizeof(double), s) != cudaSuccess ||
+      cudaMallocAsync(&u, cols * cols * sizeof(double), s) != cudaSuccess) {
+    release();
+    return fail(MLRA_ERR_CUDA, "optq: workspace allocation failed");
+  }
+  if (mlra_status st = mlra_optq_workspace(calib, m, cols, damping, h, u, stream)) {
+    release();
+    return st;
+  }
+  const uint64_t nwords = mlra_packed_word_count(static_cast<uint64_t>(rows * cols), bits);
+  cudaError_t e = cudaMallocAsync(&es, rows * cols * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&codes, rows * cols * sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = mlra::launch_rtn_grid(w, rows, cols, group, bits, scales, zeros, s);
+  if (e == cudaSuccess)
+    e = mlra::launch_optq_sweep(w, u, rows, cols, group, bits, scales, zeros, es, codes, words,
+                                nwords, s);
+  release();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(MLRA_ERR_CUDA, "optq: %s", cudaGetErrorString(e));
+  return MLRA_OK;
+}
+
 const mlra_hook* mlra_qweight_hook(const mlra_qweight* q) {
   return q && q->opaque ? &q->hook : nullptr;
 }

@@ -31,6 +31,22 @@ cudaError_t launch_quantize_rtn(const void* w, bool f64, int64_t rows, int64_t c
                                 int bits, uint32_t* words, uint64_t nwords, float* scales,
                                 float* zeros, cudaStream_t st);
 
+// compute_grid (quantize.cpp:24-36) per (row, group) of a device f64 matrix
+cudaError_t launch_rtn_grid(const double* w, int64_t rows, int64_t cols, int64_t group, int bits,
+                            float* scales, float* zeros, cudaStream_t st);
+
+// OPTQ (optq.cu): build_optq_workspace (quantize.cpp:186-211) — hessian / upper [n x n],
+// scratch 2 n^2 doubles, bad[2] = first failing pivot of the two factorizations (init INT_MAX)
+cudaError_t launch_optq_workspace(const double* calib, int64_t m, int64_t n, double damping,
+                                  double* hessian, double* upper, double* scratch, int* bad,
+                                  cudaStream_t st);
+// the column sweep (quantize.cpp:231-252) + packing; e_scratch [rows x cols] f64,
+// codes [rows x cols] u32
+cudaError_t launch_optq_sweep(const double* w, const double* upper, int64_t rows, int64_t cols,
+                              int64_t group, int bits, const float* scales, const float* zeros,
+                              double* e_scratch, uint32_t* codes, uint32_t* words, uint64_t nwords,
+                              cudaStream_t st);
+
 // AdamW (optim.cu): host-evaluated constants of AdamW::step (train.cpp:99-101, :122-127).
 struct AdamwConsts {
   double beta1, one_m_beta1, beta2, one_m_beta2, bc1, bc2, lr, eps, decay;

@@ -133,6 +133,14 @@ cudaError_t rtn_t(const T* w, int64_t rows, int64_t cols, int64_t group, int bit
 
 }  // namespace
 
+cudaError_t launch_rtn_grid(const double* w, int64_t rows, int64_t cols, int64_t group, int bits,
+                            float* scales, float* zeros, cudaStream_t st) {
+  note_launch();
+  k_rtn_grid<double><<<grid_blocks(rows * (cols / group), 8), 256, 0, st>>>(w, rows, cols, group,
+                                                                            bits, scales, zeros);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quantize_rtn(const void* w, bool f64, int64_t rows, int64_t cols, int64_t group,
                                 int bits, uint32_t* words, uint64_t nwords, float* scales,
                                 float* zeros, cudaStream_t st) {

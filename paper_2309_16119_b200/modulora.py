@@ -287,6 +287,59 @@ class RtnQuantizer:
                                scales[:ng].cpu().numpy(), zeros[:ng].cpu().numpy())
 
 
+class OptqQuantizer:
+    """The reference's calibration-aware plugin OptqQuantizer (quantize.hpp:115-125):
+    H = XᵀX + damping·mean(diag)·I, the upper Cholesky factor of H⁻¹, and the
+    error-feeding column sweep (quantize.cpp:186-255) — all on the device
+    (mlra_quantize_optq), bit-identical to quantize_optq. Returns the
+    reference's host QuantizedMatrix layout (grids as RTN's)."""
+
+    def __init__(self, damping: float = 0.01):
+        self.damping = float(damping)
+
+    def name(self) -> str:
+        return "optq"
+
+    def quantize(self, w, calib, bits: int = 4, group_size: int = 0) -> QuantizedMatrix:
+        t = torch.as_tensor(w)
+        if t.dim() != 2:
+            raise MlraError(2, "quantize: expected a 2-D weight matrix")
+        if calib is None:
+            raise MlraError(5, "optq: calibration data required")
+        x = torch.as_tensor(calib)
+        if x.dim() != 2 or (t.numel() and x.shape[1] != t.shape[1]):
+            raise MlraError(2, f"optq: calibration must be [m x {t.shape[1]}], got {tuple(x.shape)}")
+        t = t.double().contiguous().cuda()
+        x = x.double().contiguous().cuda()
+        rows, cols = t.shape
+        g = cols if group_size == 0 else group_size
+        nw = packed_word_count(rows * cols, bits) if rows and cols else 0
+        words = torch.empty(max(nw, 1), dtype=torch.int32, device="cuda")
+        ng = rows * (cols // g) if g and cols % g == 0 else 0
+        scales = torch.empty(max(ng, 1), dtype=torch.float32, device="cuda")
+        zeros = torch.empty(max(ng, 1), dtype=torch.float32, device="cuda")
+        check(lib().mlra_quantize_optq(t.data_ptr(), x.data_ptr(), rows, cols, x.shape[0], bits,
+                                       group_size, self.damping, words.data_ptr(),
+                                       scales.data_ptr(), zeros.data_ptr(), _stream_ptr(None)))
+        wh = words[:nw].cpu().numpy().view(np.uint32).copy()
+        return QuantizedMatrix(rows, cols, bits, g, PackedCodes(bits, rows * cols, wh),
+                               scales[:ng].cpu().numpy(), zeros[:ng].cpu().numpy())
+
+
+def optq_workspace(calib, damping: float = 0.01):
+    """build_optq_workspace (quantize.cpp:186-211) on the device: (hessian,
+    inv_chol_upper) as f64 device tensors, bit-identical to the reference."""
+    x = torch.as_tensor(calib).double().contiguous().cuda()
+    if x.dim() != 2:
+        raise MlraError(2, "optq: calibration must be 2-D")
+    m, n = x.shape
+    h = torch.empty(max(n, 1), max(n, 1), dtype=torch.float64, device="cuda")
+    u = torch.empty_like(h)
+    check(lib().mlra_optq_workspace(x.data_ptr(), m, n, float(damping), h.data_ptr(), u.data_ptr(),
+                                    _stream_ptr(None)))
+    return h, u
+
+
 def default_cb2_codebook() -> np.ndarray:
     """The cb2 plugin's default 256 x 8 magnitude codebook: the 256 shortest
     vectors of {1/2, 3/2, 5/2, 7/2}^8 (a shifted-lattice shell, as in QuIP#'s

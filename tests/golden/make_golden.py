@@ -256,9 +256,54 @@ def model_cases():
     return dict(xs=xs, labels=labels, loss=np.array([loss]), grads=grads)
 
 
+OPTQ_CASES = [  # rows, cols, m, bits, group, damping
+    (6, 16, 24, 4, 8, 0.01), (33, 64, 100, 3, 32, 0.01), (64, 160, 300, 2, 0, 0.05),
+    (40, 256, 512, 4, 128, 0.01), (16, 96, 64, 3, 32, 0.01), (10, 48, 200, 8, 16, 0.0),
+    (7, 9, 12, 3, 3, 0.01)]
+
+
+def optq_inputs(ci: int):
+    """Seeded inputs of OPTQ case ci (regenerated by the tests; the fixture
+    stores their digest, not the arrays)."""
+    rows, cols, m, _, _, _ = OPTQ_CASES[ci]
+    rng = np.random.default_rng(4242 + ci)
+    w = rng.normal(0.0, 0.02, (rows, cols))
+    x = rng.normal(0.0, 1.0, (m, cols))
+    x[1:] = 0.6 * x[:-1] + 0.8 * x[1:]  # correlated calibration rows
+    return w, x
+
+
+def input_digest(*arrays) -> int:
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a, np.float64).tobytes())
+    return int.from_bytes(h.digest()[:8], "little")
+
+
+def optq_cases():
+    """quantize_optq / build_optq_workspace (quantize.cpp:186-255) by the reference."""
+    out = {}
+    for ci, (rows, cols, m, bits, group, damp) in enumerate(OPTQ_CASES):
+        w, x = optq_inputs(ci)
+        out[f"c{ci}_digest"] = np.array([input_digest(w, x)], np.uint64)
+        words, scales, zeros = Ref.quantize_optq(w, x, bits, group, damp)
+        if cols <= 100:  # the workspace itself, for the small cases (fixture size)
+            h, u = Ref.optq_workspace(x, damp)
+            out.update({f"c{ci}_h": h, f"c{ci}_u": u})
+        out.update({f"c{ci}_words": words, f"c{ci}_scales": scales,
+                    f"c{ci}_zeros": zeros,
+                    f"c{ci}_meta": np.array([rows, cols, m, bits, group], np.int64),
+                    f"c{ci}_damping": np.array([damp])})
+    return out
+
+
 def main():
     if not Ref.available():
         raise SystemExit("oracle/_ref/libmlra_ref.so missing: run `make -C oracle` with /root/reference present")
+    if sys.argv[1:] == ["optq"]:
+        np.savez_compressed(os.path.join(HERE, "optq.npz"), **optq_cases())
+        return
     if sys.argv[1:] == ["model"]:
         np.savez_compressed(os.path.join(HERE, "parity_model.npz"), **model_cases())
         return
@@ -272,6 +317,7 @@ def main():
                         mix_seed_11_ada9=np.array([meta["mix_seed_11_ada9"]], np.uint64))
     checkpoint_cases()
     np.savez_compressed(os.path.join(HERE, "parity_model.npz"), **model_cases())
+    np.savez_compressed(os.path.join(HERE, "optq.npz"), **optq_cases())
     for f in sorted(os.listdir(HERE)):
         if f.endswith((".npz", ".mlra", ".json")):
             print(f, os.path.getsize(os.path.join(HERE, f)))
