@@ -14,9 +14,11 @@
 //  * k_chol_step: cholesky_lower (linalg.cpp:13-34) right-looking — step k
 //    finalizes column k and applies its term to every trailing entry, which is
 //    exactly the reference's k-ascending subtraction order per entry;
-//  * k_spd_solve: spd_inverse's per-column forward / back solves (linalg.cpp:
-//    36-58), one thread per column (the back solve's k-ascending order forbids
-//    a right-looking schedule), then k_symmetrize (:59-66);
+//  * k_fwd_solve / k_back_solve: spd_inverse's per-column solves (linalg.cpp:
+//    36-58), one thread per column (forward: 32 chains per thread through the
+//    far terms; back: a serial chain per column — its k-ascending order
+//    forbids a right-looking schedule — with operands loaded a batch ahead),
+//    then k_symmetrize (:59-66);
 //  * the column sweep (quantize.cpp:231-252) is row-parallel: for each row the
 //    residual entry r(i,k) receives e_j·U(j,k) for j ascending. k_sweep keeps
 //    that order per entry but defers the far-column terms: a CTA owns 32 rows,
@@ -24,6 +26,9 @@
 //    block as an in-order tiled product (E·U, compute-bound), then sweeps the
 //    block column by column.
 #include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -75,16 +80,17 @@ __global__ void k_damp(double* __restrict__ h, int64_t n, double damping) {
 }
 
 // Step k of the right-looking Cholesky on S (lower part, in place): column k of
-// S is final (every term j < k applied). L(:, k) = S(:, k) / sqrt(S(k, k));
+// S is final (every term j < k applied). L(:, k) = S(:, k) / sqrt(S(k, k)),
+// stored transposed (lt row k = L column k, i.e. lt = Lᵀ, upper);
 // S(i, j) -= L(i, k)·L(j, k) for k < j <= i. bad: first pivot with S(k,k) <= 0.
-__global__ void __launch_bounds__(256) k_chol_step(double* __restrict__ s, double* __restrict__ l,
+__global__ void __launch_bounds__(256) k_chol_step(double* __restrict__ s, double* __restrict__ lt,
                                                    int64_t n, int64_t k, int* __restrict__ bad) {
   const double d = s[k * n + k];
   const double lkk = sqrt(d);
   const int64_t t = n - k - 1;  // trailing extent
   if (blockIdx.y == 0 && blockIdx.x == 0) {  // finalize column k (block (0,0) also updates below)
     for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x)
-      l[i * n + k] = i == k ? lkk : __ddiv_rn(s[i * n + k], lkk);
+      lt[k * n + i] = i == k ? lkk : __ddiv_rn(s[i * n + k], lkk);
     if (threadIdx.x == 0 && !(d > 0.0)) atomicMin(bad, static_cast<int>(k));
   }
   // 32 x 32 tiles of the trailing lower triangle, 4 entries per thread
@@ -104,25 +110,98 @@ __global__ void __launch_bounds__(256) k_chol_step(double* __restrict__ s, doubl
   }
 }
 
-// spd_inverse per column `col` (one thread each): L y = e_col, then Lᵀ x = y,
-// both with the reference's k-ascending chains. y / x live column-interleaved
-// (entry i of column col at [i * n + col]) so a warp's accesses coalesce.
-__global__ void k_spd_solve(const double* __restrict__ l, int64_t n, double* __restrict__ y,
-                            double* __restrict__ inv) {
+// spd_inverse per column `col` (one thread each; y / x column-interleaved:
+// entry i of column col at [i * n + col], so a warp's accesses coalesce).
+// Forward solve L y = e_col: y[i] = (δ - Σ_{k<i} L(i,k)·y[k]) / L(i,i), k
+// ascending. The far terms (k below the current 32-row block) come first in
+// every chain, so a thread carries the 32 chains of a block at once (ILP 32)
+// through the far terms, staged 32 x 32 from Lᵀ in shared memory, then
+// finishes the block's triangle in order.
+constexpr int FB = 32;
+__global__ void __launch_bounds__(64) k_fwd_solve(const double* __restrict__ lt, int64_t n,
+                                                  double* __restrict__ y) {
+  __shared__ double sl[FB][FB + 1];  // sl[kk][q] = L(i0 + q, k0 + kk)
+  const int64_t col = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (int64_t i0 = 0; i0 < n; i0 += FB) {
+    double sv[FB];
+#pragma unroll
+    for (int q = 0; q < FB; ++q) sv[q] = (i0 + q == col) ? 1.0 : 0.0;
+    for (int64_t k0 = 0; k0 < i0; k0 += FB) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < FB * FB; t += blockDim.x) {
+        const int kk = t / FB, q = t % FB;
+        sl[kk][q] = i0 + q < n ? lt[(k0 + kk) * n + i0 + q] : 0.0;
+      }
+      __syncthreads();
+      if (col < n) {
+#pragma unroll 4
+        for (int kk = 0; kk < FB; ++kk) {
+          const double yk = y[(k0 + kk) * n + col];
+#pragma unroll
+          for (int q = 0; q < FB; ++q) sv[q] = msub(sv[q], sl[kk][q], yk);
+        }
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < FB * FB; t += blockDim.x) {  // the block's own triangle
+      const int kk = t / FB, q = t % FB;
+      sl[kk][q] = (i0 + q < n && i0 + kk < n) ? lt[(i0 + kk) * n + i0 + q] : 0.0;
+    }
+    __syncthreads();
+    if (col < n) {
+#pragma unroll
+      for (int q = 0; q < FB; ++q) {
+        if (i0 + q >= n) break;
+        double v = sv[q];
+        for (int kk = 0; kk < q; ++kk) v = msub(v, sl[kk][q], y[(i0 + kk) * n + col]);
+        y[(i0 + q) * n + col] = __ddiv_rn(v, sl[q][q]);
+      }
+    }
+  }
+}
+
+// Back solve Lᵀ x = y: x[ii] = (y[ii] - Σ_{k>ii} L(k,ii)·x[k]) / L(ii,ii), k
+// ascending — a serial chain per column (chain ii starts with x[ii+1]). The
+// operands stream in order (row ii of Lᵀ, the column's own x), so they are
+// loaded a batch ahead of the dependent subtractions.
+constexpr int BB = 8;
+__global__ void __launch_bounds__(64) k_back_solve(const double* __restrict__ lt, int64_t n,
+                                                   const double* __restrict__ y,
+                                                   double* __restrict__ x) {
   const int64_t col = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (col >= n) return;
-  for (int64_t i = 0; i < n; ++i) {
-    double s = i == col ? 1.0 : 0.0;
-    const double* li = l + i * n;
-#pragma unroll 4
-    for (int64_t k = 0; k < i; ++k) s = msub(s, __ldg(li + k), y[k * n + col]);
-    y[i * n + col] = __ddiv_rn(s, __ldg(li + i));
-  }
   for (int64_t ii = n; ii-- > 0;) {
+    const double* lr = lt + ii * n;
     double s = y[ii * n + col];
-#pragma unroll 4
-    for (int64_t k = ii + 1; k < n; ++k) s = msub(s, __ldg(l + k * n + ii), inv[k * n + col]);
-    inv[ii * n + col] = __ddiv_rn(s, __ldg(l + ii * n + ii));
+    int64_t k = ii + 1;
+    double la[BB], xa[BB];
+    if (k + BB <= n) {
+#pragma unroll
+      for (int b = 0; b < BB; ++b) {
+        la[b] = __ldg(lr + k + b);
+        xa[b] = x[(k + b) * n + col];
+      }
+      for (; k + 2 * BB <= n; k += BB) {
+        double lb[BB], xb[BB];
+#pragma unroll
+        for (int b = 0; b < BB; ++b) {  // next batch in flight
+          lb[b] = __ldg(lr + k + BB + b);
+          xb[b] = x[(k + BB + b) * n + col];
+        }
+#pragma unroll
+        for (int b = 0; b < BB; ++b) s = msub(s, la[b], xa[b]);
+#pragma unroll
+        for (int b = 0; b < BB; ++b) {
+          la[b] = lb[b];
+          xa[b] = xb[b];
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < BB; ++b) s = msub(s, la[b], xa[b]);
+      k += BB;
+    }
+    for (; k < n; ++k) s = msub(s, __ldg(lr + k), x[k * n + col]);
+    x[ii * n + col] = __ddiv_rn(s, __ldg(lr + ii));
   }
 }
 
@@ -135,15 +214,6 @@ __global__ void k_symmetrize(double* __restrict__ a, int64_t n) {
       a[i * n + j] = v;
       a[j * n + i] = v;
     }
-  }
-}
-
-// U = Lᵀ (upper), the strictly-lower part zero (transpose of a lower L).
-__global__ void k_transpose_lower(const double* __restrict__ l, int64_t n, double* __restrict__ u) {
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n * n;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = t / n, j = t % n;
-    u[t] = j >= i ? l[j * n + i] : 0.0;
   }
 }
 
@@ -255,7 +325,7 @@ int blocks_for(int64_t work, int per_block) {
   return static_cast<int>(b < 1 ? 1 : b);
 }
 
-// cholesky_lower of a (n x n, consumed as scratch) into l; bad = first failing pivot or n
+// cholesky_lower of a (n x n, consumed as scratch) into lt = Lᵀ; bad = first failing pivot
 cudaError_t cholesky(double* a, double* l, int64_t n, int* bad, cudaStream_t st) {
   for (int64_t k = 0; k < n; ++k) {
     const int64_t t = n - k - 1;
@@ -268,32 +338,68 @@ cudaError_t cholesky(double* a, double* l, int64_t n, int* bad, cudaStream_t st)
 
 }  // namespace
 
+// dev-only phase timer (MLRA_OPTQ_PROFILE=1): CUDA events on the stream, printed to stderr
+struct PhaseTimer {
+  bool on = getenv("MLRA_OPTQ_PROFILE") != nullptr;
+  cudaStream_t st;
+  cudaEvent_t ev[8];
+  const char* name[8];
+  int n = 0;
+  explicit PhaseTimer(cudaStream_t s) : st(s) {}
+  void mark(const char* nm) {
+    if (!on || n == 8) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], st);
+    name[n++] = nm;
+  }
+  ~PhaseTimer() {
+    if (!on || n < 2) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int i = 1; i < n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, "optq %-12s %9.3f ms\n", name[i], ms);
+    }
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+  }
+};
+
 cudaError_t launch_optq_workspace(const double* calib, int64_t m, int64_t n, double damping,
                                   double* hessian, double* upper, double* scratch, int* bad,
                                   cudaStream_t st) {
   // scratch: 2 n^2 doubles
   double* a = scratch;
   double* b = scratch + n * n;
+  PhaseTimer pt(st);
+  pt.mark("start");
   const unsigned nt = static_cast<unsigned>((n + HT - 1) / HT);
   note_launch();
   k_hessian<<<dim3(nt, nt), 256, 0, st>>>(calib, m, n, hessian);
   note_launch();
   k_damp<<<1, 32, 0, st>>>(hessian, n, damping);
+  pt.mark("hessian");
   cudaError_t e = cudaMemcpyAsync(a, hessian, n * n * sizeof(double), cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(b, 0, n * n * sizeof(double), st)) != cudaSuccess) return e;
-  if ((e = cholesky(a, b, n, bad, st)) != cudaSuccess) return e;  // b = L
-  // inverse through the column solves: y scratch in `a`, result in `upper` (temp)
+  if ((e = cholesky(a, b, n, bad, st)) != cudaSuccess) return e;  // b = Lᵀ
+  pt.mark("cholesky1");
+  // inverse through the column solves: y in `a`, x (the inverse) in `upper`
+  const unsigned sb = static_cast<unsigned>((n + 63) / 64);
   note_launch();
-  k_spd_solve<<<static_cast<unsigned>((n + 63) / 64), 64, 0, st>>>(b, n, a, upper);
+  k_fwd_solve<<<sb, 64, 0, st>>>(b, n, a);
+  pt.mark("fwd_solve");
+  note_launch();
+  k_back_solve<<<sb, 64, 0, st>>>(b, n, a, upper);
+  pt.mark("back_solve");
   note_launch();
   k_symmetrize<<<blocks_for(n * n, 256), 256, 0, st>>>(upper, n);
-  // second factorization (of the inverse; its pivots cannot fail once the first succeeded
-  // in exact arithmetic — a failure is still reported through `bad` as n + pivot)
+  // second factorization (of the inverse; reported through bad[1]); its Lᵀ is U
   if ((e = cudaMemsetAsync(b, 0, n * n * sizeof(double), st)) != cudaSuccess) return e;
   if ((e = cholesky(upper, b, n, bad + 1, st)) != cudaSuccess) return e;
-  note_launch();
-  k_transpose_lower<<<blocks_for(n * n, 256), 256, 0, st>>>(b, n, upper);
+  pt.mark("cholesky2");
+  e = cudaMemcpyAsync(upper, b, n * n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  pt.mark("copy");
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
