@@ -205,6 +205,73 @@ __global__ void __launch_bounds__(64) k_back_solve(const double* __restrict__ lt
   }
 }
 
+// The same back solve with the operand streams staged in shared memory: one
+// warp per 32 columns; for each chain ii the rows x[k][col0..col0+31] (256 B)
+// and Lᵀ[ii][k] of k in (ii, n) arrive in 64-row chunks by cp.async, double
+// buffered, so the dependent subtractions read shared memory while the next
+// chunk is in flight.
+constexpr int XCH = 64;
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(
+                   __cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(32) k_back_solve_sm(const double* __restrict__ lt, int64_t n,
+                                                      const double* __restrict__ y,
+                                                      double* __restrict__ x) {
+  __shared__ __align__(16) double sx[2][XCH][32];
+  __shared__ __align__(16) double sl[2][XCH];
+  const int lane = threadIdx.x;
+  const int64_t col0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int64_t col = col0 + lane;
+  const bool full = col0 + 32 <= n;  // whole 256-B rows (else per-lane scalar path)
+  for (int64_t ii = n; ii-- > 0;) {
+    const double* lr = lt + ii * n;
+    double s = col < n ? y[ii * n + col] : 0.0;
+    const int64_t k0 = ii + 1;
+    auto stage = [&](int buf, int64_t kb) {  // rows [kb, kb + XCH) ∩ [k0, n)
+      const int rows = n - kb < XCH ? static_cast<int>(n - kb) : XCH;
+      if (full) {
+        for (int t = lane; t < rows * 16; t += 32) {  // 16 x 16 B per row
+          const int r = t >> 4, c = t & 15;
+          cp16(&sx[buf][r][2 * c], x + (kb + r) * n + col0 + 2 * c);
+        }
+      } else if (col < n) {
+        for (int r = 0; r < rows; ++r) sx[buf][r][lane] = x[(kb + r) * n + col];
+      }
+      for (int r = lane; r < rows; r += 32) sl[buf][r] = __ldg(lr + kb + r);
+      cp_commit();
+    };
+    if (k0 < n) stage(0, k0);
+    int buf = 0;
+    for (int64_t kb = k0; kb < n; kb += XCH) {
+      const bool more = kb + XCH < n;
+      if (more) stage(buf ^ 1, kb + XCH);
+      if (more) cp_wait<1>(); else cp_wait<0>();
+      __syncwarp();
+      const int rows = n - kb < XCH ? static_cast<int>(n - kb) : XCH;
+      if (rows == XCH) {
+#pragma unroll 16
+        for (int r = 0; r < XCH; ++r) s = msub(s, sl[buf][r], sx[buf][r][lane]);
+      } else {
+        for (int r = 0; r < rows; ++r) s = msub(s, sl[buf][r], sx[buf][r][lane]);
+      }
+      __syncwarp();
+      buf ^= 1;
+    }
+    if (col < n) x[ii * n + col] = __ddiv_rn(s, __ldg(lr + ii));
+    __threadfence_block();
+    __syncwarp();
+  }
+}
+
 __global__ void k_symmetrize(double* __restrict__ a, int64_t n) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n * n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -389,7 +456,10 @@ cudaError_t launch_optq_workspace(const double* calib, int64_t m, int64_t n, dou
   k_fwd_solve<<<sb, 64, 0, st>>>(b, n, a);
   pt.mark("fwd_solve");
   note_launch();
-  k_back_solve<<<sb, 64, 0, st>>>(b, n, a, upper);
+  if (getenv("MLRA_OPTQ_BACK_LDG"))
+    k_back_solve<<<sb, 64, 0, st>>>(b, n, a, upper);
+  else
+    k_back_solve_sm<<<static_cast<unsigned>((n + 31) / 32), 32, 0, st>>>(b, n, a, upper);
   pt.mark("back_solve");
   note_launch();
   k_symmetrize<<<blocks_for(n * n, 256), 256, 0, st>>>(upper, n);
