@@ -1133,7 +1133,8 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   // K5b / K6 go to the side stream when a dX GEMM follows (overlap), else inline
   SideStream* side = nullptr;
   cudaStream_t cs = s;
-  if (dx) {
+  static const bool no_side = getenv("MLRA_NO_SIDE") != nullptr;  // dev A/B switch
+  if (dx && !no_side) {
     if (mlra_status st = side_stream(&side)) return st;
     cs = side->st;
     CUDA_TRY(cudaEventRecord(side->fork, s));
@@ -1162,8 +1163,10 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   // K3: dx = dy·Ŵ + (s·dyA)·Bᵀ   (lp_backward + matmul-bwd dx, lora.cpp:68)
   const mlra_status gst = run_gemm(L->q, L->strategy, L->hook, gp, sc);
   // join: the caller's stream (and the scratch frees queued on it) waits for dA/dB
-  CUDA_TRY(cudaEventRecord(side->join, cs));
-  CUDA_TRY(cudaStreamWaitEvent(s, side->join, 0));
+  if (side) {
+    CUDA_TRY(cudaEventRecord(side->join, cs));
+    CUDA_TRY(cudaStreamWaitEvent(s, side->join, 0));
+  }
   return gst;
 }
 
