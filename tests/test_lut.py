@@ -214,3 +214,21 @@ def test_lut_layer_forward_backward():
     da, db = M.grads_of_adapter(layer)
     assert rel_fro(f64(y), yr) < 4e-3 and rel_fro(f64(dx), dxr) < 4e-3
     assert rel_fro(f64(da), dar) < 1e-4 and rel_fro(f64(db), dbr) < 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [0, 1, 17, 257])
+def test_lut_fused_ragged_token_counts(m):
+    # tiny / ragged token counts take the pair kernel too (the table decode lives there)
+    d_out, d_in = 512, 768
+    qz = M.LutQuantizer()
+    dq = qz.upload(qz.quantize(orc.gaussian(81, d_out, d_in, 0.0, 0.02), None, 4, 64))
+    x = to_bf16_dev(orc.bf16_round(orc.gaussian(82, max(m, 1), d_in)))[:m]
+    g = to_bf16_dev(orc.bf16_round(orc.gaussian(83, max(m, 1), d_out)))[:m]
+    row = M.LpLinearContext(dq, S.RowMaterialize)
+    wct = M.LpLinearContext(dq, S.WeightMaterialize)
+    y = M.lp_forward(row, x, torch.float32)
+    dx = M.lp_backward(row, g, torch.float32)
+    assert y.shape == (m, d_out) and dx.shape == (m, d_in)
+    assert torch.equal(y, M.lp_forward(wct, x, torch.float32))
+    assert torch.equal(dx, M.lp_backward(wct, g, torch.float32))
