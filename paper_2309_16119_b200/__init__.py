@@ -4,6 +4,8 @@ tcgen05 GEMM kernels for sm_100a behind the reference's hot-path API.
 The compute lives in libmlra.so (include/mlra.h); this package is the host-side
 mirror of the reference interface (see modulora.py)."""
 from ._lib import MlraError, build, lib  # noqa: F401
+from .ledger import (  # noqa: F401
+    LayerDims, LedgerEvent, LedgerReport, MemoryLedger, Phase, ledger_assert_single_materialization)
 from .modulora import (  # noqa: F401
     Cb2Matrix, Codebook2Quantizer, DeviceQuantizedMatrix, DoublingQuantizer, LoraAdapter,
     LpLinearContext, LutMatrix, LutQuantizer, MaterializationStrategy, NF4_LEVELS, OptqQuantizer, ModuLoraLayer, ModuLoraLinearFunction, PackedCodes,

@@ -535,6 +535,7 @@ class LpLinearContext:
     strategy: MaterializationStrategy = MaterializationStrategy.RowMaterialize
     layer_name: str = ""
     matvec_hook: Optional[QuantizerHook] = None  # consulted under QuantizerMatvec only
+    ledger: Optional["MemoryLedger"] = None      # optional (lowprec_linear.hpp:89)
 
     def ledger_bytes(self) -> int:
         """Bytes this strategy materializes per pass (MemoryLedger semantics)."""
@@ -562,14 +563,39 @@ def _check_act(t: torch.Tensor, cols: int, what: str) -> None:
         raise MlraError(2, f"{what}: input cols {t.shape[1]} != {cols}")
 
 
+class _Charge:
+    """MaterializedBuffer (lowprec_linear.cpp:17-37): charges one pass's device
+    materialization to an optional ledger for the duration of the call (the
+    library frees its workspace, stream-ordered, before returning)."""
+
+    def __init__(self, ledger, layer: str, phase: int, nbytes: int):
+        self.ledger, self.layer, self.phase, self.nbytes = ledger, layer, phase, nbytes
+
+    def __enter__(self):
+        if self.ledger is not None and self.nbytes:
+            self.ledger.on_alloc(self.layer, self.phase, self.nbytes)
+        return self
+
+    def __exit__(self, *exc):
+        if self.ledger is not None and self.nbytes:
+            self.ledger.on_free(self.layer, self.phase, self.nbytes)
+        return False
+
+
+def _charge(ctx: "LpLinearContext", phase: int) -> _Charge:
+    led = ctx.ledger
+    return _Charge(led, ctx.layer_name, phase, ctx.ledger_bytes() if led is not None else 0)
+
+
 def lp_forward(ctx: LpLinearContext, x: torch.Tensor, out_dtype=torch.bfloat16) -> torch.Tensor:
     """lp_forward (lowprec_linear.cpp:150-196): x [m x d_in] -> [m x d_out]."""
     q = _need_q(ctx)
     _check_act(x, q.cols, "lp_forward")
     y = torch.empty(x.shape[0], q.rows, dtype=out_dtype, device=x.device)
-    check(lib().mlra_lp_forward_ex(q.handle, int(ctx.strategy), _hook_ptr(ctx.matvec_hook),
-                                   x.data_ptr(), x.stride(0), x.shape[0], y.data_ptr(),
-                                   _dtype_code(out_dtype), q.rows, _stream_ptr(None)))
+    with _charge(ctx, 0):
+        check(lib().mlra_lp_forward_ex(q.handle, int(ctx.strategy), _hook_ptr(ctx.matvec_hook),
+                                       x.data_ptr(), x.stride(0), x.shape[0], y.data_ptr(),
+                                       _dtype_code(out_dtype), q.rows, _stream_ptr(None)))
     return y
 
 
@@ -578,10 +604,11 @@ def lp_backward(ctx: LpLinearContext, grad_out: torch.Tensor, out_dtype=torch.bf
     q = _need_q(ctx)
     _check_act(grad_out, q.rows, "lp_backward")
     dx = torch.empty(grad_out.shape[0], q.cols, dtype=out_dtype, device=grad_out.device)
-    check(lib().mlra_lp_backward_ex(q.handle, int(ctx.strategy), _hook_ptr(ctx.matvec_hook),
-                                    grad_out.data_ptr(), grad_out.stride(0), grad_out.shape[0],
-                                    dx.data_ptr(), _dtype_code(out_dtype), q.cols,
-                                    _stream_ptr(None)))
+    with _charge(ctx, 1):
+        check(lib().mlra_lp_backward_ex(q.handle, int(ctx.strategy), _hook_ptr(ctx.matvec_hook),
+                                        grad_out.data_ptr(), grad_out.stride(0), grad_out.shape[0],
+                                        dx.data_ptr(), _dtype_code(out_dtype), q.cols,
+                                        _stream_ptr(None)))
     return dx
 
 
@@ -673,23 +700,30 @@ def make_layer(name: str, weights: DeviceQuantizedMatrix, rank: int, alpha: floa
                          bias_trainable=bias_trainable, strategy=MaterializationStrategy(strategy))
 
 
-def layer_forward(layer: ModuLoraLayer, x: torch.Tensor, out_dtype=torch.bfloat16):
+def _layer_ctx(layer: ModuLoraLayer, ledger) -> "LpLinearContext":
+    return LpLinearContext(layer.weights, layer.strategy, layer.name, layer.matvec_hook, ledger)
+
+
+def layer_forward(layer: ModuLoraLayer, x: torch.Tensor, out_dtype=torch.bfloat16, ledger=None):
     """layer_forward (lora.cpp:52-72). Returns (y, xb); xb = x·B is what the
-    backward pass needs besides x (the tape's saved value)."""
+    backward pass needs besides x (the tape's saved value). ``ledger``: an
+    optional MemoryLedger charged with the pass's device materialization."""
     _check_act(x, layer.d_in(), f"layer '{layer.name}'")
     m = x.shape[0]
     y = torch.empty(m, layer.d_out(), dtype=out_dtype, device=x.device)
     xb = torch.empty(m, layer.adapter.rank, dtype=torch.float32, device=x.device)
     L = layer._c()
-    check(lib().mlra_lora_forward(C.byref(L), x.data_ptr(), x.stride(0), m, y.data_ptr(),
-                                  _dtype_code(out_dtype), layer.d_out(), xb.data_ptr(),
-                                  _stream_ptr(None)))
+    with _charge(_layer_ctx(layer, ledger), 0):
+        check(lib().mlra_lora_forward(C.byref(L), x.data_ptr(), x.stride(0), m, y.data_ptr(),
+                                      _dtype_code(out_dtype), layer.d_out(), xb.data_ptr(),
+                                      _stream_ptr(None)))
     return y, xb
 
 
 def layer_backward(layer: ModuLoraLayer, x: torch.Tensor, xb: torch.Tensor, dy: torch.Tensor,
                    need_dx: bool = True, dx_dtype=torch.bfloat16,
-                   da: Optional[torch.Tensor] = None, db: Optional[torch.Tensor] = None):
+                   da: Optional[torch.Tensor] = None, db: Optional[torch.Tensor] = None,
+                   ledger=None):
     """Tape replay of layer_forward's records (autodiff.cpp:101-193) for the
     upstream gradient dy. Stores dA/dB (and dbias when trainable) on the layer
     (grads_of_adapter) and returns dx (None when need_dx is False). da/db may
@@ -709,10 +743,11 @@ def layer_backward(layer: ModuLoraLayer, x: torch.Tensor, xb: torch.Tensor, dy: 
     dbias = torch.empty(layer.d_out(), dtype=torch.float32, device=x.device) if layer.bias_trainable else None
     dx = torch.empty(m, layer.d_in(), dtype=dx_dtype, device=x.device) if need_dx else None
     L = layer._c()
-    check(lib().mlra_lora_backward(C.byref(L), x.data_ptr(), x.stride(0), xb.data_ptr(),
-                                   dy.data_ptr(), dy.stride(0), m, _ptr(dx),
-                                   _dtype_code(dx_dtype), layer.d_in(), da.data_ptr(),
-                                   db.data_ptr(), _ptr(dbias), _stream_ptr(None)))
+    with _charge(_layer_ctx(layer, ledger if need_dx else None), 1):
+        check(lib().mlra_lora_backward(C.byref(L), x.data_ptr(), x.stride(0), xb.data_ptr(),
+                                       dy.data_ptr(), dy.stride(0), m, _ptr(dx),
+                                       _dtype_code(dx_dtype), layer.d_in(), da.data_ptr(),
+                                       db.data_ptr(), _ptr(dbias), _stream_ptr(None)))
     layer.adapter.grad_a, layer.adapter.grad_b = da, db
     layer.grad_bias = dbias
     layer._grads_ready = True
