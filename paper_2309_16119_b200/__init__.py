@@ -8,7 +8,8 @@ from .ledger import (  # noqa: F401
     LayerDims, LedgerEvent, LedgerReport, MemoryLedger, Phase, ledger_assert_single_materialization)
 from .modulora import (  # noqa: F401
     Cb2Matrix, Codebook2Quantizer, DeviceQuantizedMatrix, DoublingQuantizer, LoraAdapter,
-    LpLinearContext, LutMatrix, LutQuantizer, MaterializationStrategy, NF4_LEVELS, OptqQuantizer, ModuLoraLayer, ModuLoraLinearFunction, PackedCodes,
+    LpLinearContext, LpLinearFunction, LutMatrix, LutQuantizer, MaterializationStrategy, NF4_LEVELS, OptqQuantizer, ModuLoraLayer, ModuLoraLinearFunction, PackedCodes,
     QuantizedMatrix, QuantizerHook, RtnQuantizer, default_cb2_codebook, dequantize,
     dequantize_row, dequantize_tile, grads_of_adapter, init_adapter, layer_backward, layer_forward,
-    lp_backward, lp_forward, make_layer, normal_float_levels, optq_workspace, pack_codes, packed_word_count, parse_strategy, strategy_name)
+    lp_backward, lp_forward, make_layer, normal_float_levels, optq_workspace, pack_codes, quantized_matvec,
+    quantized_matvec_transposed, unpack_codes, packed_word_count, parse_strategy, strategy_name)

@@ -761,6 +761,48 @@ def grads_of_adapter(layer: ModuLoraLayer):
     return layer.adapter.grad_a, layer.adapter.grad_b
 
 
+def quantized_matvec(q: DeviceQuantizedMatrix, v: torch.Tensor) -> torch.Tensor:
+    """quantized_matvec (quantize.cpp:268-283): Ŵ·v for one vector (as bf16
+    operands into the fused kernel, fp32 result)."""
+    v = v.reshape(1, -1).to(torch.bfloat16).contiguous()
+    return lp_forward(LpLinearContext(q, MaterializationStrategy.QuantizerMatvec), v, torch.float32)[0]
+
+
+def quantized_matvec_transposed(q: DeviceQuantizedMatrix, v: torch.Tensor) -> torch.Tensor:
+    """quantized_matvec_transposed (quantize.cpp:285-300): Ŵᵀ·v."""
+    v = v.reshape(1, -1).to(torch.bfloat16).contiguous()
+    return lp_backward(LpLinearContext(q, MaterializationStrategy.QuantizerMatvec), v, torch.float32)[0]
+
+
+def unpack_codes(words: np.ndarray, count: int, bits: int) -> np.ndarray:
+    """unpack (bitpack.cpp:93-104): the reference bitstream back to u32 codes,
+    vectorised on the host (code i at bit i*bits, LSB first)."""
+    w = np.ascontiguousarray(words, np.uint32)
+    if w.size != (count * bits + 31) // 32:
+        raise MlraError(7, f"bitpack: corrupted length metadata: {w.size} words for {count} codes")
+    if count == 0:
+        return np.zeros(0, np.uint32)
+    bitv = np.unpackbits(w.view(np.uint8), bitorder="little")[:count * bits]
+    return (bitv.reshape(count, bits).astype(np.uint32) << np.arange(bits, dtype=np.uint32)).sum(
+        1, dtype=np.uint32)
+
+
+class LpLinearFunction(torch.autograd.Function):
+    """LpLinearFunction (lowprec_linear.hpp:96-112): the frozen quantized linear
+    alone on the tape — forward y = x·Ŵᵀ, backward dX = dY·Ŵ (re-dequantized in
+    the fused kernel, never cached); no gradient for the quantized weights."""
+
+    @staticmethod
+    def forward(ctx, x, lp_ctx: "LpLinearContext"):
+        ctx.lp = lp_ctx
+        return lp_forward(lp_ctx, x.to(torch.bfloat16).contiguous(), torch.float32)
+
+    @staticmethod
+    def backward(ctx, dy):
+        dx = lp_backward(ctx.lp, dy.to(torch.bfloat16).contiguous(), torch.float32)
+        return dx, None
+
+
 class ModuLoraLinearFunction(torch.autograd.Function):
     """The reference's CustomFunction plug-in point (autodiff.hpp:77-89) as a
     torch.autograd.Function: forward saves only x and xb (never Ŵ); backward

@@ -132,3 +132,28 @@ def test_lp_forward_backward_charge_the_ledger():
     ev = led.events()
     assert len(ev) == 4 and ev[0].phase == Phase.Forward and ev[0].alloc
     assert ev[2].phase == Phase.Backward and ev[2].alloc
+
+
+@pytest.mark.gpu
+def test_quantized_matvec_and_lp_linear_function():
+    # quantize.cpp:268-300 (one vector) and the LpLinearFunction tape node
+    # (lowprec_linear.cpp:249-266) against the f64 oracle on the same bf16 operands
+    from oracle import oracle as orc
+    from tests.gpu_util import random_quantized
+    q, words, scales, zeros = random_quantized(300, 520, 3, 40, 55)
+    dq = M.DeviceQuantizedMatrix(q)
+    w = orc.bf16_round(orc.dequantize(words, 300, 520, 3, 40, scales, zeros))
+    v = orc.bf16_round(orc.gaussian(56, 1, 520))[0]
+    u = orc.bf16_round(orc.gaussian(57, 1, 300))[0]
+    y = M.quantized_matvec(dq, torch.from_numpy(v).cuda()).double().cpu().numpy()
+    yt = M.quantized_matvec_transposed(dq, torch.from_numpy(u).cuda()).double().cpu().numpy()
+    assert np.linalg.norm(y - w @ v) <= 1e-5 * np.linalg.norm(w @ v)
+    assert np.linalg.norm(yt - w.T @ u) <= 1e-5 * np.linalg.norm(w.T @ u)
+    x = torch.from_numpy(orc.bf16_round(orc.gaussian(58, 7, 520))).float().cuda().requires_grad_(True)
+    out = M.LpLinearFunction.apply(x, M.LpLinearContext(dq, S.RowMaterialize, "lp"))
+    g = torch.from_numpy(orc.bf16_round(orc.gaussian(59, 7, 300))).float().cuda()
+    out.backward(g)
+    xr = x.detach().double().cpu().numpy()
+    assert np.linalg.norm(out.detach().double().cpu().numpy() - xr @ w.T) <= 1e-5 * np.linalg.norm(xr @ w.T)
+    gd = g.double().cpu().numpy()
+    assert np.linalg.norm(x.grad.double().cpu().numpy() - gd @ w) <= 1e-5 * np.linalg.norm(gd @ w)

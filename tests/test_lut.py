@@ -232,3 +232,13 @@ def test_lut_fused_ragged_token_counts(m):
     assert y.shape == (m, d_out) and dx.shape == (m, d_in)
     assert torch.equal(y, M.lp_forward(wct, x, torch.float32))
     assert torch.equal(dx, M.lp_backward(wct, g, torch.float32))
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 8])
+def test_unpack_codes_inverts_pack(bits):
+    c = np.random.default_rng(bits).integers(0, 1 << bits, 1001).astype(np.uint32)
+    w = M.pack_codes(c, bits)
+    assert np.array_equal(M.unpack_codes(w, c.size, bits), c)
+    assert np.array_equal(M.unpack_codes(w, c.size, bits), orc.unpack(w, c.size, bits))
+    with pytest.raises(MlraError):
+        M.unpack_codes(w[:-1], c.size, bits)
