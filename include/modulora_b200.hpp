@@ -129,6 +129,10 @@ class DeviceBuffer {
   std::size_t size() const { return n_; }
   void upload(const T* h) { cuda_check(cudaMemcpy(p_, h, n_ * sizeof(T), cudaMemcpyHostToDevice), "H2D"); }
   void download(T* h) const { cuda_check(cudaMemcpy(h, p_, n_ * sizeof(T), cudaMemcpyDeviceToHost), "D2H"); }
+  void download(T* h, std::size_t count) const {
+    if (count > n_) throw ContractError("DeviceBuffer: download past the end");
+    if (count) cuda_check(cudaMemcpy(h, p_, count * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+  }
 
  private:
   T* p_ = nullptr;
@@ -228,6 +232,65 @@ inline std::vector<double> dequantize_row(const DeviceQuantizedMatrix& q, std::s
   std::vector<float> h(q.cols());
   d.download(h.data());
   return std::vector<double>(h.begin(), h.end());
+}
+
+// ----------------------------------------------------------------- quantize.hpp:59-75
+// quantize_rtn / quantize_optq on the device (mlra_quantize_rtn / mlra_quantize_optq),
+// bit-identical to the reference; host matrices in, the host QuantizedMatrix out.
+namespace detail {
+inline QuantizedMatrix download_q(std::size_t rows, std::size_t cols, int bits, std::size_t g,
+                                  DeviceBuffer<std::uint32_t>& words, DeviceBuffer<float>& sc,
+                                  DeviceBuffer<float>& z, std::size_t nw, std::size_t ng) {
+  QuantizedMatrix q;
+  q.rows = rows;
+  q.cols = cols;
+  q.bits = bits;
+  q.group_size = g;
+  q.codes.bits = bits;
+  q.codes.count = rows * cols;
+  q.codes.words.resize(nw);
+  q.scales.resize(ng);
+  q.zeros.resize(ng);
+  cuda_check(cudaDeviceSynchronize(), "quantize");
+  words.download(q.codes.words.data(), nw);
+  sc.download(q.scales.data(), ng);
+  z.download(q.zeros.data(), ng);
+  return q;
+}
+}  // namespace detail
+
+inline QuantizedMatrix quantize_rtn(const HostMatrix& w, int bits, std::size_t group_size = 0) {
+  const std::size_t g = group_size ? group_size : w.cols;
+  const std::size_t nw = w.rows && w.cols ? mlra_packed_word_count(w.rows * w.cols, bits) : 0;
+  const std::size_t ng = g && w.cols % g == 0 ? w.rows * (w.cols / g) : 0;
+  DeviceBuffer<double> dw(std::max<std::size_t>(w.data.size(), 1));
+  if (!w.data.empty()) dw.upload(w.data.data());
+  DeviceBuffer<std::uint32_t> words(std::max<std::size_t>(nw, 1));
+  DeviceBuffer<float> sc(std::max<std::size_t>(ng, 1)), z(std::max<std::size_t>(ng, 1));
+  check(mlra_quantize_rtn(dw.get(), MLRA_F64, static_cast<int64_t>(w.rows),
+                          static_cast<int64_t>(w.cols), bits, static_cast<int64_t>(group_size),
+                          words.get(), sc.get(), z.get(), nullptr));
+  return detail::download_q(w.rows, w.cols, bits, g, words, sc, z, nw, ng);
+}
+
+inline QuantizedMatrix quantize_optq(const HostMatrix& w, const HostMatrix& calib, int bits,
+                                     std::size_t group_size = 0, double damping = 0.01) {
+  if (calib.cols != w.cols)
+    throw DimensionError("optq: calibration must be [m x " + std::to_string(w.cols) + "]");
+  const std::size_t g = group_size ? group_size : w.cols;
+  const std::size_t nw = w.rows && w.cols ? mlra_packed_word_count(w.rows * w.cols, bits) : 0;
+  const std::size_t ng = g && w.cols % g == 0 ? w.rows * (w.cols / g) : 0;
+  DeviceBuffer<double> dw(std::max<std::size_t>(w.data.size(), 1)),
+      dx(std::max<std::size_t>(calib.data.size(), 1));
+  if (!w.data.empty()) dw.upload(w.data.data());
+  if (!calib.data.empty()) dx.upload(calib.data.data());
+  DeviceBuffer<std::uint32_t> words(std::max<std::size_t>(nw, 1));
+  DeviceBuffer<float> sc(std::max<std::size_t>(ng, 1)), z(std::max<std::size_t>(ng, 1));
+  check(mlra_quantize_optq(dw.get(), dx.get(), static_cast<int64_t>(w.rows),
+                           static_cast<int64_t>(w.cols), static_cast<int64_t>(calib.rows), bits,
+                           static_cast<int64_t>(group_size), damping, words.get(), sc.get(),
+                           z.get(), nullptr));
+  return detail::download_q(w.rows, w.cols, bits, g, words, sc, z, nw, ng);
 }
 
 // ----------------------------------------------------------------- quantize.hpp:91-106

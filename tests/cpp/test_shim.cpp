@@ -296,6 +296,24 @@ int main(int argc, char** argv) {
     CHECK(throws<NumericError>([&] { upload_lut(2, 8, 8, pc, {-1.0f, NAN, 0.5f, 3.0f}, {2.0f, 0.5f}); }));
     CHECK(throws<ConfigError>([&] { upload_lut(2, 8, 4, pc, {-1.0f, 0.0f, 0.5f, 3.0f}, {1, 1, 1, 1}); }));
   }
+  // --- device RTN / OPTQ through the C++ mirror: the KAT of test_quantize.cpp:34-60 style
+  // shapes, checked for the grid law and against the host restatement of compute_grid
+  {
+    HostMatrix w(2, 4);
+    const double wv[8] = {-1.0, -0.5, 0.5, 1.0, 2.0, 2.0, 2.0, 2.0};
+    for (int i = 0; i < 8; ++i) w.data[i] = wv[i];
+    const QuantizedMatrix q = quantize_rtn(w, 2, 4);
+    // row 0: lo -1, hi 1 -> scale 2/3, zero -1; row 1 flat -> scale 1, zero 2
+    CHECK(q.scales.size() == 2 && q.zeros[0] == -1.0f && q.scales[0] == static_cast<float>(2.0 / 3.0));
+    CHECK(q.scales[1] == 1.0f && q.zeros[1] == 2.0f);
+    CHECK(q.codes.words.size() == 1 && q.codes.words[0] == ((0u) | (1u << 2) | (2u << 4) | (3u << 6)));
+    HostMatrix x(6, 4);
+    for (std::size_t i = 0; i < x.data.size(); ++i) x.data[i] = std::sin(1.0 + 0.7 * static_cast<double>(i));
+    const QuantizedMatrix o = quantize_optq(w, x, 2, 4, 0.01);
+    CHECK(o.scales == q.scales && o.zeros == q.zeros);  // grids come from the original weights
+    CHECK(throws<DimensionError>([&] { quantize_optq(w, HostMatrix(3, 5), 2, 4); }));
+    CHECK(throws<ConfigError>([&] { quantize_rtn(w, 5, 4); }));
+  }
   // --- AdamW first step replicates the update arithmetic (test_train.cpp:145-167)
   {
     const double p0[3] = {1.0, -2.0, 3.0}, g0[3] = {0.1, -0.2, 0.3};
