@@ -40,6 +40,8 @@ __device__ __forceinline__ double msub(double s, double a, double b) {
   return __dsub_rn(s, __dmul_rn(a, b));
 }
 
+constexpr int CP = 32;  // panel width of the blocked factor / solve kernels
+
 // H[n x n] = Xᵀ X, X [m x n] row-major: H(i,j) = ((0 + x0i·x0j) + x1i·x1j) + ...
 constexpr int HT = 32;
 __global__ void __launch_bounds__(256) k_hessian(const double* __restrict__ x, int64_t m, int64_t n,
@@ -160,6 +162,70 @@ __global__ void __launch_bounds__(64) k_fwd_solve(const double* __restrict__ lt,
   }
 }
 
+// Blocked forward solves for all columns at once (Y = L⁻¹ column by column,
+// Y[i][col] at [i * n + col]): the chain of y[i][col] is δ − Σ_{k<i} L(i,k)·y[k][col]
+// with k ascending, then / L(i,i). Row panels of 32: the earlier panels'
+// terms arrive through the trailing updates (k ascending per panel and
+// inside it), the panel's own terms in k_fwd_panel. Entries with col > i stay
+// exactly +0 (every term multiplies a +0 y), so those tiles are skipped.
+__global__ void k_identity(double* __restrict__ y, int64_t n) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n * n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[t] = (t / n == t % n) ? 1.0 : 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_fwd_panel(const double* __restrict__ lt, int64_t n,
+                                                   int64_t p0, double* __restrict__ y) {
+  __shared__ double dl[CP][CP + 1];  // dl[i][k] = L(p0 + i, p0 + k)
+  const int pw = n - p0 < CP ? static_cast<int>(n - p0) : CP;
+  for (int t = threadIdx.x; t < CP * CP; t += blockDim.x) {
+    const int i = t / CP, k = t % CP;
+    dl[i][k] = (i < pw && k <= i) ? lt[(p0 + k) * n + p0 + i] : 0.0;
+  }
+  __syncthreads();
+  const int64_t col = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (col >= n || col >= p0 + pw) return;  // col beyond the panel: its rows here stay +0
+  double yv[CP];
+#pragma unroll
+  for (int i = 0; i < CP; ++i) {
+    if (i < pw) {
+      double v = y[(p0 + i) * n + col];
+#pragma unroll
+      for (int k = 0; k < CP; ++k)
+        if (k < i) v = msub(v, dl[i][k], yv[k]);
+      yv[i] = __ddiv_rn(v, dl[i][i]);
+      y[(p0 + i) * n + col] = yv[i];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fwd_trail(const double* __restrict__ lt, int64_t n,
+                                                   int64_t p0, double* __restrict__ y) {
+  __shared__ double li[CP][CP + 1], yp[CP][CP + 1];  // li[k][row], yp[k][col]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t r0 = p0 + CP + static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  if (c0 > r0 + 31) return;  // every column past every row of the tile: exact zeros
+  for (int k = ty; k < CP; k += 8) {
+    li[k][tx] = r0 + tx < n ? lt[(p0 + k) * n + r0 + tx] : 0.0;
+    yp[k][tx] = c0 + tx < n ? y[(p0 + k) * n + c0 + tx] : 0.0;
+  }
+  __syncthreads();
+  const int64_t col = c0 + tx;
+  if (col >= n) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty * 4 + q;
+    const int64_t i = r0 + r;
+    if (i < n) {
+      double v = y[i * n + col];
+#pragma unroll
+      for (int k = 0; k < CP; ++k) v = msub(v, li[k][r], yp[k][tx]);
+      y[i * n + col] = v;
+    }
+  }
+}
+
 // Back solve Lᵀ x = y: x[ii] = (y[ii] - Σ_{k>ii} L(k,ii)·x[k]) / L(ii,ii), k
 // ascending — a serial chain per column (chain ii starts with x[ii+1]). The
 // operands stream in order (row ii of Lᵀ, the column's own x), so they are
@@ -223,11 +289,13 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+constexpr int XNB = 4;  // chunk buffers: up to XNB - 1 chunks in flight ahead of the chain
 __global__ void __launch_bounds__(32) k_back_solve_sm(const double* __restrict__ lt, int64_t n,
                                                       const double* __restrict__ y,
                                                       double* __restrict__ x) {
-  __shared__ __align__(16) double sx[2][XCH][32];
-  __shared__ __align__(16) double sl[2][XCH];
+  extern __shared__ __align__(16) double bsm[];
+  double (*sx)[XCH][32] = reinterpret_cast<double (*)[XCH][32]>(bsm);
+  double (*sl)[XCH] = reinterpret_cast<double (*)[XCH]>(bsm + XNB * XCH * 32);
   const int lane = threadIdx.x;
   const int64_t col0 = static_cast<int64_t>(blockIdx.x) * 32;
   const int64_t col = col0 + lane;
@@ -236,41 +304,49 @@ __global__ void __launch_bounds__(32) k_back_solve_sm(const double* __restrict__
     const double* lr = lt + ii * n;
     double s = col < n ? y[ii * n + col] : 0.0;
     const int64_t k0 = ii + 1;
-    auto stage = [&](int buf, int64_t kb) {  // rows [kb, kb + XCH) ∩ [k0, n)
+    const int nch = static_cast<int>((n - k0 + XCH - 1) / XCH);
+    auto stage = [&](int c) {  // chunk c: rows [k0 + c·XCH, +XCH) ∩ [k0, n), buffer c % XNB
+      const int buf = c % XNB;
+      const int64_t kb = k0 + static_cast<int64_t>(c) * XCH;
       const int rows = n - kb < XCH ? static_cast<int>(n - kb) : XCH;
       if (full) {
         for (int t = lane; t < rows * 16; t += 32) {  // 16 x 16 B per row
-          const int r = t >> 4, c = t & 15;
-          cp16(&sx[buf][r][2 * c], x + (kb + r) * n + col0 + 2 * c);
+          const int r = t >> 4, cc = t & 15;
+          cp16(&sx[buf][r][2 * cc], x + (kb + r) * n + col0 + 2 * cc);
         }
       } else if (col < n) {
         for (int r = 0; r < rows; ++r) sx[buf][r][lane] = x[(kb + r) * n + col];
       }
       for (int r = lane; r < rows; r += 32) sl[buf][r] = __ldg(lr + kb + r);
-      cp_commit();
     };
-    if (k0 < n) stage(0, k0);
-    int buf = 0;
-    for (int64_t kb = k0; kb < n; kb += XCH) {
-      const bool more = kb + XCH < n;
-      if (more) stage(buf ^ 1, kb + XCH);
-      if (more) cp_wait<1>(); else cp_wait<0>();
+    for (int c = 0; c < XNB - 1; ++c) {  // prologue: one commit group per slot
+      if (c < nch) stage(c);
+      cp_commit();
+    }
+    for (int c = 0; c < nch; ++c) {
+      if (c + XNB - 1 < nch) stage(c + XNB - 1);
+      cp_commit();
+      cp_wait<XNB - 1>();  // chunk c has landed
       __syncwarp();
+      const int buf = c % XNB;
+      const int64_t kb = k0 + static_cast<int64_t>(c) * XCH;
       const int rows = n - kb < XCH ? static_cast<int>(n - kb) : XCH;
+      const double* slb = sl[buf];
       if (rows == XCH) {
 #pragma unroll 16
-        for (int r = 0; r < XCH; ++r) s = msub(s, sl[buf][r], sx[buf][r][lane]);
+        for (int r = 0; r < XCH; ++r) s = msub(s, slb[r], sx[buf][r][lane]);
       } else {
-        for (int r = 0; r < rows; ++r) s = msub(s, sl[buf][r], sx[buf][r][lane]);
+        for (int r = 0; r < rows; ++r) s = msub(s, slb[r], sx[buf][r][lane]);
       }
       __syncwarp();
-      buf ^= 1;
     }
+    cp_wait<0>();
     if (col < n) x[ii * n + col] = __ddiv_rn(s, __ldg(lr + ii));
     __threadfence_block();
     __syncwarp();
   }
 }
+constexpr int kBackSmem = XNB * XCH * 32 * 8 + XNB * XCH * 8;
 
 __global__ void k_symmetrize(double* __restrict__ a, int64_t n) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n * n;
@@ -392,13 +468,111 @@ int blocks_for(int64_t work, int per_block) {
   return static_cast<int>(b < 1 ? 1 : b);
 }
 
+// Blocked right-looking Cholesky, 32-column panels. The order of every chain
+// is the reference's: entry (i, j) receives its terms k ascending — the terms
+// of earlier panels from the trailing updates (in panel order, k ascending
+// inside each), then the panel's own terms k in [p0, j) inside k_chol_panel.
+// Panel p0: every CTA factors the 32 x 32 diagonal block into shared memory
+// (column by column, as cholesky_lower does), then one thread per panel row
+// i >= p0 + 32 finishes its 32 entries L(i, p0..p0+31) from registers.
+__global__ void __launch_bounds__(256) k_chol_panel(const double* __restrict__ s,
+                                                    double* __restrict__ lt, int64_t n, int64_t p0,
+                                                    int* __restrict__ bad) {
+  __shared__ double d[CP][CP + 1];  // d[i][j]: S then L of the diagonal block
+  const int pw = n - p0 < CP ? static_cast<int>(n - p0) : CP;
+  for (int t = threadIdx.x; t < CP * CP; t += blockDim.x) {
+    const int i = t / CP, j = t % CP;
+    d[i][j] = (i < pw && j <= i) ? s[(p0 + i) * n + p0 + j] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < pw; ++j) {
+    if (threadIdx.x == 0) {
+      double v = d[j][j];
+      for (int k = 0; k < j; ++k) v = msub(v, d[j][k], d[j][k]);
+      if (!(v > 0.0) && blockIdx.x == 0) atomicMin(bad, static_cast<int>(p0 + j));
+      d[j][j] = sqrt(v);
+    }
+    __syncthreads();
+    const int i = j + 1 + static_cast<int>(threadIdx.x);
+    if (i < pw) {
+      double v = d[i][j];
+      for (int k = 0; k < j; ++k) v = msub(v, d[i][k], d[j][k]);
+      d[i][j] = __ddiv_rn(v, d[j][j]);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0)  // the diagonal block's columns of Lᵀ
+    for (int t = threadIdx.x; t < CP * CP; t += blockDim.x) {
+      const int i = t / CP, j = t % CP;
+      if (i < pw && j <= i) lt[(p0 + j) * n + p0 + i] = d[i][j];
+    }
+  const int64_t i = p0 + pw + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double lr[CP];
+#pragma unroll
+  for (int j = 0; j < CP; ++j) {
+    if (j < pw) {
+      double v = s[i * n + p0 + j];
+#pragma unroll
+      for (int k = 0; k < CP; ++k)
+        if (k < j) v = msub(v, lr[k], d[j][k]);
+      lr[j] = __ddiv_rn(v, d[j][j]);
+      lt[(p0 + j) * n + i] = lr[j];
+    }
+  }
+}
+
+// Trailing update after panel p0: S(i, j) -= L(i, k)·L(j, k), k = p0 .. p0+31
+// ascending, for p0 + 32 <= j <= i. 32 x 32 tiles of the lower triangle.
+__global__ void __launch_bounds__(256) k_chol_trail(double* __restrict__ s,
+                                                    const double* __restrict__ lt, int64_t n,
+                                                    int64_t p0) {
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  if (bj > bi) return;
+  __shared__ double li[CP][CP + 1], lj[CP][CP + 1];  // [k][row]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t q0 = p0 + CP, i0 = q0 + bi * 32, j0 = q0 + bj * 32;
+  for (int k = ty; k < CP; k += 8) {
+    li[k][tx] = i0 + tx < n ? lt[(p0 + k) * n + i0 + tx] : 0.0;
+    lj[k][tx] = j0 + tx < n ? lt[(p0 + k) * n + j0 + tx] : 0.0;
+  }
+  __syncthreads();
+  const int64_t j = j0 + tx;
+  if (j >= n) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty * 4 + q;
+    const int64_t i = i0 + r;
+    if (i < n && i >= j) {
+      double v = s[i * n + j];
+#pragma unroll
+      for (int k = 0; k < CP; ++k) v = msub(v, li[k][r], lj[k][tx]);
+      s[i * n + j] = v;
+    }
+  }
+}
+
 // cholesky_lower of a (n x n, consumed as scratch) into lt = Lᵀ; bad = first failing pivot
 cudaError_t cholesky(double* a, double* l, int64_t n, int* bad, cudaStream_t st) {
-  for (int64_t k = 0; k < n; ++k) {
-    const int64_t t = n - k - 1;
-    const unsigned nb = static_cast<unsigned>(t > 0 ? (t + 31) / 32 : 1);
+  if (getenv("MLRA_OPTQ_CHOL_STEP")) {  // dev A/B: one launch per column
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t t = n - k - 1;
+      const unsigned nb = static_cast<unsigned>(t > 0 ? (t + 31) / 32 : 1);
+      note_launch();
+      k_chol_step<<<dim3(nb, nb), 256, 0, st>>>(a, l, n, k, bad);
+    }
+    return cudaGetLastError();
+  }
+  for (int64_t p0 = 0; p0 < n; p0 += CP) {
+    const int64_t rest = n - p0 - CP;  // rows below the diagonal block
+    const unsigned pb = static_cast<unsigned>(rest > 0 ? (rest + 255) / 256 : 1);
     note_launch();
-    k_chol_step<<<dim3(nb, nb), 256, 0, st>>>(a, l, n, k, bad);
+    k_chol_panel<<<pb, 256, 0, st>>>(a, l, n, p0, bad);
+    if (rest > 0) {
+      const unsigned tb = static_cast<unsigned>((rest + 31) / 32);
+      note_launch();
+      k_chol_trail<<<dim3(tb, tb), 256, 0, st>>>(a, l, n, p0);
+    }
   }
   return cudaGetLastError();
 }
@@ -452,14 +626,33 @@ cudaError_t launch_optq_workspace(const double* calib, int64_t m, int64_t n, dou
   pt.mark("cholesky1");
   // inverse through the column solves: y in `a`, x (the inverse) in `upper`
   const unsigned sb = static_cast<unsigned>((n + 63) / 64);
-  note_launch();
-  k_fwd_solve<<<sb, 64, 0, st>>>(b, n, a);
+  if (getenv("MLRA_OPTQ_FWD_THREAD")) {  // dev A/B: one thread per column, 32 chains each
+    note_launch();
+    k_fwd_solve<<<sb, 64, 0, st>>>(b, n, a);
+  } else {
+    note_launch();
+    k_identity<<<blocks_for(n * n, 256), 256, 0, st>>>(a, n);
+    for (int64_t p0 = 0; p0 < n; p0 += CP) {
+      note_launch();
+      k_fwd_panel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(b, n, p0, a);
+      const int64_t rest = n - p0 - CP;
+      if (rest > 0) {
+        note_launch();
+        k_fwd_trail<<<dim3(static_cast<unsigned>((n + 31) / 32),
+                           static_cast<unsigned>((rest + 31) / 32)),
+                      256, 0, st>>>(b, n, p0, a);
+      }
+    }
+  }
   pt.mark("fwd_solve");
   note_launch();
   if (getenv("MLRA_OPTQ_BACK_LDG"))
     k_back_solve<<<sb, 64, 0, st>>>(b, n, a, upper);
   else
-    k_back_solve_sm<<<static_cast<unsigned>((n + 31) / 32), 32, 0, st>>>(b, n, a, upper);
+  {
+    cudaFuncSetAttribute(k_back_solve_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, kBackSmem);
+    k_back_solve_sm<<<static_cast<unsigned>((n + 31) / 32), 32, kBackSmem, st>>>(b, n, a, upper);
+  }
   pt.mark("back_solve");
   note_launch();
   k_symmetrize<<<blocks_for(n * n, 256), 256, 0, st>>>(upper, n);
