@@ -119,3 +119,23 @@ def test_optq_errors():
             orc.Ref.quantize_optq(w, xs, 4, 8, 0.0)
     # damping rescues it, as in the reference
     M.OptqQuantizer(0.01).quantize(w, xs, 4, 8)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols,m,bits,group", [(300, 640, 900, 4, 128), (96, 1024, 1500, 3, 64)])
+def test_optq_bit_exact_vs_live_reference_medium(rows, cols, m, bits, group):
+    # beyond the fixtures: the compiled reference (oracle/_ref, travels with the
+    # repo) on medium shapes — several Cholesky panels, many sweep blocks
+    if not orc.Ref.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(rows + cols)
+    w = rng.normal(0.0, 0.02, (rows, cols))
+    x = rng.normal(0.0, 1.0, (m, cols))
+    x[1:] = 0.5 * x[:-1] + 0.85 * x[1:]
+    words, scales, zeros = orc.Ref.quantize_optq(w, x, bits, group, 0.01)
+    q = M.OptqQuantizer(0.01).quantize(w, x, bits, group)
+    assert np.array_equal(q.scales, scales) and np.array_equal(q.zeros, zeros)
+    assert np.array_equal(q.codes.words, words)
+    h, u = orc.Ref.optq_workspace(x, 0.01)
+    hd, ud = M.optq_workspace(x, 0.01)
+    assert np.array_equal(hd.cpu().numpy(), h) and np.array_equal(ud.cpu().numpy(), u)
