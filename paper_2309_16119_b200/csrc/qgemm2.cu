@@ -39,6 +39,7 @@ using namespace qg;
 
 constexpr double kSkMinIdleBlocks = 50.0;  // stream-K only when it recovers more than this
 constexpr int64_t kSkMinBlocksPerPair = 8;
+constexpr double kSkMaxWaves = 1.25;  // stream-K only below this many waves of whole tiles
 constexpr int HB = 128;            // tokens per CTA per accumulator (MMA N=256 split in two)
 constexpr int HB_TILE = HB * BK * 2;  // 16 KB
 constexpr int PAIR_ROWS = 2 * BM;  // 256 weight-side rows per pair tile
@@ -699,11 +700,17 @@ void qgemm2_plan(GemmArgs& p) {
   // Whole tiles leave n_kb * (waves - tiles/slots) k-blocks of every pair's time
   // idle in the last wave; stream-K pays a roughly fixed fix-up cost (owners
   // read their contributors' partials chunk by chunk at the end). Measured
-  // break-even is ~45 k-blocks (m in {512..4096} at LLaMA-7B shapes).
+  // break-even is ~45 k-blocks (m in {512..4096} at LLaMA-7B shapes, all of
+  // them at most one wave of tiles).
   const int64_t waves = (tiles + slots - 1) / slots;
   const double idle_kb = static_cast<double>(n_kb) *
                          (static_cast<double>(waves) - static_cast<double>(tiles) / slots);
   if (mode == 2 && idle_kb < kSkMinIdleBlocks) return;
+  // With more than ~1.25 waves of whole tiles, splitting every tile across
+  // pairs costs more in partial traffic and fix-ups than the last wave's idle
+  // time it recovers (measured: cfg3 5.69 vs 6.18 ms, cfg4 b3 2.37 vs 2.51 ms
+  // per step with whole tiles), so stream-K is kept for the under-filled cases.
+  if (mode == 2 && static_cast<double>(tiles) > kSkMaxWaves * static_cast<double>(slots)) return;
   // every pair needs a few k-blocks of its own, so cuts never collide
   const int64_t total = tiles * n_kb;
   int64_t pairs = slots;
