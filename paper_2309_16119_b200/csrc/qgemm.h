@@ -46,8 +46,6 @@ struct GemmArgs {
   // entry sk_pairs is the end). Precomputed on the host so the device schedule
   // needs no division and stays on the uniform datapath.
   int sk_pairs;
-  int sk_full;           // hybrid: tiles [0, sk_full) whole, strided by the pair count, before
-                         // the cut ranges (which then cover only the tail tiles); 0 = plain
   float* sk_ws;          // [sk_pairs x 2 CTAs x 512 tokens x 128 rows] fp32 partials
   unsigned* sk_flags;    // [sk_pairs x 2], zeroed before the launch
   int sk_tile[129];

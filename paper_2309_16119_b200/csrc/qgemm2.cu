@@ -40,7 +40,6 @@ using namespace qg;
 constexpr double kSkMinIdleBlocks = 50.0;  // stream-K only when it recovers more than this
 constexpr int64_t kSkMinBlocksPerPair = 8;
 constexpr double kSkMaxWaves = 1.25;  // stream-K only below this many waves of whole tiles
-constexpr double kSkFixupBlocks = 56.0;  // fix-up cost in pair k-block units (cost model)
 constexpr int HB = 128;            // tokens per CTA per accumulator (MMA N=256 split in two)
 constexpr int HB_TILE = HB * BK * 2;  // 16 KB
 constexpr int PAIR_ROWS = 2 * BM;  // 256 weight-side rows per pair tile
@@ -61,15 +60,12 @@ static_assert(kSkSlotFloats == 2LL * PAIR_TOK * BM, "stream-K slot = both CTAs' 
 //    its accumulators as a partial and publishes a flag. Owners process their
 //    part last in their range, so the partials they need are normally ready.
 struct SegSched {
-  int t, kb, t_end, kb_end, n_kb, n_tiles, stride, wt, full;
+  int t, kb, t_end, kb_end, n_kb, n_tiles, stride;
   bool sk;
   __device__ void init(const GemmArgs& p, int cid, int ncl, int tiles, int nkb) {
     n_kb = nkb;
     n_tiles = tiles;
     sk = p.sk_pairs != 0;
-    stride = ncl;
-    wt = cid;  // hybrid prefix: whole tiles cid, cid + ncl, ... < full
-    full = sk ? p.sk_full : 0;
     if (sk) {
       // called by full, converged warps: the REDUX broadcast puts the cuts in
       // uniform registers, keeping the MMA issuer's loop (and its smem
@@ -82,16 +78,10 @@ struct SegSched {
           __reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_off[cid + 1])));
     } else {
       t = cid;
+      stride = ncl;
     }
   }
   __device__ bool next(int& tile, int& kb0, int& kb1) {
-    if (wt < full) {
-      tile = wt;
-      kb0 = 0;
-      kb1 = n_kb;
-      wt += stride;
-      return true;
-    }
     if (!sk) {
       if (t >= n_tiles) return false;
       tile = t;
@@ -108,14 +98,11 @@ struct SegSched {
     kb = 0;
     return true;
   }
-  // whole-tile segments of the hybrid prefix still to come
-  __device__ int whole() const { return wt < full ? (full - 1 - wt) / stride + 1 : 0; }
   // number of segments next() will yield
   __device__ int count() const {
     if (!sk) return t < n_tiles ? (n_tiles - 1 - t) / stride + 1 : 0;
-    const int w = whole();
-    if (t > t_end || (t == t_end && kb >= kb_end)) return w;
-    return w + t_end - t + (kb_end > 0 ? 1 : 0);
+    if (t > t_end || (t == t_end && kb >= kb_end)) return 0;
+    return t_end - t + (kb_end > 0 ? 1 : 0);
   }
   // pairs (cid, q_end) whose ranges start inside `tile` (the owner's contributors)
   __device__ static int contrib_end(const GemmArgs& p, int cid, int tile) {
@@ -185,8 +172,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       __reduce_min_sync(0xffffffffu, static_cast<unsigned>(sched.sk ? sched.kb : 0)));
   const int mma_kb_last = static_cast<int>(
       __reduce_min_sync(0xffffffffu, static_cast<unsigned>(sched.sk ? sched.kb_end : 0)));
-  const int mma_nwhole =  // hybrid prefix length: the first cut segment follows it
-      static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(sched.whole())));
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_act);
@@ -306,7 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       };
       for (int sg = 0; sg < mma_nseg; ++sg) {
-        const int kb0 = sg == mma_nwhole ? mma_kb_first : 0;
+        const int kb0 = sg == 0 ? mma_kb_first : 0;
         const int kb1 = (sg == mma_nseg - 1 && mma_kb_last > 0) ? mma_kb_last : n_kb;
         // The epilogue drains accumulator 0 first and releases it early
         // (tempty): the first `pre` k-blocks' accumulator-0 MMAs of this tile
@@ -705,12 +690,11 @@ cudaError_t launch2_mo(const GemmMaps& maps, const QWeightDev& q, const GemmArgs
 
 void qgemm2_plan(GemmArgs& p) {
   p.sk_pairs = 0;
-  p.sk_full = 0;
   const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
   const int64_t n_kb = p.n_kb_main + p.n_kb_lora;
   int64_t slots = sm_total() / 2;
   if (slots > kMaxSkPairs) slots = kMaxSkPairs;
-  int mode = 2;  // MLRA_SK=0: whole tiles; 1: always stream-K; 3: hybrid; default: when waves quantize
+  int mode = 2;  // MLRA_SK=0: whole tiles; 1: always stream-K; default: when waves quantize
   if (const char* e = getenv("MLRA_SK")) mode = atoi(e);
   if (mode == 0 || tiles <= 0) return;
   // Whole tiles leave n_kb * (waves - tiles/slots) k-blocks of every pair's time
@@ -722,26 +706,6 @@ void qgemm2_plan(GemmArgs& p) {
   const double idle_kb = static_cast<double>(n_kb) *
                          (static_cast<double>(waves) - static_cast<double>(tiles) / slots);
   if (mode == 2 && idle_kb < kSkMinIdleBlocks) return;
-  if (mode == 3 && tiles > slots) {
-    // hybrid (MLRA_SK=3 only): the full waves as whole tiles, the cut ranges
-    // over the tail only. Measured not to pay at cfg3 / cfg4 (5.77 vs 5.63 ms,
-    // 2.38 vs 2.38 ms per step against whole tiles), so the default keeps whole
-    // tiles above kSkMaxWaves; kept, tested, for other shapes and for A/B.
-    const int64_t full = tiles / slots * slots, tail = tiles - full;
-    if (tail == 0) return;
-    const int64_t tail_total = tail * n_kb;
-    if (tail_total / slots < kSkMinBlocksPerPair) return;
-    for (int64_t q = 0; q <= slots; ++q) {
-      int64_t b = full * n_kb + tail_total * q / slots;
-      if ((b % n_kb) & 1) ++b;  // even offset: a Q-ring stage holds two k-blocks
-      p.sk_tile[q] = static_cast<int>(b / n_kb);
-      p.sk_off[q] = static_cast<int>(b % n_kb);
-    }
-    p.sk_full = static_cast<int>(full);
-    p.sk_pairs = static_cast<int>(slots);
-    return;
-  }
-  if (mode == 3) return;
   // With more than ~1.25 waves of whole tiles, splitting every tile across
   // pairs costs more in partial traffic and fix-ups than the last wave's idle
   // time it recovers (measured: cfg3 5.69 vs 6.18 ms, cfg4 b3 2.37 vs 2.51 ms
@@ -774,9 +738,7 @@ bool qgemm_prefer_pair(const GemmArgs& p0) {
   const double n_kb = static_cast<double>(p.n_kb_main + p.n_kb_lora);
   const int64_t tiles2 = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
   const int64_t tiles1 = (p.m_total / BM) * ((p.tokens + 255) / 256);
-  const double pair = p.sk_pairs ? static_cast<double>(p.sk_full / p.sk_pairs) * n_kb +
-                                       static_cast<double>(tiles2 - p.sk_full) * n_kb / p.sk_pairs +
-                                       kSkFixupBlocks
+  const double pair = p.sk_pairs ? static_cast<double>(tiles2) * n_kb / p.sk_pairs + 56.0
                                  : static_cast<double>((tiles2 + slots - 1) / slots) * n_kb;
   const double cta1 = static_cast<double>((tiles1 + sms - 1) / sms) * n_kb * 0.75;
   return cta1 >= 0.95 * pair;

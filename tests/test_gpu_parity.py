@@ -375,31 +375,3 @@ def test_fresh_adapter_equals_base_and_zero_base():
     s = 16.0 / r
     ref = orc.bf16_round(s * f64(xb)) @ orc.bf16_round(f64(zl.adapter.a)).T
     assert rel_fro(f64(yz), ref) <= 1e-5
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("rows,cols,m,mn", [
-    (8192, 2048, 2560, False),   # 32 x 5 = 160 tiles: 2 full waves + a 12-tile tail
-    (2048, 4096, 5632, True),    # dX: 8 x 11 = 88 tiles: 1 wave + 14
-    (4096, 1536, 4864, False)])  # 16 x 10 = 160 tiles
-def test_hybrid_stream_k_matches_whole_tiles(rows, cols, m, mn, monkeypatch):
-    """Hybrid stream-K (the full waves as whole tiles strided over the pairs,
-    only the tail wave cut into ranges) computes the same products as whole
-    tiles; only the fp32 order across the cuts of the tail tiles differs."""
-    q, words, sc, z = random_quantized(rows, cols, 3, 128, seed=rows + m + 11 * mn)
-    dq = M.DeviceQuantizedMatrix(q)
-    ctx = M.LpLinearContext(dq, M.MaterializationStrategy.RowMaterialize)
-    a = to_bf16_dev(orc.bf16_round(orc.gaussian(19, m, rows if mn else cols)))
-    f = M.lp_backward if mn else M.lp_forward
-    monkeypatch.setenv("MLRA_GEMM", "2")
-    outs = {}
-    for sk in ("0", "3"):
-        monkeypatch.setenv("MLRA_SK", sk)
-        outs[sk] = f(ctx, a, out_dtype=torch.float32)
-    torch.cuda.synchronize()
-    o0, o3 = f64(outs["0"]), f64(outs["3"])
-    assert rel_fro(o3, o0) <= 1e-5
-    # the whole-tile prefix is bit-identical to the whole-tile schedule: count exact rows
-    assert np.mean(np.all(o3 == o0, axis=1)) > 0.5 if mn else np.mean(np.all(o3 == o0, axis=0)) > 0.5
-    monkeypatch.setenv("MLRA_SK", "3")
-    assert np.array_equal(f64(f(ctx, a, out_dtype=torch.float32)), o3)  # repeatable
