@@ -371,6 +371,18 @@ MLRA_API mlra_status mlra_checkpoint_upload(const mlra_checkpoint* c, int64_t i,
 /* Replace layer i's adapter factors (host f64, rows x rank and cols x rank). */
 MLRA_API mlra_status mlra_checkpoint_set_adapter(mlra_checkpoint* c, int64_t i, const double* a,
                                                  const double* b);
+/* The adapter section in file order (inspect_layout's adapter list,
+ * checkpoint.cpp:294-296): the record's layer name, offset and size. */
+MLRA_API int64_t mlra_checkpoint_adapter_count(const mlra_checkpoint* c);
+MLRA_API mlra_status mlra_checkpoint_adapter(const mlra_checkpoint* c, int64_t i,
+                                             const char** layer_name, uint64_t* offset,
+                                             uint64_t* size);
+/* load_model's assemble_model checks (model.cpp:472-531) -> MLRA_ERR_CONFIG: one
+ * adapter per layer, unique layer names, the parity transformer's layer names
+ * (parity_transformer != 0) or chained dims, adapter i naming layer i, rank >= 1
+ * and alpha > 0, bias length d_out. */
+MLRA_API mlra_status mlra_checkpoint_assemble_check(const mlra_checkpoint* c,
+                                                    int parity_transformer);
 /* save_model's encoding (checkpoint.cpp:93-130, 307-314) to `path`. */
 MLRA_API mlra_status mlra_checkpoint_save(const mlra_checkpoint* c, const char* path);
 

@@ -28,7 +28,8 @@ EXPORTS = [
     "mlra_adamw_step", "mlra_last_format_error", "mlra_checkpoint_load", "mlra_checkpoint_free",
     "mlra_checkpoint_layer_count", "mlra_checkpoint_layer", "mlra_checkpoint_config_json",
     "mlra_checkpoint_frozen_hash", "mlra_checkpoint_file_hash", "mlra_checkpoint_upload",
-    "mlra_checkpoint_set_adapter", "mlra_checkpoint_save", "mlra_quantize_rtn",
+    "mlra_checkpoint_set_adapter", "mlra_checkpoint_save", "mlra_checkpoint_adapter_count",
+    "mlra_checkpoint_adapter", "mlra_checkpoint_assemble_check", "mlra_quantize_rtn",
     "mlra_dp_unique_id", "mlra_dp_init", "mlra_allreduce_lora_grads", "mlra_dp_destroy",
     "mlra_mix_seed", "mlra_gaussian_fill", "mlra_lut_create", "mlra_optq_workspace",
     "mlra_quantize_optq",
@@ -173,6 +174,13 @@ def lib() -> C.CDLL:
         L.mlra_checkpoint_set_adapter.argtypes = [vp, i64, vp, vp]
         L.mlra_checkpoint_save.restype = i32
         L.mlra_checkpoint_save.argtypes = [vp, C.c_char_p]
+        L.mlra_checkpoint_adapter_count.restype = i64
+        L.mlra_checkpoint_adapter_count.argtypes = [vp]
+        L.mlra_checkpoint_adapter.restype = i32
+        L.mlra_checkpoint_adapter.argtypes = [vp, i64, C.POINTER(C.c_char_p), C.POINTER(u64),
+                                              C.POINTER(u64)]
+        L.mlra_checkpoint_assemble_check.restype = i32
+        L.mlra_checkpoint_assemble_check.argtypes = [vp, i32]
         L.mlra_quantize_rtn.restype = i32
         L.mlra_quantize_rtn.argtypes = [vp, i32, i64, i64, i32, i64, vp, vp, vp, vp]
         L.mlra_dp_unique_id.restype = i32

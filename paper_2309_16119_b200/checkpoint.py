@@ -7,7 +7,9 @@
   save_model(model, path) (:93-130, :307-314) Checkpoint.save: byte-identical re-encoding
   inspect_layout(path) (:320-322)             Checkpoint.layout()
   ToyModel::frozen_state_hash (model.cpp:203) Checkpoint.frozen_hash(); fnv1a64 file digest
-  (assemble_model from the config JSON)       not on the hot path: config JSON kept verbatim
+  assemble_model (model.cpp:472-531)          load_model: the same structural checks
+                                              (ConfigError); to_layers() takes strategy and
+                                              bias_trainable from the config JSON
 
 Each layer's packed words go to HBM verbatim (``upload``): at LLaMA shapes the
 reference bitstream already is the device layout.
@@ -102,11 +104,32 @@ class Checkpoint:
         return [self.layer(i) for i in range(len(self))]
 
     def layout(self) -> dict:
-        """inspect_layout (checkpoint.cpp:320-322): record offsets and sizes."""
+        """inspect_layout (checkpoint.cpp:320-322): record offsets and sizes; the
+        adapters in adapter-section (file) order."""
         recs = self.layers()
+        ads = []
+        for i in range(int(lib().mlra_checkpoint_adapter_count(self._h))):
+            name, off, size = C.c_char_p(), C.c_uint64(), C.c_uint64()
+            check(lib().mlra_checkpoint_adapter(self._h, i, C.byref(name), C.byref(off),
+                                                C.byref(size)))
+            ads.append((name.value.decode(), off.value, size.value))
         return {"version": self.version(),
-                "layers": [(r.name, r.offset, r.size) for r in recs],
-                "adapters": [(r.name, r.adapter_offset, r.adapter_size) for r in recs if r.rank]}
+                "layers": [(r.name, r.offset, r.size) for r in recs], "adapters": ads}
+
+    def config(self) -> dict:
+        """The model config JSON (model_config_from_json, model.cpp:123-166)."""
+        import json
+        try:
+            return json.loads(self.config_json())
+        except ValueError as e:
+            raise MlraError(3, f"model config: invalid JSON: {e}") from None
+
+    def assemble_check(self) -> None:
+        """assemble_model's structural checks (model.cpp:472-531) -> ConfigError."""
+        kind = self.config().get("kind", "mlp")
+        if kind not in ("mlp", "parity_transformer"):
+            raise MlraError(3, f"unknown model kind '{kind}' (expected mlp or parity_transformer)")
+        check(lib().mlra_checkpoint_assemble_check(self._h, int(kind == "parity_transformer")))
 
     def frozen_hash(self) -> int:
         return int(lib().mlra_checkpoint_frozen_hash(self._h))
@@ -121,19 +144,27 @@ class Checkpoint:
         check(lib().mlra_checkpoint_upload(self._h, i, _stream_ptr(stream), C.byref(h)))
         return DeviceQuantizedMatrix._wrap(h, rec.rows, rec.cols, rec.bits, rec.group_size)
 
-    def to_layers(self, strategy=MaterializationStrategy.RowMaterialize) -> List[ModuLoraLayer]:
-        """Device ModuLoraLayers: frozen weights uploaded, bias and adapter
-        factors as fp32 device tensors (the f64 values stay available through
-        layer(i).a / .b for an exact AdamW master copy)."""
+    def to_layers(self, strategy=None, bias_trainable=None) -> List[ModuLoraLayer]:
+        """Device ModuLoraLayers as assemble_model builds them (model.cpp:508-531):
+        frozen weights uploaded, bias and adapter factors as fp32 device tensors
+        (the f64 values stay available through layer(i).a / .b for an exact AdamW
+        master copy); strategy and bias_trainable from the config JSON unless
+        given explicitly."""
+        from .modulora import parse_strategy
+        self.assemble_check()
+        cfg = self.config()
+        if strategy is None:
+            strategy = parse_strategy(cfg.get("strategy", "row"))
+        if bias_trainable is None:
+            bias_trainable = bool(cfg.get("bias_trainable", False))
         out = []
         for i in range(len(self)):
             r = self.layer(i)
-            if not r.rank:
-                raise MlraError(5, f"checkpoint: layer '{r.name}' has no adapter")
             ad = LoraAdapter(torch.from_numpy(r.a.astype(np.float32)).cuda(),
                              torch.from_numpy(r.b.astype(np.float32)).cuda(), r.rank, float(r.alpha))
             out.append(ModuLoraLayer(r.name, self.upload(i), ad,
                                      bias=torch.from_numpy(r.bias).cuda(),
+                                     bias_trainable=bool(bias_trainable),
                                      strategy=MaterializationStrategy(strategy)))
         return out
 
@@ -150,8 +181,11 @@ class Checkpoint:
 
 
 def load_model(path: str) -> Checkpoint:
-    """load_model (checkpoint.hpp:43) — parse + validate; see Checkpoint."""
-    return Checkpoint.load(path)
+    """load_model (checkpoint.cpp:324-327): parse + validation (FormatError / IoError),
+    then assemble_model's checks (ConfigError)."""
+    c = Checkpoint.load(path)
+    c.assemble_check()
+    return c
 
 
 def inspect_layout(path: str) -> dict:

@@ -437,43 +437,104 @@ struct Planes {
   __nv_bfloat16* hi[4];
   __nv_bfloat16* lo[4];
   int64_t rc[4];
+  int64_t rows_t[4];
   int64_t ldt = 0;
 };
 
-mlra_status make_planes(Scratch& sc, mlra::PrepBatch& pb, const float* F, int64_t rows, int64_t r,
-                        bool ones, Planes* pl) {
+mlra_status alloc_planes(Scratch& sc, int64_t rows, int64_t r, bool ones, Planes* pl) {
   pl->ldt = round_up(rows, 64);
   pl->n = static_cast<int>((r + 63) / 64);
   for (int c = 0; c < pl->n; ++c) {
     const int64_t j0 = 64 * c, rc = r - j0 < 64 ? r - j0 : 64;
-    const bool o = ones && c == 0;
-    const int64_t rows_t = mlra::thin_rows(rc, o);
+    const int64_t rows_t = mlra::thin_rows(rc, ones && c == 0);
     auto* hi = sc.get<__nv_bfloat16>(static_cast<size_t>(2 * rows_t * pl->ldt));
     if (!hi) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
     pl->hi[c] = hi;
     pl->lo[c] = hi + rows_t * pl->ldt;
     pl->rc[c] = rc;
-    pb.split_t(F + j0, rows, rc, r, o, pl->hi[c], pl->lo[c], rows_t, pl->ldt);
+    pl->rows_t[c] = rows_t;
   }
   return MLRA_OK;
 }
 
-// out[m x r] += act[m x kd] · W   (K4 / K5a; out pre-zeroed; W as planes)
-mlra_status rows_product(Scratch& sc, const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
-                         const Planes& W, float* out, int64_t r) {
-  for (int c = 0; c < W.n; ++c)
-    CUDA_TRY(mlra::launch_rowmma(act, lda, m, kd, W.hi[c], W.lo[c], W.ldt, out + 64 * c, r,
-                                 W.rc[c], sc.st));
+mlra_status make_planes(Scratch& sc, mlra::PrepBatch& pb, const float* F, int64_t rows, int64_t r,
+                        bool ones, Planes* pl) {
+  if (mlra_status st = alloc_planes(sc, rows, r, ones, pl)) return st;
+  for (int c = 0; c < pl->n; ++c)
+    pb.split_t(F + 64 * c, rows, pl->rc[c], r, ones && c == 0, pl->hi[c], pl->lo[c],
+               pl->rows_t[c], pl->ldt);
   return MLRA_OK;
 }
 
-// out[nd x r] += scale · actᵀ · V  (+ colsum[n] += Σ_t act[t, n])  (K5b / K6)
-mlra_status cols_product(cudaStream_t st, const __nv_bfloat16* act, int64_t lda, int64_t m,
-                         int64_t nd, const Planes& V, float scale, float* out, int64_t r,
-                         float* colsum) {
-  for (int c = 0; c < V.n; ++c)
-    CUDA_TRY(mlra::launch_colmma(act, lda, m, nd, V.hi[c], V.lo[c], V.ldt, scale, out + 64 * c, r,
-                                 V.rc[c], c == 0 ? colsum : nullptr, st));
+// Workspace of a skinny product (partial slots + per-tile counters); the
+// counters are zeroed by the pass's prep launch and reset by the finishers, so
+// every chunk launch of the pass (same stream) reuses them.
+struct ThinWs {
+  float* ws = nullptr;
+  int64_t ws_floats = 0;
+  int* cnt = nullptr;
+};
+mlra_status thin_ws(Scratch& sc, mlra::PrepBatch& pb, bool row, int64_t m, int64_t d, int64_t r,
+                    bool ones, ThinWs* w) {
+  int64_t wf = 0, nc = 0;
+  for (int64_t j0 = 0; j0 < r; j0 += 64) {  // the largest chunk's needs
+    int64_t f, c;
+    mlra::thin_ws_size(row, m, d, r - j0 < 64 ? r - j0 : 64, ones && j0 == 0, &f, &c);
+    wf = f > wf ? f : wf;
+    nc = c > nc ? c : nc;
+  }
+  w->ws = sc.get<float>(static_cast<size_t>(wf));
+  w->ws_floats = wf;
+  w->cnt = sc.get<int>(static_cast<size_t>(nc));
+  if (!w->ws || !w->cnt) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
+  pb.zero_f32(reinterpret_cast<float*>(w->cnt), nc);
+  return MLRA_OK;
+}
+
+// out[m x r] = act[m x kd] · W   (K4 / K5a; W as planes). Optionally also the
+// padded bf16(pad_scale · out) operand [m x rp] and the transposed hi/lo planes
+// of out (tp, allocated by alloc_planes over m rows).
+mlra_status rows_product(cudaStream_t st, const ThinWs& w, const __nv_bfloat16* act, int64_t lda,
+                         int64_t m, int64_t kd, const Planes& W, float* out, int64_t r,
+                         __nv_bfloat16* pad, int64_t rp, float pad_scale, const Planes* tp) {
+  for (int c = 0; c < W.n; ++c) {
+    mlra::ThinOut o;
+    o.out = out + 64 * c;
+    o.ldo = r;
+    o.ws = w.ws;
+    o.ws_floats = w.ws_floats;
+    o.cnt = w.cnt;
+    if (pad) {
+      o.pad = pad + 64 * c;
+      o.ldp = rp;
+      o.pad_cols = 64;
+      o.pad_scale = pad_scale;
+    }
+    if (tp) {
+      o.thi = tp->hi[c];
+      o.ldt = tp->ldt;
+      o.t_rows = static_cast<int>(tp->rows_t[c]);
+    }
+    CUDA_TRY(mlra::launch_rowmma(act, lda, m, kd, W.hi[c], W.lo[c], W.ldt, W.rc[c], o, st));
+  }
+  return MLRA_OK;
+}
+
+// out[nd x r] = scale · actᵀ · V  (+ colsum[n] = Σ_t act[t, n])  (K5b / K6)
+mlra_status cols_product(cudaStream_t st, const ThinWs& w, const __nv_bfloat16* act, int64_t lda,
+                         int64_t m, int64_t nd, const Planes& V, float scale, float* out,
+                         int64_t r, float* colsum) {
+  for (int c = 0; c < V.n; ++c) {
+    mlra::ThinOut o;
+    o.out = out + 64 * c;
+    o.ldo = r;
+    o.scale = scale;
+    o.colsum = c == 0 ? colsum : nullptr;
+    o.ws = w.ws;
+    o.ws_floats = w.ws_floats;
+    o.cnt = w.cnt;
+    CUDA_TRY(mlra::launch_colmma(act, lda, m, nd, V.hi[c], V.lo[c], V.ldt, V.rc[c], o, st));
+  }
   return MLRA_OK;
 }
 
@@ -1054,19 +1115,19 @@ mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, in
   auto* xbs = sc.get<__nv_bfloat16>(static_cast<size_t>(m * rp));
   auto* apad = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows_pad * rp));
   if (!xbs || !apad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  // one launch: B -> transposed hi/lo planes, A -> padded bf16 operand, xb = 0
+  // one launch: B -> transposed hi/lo planes, A -> padded bf16 operand, counters = 0
   mlra::PrepBatch pb;
   Planes bt;
+  ThinWs tw;
   if (mlra_status st = make_planes(sc, pb, L->b, d.cols, r, false, &bt)) return st;
   pb.pad(L->a, d.rows, r, r, 1.0f, apad, d.rows_pad, rp);
-  pb.zero_f32(xb, m * r);
+  if (mlra_status st = thin_ws(sc, pb, true, m, d.cols, r, false, &tw)) return st;
   CUDA_TRY(mlra::launch_prep(pb, s));
-  // K4: xb = x·B (matmul(t, x, B), lora.cpp:68)
-  if (mlra_status st = rows_product(sc, gp.act, gp.ld_act, m, d.cols, bt, xb, r)) return st;
-  // bf16(s·xb), zero padded: the extra-K LoRA operand
-  mlra::PrepBatch pb2;
-  pb2.pad(xb, m, r, r, scaling, xbs, m, rp);
-  CUDA_TRY(mlra::launch_prep(pb2, s));
+  // K4: xb = x·B (matmul(t, x, B), lora.cpp:68), finished with bf16(s·xb) zero
+  // padded to rp columns: the extra-K LoRA operand of the GEMM
+  if (mlra_status st = rows_product(s, tw, gp.act, gp.ld_act, m, d.cols, bt, xb, r, xbs, rp,
+                                    scaling, nullptr))
+    return st;
   gp.k_red_valid = d.cols;
   gp.act_lora = xbs;
   gp.w_lora = apad;
@@ -1113,23 +1174,25 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   auto* dyas = sc.get<__nv_bfloat16>(static_cast<size_t>(m * rp));
   auto* bpad = dx ? sc.get<__nv_bfloat16>(static_cast<size_t>(d.cols_pad * rp)) : nullptr;
   if (!dyA || !dyas || (dx && !bpad)) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  // one launch: A, xb -> transposed hi/lo planes, B -> padded operand, zero the outputs
+  // one launch: A, xb -> transposed hi/lo planes, B -> padded operand, counters = 0
+  // (dA, dB, dbias, dyA are stored by the skinny kernels' finishers: no zero-fill)
   mlra::PrepBatch pb;
   Planes at, xbt, dyat;
+  ThinWs w_row, w_da, w_db;
   if (mlra_status st = make_planes(sc, pb, L->a, d.rows, r, false, &at)) return st;
   if (mlra_status st = make_planes(sc, pb, xb, m, r, dbias != nullptr, &xbt)) return st;
+  if (mlra_status st = alloc_planes(sc, m, r, false, &dyat)) return st;
   if (dx) pb.pad(L->b, d.cols, r, r, 1.0f, bpad, d.cols_pad, rp);
-  pb.zero_f32(dyA, m * r);
-  pb.zero_f32(da, d.rows * r);
-  pb.zero_f32(db, d.cols * r);
-  if (dbias) pb.zero_f32(dbias, d.rows);
+  if (mlra_status st = thin_ws(sc, pb, true, m, d.rows, r, false, &w_row)) return st;
+  if (mlra_status st = thin_ws(sc, pb, false, m, d.rows, r, dbias != nullptr, &w_da)) return st;
+  if (mlra_status st = thin_ws(sc, pb, false, m, d.cols, r, false, &w_db)) return st;
   CUDA_TRY(mlra::launch_prep(pb, s));
-  // K5a: dyA = dy·A ; d(xb) = s·dyA (autodiff.cpp:150-152 on record lora.cpp:69)
-  if (mlra_status st = rows_product(sc, dya, lddya, m, d.rows, at, dyA, r)) return st;
-  mlra::PrepBatch pb2;
-  pb2.pad(dyA, m, r, r, scaling, dyas, m, rp);  // extra-K operand of the dX GEMM
-  if (mlra_status st = make_planes(sc, pb2, dyA, m, r, false, &dyat)) return st;
-  CUDA_TRY(mlra::launch_prep(pb2, s));
+  // K5a: dyA = dy·A ; d(xb) = s·dyA (autodiff.cpp:150-152 on record lora.cpp:69),
+  // finished with bf16(s·dyA) (the dX GEMM's extra-K operand) and dyA's
+  // transposed hi/lo planes (the dB product's factor)
+  if (mlra_status st = rows_product(s, w_row, dya, lddya, m, d.rows, at, dyA, r, dyas, rp,
+                                    scaling, &dyat))
+    return st;
   // K5b / K6 go to the side stream when a dX GEMM follows (overlap), else inline
   SideStream* side = nullptr;
   cudaStream_t cs = s;
@@ -1141,10 +1204,10 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
     CUDA_TRY(cudaStreamWaitEvent(cs, side->fork, 0));
   }
   // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
-  if (mlra_status st = cols_product(cs, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias))
+  if (mlra_status st = cols_product(cs, w_da, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias))
     return st;
   // K6: dB = s·xᵀ·dyA   (autodiff.cpp:153-155 on record lora.cpp:68)
-  if (mlra_status st = cols_product(cs, xa, ldxa, m, d.cols, dyat, scaling, db, r, nullptr))
+  if (mlra_status st = cols_product(cs, w_db, xa, ldxa, m, d.cols, dyat, scaling, db, r, nullptr))
     return st;
   if (!dx) return MLRA_OK;  // frozen input: no dX (autodiff.cpp:136)
   GemmPlan gp{};

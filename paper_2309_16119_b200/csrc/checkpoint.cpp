@@ -43,16 +43,18 @@ struct Layer {
   std::vector<uint32_t> words;
   std::vector<float> scales, zeros, bias;
   uint64_t off = 0, size = 0;
-  // adapter (filled from the adapter section)
-  bool has_adapter = false;
+  int64_t adapter = -1;  // index of the first adapter record naming this layer
+};
+
+// One adapter record, in adapter-section (file) order (checkpoint.cpp:271-302);
+// duplicates and out-of-order records survive the parse, as in the reference,
+// and are rejected by assemble_model's checks (mlra_checkpoint_assemble_check).
+struct Adapter {
+  size_t layer;  // owning layer
   uint32_t rank = 0;
   float alpha = 0.0f;
   std::vector<double> a, b;
-  uint64_t a_off = 0, a_size = 0;
-};
-
-struct AdapterRef {
-  size_t layer;  // owning layer (adapters keep their file order, checkpoint.cpp:116-124)
+  uint64_t off = 0, size = 0;
 };
 
 bool supported_bits(int b) { return b == 2 || b == 3 || b == 4 || b == 8; }
@@ -174,7 +176,7 @@ struct mlra_checkpoint {
   uint16_t version = 0;
   std::string config_json;
   std::vector<Layer> layers;
-  std::vector<AdapterRef> adapters;  // adapter section order
+  std::vector<Adapter> adapters;  // adapter section order
 
   void parse(const std::vector<uint8_t>& buf) {
     Reader r{buf};
@@ -272,14 +274,16 @@ struct mlra_checkpoint {
       r.need_array(static_cast<uint64_t>(L.cols) * rank, 8, "adapter B");
       std::vector<double> b(static_cast<size_t>(L.cols) * rank);
       for (double& v : b) v = r.f64("adapter B");
-      L.has_adapter = true;
-      L.rank = rank;
-      L.alpha = alpha;
-      L.a = std::move(a);
-      L.b = std::move(b);
-      L.a_off = rec;
-      L.a_size = r.off - rec;
-      adapters.push_back(AdapterRef{owner});
+      if (L.adapter < 0) L.adapter = static_cast<int64_t>(adapters.size());
+      Adapter ad;
+      ad.layer = owner;
+      ad.rank = rank;
+      ad.alpha = alpha;
+      ad.a = std::move(a);
+      ad.b = std::move(b);
+      ad.off = rec;
+      ad.size = r.off - rec;
+      adapters.push_back(std::move(ad));
     }
     if (r.off != buf.size())
       bad_field(r.off, std::to_string(buf.size() - r.off) + " trailing bytes after adapter section");
@@ -305,13 +309,12 @@ struct mlra_checkpoint {
       for (float v : s.bias) put_f32(b, v);
     }
     put_u32(b, static_cast<uint32_t>(adapters.size()));
-    for (const AdapterRef& ar : adapters) {
-      const Layer& L = layers[ar.layer];
-      put_str(b, L.name);
-      put_u32(b, L.rank);
-      put_f32(b, L.alpha);
-      for (double v : L.a) put_f64(b, v);
-      for (double v : L.b) put_f64(b, v);
+    for (const Adapter& ad : adapters) {
+      put_str(b, layers[ad.layer].name);
+      put_u32(b, ad.rank);
+      put_f32(b, ad.alpha);
+      for (double v : ad.a) put_f64(b, v);
+      for (double v : ad.b) put_f64(b, v);
     }
     return b;
   }
@@ -373,14 +376,15 @@ mlra_status mlra_checkpoint_layer(const mlra_checkpoint* c, int64_t i, mlra_ckpt
   o->scales = L.scales.data();
   o->zeros = L.zeros.data();
   o->bias = L.bias.data();
-  o->rank = L.has_adapter ? L.rank : 0;
-  o->alpha = L.alpha;
-  o->a = L.a.data();
-  o->b = L.b.data();
+  const Adapter* ad = L.adapter >= 0 ? &c->adapters[static_cast<size_t>(L.adapter)] : nullptr;
+  o->rank = ad ? ad->rank : 0;
+  o->alpha = ad ? ad->alpha : 0.0f;
+  o->a = ad ? ad->a.data() : nullptr;
+  o->b = ad ? ad->b.data() : nullptr;
   o->record_offset = L.off;
   o->record_size = L.size;
-  o->adapter_offset = L.a_off;
-  o->adapter_size = L.a_size;
+  o->adapter_offset = ad ? ad->off : 0;
+  o->adapter_size = ad ? ad->size : 0;
   return MLRA_OK;
 }
 
@@ -429,11 +433,63 @@ mlra_status mlra_checkpoint_set_adapter(mlra_checkpoint* c, int64_t i, const dou
                                         const double* b) {
   if (bad_handle(c, i)) return mlra::set_error(MLRA_ERR_RANGE, "checkpoint: layer index out of range");
   Layer& L = c->layers[static_cast<size_t>(i)];
-  if (!L.has_adapter)
+  if (L.adapter < 0)
     return mlra::set_error(MLRA_ERR_CONTRACT, "checkpoint: layer '" + L.name + "' has no adapter");
   if (!a || !b) return mlra::set_error(MLRA_ERR_CONTRACT, "checkpoint: null adapter factors");
-  std::memcpy(L.a.data(), a, L.a.size() * sizeof(double));
-  std::memcpy(L.b.data(), b, L.b.size() * sizeof(double));
+  Adapter& ad = c->adapters[static_cast<size_t>(L.adapter)];
+  std::memcpy(ad.a.data(), a, ad.a.size() * sizeof(double));
+  std::memcpy(ad.b.data(), b, ad.b.size() * sizeof(double));
+  return MLRA_OK;
+}
+
+int64_t mlra_checkpoint_adapter_count(const mlra_checkpoint* c) {
+  return c ? static_cast<int64_t>(c->adapters.size()) : 0;
+}
+
+mlra_status mlra_checkpoint_adapter(const mlra_checkpoint* c, int64_t i, const char** layer_name,
+                                    uint64_t* offset, uint64_t* size) {
+  if (!c || i < 0 || i >= static_cast<int64_t>(c->adapters.size()))
+    return mlra::set_error(MLRA_ERR_RANGE, "checkpoint: adapter index out of range");
+  const Adapter& ad = c->adapters[static_cast<size_t>(i)];
+  if (layer_name) *layer_name = c->layers[ad.layer].name.c_str();
+  if (offset) *offset = ad.off;
+  if (size) *size = ad.size;
+  return MLRA_OK;
+}
+
+// assemble_model's structural checks (model.cpp:472-531), in its order, as ConfigError.
+mlra_status mlra_checkpoint_assemble_check(const mlra_checkpoint* c, int parity_transformer) {
+  if (!c) return mlra::set_error(MLRA_ERR_CONTRACT, "checkpoint: null argument");
+  const auto& L = c->layers;
+  const auto cfg = [](const std::string& m) { return mlra::set_error(MLRA_ERR_CONFIG, m); };
+  if (c->adapters.size() != L.size())
+    return cfg("assemble_model: expected exactly one adapter per layer");
+  for (size_t i = 0; i < L.size(); ++i)
+    for (size_t k = 0; k < i; ++k)
+      if (L[k].name == L[i].name)
+        return cfg("assemble_model: duplicate layer name '" + L[i].name + "'");
+  static const char* kNames[] = {"attn_q", "attn_k", "attn_v", "attn_o", "mlp_in", "mlp_out", "head"};
+  if (parity_transformer) {
+    if (L.size() != 7) return cfg("assemble_model: parity_transformer needs 7 layers");
+    for (size_t i = 0; i < 7; ++i)
+      if (L[i].name != kNames[i])
+        return cfg("assemble_model: layer " + std::to_string(i) + " must be '" + kNames[i] +
+                   "', got '" + L[i].name + "'");
+  } else {
+    for (size_t i = 1; i < L.size(); ++i)
+      if (L[i].cols != L[i - 1].rows)
+        return cfg("assemble_model: chain dimension mismatch at layer '" + L[i].name + "'");
+  }
+  for (size_t i = 0; i < L.size(); ++i) {
+    const Adapter& ad = c->adapters[i];
+    if (ad.layer != i)
+      return cfg("assemble_model: adapter " + std::to_string(i) + " names layer '" +
+                 L[ad.layer].name + "', expected '" + L[i].name + "'");
+    if (ad.rank == 0 || !(ad.alpha > 0.0f))
+      return cfg("assemble_model: adapter for '" + L[i].name + "' has invalid rank or alpha");
+    if (L[i].bias.size() != L[i].rows)
+      return cfg("assemble_model: bias length for '" + L[i].name + "' must equal d_out");
+  }
   return MLRA_OK;
 }
 

@@ -116,14 +116,36 @@ cudaError_t launch_prep(const PrepBatch& b, cudaStream_t st);
 // Skinny rank-r products on tensor cores (thin_mma.cu); r <= 64 per call. Factors are passed
 // transposed and split into bf16 hi/lo planes [thin_rows(r) x ld] (PrepBatch::split_t).
 int thin_rows(int64_t r, bool ones);
-// out[m x r] += act[m x kd] · W      (W given as Wt hi/lo [rows x ldw])
+// Where a skinny product's finished tiles go (thin_mma.cu thin_flush). Outputs are
+// stored, not accumulated: no zero-fill needed.
+struct ThinOut {
+  float* out = nullptr;            // [n_out x ldo] fp32: out[row, j] = scale · v (j < rc)
+  int64_t ldo = 0;
+  float scale = 1.0f;
+  int rc = 0;                      // set by the launcher (= r of this call)
+  float* colsum = nullptr;         // colmma: colsum[row] = v of the ones column (j == rc)
+  __nv_bfloat16* pad = nullptr;    // rowmma: bf16(pad_scale · v) [n_out x ldp], cols [rc, pad_cols) = 0
+  int64_t ldp = 0;
+  int pad_cols = 0;
+  float pad_scale = 1.0f;
+  __nv_bfloat16* thi = nullptr;    // rowmma: transposed hi/lo planes [t_rows x ldt] (lo after hi)
+  int64_t ldt = 0;
+  int t_rows = 0;
+  float* ws = nullptr;             // per-CTA partial slots (thin_ws_size floats)
+  int64_t ws_floats = 0;           // capacity of ws (checked against the launch's grid)
+  int* cnt = nullptr;              // per-tile contributor counters, zero before the first
+                                   // launch; the finisher resets its tile's counter to 0
+};
+// Workspace of one launch: ws floats and counters (ints).
+void thin_ws_size(bool row, int64_t m, int64_t d, int64_t r, bool ones, int64_t* ws_floats,
+                  int64_t* n_cnt);
+// out[m x r] = act[m x kd] · W      (W given as Wt hi/lo [rows x ldw])
 cudaError_t launch_rowmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
                           const __nv_bfloat16* wt_hi, const __nv_bfloat16* wt_lo, int64_t ldw,
-                          float* out, int64_t ldo, int64_t r, cudaStream_t st);
-// out[nd x r] += scale · actᵀ · V    (V given as Vt hi/lo [rows x ldv]); colsum[n] += Σ_t act
+                          int64_t r, const ThinOut& o, cudaStream_t st);
+// out[nd x r] = scale · actᵀ · V    (V given as Vt hi/lo [rows x ldv]); colsum[n] = Σ_t act
 cudaError_t launch_colmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t nd,
                           const __nv_bfloat16* vt_hi, const __nv_bfloat16* vt_lo, int64_t ldv,
-                          float scale, float* out, int64_t ldo, int64_t r, float* colsum,
-                          cudaStream_t st);
+                          int64_t r, const ThinOut& o, cudaStream_t st);
 
 }  // namespace mlra

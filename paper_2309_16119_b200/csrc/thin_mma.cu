@@ -11,8 +11,17 @@
 // These are HBM-bound (r flop/B): each CTA streams 64 x 64 activation chunks
 // through a TMA ring and runs bf16 mma.sync m16n8k16 against the rank-r factor. The fp32 factor is split into bf16 hi + lo parts (two MMAs),
 // so the product keeps ~16 mantissa bits (fp32-grade
-// intermediates); activations are exact bf16. Split-K / split-token CTAs
-// combine with fp32 atomics.
+// intermediates); activations are exact bf16.
+//
+// Deterministic reduction: a CTA leaving an output tile writes its fp32 partial
+// to its own slot; the last contributor of the tile (per-tile counter) sums the
+// contributors' slots in CTA order and stores the result. No atomics touch the
+// outputs, so XB, dYA, dA, dB and dbias are bitwise reproducible run to run, as
+// the reference's fixed-order loops are (matrix.cpp:81-97, test_train.cpp:328-387),
+// and the outputs need no zero-fill. The finisher also writes the derived
+// operands the next kernels consume (bf16(s·XB) / bf16(s·dYA) padded extra-K
+// operands of the GEMM, the transposed hi/lo planes of dYA for dB), so a layer
+// pass needs no conversion launch between the skinny product and the GEMM.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -49,10 +58,11 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], 
 }
 
 // Work decomposition (both kernels): the (output tile x reduction chunk) space
-// is flattened tile-major into U units of 64 x 64 activations and cut into
+// is flattened tile-major into U units of TM x 64 activations and cut into
 // gridDim.x equal contiguous ranges — one resident wave, every CTA streaming
 // the same number of chunks through one continuous pipeline. A CTA flushes its
-// fp32 partials (atomics) whenever its range leaves an output tile.
+// fp32 partials to its slot whenever its range leaves an output tile; the
+// tile's last contributor finishes it (thin_flush).
 //
 // Operand staging is TMA (cp.async.bulk.tensor, SWIZZLE_128B): one elected
 // thread issues the activation chunk and the hi+lo factor chunk per unit into
@@ -92,11 +102,96 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 
+// CTA whose contiguous unit range [u0(c), u0(c+1)) contains unit u, for
+// u0(c) = floor(c·U/G): the largest c with c·U/G < u + 1.
+__device__ __forceinline__ int cta_of_unit(int64_t u, int64_t units, int64_t G) {
+  return static_cast<int>(((u + 1) * G - 1) / units);
+}
+__device__ __forceinline__ int first_tile_of(int c, int64_t units, int64_t G, int chunks) {
+  return static_cast<int>(c * units / G) / chunks;
+}
+
+// Flush of one output tile (all threads of the CTA, uniform): the fragment
+// partials go to this CTA's slot (slot 0 when `tile` is the first tile of its
+// range, else slot 1; layout [ROWS cols][TM rows]); when every contributor has
+// written (counter), the last one sums the slots in CTA order and stores.
+template <int NT>
+__device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
+                           const ThinOut& o, int64_t n_out) {
+  constexpr int ROWS = 8 * NT;
+  __shared__ int s_last;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int which = tile == first_tile_of(c, units, G, chunks) ? 0 : 1;
+  float* slot = o.ws + (static_cast<int64_t>(c) * 2 + which) * (TM * ROWS);
+  const int ra = warp * 16 + g;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int j = n * 8 + 2 * tq;
+    slot[j * TM + ra] = acc[n][0];
+    slot[(j + 1) * TM + ra] = acc[n][1];
+    slot[j * TM + ra + 8] = acc[n][2];
+    slot[(j + 1) * TM + ra + 8] = acc[n][3];
+    acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
+  }
+  const int c_lo = cta_of_unit(static_cast<int64_t>(tile) * chunks, units, G);
+  const int c_hi = cta_of_unit(static_cast<int64_t>(tile + 1) * chunks - 1, units, G);
+  if (c_lo != c_hi) {
+    __threadfence();  // this CTA's partial visible before it is counted
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int old = atomicAdd(o.cnt + tile, 1);
+      s_last = old == c_hi - c_lo;
+      if (s_last) o.cnt[tile] = 0;  // self-resetting for the next launch on this stream
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+  } else {
+    __syncthreads();
+  }
+  // finisher: v(row, j) = Σ_{q = c_lo..c_hi} slot_q(row, j), in CTA order
+  for (int idx = threadIdx.x; idx < TM * ROWS; idx += TTHREADS) {
+    const int j = idx / TM, tr = idx - j * TM;
+    float v = 0.0f;
+    for (int q = c_lo; q <= c_hi; ++q) {
+      const int wq = tile == first_tile_of(q, units, G, chunks) ? 0 : 1;
+      v += __ldcg(o.ws + (static_cast<int64_t>(q) * 2 + wq) * (TM * ROWS) + j * TM + tr);
+    }
+    const int64_t row = static_cast<int64_t>(tile) * TM + tr;
+    if (row < n_out) {
+      if (j < o.rc) {
+        o.out[row * o.ldo + j] = o.scale * v;
+        if (o.pad) o.pad[row * o.ldp + j] = __float2bfloat16_rn(o.pad_scale * v);
+      } else if (j == o.rc && o.colsum) {
+        o.colsum[row] = v;
+      }
+    }
+    if (o.thi && row < o.ldt && j < o.t_rows) {  // transposed hi/lo planes (zero padded)
+      const float tv = (row < n_out && j < o.rc) ? v : 0.0f;
+      const __nv_bfloat16 h = __float2bfloat16_rn(tv);
+      o.thi[static_cast<int64_t>(j) * o.ldt + row] = h;
+      o.thi[static_cast<int64_t>(o.t_rows + j) * o.ldt + row] =
+          __float2bfloat16_rn(tv - __bfloat162float(h));
+    }
+  }
+  if (o.pad) {  // zero the pad columns [rc, pad_cols) of the bf16 operand
+    const int pc = o.pad_cols - o.rc;
+    for (int idx = threadIdx.x; idx < TM * pc; idx += TTHREADS) {
+      const int tr = idx / pc, j = o.rc + idx - tr * pc;
+      const int64_t row = static_cast<int64_t>(tile) * TM + tr;
+      if (row < n_out) o.pad[row * o.ldp + j] = __float2bfloat16_rn(0.0f);
+    }
+  }
+  __syncthreads();  // the slot is rewritten by this CTA's next flush
+}
+
 // out[t, j] (+)= Σ_k act[t, k] · Wt[j, k]   (Wt = W transposed, hi/lo bf16 planes)
 template <int NT>
 __global__ void __launch_bounds__(TTHREADS)
     k_rowmma(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap fac_map,
-             int64_t m, int kchunks, int units, float* __restrict__ out, int64_t ldo, int rc) {
+             int64_t m, int kchunks, int units, const ThinOut o) {
   using L = ThinSmem<NT>;
   constexpr int ROWS = L::ROWS;
   extern __shared__ __align__(16) unsigned char thin_raw[];
@@ -151,32 +246,17 @@ __global__ void __launch_bounds__(TTHREADS)
     }
     __syncthreads();
     const int tile = u / kchunks;
-    if (u + 1 == u1 || (u + 1) / kchunks != tile) {  // leaving this token tile: flush
-      const int64_t ta = static_cast<int64_t>(tile) * TM + warp * 16 + g, tb = ta + 8;
-#pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        const int j = n * 8 + 2 * tq;
-        if (ta < m) {
-          if (j < rc) atomicAdd(out + ta * ldo + j, acc[n][0]);
-          if (j + 1 < rc) atomicAdd(out + ta * ldo + j + 1, acc[n][1]);
-        }
-        if (tb < m) {
-          if (j < rc) atomicAdd(out + tb * ldo + j, acc[n][2]);
-          if (j + 1 < rc) atomicAdd(out + tb * ldo + j + 1, acc[n][3]);
-        }
-        acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
-      }
-    }
+    if (u + 1 == u1 || (u + 1) / kchunks != tile)  // leaving this token tile
+      thin_flush<NT>(acc, tile, kchunks, units, o, m);
   }
 }
 
 // out[n, j] += scale · Σ_t act[t, n] · Vt[j, t]   (Vt = V transposed, hi/lo bf16 planes)
-// Columns j >= rc of the product go to colsum (the ones column) when j == rc.
+// Column j == rc of the product (the ones column) goes to colsum.
 template <int NT>
 __global__ void __launch_bounds__(TTHREADS)
     k_colmma(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap fac_map,
-             int64_t nd, int tchunks, int units, float scale, float* __restrict__ out,
-             int64_t ldo, int rc, float* __restrict__ colsum) {
+             int64_t nd, int tchunks, int units, const ThinOut o) {
   using L = ThinSmem<NT>;
   constexpr int ROWS = L::ROWS;
   extern __shared__ __align__(16) unsigned char thin_raw[];
@@ -236,24 +316,8 @@ __global__ void __launch_bounds__(TTHREADS)
     }
     __syncthreads();
     const int nt = u / tchunks;
-    if (u + 1 == u1 || (u + 1) / tchunks != nt) {  // leaving this n tile: flush
-      const int64_t na = static_cast<int64_t>(nt) * TM + warp * 16 + g, nb = na + 8;
-#pragma unroll
-      for (int n = 0; n < NT; ++n) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = n * 8 + 2 * tq + h;
-          if (j < rc) {
-            if (na < nd) atomicAdd(out + na * ldo + j, scale * acc[n][h]);
-            if (nb < nd) atomicAdd(out + nb * ldo + j, scale * acc[n][2 + h]);
-          } else if (j == rc && colsum != nullptr) {
-            if (na < nd) atomicAdd(colsum + na, acc[n][h]);
-            if (nb < nd) atomicAdd(colsum + nb, acc[n][2 + h]);
-          }
-        }
-        acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
-      }
-    }
+    if (u + 1 == u1 || (u + 1) / tchunks != nt)  // leaving this n tile
+      thin_flush<NT>(acc, nt, tchunks, units, o, nd);
   }
 }
 
@@ -358,60 +422,82 @@ cudaError_t thin_map(CUtensorMap* m, const void* base, int64_t inner, int64_t ou
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Grid of one launch: one resident wave. The dynamic-smem opt-in is set first,
+// so the occupancy query (and the workspace sized from it) matches the launch.
+template <int NT>
+int thin_ctas(bool row, int64_t units) {
+  const int smem = ThinSmem<NT>::BYTES;
+  static bool attr_row = false, attr_col = false;
+  bool& attr = row ? attr_row : attr_col;
+  if (!attr) {
+    const cudaError_t e =
+        row ? cudaFuncSetAttribute(k_rowmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+            : cudaFuncSetAttribute(k_colmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return 0;
+    attr = true;
+  }
+  return row ? wave_ctas(k_rowmma<NT>, smem, units) : wave_ctas(k_colmma<NT>, smem, units);
+}
+
+template <int NT>
+void ws_size_nt(bool row, int64_t m, int64_t d, int64_t* ws_floats, int64_t* n_cnt) {
+  const int64_t tiles = row ? (m + TM - 1) / TM : (d + TM - 1) / TM;
+  const int64_t chunks = row ? (d + TILE - 1) / TILE : (m + TILE - 1) / TILE;
+  const int64_t units = tiles * chunks;
+  const int64_t ctas = units > 0 ? thin_ctas<NT>(row, units) : 0;
+  *ws_floats = ctas * 2 * TM * 8 * NT;
+  *n_cnt = tiles;
+}
+
 template <int NT>
 cudaError_t rowmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
-                      const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t ldw, float* out,
-                      int64_t ldo, int64_t r, cudaStream_t st) {
+                      const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t ldw, int64_t r,
+                      ThinOut o, cudaStream_t st) {
   constexpr int ROWS = 8 * NT;
   const int64_t tb = (m + TM - 1) / TM;
   const int64_t kchunks = (kd + TILE - 1) / TILE;
   const int64_t units = tb * kchunks;
   if (units <= 0) return cudaSuccess;
-  if (units > INT32_MAX || lo != hi + ROWS * ldw) return cudaErrorInvalidValue;
+  if (units > INT32_MAX || lo != hi + ROWS * ldw || !o.ws || !o.cnt || !o.out)
+    return cudaErrorInvalidValue;
   CUtensorMap am, fm;
   cudaError_t e = thin_map(&am, act, kd, m, lda, TM);
   if (e == cudaSuccess) e = thin_map(&fm, hi, ldw, 2 * ROWS, ldw, 2 * ROWS);
   if (e != cudaSuccess) return e;
   const int smem = ThinSmem<NT>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(k_rowmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int ctas = wave_ctas(k_rowmma<NT>, smem, units);
+  const int ctas = thin_ctas<NT>(true, units);
+  if (ctas <= 0 || o.ws_floats < static_cast<int64_t>(ctas) * 2 * TM * ROWS)
+    return cudaErrorInvalidValue;
+  o.rc = static_cast<int>(r);
   note_launch();
   k_rowmma<NT><<<ctas, TTHREADS, smem, st>>>(am, fm, m, static_cast<int>(kchunks),
-                                        static_cast<int>(units), out, ldo, static_cast<int>(r));
+                                             static_cast<int>(units), o);
   return cudaGetLastError();
 }
 
 template <int NT>
 cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t nd,
-                      const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t ldv, float scale,
-                      float* out, int64_t ldo, int64_t r, float* colsum, cudaStream_t st) {
+                      const __nv_bfloat16* hi, const __nv_bfloat16* lo, int64_t ldv, int64_t r,
+                      ThinOut o, cudaStream_t st) {
   constexpr int ROWS = 8 * NT;
   const int64_t nb = (nd + TM - 1) / TM;
   const int64_t tchunks = (m + TILE - 1) / TILE;
   const int64_t units = nb * tchunks;
   if (units <= 0) return cudaSuccess;
-  if (units > INT32_MAX || lo != hi + ROWS * ldv) return cudaErrorInvalidValue;
+  if (units > INT32_MAX || lo != hi + ROWS * ldv || !o.ws || !o.cnt || !o.out)
+    return cudaErrorInvalidValue;
   CUtensorMap am, fm;
   cudaError_t e = thin_map(&am, act, nd, m, lda, TILE);
   if (e == cudaSuccess) e = thin_map(&fm, hi, ldv, 2 * ROWS, ldv, 2 * ROWS);
   if (e != cudaSuccess) return e;
   const int smem = ThinSmem<NT>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(k_colmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int ctas = wave_ctas(k_colmma<NT>, smem, units);
+  const int ctas = thin_ctas<NT>(false, units);
+  if (ctas <= 0 || o.ws_floats < static_cast<int64_t>(ctas) * 2 * TM * ROWS)
+    return cudaErrorInvalidValue;
+  o.rc = static_cast<int>(r);
   note_launch();
   k_colmma<NT><<<ctas, TTHREADS, smem, st>>>(am, fm, nd, static_cast<int>(tchunks),
-                                        static_cast<int>(units), scale, out, ldo,
-                                        static_cast<int>(r), colsum);
+                                             static_cast<int>(units), o);
   return cudaGetLastError();
 }
 
@@ -452,22 +538,41 @@ int thin_rows(int64_t r, bool ones) { return static_cast<int>((r + (ones ? 1 : 0
     default: return cudaErrorInvalidValue;     \
   }
 
+void thin_ws_size(bool row, int64_t m, int64_t d, int64_t r, bool ones, int64_t* ws_floats,
+                  int64_t* n_cnt) {
+  *ws_floats = *n_cnt = 0;
+#define CALL_WS(N) (ws_size_nt<N>(row, m, d, ws_floats, n_cnt), 0)
+  const int nt = thin_rows(r, ones) / 8;
+  switch (nt) {
+    case 1: CALL_WS(1); break;
+    case 2: CALL_WS(2); break;
+    case 3: CALL_WS(3); break;
+    case 4: CALL_WS(4); break;
+    case 5: CALL_WS(5); break;
+    case 6: CALL_WS(6); break;
+    case 7: CALL_WS(7); break;
+    case 8: CALL_WS(8); break;
+    case 9: CALL_WS(9); break;
+    default: break;
+  }
+#undef CALL_WS
+}
+
 cudaError_t launch_rowmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
                           const __nv_bfloat16* wt_hi, const __nv_bfloat16* wt_lo, int64_t ldw,
-                          float* out, int64_t ldo, int64_t r, cudaStream_t st) {
+                          int64_t r, const ThinOut& o, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-#define CALL_ROW(N) rowmma_nt<N>(act, lda, m, kd, wt_hi, wt_lo, ldw, out, ldo, r, st)
+#define CALL_ROW(N) rowmma_nt<N>(act, lda, m, kd, wt_hi, wt_lo, ldw, r, o, st)
   MLRA_NT_DISPATCH(thin_rows(r, false) / 8, CALL_ROW)
 #undef CALL_ROW
 }
 
 cudaError_t launch_colmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t nd,
                           const __nv_bfloat16* vt_hi, const __nv_bfloat16* vt_lo, int64_t ldv,
-                          float scale, float* out, int64_t ldo, int64_t r, float* colsum,
-                          cudaStream_t st) {
+                          int64_t r, const ThinOut& o, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-#define CALL_COL(N) colmma_nt<N>(act, lda, m, nd, vt_hi, vt_lo, ldv, scale, out, ldo, r, colsum, st)
-  MLRA_NT_DISPATCH(thin_rows(r, colsum != nullptr) / 8, CALL_COL)
+#define CALL_COL(N) colmma_nt<N>(act, lda, m, nd, vt_hi, vt_lo, ldv, r, o, st)
+  MLRA_NT_DISPATCH(thin_rows(r, o.colsum != nullptr) / 8, CALL_COL)
 #undef CALL_COL
 }
 

@@ -41,9 +41,13 @@ class _Linear(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, anchor, layer: ModuLoraLayer, sink):
-        y, xb = layer_forward(layer, x, out_dtype=torch.float32)
+        # x is the fp32 activation: the bf16 operand is made here, so the
+        # fp32 dx returned by backward matches the input's dtype and reaches
+        # the residual stream unrounded
+        x16 = x.to(torch.bfloat16).contiguous()
+        y, xb = layer_forward(layer, x16, out_dtype=torch.float32)
         ctx.layer, ctx.sink = layer, sink
-        ctx.save_for_backward(x, xb)
+        ctx.save_for_backward(x16, xb)
         return y
 
     @staticmethod
@@ -85,7 +89,7 @@ class ParityTransformer:
 
     def _lin(self, i: int, h: torch.Tensor) -> torch.Tensor:
         lead = h.shape[:-1]
-        x = h.reshape(-1, h.shape[-1]).to(torch.bfloat16).contiguous()
+        x = h.reshape(-1, h.shape[-1]).float()
         y = _Linear.apply(x, self._anchor, self.layers[i], self.sink)
         return y.reshape(*lead, y.shape[-1])
 
@@ -129,9 +133,16 @@ class _Sink:
         self.views = bucket.views
         self.group = group
         self.works = []
+        self.weight = None  # (local batch, global-batch tensor, its all-reduce) when distributed
 
     def layer_done(self, L: ModuLoraLayer) -> None:
         names = [f"{L.name}.dA", f"{L.name}.dB"] + ([f"{L.name}.dbias"] if L.bias_trainable else [])
+        if self.weight is not None:
+            n_local, total, cw = self.weight
+            if cw is not None:
+                cw.wait()
+                self.weight = (n_local, total, None)
+            self.bucket.slice_of(names).mul_(n_local / total)  # device-side, no host sync
         w = self.bucket.allreduce_async(names, group=self.group)
         if w is not None:
             self.works.append(w)
@@ -145,8 +156,9 @@ class _Sink:
 class TransformerTrainer:
     """One data-parallel training step of the parity transformer (train.cpp:136-176
     per step: zero grads, loss, backward, AdamW): each rank runs its share of the
-    batch; gradients are sum-all-reduced per layer during the backward and
-    scaled by 1/world, i.e. the gradient of the global mean loss."""
+    batch; gradients are sum-all-reduced per layer during the backward, each
+    rank's contribution weighted by local_batch / global_batch, i.e. the
+    gradient of the global mean loss even when the local batches differ."""
 
     def __init__(self, model: ParityTransformer, config: TrainConfig, group=None):
         config.validate()
@@ -168,6 +180,16 @@ class TransformerTrainer:
     def loss_and_grads(self, x: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
         """Forward + backward; leaves the (world-averaged) gradients in
         ``self.grads.flat`` and returns the local loss (a device scalar)."""
+        world = self._world()
+        count = None
+        if world > 1:
+            import torch.distributed as dist
+            n_local = x.shape[0] if x.dim() == 3 else 1
+            count = torch.tensor([float(n_local)], device=self.grads.flat.device)
+            cw = dist.all_reduce(count, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+            # the local mean loss's gradient, weighted by this rank's share of the
+            # global batch: the per-layer sums then form the global mean's gradient
+            self.sink.weight = (n_local, count, cw)
         self.model.sink = self.sink
         try:
             loss = self.model.loss(x, labels)
@@ -175,9 +197,7 @@ class TransformerTrainer:
         finally:
             self.model.sink = None
         self.sink.wait()
-        world = self._world()
-        if world > 1:
-            self.grads.flat.mul_(1.0 / world)
+        self.sink.weight = None
         return loss.detach()
 
     def step(self, x: torch.Tensor, labels: torch.Tensor, check_finite: bool = True) -> torch.Tensor:

@@ -733,6 +733,16 @@ def layer_backward(layer: ModuLoraLayer, x: torch.Tensor, xb: torch.Tensor, dy: 
     _check_act(x, layer.d_in(), f"layer '{layer.name}' backward")
     m = x.shape[0]
     r = layer.adapter.rank
+    # the C ABI takes one token count: every per-token operand must have m rows
+    # (lowprec_linear.cpp:202-206 DimensionError), on x's device
+    if dy.shape[0] != m:
+        raise MlraError(2, f"layer '{layer.name}' backward: grad rows {dy.shape[0]} != input rows {m}")
+    if (xb.dim() != 2 or tuple(xb.shape) != (m, r) or xb.dtype != torch.float32
+            or not xb.is_contiguous() or xb.device != x.device):
+        raise MlraError(2, f"layer '{layer.name}' backward: xb must be a contiguous fp32 ({m}, {r}) "
+                           f"tensor on {x.device}, got {tuple(xb.shape)} {xb.dtype} on {xb.device}")
+    if dy.device != x.device:
+        raise MlraError(2, f"layer '{layer.name}' backward: dy on {dy.device}, x on {x.device}")
     if da is None:
         da = torch.empty(layer.d_out(), r, dtype=torch.float32, device=x.device)
     if db is None:

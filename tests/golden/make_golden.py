@@ -195,6 +195,75 @@ def corruptions(buf: bytes):
     return out
 
 
+def record_offsets(buf: bytes):
+    """Walk a checkpoint (checkpoint.hpp:4-24): layer records [(name, off, size)],
+    the adapter-count offset, adapter records [(name, off, size, alpha_off)]."""
+    import struct
+    o = 6
+    (clen,) = struct.unpack_from("<I", buf, o)
+    o += 4 + clen
+    (nl,) = struct.unpack_from("<I", buf, o)
+    o += 4
+    layers, dims = [], {}
+    for _ in range(nl):
+        off = o
+        (n,) = struct.unpack_from("<I", buf, o)
+        name = buf[o + 4:o + 4 + n].decode()
+        o += 4 + n
+        rows, cols = struct.unpack_from("<II", buf, o)
+        o += 9
+        (group,) = struct.unpack_from("<I", buf, o)
+        o += 4
+        (nw,) = struct.unpack_from("<I", buf, o)
+        o += 4 + 4 * nw + 8 * rows * (cols // group)
+        (nb,) = struct.unpack_from("<I", buf, o)
+        o += 4 + 4 * nb
+        layers.append((name, off, o - off))
+        dims[name] = (rows, cols)
+    n_ad_off = o
+    (na,) = struct.unpack_from("<I", buf, o)
+    o += 4
+    ads = []
+    for _ in range(na):
+        off = o
+        (n,) = struct.unpack_from("<I", buf, o)
+        name = buf[o + 4:o + 4 + n].decode()
+        o += 4 + n
+        (r,) = struct.unpack_from("<I", buf, o)
+        alpha_off = o + 4
+        rows, cols = dims[name]
+        o += 8 + 8 * r * (rows + cols)
+        ads.append((name, off, o - off, alpha_off))
+    return layers, n_ad_off, ads
+
+
+def structural_corruptions(buf: bytes):
+    """Well-formed files whose adapter section load_model's assemble_model rejects
+    (model.cpp:472-531) or accepts: name -> bytes."""
+    import struct
+    layers, n_ad_off, ads = record_offsets(buf)
+    head, tail = buf[:n_ad_off], buf[n_ad_off + 4:]
+    recs = [buf[a[1]:a[1] + a[2]] for a in ads]
+
+    def with_recs(rs):
+        return head + struct.pack("<I", len(rs)) + b"".join(rs)
+
+    out = {"dup_last_adapter": with_recs(recs + [recs[-1]]),
+           "missing_last_adapter": with_recs(recs[:-1]),
+           "no_adapters": with_recs([])}
+    if len(recs) > 1:
+        out["swapped_adapters"] = with_recs([recs[1], recs[0]] + recs[2:])
+        out["dup_first_for_second"] = with_recs([recs[0], recs[0]] + recs[2:])
+    b = bytearray(buf)
+    b[ads[0][3]:ads[0][3] + 4] = struct.pack("<f", 0.0)
+    out["alpha_zero"] = bytes(b)
+    b = bytearray(buf)
+    b[ads[-1][3]:ads[-1][3] + 4] = struct.pack("<f", -2.0)
+    out["alpha_negative"] = bytes(b)
+    assert tail == b"".join(recs)
+    return out
+
+
 def checkpoint_cases():
     import ctypes as C
     import json
@@ -219,6 +288,10 @@ def checkpoint_cases():
         expect[name] = probe(path)
         buf = open(path, "rb").read()
         for cname, data in corruptions(buf).items():
+            with open(tmp, "wb") as fh:
+                fh.write(data)
+            expect[f"{name}:{cname}"] = probe(tmp)
+        for cname, data in structural_corruptions(buf).items():
             with open(tmp, "wb") as fh:
                 fh.write(data)
             expect[f"{name}:{cname}"] = probe(tmp)
@@ -303,6 +376,9 @@ def main():
         raise SystemExit("oracle/_ref/libmlra_ref.so missing: run `make -C oracle` with /root/reference present")
     if sys.argv[1:] == ["optq"]:
         np.savez_compressed(os.path.join(HERE, "optq.npz"), **optq_cases())
+        return
+    if sys.argv[1:] == ["checkpoints"]:
+        checkpoint_cases()
         return
     if sys.argv[1:] == ["model"]:
         np.savez_compressed(os.path.join(HERE, "parity_model.npz"), **model_cases())

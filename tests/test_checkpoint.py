@@ -124,3 +124,78 @@ def test_checkpoint_layers_run_forward_backward():
         b32 = r.b.astype(np.float32).astype(np.float64)
         yr, _ = orc.layer_forward(w, a32, b32, r.alpha, r.bias.astype(np.float64), x64)
         assert np.linalg.norm(y.double().cpu().numpy() - yr) <= 4e-3 * np.linalg.norm(yr) + 1e-6
+
+
+STRUCT = ["dup_last_adapter", "missing_last_adapter", "no_adapters", "swapped_adapters",
+          "dup_first_for_second", "alpha_zero", "alpha_negative"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_assemble_model_checks_match_reference(name, tmp_path):
+    """adapter sections the reference's load_model rejects in
+    assemble_model (model.cpp:472-531: one adapter per layer, in layer order,
+    rank >= 1, alpha > 0) are rejected by load_model with the same ConfigError;
+    the parse alone (inspect_layout) still accepts them, keeps every record in
+    file order and re-encodes byte-identically."""
+    from tests.golden.make_golden import record_offsets, structural_corruptions
+    buf = open(os.path.join(GOLDEN, name), "rb").read()
+    for cname, data in structural_corruptions(buf).items():
+        want = EXPECT[f"{name}:{cname}"]
+        p = str(tmp_path / "s.mlra")
+        with open(p, "wb") as fh:
+            fh.write(data)
+        c = Checkpoint.load(p)
+        assert [a[:3] for a in record_offsets(data)[2]] == c.layout()["adapters"], cname
+        out = str(tmp_path / "s2.mlra")
+        c.save(out)
+        assert open(out, "rb").read() == data, cname
+        if want["status"] == 0:
+            assert load_model(p).frozen_hash() == want["frozen_hash"]
+            continue
+        with pytest.raises(MlraError) as e:
+            load_model(p)
+        assert e.value.status == want["status"] and e.value.kind == "ConfigError", cname
+
+
+def test_to_layers_follows_the_config(tmp_path):
+    """to_layers() takes strategy and bias_trainable from the config JSON
+    (assemble_model, model.cpp:527-529) unless the caller overrides them."""
+    import paper_2309_16119_b200.checkpoint as CK
+    c = Checkpoint.load(os.path.join(GOLDEN, "parity_b4.mlra"))
+    cfg = c.config()
+    assert "strategy" in cfg and "bias_trainable" in cfg
+    seen = {}
+
+    class Probe(CK.Checkpoint):
+        def upload(self, i, stream=None):
+            return None
+
+    orig_torch = CK.torch
+
+    class _T:  # no GPU here: keep the factors on the host
+        def __getattr__(self, k):
+            return getattr(orig_torch, k)
+
+        @staticmethod
+        def from_numpy(a):
+            class _W:
+                def __init__(self, t):
+                    self.t = t
+
+                def cuda(self):
+                    return self.t
+            return _W(orig_torch.from_numpy(a))
+    CK.torch = _T()
+    try:
+        p = Probe(c._h)
+        c._h = None
+        layers = p.to_layers()
+        seen["strategy"] = {int(L.strategy) for L in layers}
+        seen["bias"] = {L.bias_trainable for L in layers}
+        forced = p.to_layers(bias_trainable=True)
+        assert all(L.bias_trainable for L in forced)
+    finally:
+        CK.torch = orig_torch
+    from paper_2309_16119_b200.modulora import parse_strategy
+    assert seen["strategy"] == {int(parse_strategy(cfg["strategy"]))}
+    assert seen["bias"] == {bool(cfg["bias_trainable"])}
