@@ -102,6 +102,12 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // CTA whose contiguous unit range [u0(c), u0(c+1)) contains unit u, for
 // u0(c) = floor(c·U/G): the largest c with c·U/G < u + 1.
 __device__ __forceinline__ int cta_of_unit(int64_t u, int64_t units, int64_t G) {
@@ -113,75 +119,142 @@ __device__ __forceinline__ int first_tile_of(int c, int64_t units, int64_t G, in
 
 // Flush of one output tile (all threads of the CTA, uniform): the fragment
 // partials go to this CTA's slot (slot 0 when `tile` is the first tile of its
-// range, else slot 1; layout [ROWS cols][TM rows]); when every contributor has
-// written (counter), the last one sums the slots in CTA order and stores.
+// range, else slot 1; row-major [TM rows][ROWS cols], the output's own order);
+// when every contributor has written (counter), the last one sums the slots in
+// CTA order and stores.
 template <int NT>
 __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
                            const ThinOut& o, int64_t n_out) {
   constexpr int ROWS = 8 * NT;
+  constexpr int SLOT = TM * ROWS;
   __shared__ int s_last;
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int which = tile == first_tile_of(c, units, G, chunks) ? 0 : 1;
-  float* slot = o.ws + (static_cast<int64_t>(c) * 2 + which) * (TM * ROWS);
+  float* slot = o.ws + (static_cast<int64_t>(c) * 2 + which) * SLOT;
   const int ra = warp * 16 + g;
 #pragma unroll
   for (int n = 0; n < NT; ++n) {
     const int j = n * 8 + 2 * tq;
-    slot[j * TM + ra] = acc[n][0];
-    slot[(j + 1) * TM + ra] = acc[n][1];
-    slot[j * TM + ra + 8] = acc[n][2];
-    slot[(j + 1) * TM + ra + 8] = acc[n][3];
+    *reinterpret_cast<float2*>(slot + ra * ROWS + j) = make_float2(acc[n][0], acc[n][1]);
+    *reinterpret_cast<float2*>(slot + (ra + 8) * ROWS + j) = make_float2(acc[n][2], acc[n][3]);
     acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
   }
   const int c_lo = cta_of_unit(static_cast<int64_t>(tile) * chunks, units, G);
   const int c_hi = cta_of_unit(static_cast<int64_t>(tile + 1) * chunks - 1, units, G);
+  // bar.sync orders the CTA's slot stores before thread 0's acq_rel atomic (a
+  // cumulative gpu-scope release); the finisher's thread 0 acquires every other
+  // contributor's release through the same counter and the second bar.sync
+  // passes that on to its threads, whose L2 (.cg) loads then see the slots.
+  // (A per-thread __threadfence() here is a fence.sc per thread: measured
+  // ~3x slower for the whole kernel.)
+  __syncthreads();
   if (c_lo != c_hi) {
-    __threadfence();  // this CTA's partial visible before it is counted
-    __syncthreads();
     if (threadIdx.x == 0) {
-      const int old = atomicAdd(o.cnt + tile, 1);
+      const int old = atom_add_acq_rel_gpu(o.cnt + tile, 1);
       s_last = old == c_hi - c_lo;
       if (s_last) o.cnt[tile] = 0;  // self-resetting for the next launch on this stream
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
-  } else {
-    __syncthreads();
   }
-  // finisher: v(row, j) = Σ_{q = c_lo..c_hi} slot_q(row, j), in CTA order
-  for (int idx = threadIdx.x; idx < TM * ROWS; idx += TTHREADS) {
-    const int j = idx / TM, tr = idx - j * TM;
-    float v = 0.0f;
-    for (int q = c_lo; q <= c_hi; ++q) {
-      const int wq = tile == first_tile_of(q, units, G, chunks) ? 0 : 1;
-      v += __ldcg(o.ws + (static_cast<int64_t>(q) * 2 + wq) * (TM * ROWS) + j * TM + tr);
-    }
-    const int64_t row = static_cast<int64_t>(tile) * TM + tr;
-    if (row < n_out) {
-      if (j < o.rc) {
-        o.out[row * o.ldo + j] = o.scale * v;
-        if (o.pad) o.pad[row * o.ldp + j] = __float2bfloat16_rn(o.pad_scale * v);
-      } else if (j == o.rc && o.colsum) {
-        o.colsum[row] = v;
+  // Finisher: v(row, j) = Σ_{q = c_lo..c_hi} slot_q(row, j), in CTA order. Every
+  // contributor after c_lo starts its range inside this tile, so its slot is 0;
+  // c_lo's is 0 only when the tile is its first. The finisher is the launch's
+  // tail, so it is built for memory-level parallelism and coalescing: each
+  // thread owns PER float4s = 4 consecutive columns of one row, keeps QB·PER
+  // loads in flight, and stores row-major (16-B fp32 / 8-B bf16 stores; measured:
+  // scattered 4-B stores made the tail ~10 us of a 28 us launch).
+  constexpr int C4 = ROWS / 4;                  // float4s per slot row
+  constexpr int PER = SLOT / (4 * TTHREADS);    // float4 positions per thread (= NT)
+  static_assert(SLOT % (4 * TTHREADS) == 0, "slot must tile the CTA in float4s");
+  constexpr int QB = 8 / PER > 0 ? 8 / PER : 1;
+  const float* s0 = o.ws + (static_cast<int64_t>(c_lo) * 2 +
+                            (tile == first_tile_of(c_lo, units, G, chunks) ? 0 : 1)) * SLOT;
+  float4 acc4[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k)
+    acc4[k] = __ldcg(reinterpret_cast<const float4*>(s0) + threadIdx.x + k * TTHREADS);
+  for (int q0 = c_lo + 1; q0 <= c_hi; q0 += QB) {
+    float4 buf[QB][PER];
+#pragma unroll
+    for (int i = 0; i < QB; ++i) {
+      if (q0 + i <= c_hi) {
+        const float4* p = reinterpret_cast<const float4*>(o.ws + static_cast<int64_t>(q0 + i) * 2 * SLOT);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) buf[i][k] = __ldcg(p + threadIdx.x + k * TTHREADS);
       }
     }
-    if (o.thi && row < o.ldt && j < o.t_rows) {  // transposed hi/lo planes (zero padded)
-      const float tv = (row < n_out && j < o.rc) ? v : 0.0f;
-      const __nv_bfloat16 h = __float2bfloat16_rn(tv);
-      o.thi[static_cast<int64_t>(j) * o.ldt + row] = h;
-      o.thi[static_cast<int64_t>(o.t_rows + j) * o.ldt + row] =
-          __float2bfloat16_rn(tv - __bfloat162float(h));
+#pragma unroll
+    for (int i = 0; i < QB; ++i) {
+      if (q0 + i <= c_hi) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          acc4[k].x += buf[i][k].x;
+          acc4[k].y += buf[i][k].y;
+          acc4[k].z += buf[i][k].z;
+          acc4[k].w += buf[i][k].w;
+        }
+      }
     }
   }
-  if (o.pad) {  // zero the pad columns [rc, pad_cols) of the bf16 operand
-    const int pc = o.pad_cols - o.rc;
-    for (int idx = threadIdx.x; idx < TM * pc; idx += TTHREADS) {
-      const int tr = idx / pc, j = o.rc + idx - tr * pc;
+  const bool vec_out = (o.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0;
+  const bool vec_pad = o.pad && (o.ldp & 3) == 0 && (reinterpret_cast<uintptr_t>(o.pad) & 7) == 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int p4 = threadIdx.x + k * TTHREADS;
+    const int tr = p4 / C4, j = 4 * (p4 - tr * C4);
+    const int64_t row = static_cast<int64_t>(tile) * TM + tr;
+    const float vv[4] = {acc4[k].x, acc4[k].y, acc4[k].z, acc4[k].w};
+    if (row < n_out) {
+      if (vec_out && j + 4 <= o.rc) {
+        *reinterpret_cast<float4*>(o.out + row * o.ldo + j) =
+            make_float4(o.scale * vv[0], o.scale * vv[1], o.scale * vv[2], o.scale * vv[3]);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (j + kk < o.rc) o.out[row * o.ldo + j + kk] = o.scale * vv[kk];
+      }
+      if (o.colsum && j <= o.rc && o.rc < j + 4) o.colsum[row] = vv[o.rc - j];
+      if (o.pad) {  // bf16(pad_scale · v), zero beyond rc (the padded extra-K operand)
+        __nv_bfloat16 h[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          h[kk] = __float2bfloat16_rn(j + kk < o.rc ? o.pad_scale * vv[kk] : 0.0f);
+        if (vec_pad && j + 4 <= o.pad_cols) {
+          *reinterpret_cast<uint2*>(o.pad + row * o.ldp + j) = *reinterpret_cast<const uint2*>(h);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            if (j + kk < o.pad_cols) o.pad[row * o.ldp + j + kk] = h[kk];
+        }
+      }
+    }
+    if (o.thi && row < o.ldt) {  // transposed hi/lo planes [t_rows x ldt] (zero padded)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (j + kk < o.t_rows) {
+          const float tv = (row < n_out && j + kk < o.rc) ? vv[kk] : 0.0f;
+          const __nv_bfloat16 h = __float2bfloat16_rn(tv);
+          o.thi[static_cast<int64_t>(j + kk) * o.ldt + row] = h;
+          o.thi[static_cast<int64_t>(o.t_rows + j + kk) * o.ldt + row] =
+              __float2bfloat16_rn(tv - __bfloat162float(h));
+        }
+      }
+    }
+  }
+  if (o.pad && o.pad_cols > ROWS) {  // zero pad columns [ROWS, pad_cols): 8-B stores
+    const int pc4 = (o.pad_cols - ROWS) / 4;
+    for (int idx = threadIdx.x; idx < TM * pc4; idx += TTHREADS) {
+      const int tr = idx / pc4, j = ROWS + 4 * (idx - tr * pc4);
       const int64_t row = static_cast<int64_t>(tile) * TM + tr;
-      if (row < n_out) o.pad[row * o.ldp + j] = __float2bfloat16_rn(0.0f);
+      if (row < n_out) {
+        if (vec_pad)
+          *reinterpret_cast<uint2*>(o.pad + row * o.ldp + j) = make_uint2(0u, 0u);
+        else
+          for (int kk = 0; kk < 4; ++kk) o.pad[row * o.ldp + j + kk] = __float2bfloat16_rn(0.0f);
+      }
     }
   }
   __syncthreads();  // the slot is rewritten by this CTA's next flush
@@ -189,7 +262,7 @@ __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
 
 // out[t, j] (+)= Σ_k act[t, k] · Wt[j, k]   (Wt = W transposed, hi/lo bf16 planes)
 template <int NT>
-__global__ void __launch_bounds__(TTHREADS)
+__global__ void __launch_bounds__(TTHREADS, 3)
     k_rowmma(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap fac_map,
              int64_t m, int kchunks, int units, const ThinOut o) {
   using L = ThinSmem<NT>;
@@ -254,7 +327,7 @@ __global__ void __launch_bounds__(TTHREADS)
 // out[n, j] += scale · Σ_t act[t, n] · Vt[j, t]   (Vt = V transposed, hi/lo bf16 planes)
 // Column j == rc of the product (the ones column) goes to colsum.
 template <int NT>
-__global__ void __launch_bounds__(TTHREADS)
+__global__ void __launch_bounds__(TTHREADS, 3)
     k_colmma(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap fac_map,
              int64_t nd, int tchunks, int units, const ThinOut o) {
   using L = ThinSmem<NT>;
