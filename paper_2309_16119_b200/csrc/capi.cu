@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "qgemm.h"
+#include "qgemm_dev.cuh"
 
 using mlra::QWeightDev;
 
@@ -236,14 +237,17 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
   a.bias = gp.bias;
   a.out_pairs = !gp.out_f32 && gp.ldo % 2 == 0 &&
                 reinterpret_cast<uintptr_t>(gp.out) % 4 == 0 ? 1 : 0;
-  // CTA-pair kernel (512 tokens per tile) or the 1-CTA kernel (256), by the
-  // cost model; MLRA_GEMM=1|2 forces the 1-CTA / pair kernel (tests cover both).
+  // CTA-pair kernel (512 tokens per tile) or the 1-CTA kernel (256 or 128), by
+  // the cost model; MLRA_GEMM=1|2|3 forces the 1-CTA (256) / pair / 1-CTA (128)
+  // kernel (tests cover all three).
   a.cb2_codebook = gp.cb2_codebook;
   a.lut = gp.lut;
-  bool pair = mlra::qgemm_prefer_pair(a);
-  if (const char* force = getenv("MLRA_GEMM")) pair = atoi(force) == 2;
-  if (gp.cb2_codebook || gp.lut) pair = true;  // the plugin decodes live in the pair kernel
-  const uint32_t tbox = pair ? 128 : 256;
+  int kind = mlra::qgemm_choose(a);
+  if (const char* force = getenv("MLRA_GEMM")) kind = atoi(force);
+  if (gp.cb2_codebook || gp.lut) kind = 2;  // the plugin decodes live in the pair kernel
+  const bool pair = kind == 2;
+  a.bn = kind == 3 ? 128 : 256;
+  const uint32_t tbox = pair ? 128 : static_cast<uint32_t>(a.bn);
   mlra_status st = make_map(&maps.act, gp.act, gp.k_red_valid, gp.tokens, gp.ld_act, 64, tbox);
   if (st) return st;
   if (a.n_kb_lora) {
@@ -289,8 +293,14 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
       a.q_stages = 0;
     }
   }
+  if (kind == 3 && a.q_stages > 0) {  // the 128-token 1-CTA kernel's deeper ring leaves less room
+    const int room = (mlra::qg::SMEM_LIMIT - mlra::qg::qgemm1_smem_fixed(128)) / a.q_stage_bytes;
+    a.q_stages = room < 2 ? 0 : (a.q_stages > room ? room : a.q_stages);  // 0: LDG path
+  }
   if (const char* tr = getenv("MLRA_TRACE"))  // dev-only: MMA-thread wait cycles per CTA pair
     a.trace = reinterpret_cast<unsigned long long*>(strtoull(tr, nullptr, 0));
+  if (const char* tr = getenv("MLRA_TRACE2"))  // dev-only: per-CTA timeline (globaltimer)
+    a.trace2 = reinterpret_cast<unsigned long long*>(strtoull(tr, nullptr, 0));
   if (pair) {
     mlra::qgemm2_plan(a);
     if (a.sk_pairs) {  // stream-K: fp32 partial slots + zeroed publish flags

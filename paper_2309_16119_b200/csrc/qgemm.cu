@@ -40,7 +40,15 @@ namespace {
 
 using namespace qg;
 
-template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA>
+#ifndef MLRA_NSPLIT
+#define MLRA_NSPLIT 2
+#endif
+
+// TBN = tokens per tile (MMA N): 256, or 128 for small token counts, where
+// 256-token tiles leave most SMs idle (cfg1: 64 vs 128 CTAs at m=512). Each
+// dequantized weight tile then feeds half the MMA work, so TBN=128 only pays
+// below ~1.5 waves of 256-token tiles (cost model: qgemm_choose, qgemm2.cu).
+template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA, int TBN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tm_act,
                  const __grid_constant__ CUtensorMap tm_act_lora,
@@ -49,6 +57,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                  const __grid_constant__ CUtensorMap tm_codes,
                  const __grid_constant__ CUtensorMap tm_grid, const QWeightDev q,
                  const GemmArgs p) {
+  constexpr int BN = TBN;
+  constexpr int T_TILE = BN * BK * 2;
+  constexpr int STAGES = qgemm1_stages(TBN);
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators (a power of 2 >= 32)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -65,6 +77,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // dev-only (MLRA_TRACE2): per CTA [0] total cycles, [1] MMA wait on full,
+  // [2..4] / [5..7] dequant group 0 / 1: wait qfull, wait empty, compute+arrive
+  unsigned long long* tl = p.trace2 ? p.trace2 + 8 * blockIdx.x : nullptr;
+  const long long t_entry = clock64();
   const int n_kb_main = p.n_kb_main;
   const int n_kb = p.n_kb_main + p.n_kb_lora;
   const TileIter it{static_cast<int>(p.m_total / BM), static_cast<int>((p.tokens + BN - 1) / BN)};
@@ -141,8 +157,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc_main = idesc_bf16(BM, BN, MN ? 1u : 0u, 0u);
-      constexpr uint32_t idesc_kmaj = idesc_bf16(BM, BN, 0u, 0u);
+      // The token tile is issued as NSPLIT independent MMAs per k16 step (column
+      // halves of the accumulator, adjacent in TMEM so the epilogue is unchanged):
+      // back-to-back MMAs into one accumulator serialise on it, so with a single
+      // chain the 1-CTA kernel ran at ~250 cycles per MMA whatever N was.
+      constexpr int NSPLIT = MLRA_NSPLIT;
+      constexpr int NH = BN / NSPLIT;
+      constexpr uint32_t idesc_main = idesc_bf16(BM, NH, MN ? 1u : 0u, 0u);
+      constexpr uint32_t idesc_kmaj = idesc_bf16(BM, NH, 0u, 0u);
       int s = 0;
       uint32_t ph = 0;
       int local = 0;
@@ -153,7 +175,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = 0; kb < n_kb; ++kb) {
+          const long long f0 = tl ? clock64() : 0;
           mbar_wait(&full[s], ph);
+          if (tl) tl[1] += clock64() - f0;
           tc_fence_after();
           const bool lora = kb >= n_kb_main;
           const int nk16 = (lora && kb == n_kb - 1) ? p.lora_k16_last : BK / 16;
@@ -169,8 +193,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               adesc = sdesc_sw128(sw + k * 32, 16, 1024);
               idesc = idesc_kmaj;
             }
-            const uint64_t bdesc = sdesc_sw128(st + k * 32, 16, 1024);
-            tc_mma_f16(tmem_d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+#pragma unroll
+            for (int h = 0; h < NSPLIT; ++h) {
+              const uint64_t bdesc = sdesc_sw128(st + h * NH * 128 + k * 32, 16, 1024);
+              tc_mma_f16(tmem_d + h * NH, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
           }
           tc_commit(&empty[s]);
           if (++s == STAGES) {
@@ -299,8 +326,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool main = kb < n_kb_main;
           const int kp = kb & 1;
           if ((s & 1) == grp) {
+            const long long c0 = tl ? clock64() : 0;
             if (main) mbar_wait(&qfull[qs], qph);
+            const long long c1 = tl ? clock64() : 0;
             mbar_wait(&empty[s], ph ^ 1);
+            const long long c2 = tl ? clock64() : 0;
             if (main) {
               const uint32_t qc = sQ32 + qs * p.q_stage_bytes;
               const uint32_t qg = qc + p.q_codes_bytes;
@@ -317,6 +347,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) {
               mbar_arrive(&full[s]);
               if (main) mbar_arrive(&qempty[qs]);
+            }
+            if (tl && gtid == 0) {  // dev-only: group leader's wait/compute cycles
+              const long long c3 = clock64();
+              atomicAdd(reinterpret_cast<unsigned long long*>(tl + 2 + 3 * grp), c1 - c0);
+              atomicAdd(reinterpret_cast<unsigned long long*>(tl + 3 + 3 * grp), c2 - c1);
+              atomicAdd(reinterpret_cast<unsigned long long*>(tl + 4 + 3 * grp), c3 - c2);
             }
           }
           if (main && kp == 1) {
@@ -372,6 +408,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (tl && threadIdx.x == 0) tl[0] = clock64() - t_entry;
   if (warp == 1) tmem_dealloc(tmem_base, TMEM_COLS);
 }
 
@@ -385,14 +422,14 @@ int num_sms() {
   return sms;
 }
 
-template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA>
+template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA, int TBN>
 cudaError_t launch_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                      cudaStream_t stream) {
-  auto kern = qgemm_kernel<BITS, W_TMA, MN, OUT_F32, QTMA>;
-  const int smem = SMEM_FIXED + p.q_stages * p.q_stage_bytes;
+  auto kern = qgemm_kernel<BITS, W_TMA, MN, OUT_F32, QTMA, TBN>;
+  const int smem = qgemm1_smem_fixed(TBN) + p.q_stages * p.q_stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int64_t tiles = (p.m_total / BM) * ((p.tokens + BN - 1) / BN);
+  const int64_t tiles = (p.m_total / BM) * ((p.tokens + TBN - 1) / TBN);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
   note_launch();
   kern<<<grid, NUM_THREADS, smem, stream>>>(maps.act, maps.act_lora, maps.w, maps.w_lora,
@@ -400,13 +437,30 @@ cudaError_t launch_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& 
   return cudaGetLastError();
 }
 
-template <int BITS, bool W_TMA, bool QTMA>
+template <int BITS, bool W_TMA, bool QTMA, int TBN>
 cudaError_t launch_mo(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p, bool mn,
                       bool out_f32, cudaStream_t st) {
-  if (mn) return out_f32 ? launch_t<BITS, W_TMA, true, true, QTMA>(maps, q, p, st)
-                         : launch_t<BITS, W_TMA, true, false, QTMA>(maps, q, p, st);
-  return out_f32 ? launch_t<BITS, W_TMA, false, true, QTMA>(maps, q, p, st)
-                 : launch_t<BITS, W_TMA, false, false, QTMA>(maps, q, p, st);
+  if (mn) return out_f32 ? launch_t<BITS, W_TMA, true, true, QTMA, TBN>(maps, q, p, st)
+                         : launch_t<BITS, W_TMA, true, false, QTMA, TBN>(maps, q, p, st);
+  return out_f32 ? launch_t<BITS, W_TMA, false, true, QTMA, TBN>(maps, q, p, st)
+                 : launch_t<BITS, W_TMA, false, false, QTMA, TBN>(maps, q, p, st);
+}
+
+template <int TBN>
+cudaError_t launch_bits(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p, bool w_tma,
+                        bool mn, bool out_f32, cudaStream_t stream) {
+  if (w_tma) return launch_mo<4, true, false, TBN>(maps, q, p, mn, out_f32, stream);
+  const bool qtma = p.q_stages > 0;
+  switch (q.bits) {
+    case 2: return qtma ? launch_mo<2, false, true, TBN>(maps, q, p, mn, out_f32, stream)
+                        : launch_mo<2, false, false, TBN>(maps, q, p, mn, out_f32, stream);
+    case 3: return qtma ? launch_mo<3, false, true, TBN>(maps, q, p, mn, out_f32, stream)
+                        : launch_mo<3, false, false, TBN>(maps, q, p, mn, out_f32, stream);
+    case 4: return qtma ? launch_mo<4, false, true, TBN>(maps, q, p, mn, out_f32, stream)
+                        : launch_mo<4, false, false, TBN>(maps, q, p, mn, out_f32, stream);
+    case 8: return launch_mo<8, false, false, TBN>(maps, q, p, mn, out_f32, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace
@@ -425,18 +479,9 @@ int qgemm_max_q_stages(int q_stage_bytes, int extra_smem) {
 cudaError_t qgemm_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,
                          bool w_tma, bool mn, bool out_f32, cudaStream_t stream) {
   if (p.tokens <= 0 || p.m_total <= 0) return cudaSuccess;
-  if (w_tma) return launch_mo<4, true, false>(maps, q, p, mn, out_f32, stream);
-  const bool qtma = p.q_stages > 0;
-  switch (q.bits) {
-    case 2: return qtma ? launch_mo<2, false, true>(maps, q, p, mn, out_f32, stream)
-                        : launch_mo<2, false, false>(maps, q, p, mn, out_f32, stream);
-    case 3: return qtma ? launch_mo<3, false, true>(maps, q, p, mn, out_f32, stream)
-                        : launch_mo<3, false, false>(maps, q, p, mn, out_f32, stream);
-    case 4: return qtma ? launch_mo<4, false, true>(maps, q, p, mn, out_f32, stream)
-                        : launch_mo<4, false, false>(maps, q, p, mn, out_f32, stream);
-    case 8: return launch_mo<8, false, false>(maps, q, p, mn, out_f32, stream);
-    default: return cudaErrorInvalidValue;
-  }
+  if (p.bn == 128) return launch_bits<128>(maps, q, p, w_tma, mn, out_f32, stream);
+  if (p.bn == 256) return launch_bits<256>(maps, q, p, w_tma, mn, out_f32, stream);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace mlra

@@ -24,6 +24,7 @@ struct GemmArgs {
   int n_kb_lora;     // extra 64-wide LoRA blocks (ceil(r/64)), 0 = none
   int lora_k16_last; // useful 16-wide MMA steps in the last LoRA block
   int64_t tokens;    // m
+  int bn;            // 1-CTA kernel: tokens per tile (128 or 256)
   void* out;         // [tokens x ldo], f32 or bf16
   int64_t ldo;
   const float* bias; // [m_valid] or nullptr
@@ -39,6 +40,7 @@ struct GemmArgs {
   int q_group_div128; // group / 128 when group >= 128
   uint32_t q_group_magic; // ceil(2^32 / (group/128)) when group/128 > 1, else 0
   unsigned long long* trace;  // dev-only: per-CTA MMA-thread wait cycles (MLRA_TRACE), else null
+  unsigned long long* trace2; // dev-only: per-CTA globaltimer timeline, 8 slots (MLRA_TRACE2)
   // Stream-K (pair kernel only): 0 = whole tiles strided over the grid; else
   // the tile x k-block space is cut into sk_pairs contiguous ranges. Split
   // tiles are finished by their first segment's pair from fp32 partials.
@@ -46,6 +48,7 @@ struct GemmArgs {
   // entry sk_pairs is the end). Precomputed on the host so the device schedule
   // needs no division and stays on the uniform datapath.
   int sk_pairs;
+  int split;             // > 0: split-K mode, S pairs per tile (pair q = tile*S + s)
   float* sk_ws;          // [sk_pairs x 2 CTAs x 512 tokens x 128 rows] fp32 partials
   unsigned* sk_flags;    // [sk_pairs x 2], zeroed before the launch
   int sk_tile[129];
@@ -66,9 +69,9 @@ cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmA
 // Plans the pair kernel's schedule: sets p.sk_pairs (0 = whole tiles) and the
 // per-pair cut tables. The caller provides sk_ws / sk_flags when sk_pairs > 0.
 void qgemm2_plan(GemmArgs& p);
-// true: the pair kernel (with its planned schedule) is expected to beat the
-// 1-CTA kernel for this GEMM (cost model in qgemm2.cu).
-bool qgemm_prefer_pair(const GemmArgs& p);
+// Kernel choice by cost model (qgemm2.cu): 2 = the pair kernel with its planned
+// schedule, 1 = the 1-CTA kernel with 256-token tiles, 3 = 1-CTA with 128.
+int qgemm_choose(const GemmArgs& p);
 constexpr int kMaxSkPairs = 128;
 constexpr int kCb2SmemBytes = 256 * 16;  // the cb2 codebook staged in shared memory
 constexpr int kLutSmemBytes = 64;         // the lut plugin's 16 levels in shared memory

@@ -39,7 +39,19 @@ using namespace qg;
 
 constexpr double kSkMinIdleBlocks = 50.0;  // stream-K only when it recovers more than this
 constexpr int64_t kSkMinBlocksPerPair = 8;
+constexpr int64_t kSplitMinBlocks = 8;  // split-K: k-blocks per pair at least
+#ifndef MLRA_SPLIT_FIX
+#define MLRA_SPLIT_FIX 10.0
+#endif
+constexpr double kSplitFixUnits = MLRA_SPLIT_FIX;  // split-K drain + distributed fix-up
 constexpr double kSkMaxWaves = 1.25;  // stream-K only below this many waves of whole tiles
+#ifndef MLRA_COST128
+#define MLRA_COST128 0.45
+#endif
+constexpr double kCost128 = MLRA_COST128;  // 1-CTA 128-token k-block wave, pair units
+constexpr uint32_t TMEM_COLS = 512;  // two N=256 accumulators
+constexpr int kFixChunkBytes = 32 * 128 * 4;  // one stream-K partial chunk: 32 tokens x 128 rows
+constexpr int kFixSlots = STAGES * (W_TILE + T_TILE) / kFixChunkBytes;  // staged in the idle ring
 constexpr int HB = 128;            // tokens per CTA per accumulator (MMA N=256 split in two)
 constexpr int HB_TILE = HB * BK * 2;  // 16 KB
 constexpr int PAIR_ROWS = 2 * BM;  // 256 weight-side rows per pair tile
@@ -120,6 +132,21 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void epi_bar_sync() {  // the 4 epilogue warps only
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
@@ -151,12 +178,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = qempty + MAX_QS;
   uint64_t* tempty = tfull + 1;    // accumulator 0 (tokens 0..255 of the pair tile) drained
   uint64_t* tempty1 = tempty + 1;  // accumulator 1 drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty1 + 1);
+  uint64_t* fixb = tempty1 + 1;    // stream-K owner fix-up: staged partial chunks landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixb + kFixSlots);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  // dev-only timeline (MLRA_TRACE2): globaltimer ns per CTA at entry, MMA done,
+  // each epilogue tile's tfull, contributor flags seen, epilogue done
+  unsigned long long* tl = p.trace2 ? p.trace2 + 8 * blockIdx.x : nullptr;
+  if (tl && threadIdx.x == 0) tl[0] = gtime();
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int n_kb_main = p.n_kb_main;
   const int n_kb = p.n_kb_main + p.n_kb_lora;
@@ -195,6 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     mbar_init(tfull, 1);
     mbar_init(tempty, 2 * 4);
     mbar_init(tempty1, 2 * 4);
+    for (int i = 0; i < kFixSlots; ++i) mbar_init(&fixb[i], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc2(tmem_slot, TMEM_COLS);
@@ -342,6 +375,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         tc_commit_2sm_mc(tfull, 0x3);
       }
+      if (tl) tl[1] = gtime();
       if (p.trace) {  // dev-only instrumentation (MLRA_TRACE)
         p.trace[4 * cid + 0] = clock64() - t_start;
         p.trace[4 * cid + 1] = t_full;
@@ -394,15 +428,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       // stream-K roles: a segment starting mid-tile writes a partial; one that
       // starts at k-block 0 but ends early adds pairs [cid+1, q_end)'s partials
       const bool contrib = kb0 != 0;
-      const int q_end = (!contrib && kb1 != n_kb) ? SegSched::contrib_end(p, cid, tile) : cid + 1;
+      const bool split = p.split > 0;  // split-K: one (tile, k-range) unit per pair
+      const int q_end = (!split && !contrib && kb1 != n_kb) ? SegSched::contrib_end(p, cid, tile)
+                                                            : cid + 1;
       const int r_in = qd * 32 + lane;
       mbar_wait_backoff<EPI_NS>(tfull, local & 1);
       tc_fence_after();
+      if (tl && qd == 0 && lane == 0) tl[2] = gtime();
       const int64_t wrow = static_cast<int64_t>(mp) * PAIR_ROWS + rank * BM + r_in;
       const bool row_ok = wrow < p.m_valid;
       const float bias = (p.bias != nullptr && row_ok) ? p.bias[wrow] : 0.0f;
       for (int q = cid + 1; q < q_end; ++q)
         while (ld_acquire_gpu(&p.sk_flags[2 * q + rank]) == 0) __nanosleep(128);
+      if (tl && qd == 0 && lane == 0) tl[3] = gtime();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
       const int64_t tbase = static_cast<int64_t>(np) * PAIR_TOK;
       // bf16 output, paired rows: lanes 2i / 2i+1 swap half their tokens with one
@@ -492,7 +530,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (cc + 2 < 16) tc_wait_ld();
         }
       };
-      if (contrib) {
+      if (split) {
+        // Split-K with a distributed fix-up: the S pairs of a tile each own
+        // 16/S of its 16 token chunks. Each drains the chunks it does not own
+        // as fp32 partials, publishes, waits for the tile's other pairs, then
+        // finishes its own chunks: its TMEM accumulator (no further segment
+        // overwrites it) plus the others' partials staged into its idle
+        // operand ring by bulk copies, summed in pair order (deterministic).
+        // Every pair reads ~(S-1)/S of one tile's partials instead of one
+        // owner reading all of them (the stream-K fix-up's tail).
+        const int S = p.split, q0 = tile * S, sidx = cid - q0;
+        const int c0 = 16 * sidx / S, c1 = 16 * (sidx + 1) / S;
+        drain([&](uint32_t(&r)[32], int cc) {
+          if (!row_ok || (cc >= c0 && cc < c1)) return;
+          float* d = slot_of(cid, cc);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) d[j * BM] = __uint_as_float(r[j]);
+        });
+        __threadfence();  // publish this CTA's partials to the tile's other pairs
+        epi_bar_sync();
+        if (qd == 0 && lane == 0) st_release_gpu(&p.sk_flags[2 * cid + rank], 1u);
+        for (int q = q0; q < q0 + S; ++q)
+          if (q != cid)
+            while (ld_acquire_gpu(&p.sk_flags[2 * q + rank]) == 0) __nanosleep(64);
+        if (tl && qd == 0 && lane == 0) tl[3] = gtime();
+        const int nq = S - 1, nc = c1 - c0;
+        const int depth = kFixSlots / nq < nc ? (kFixSlots / nq > 0 ? kFixSlots / nq : 1) : nc;
+        const bool issuer = qd == 0 && lane == 0;
+        const uint32_t ring = smem_u32(smem);
+        auto issue = [&](int ci) {
+          for (int i = 0; i < nq; ++i) {
+            const int q = q0 + i + (i >= sidx ? 1 : 0);
+            const int jb = ci * nq + i, slot = jb % kFixSlots;
+            mbar_arrive_expect_tx(&fixb[slot], kFixChunkBytes);
+            bulk_g2s(ring + slot * kFixChunkBytes, slot_of(q, c0 + ci) - r_in, kFixChunkBytes,
+                     &fixb[slot]);
+          }
+        };
+        if (issuer) {
+          fence_proxy_async_global();  // acquired partials (generic writes) -> async-proxy reads
+          for (int ci = 0; ci < depth; ++ci) issue(ci);
+        }
+        for (int ci = 0; ci < nc; ++ci) {
+          const int cc = c0 + ci;
+          uint32_t own[32], r[32];
+          tmem_ld_32x32b_x32(taddr + cc * 32, own);
+          tc_wait_ld();
+          for (int qi = 0; qi < S; ++qi) {  // pair order
+            if (qi == sidx) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                r[j] = qi == 0 ? own[j]
+                               : __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(own[j]));
+            } else {
+              const int i = qi - (qi > sidx ? 1 : 0);
+              const int jb = ci * nq + i, slot = jb % kFixSlots;
+              mbar_wait(&fixb[slot], static_cast<uint32_t>(jb / kFixSlots) & 1u);
+              const float* src =
+                  reinterpret_cast<const float*>(smem + slot * kFixChunkBytes) + r_in;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                r[j] = qi == 0 ? __float_as_uint(src[j * BM])
+                               : __float_as_uint(__uint_as_float(r[j]) + src[j * BM]);
+            }
+          }
+          store_chunk(r, cc);
+          epi_bar_sync();  // every epilogue thread is done with this chunk's slots
+          if (issuer && ci + depth < nc) issue(ci + depth);
+        }
+      } else if (contrib) {
         drain([&](uint32_t(&r)[32], int cc) {
           if (!row_ok) return;
           float* d = slot_of(cid, cc);
@@ -502,6 +608,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         __threadfence();  // publish this CTA's partial to the tile's owner
         epi_bar_sync();
         if (qd == 0 && lane == 0) st_release_gpu(&p.sk_flags[2 * cid + rank], 1u);
+      } else if (q_end > cid + 1 && q_end - cid - 1 <= kFixSlots && sc.count() == 0) {
+        // Stream-K owner of its range's last segment: the operand ring is idle
+        // (every MMA of this CTA has completed), so the contributors' partial
+        // chunks (16 KB each: 32 tokens x 128 rows fp32, contiguous) are staged
+        // into it by bulk copies, D chunks ahead of the drain, and added from
+        // shared memory in pair order. (Loading them straight from L2 in the
+        // drain cost one L2 round trip per (chunk, contributor): ~35 us of fix-up
+        // per launch at cfg1, scripts/timeline.py.)
+        const int nc = q_end - cid - 1;
+        const int depth = kFixSlots / nc < 16 ? kFixSlots / nc : 16;
+        const bool issuer = qd == 0 && lane == 0;
+        const uint32_t ring = smem_u32(smem);
+        auto issue = [&](int cc) {
+          for (int i = 0; i < nc; ++i) {
+            const int jb = cc * nc + i, slot = jb % kFixSlots;
+            mbar_arrive_expect_tx(&fixb[slot], kFixChunkBytes);
+            bulk_g2s(ring + slot * kFixChunkBytes, slot_of(cid + 1 + i, cc) - r_in,
+                     kFixChunkBytes, &fixb[slot]);
+          }
+        };
+        if (issuer) {
+          fence_proxy_async_global();  // acquired partials (generic writes) -> async-proxy reads
+          for (int cc = 0; cc < depth; ++cc) issue(cc);
+        }
+        drain([&](uint32_t(&r)[32], int cc) {
+          for (int i = 0; i < nc; ++i) {  // pair order: deterministic sums
+            const int jb = cc * nc + i, slot = jb % kFixSlots;
+            mbar_wait(&fixb[slot], static_cast<uint32_t>(jb / kFixSlots) & 1u);
+            const float* src = reinterpret_cast<const float*>(smem + slot * kFixChunkBytes) + r_in;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              r[j] = __float_as_uint(__uint_as_float(r[j]) + src[j * BM]);
+          }
+          store_chunk(r, cc);
+          epi_bar_sync();  // every epilogue thread is done with chunk cc's slots
+          if (issuer && cc + depth < 16) issue(cc + depth);
+        });
       } else if (q_end > cid + 1) {
         drain([&](uint32_t(&r)[32], int cc) {
           if (!row_ok) return;
@@ -516,6 +659,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       } else {
         drain([&](uint32_t(&r)[32], int cc) { store_chunk(r, cc); });
       }
+      if (tl && qd == 0 && lane == 0) tl[4] = gtime();
     }
   } else if (warp >= DQ_WARP0) {
     // ------------------------------------------------------------ dequant producers (both CTAs)
@@ -690,6 +834,7 @@ cudaError_t launch2_mo(const GemmMaps& maps, const QWeightDev& q, const GemmArgs
 
 void qgemm2_plan(GemmArgs& p) {
   p.sk_pairs = 0;
+  p.split = 0;
   const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
   const int64_t n_kb = p.n_kb_main + p.n_kb_lora;
   int64_t slots = sm_total() / 2;
@@ -712,6 +857,26 @@ void qgemm2_plan(GemmArgs& p) {
   // per step with whole tiles), so stream-K is kept for the under-filled cases.
   if (mode == 2 && static_cast<double>(tiles) > kSkMaxWaves * static_cast<double>(slots)) return;
   // every pair needs a few k-blocks of its own, so cuts never collide
+  // Split-K (every pair one (tile, k-range) unit, distributed fix-up) when the
+  // tiles leave at least half the pairs idle; MLRA_SK=4 forces it, 1 stream-K.
+  if (mode != 1) {
+    int64_t S = slots / tiles;
+    if (S > n_kb / kSplitMinBlocks) S = n_kb / kSplitMinBlocks;
+    if (S > 16) S = 16;
+    if (S >= 2 && (mode == 4 || 2 * tiles <= slots)) {
+      for (int64_t q = 0; q <= tiles * S; ++q) {
+        const int64_t t = q / S, sp = q % S;
+        int64_t b = n_kb * sp / S;
+        if (b & 1) ++b;  // even offset: a Q-ring stage holds two k-blocks
+        p.sk_tile[q] = static_cast<int>(t);
+        p.sk_off[q] = static_cast<int>(b);
+      }
+      p.sk_pairs = static_cast<int>(tiles * S);
+      p.split = static_cast<int>(S);
+      return;
+    }
+  }
+  if (mode == 4) return;
   const int64_t total = tiles * n_kb;
   int64_t pairs = slots;
   if (total / pairs < kSkMinBlocksPerPair) pairs = total / kSkMinBlocksPerPair;
@@ -726,22 +891,28 @@ void qgemm2_plan(GemmArgs& p) {
 }
 
 // Kernel choice for a GEMM of p.tokens tokens (p's tile extents set, schedule
-// not yet planned). Costs in k-block-waves of the pair kernel, fitted to
-// graph-timed sweeps over m in {512..2048} at the LLaMA-7B shapes
-// (scripts/sk_probe.py): a pair k-block wave ~0.8 us, a 1-CTA k-block wave
-// ~0.6 us (0.75 units), stream-K's partial write + in-order fix-up ~56 units.
-bool qgemm_prefer_pair(const GemmArgs& p0) {
-  if (p0.tokens <= 256) return false;
+// not yet planned). Costs in pair-k-block-wave units, fitted to graph-timed
+// sweeps at the LLaMA-7B shapes (scripts/sk_probe.py): a pair k-block wave
+// ~0.8 us, a 1-CTA k-block wave ~0.6 us (0.75 units) with 256-token tiles and
+// ~0.35 us (0.45 units) with 128-token tiles, stream-K's partial write +
+// in-order fix-up ~56 units, split-K's distributed fix-up ~kSplitFixUnits.
+// Returns 2 (pair), 1 (1-CTA, 256) or 3 (1-CTA, 128).
+int qgemm_choose(const GemmArgs& p0) {
   GemmArgs p = p0;
   qgemm2_plan(p);
   const int64_t sms = sm_total(), slots = sms / 2;
   const double n_kb = static_cast<double>(p.n_kb_main + p.n_kb_lora);
   const int64_t tiles2 = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
   const int64_t tiles1 = (p.m_total / BM) * ((p.tokens + 255) / 256);
-  const double pair = p.sk_pairs ? static_cast<double>(tiles2) * n_kb / p.sk_pairs + 56.0
-                                 : static_cast<double>((tiles2 + slots - 1) / slots) * n_kb;
+  const int64_t tiles3 = (p.m_total / BM) * ((p.tokens + 127) / 128);
+  const double pair = p0.tokens <= 256 ? 1e30
+                      : p.sk_pairs ? static_cast<double>(tiles2) * n_kb / p.sk_pairs +
+                                         (p.split ? kSplitFixUnits : 56.0)
+                                   : static_cast<double>((tiles2 + slots - 1) / slots) * n_kb;
   const double cta1 = static_cast<double>((tiles1 + sms - 1) / sms) * n_kb * 0.75;
-  return cta1 >= 0.95 * pair;
+  const double cta3 = static_cast<double>((tiles3 + sms - 1) / sms) * n_kb * kCost128;
+  if (cta3 < 0.95 * cta1 && cta3 < 0.95 * pair) return 3;
+  return cta1 >= 0.95 * pair ? 2 : 1;
 }
 
 cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& p,

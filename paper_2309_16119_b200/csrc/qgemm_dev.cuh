@@ -11,7 +11,6 @@ namespace mlra {
 namespace qg {
 
 constexpr int BM = 128;
-constexpr int BN = 256;
 constexpr int BK = 64;
 #ifndef MLRA_PROD_NS
 #define MLRA_PROD_NS 128  // backoff of the TMA producers' empty/qempty waits
@@ -27,16 +26,25 @@ constexpr int PROD_NS = MLRA_PROD_NS;
 constexpr int EPI_NS = MLRA_EPI_NS;
 constexpr int MAX_QS = 4;
 constexpr int W_TILE = BM * BK * 2;  // 16 KB
-constexpr int T_TILE = BN * BK * 2;  // 32 KB
+constexpr int T_TILE = 256 * BK * 2;  // 32 KB: the pair kernel's stage (2 x 128 tokens), the 1-CTA kernel's at 256 tokens
 constexpr int EPI_WARP0 = 4;
 constexpr int DQ_WARP0 = 8;
 constexpr int NUM_DQ_WARPS = 8;
 constexpr int NUM_DQ_THREADS = NUM_DQ_WARPS * 32;
 constexpr int NUM_THREADS = (DQ_WARP0 + NUM_DQ_WARPS) * 32;
 constexpr int UNITS_PER_GROUP_THREAD = (BM * BK / 8) / (NUM_DQ_THREADS / 2);  // 8
-constexpr uint32_t TMEM_COLS = 512;
 constexpr int SMEM_LIMIT = 232448;
 constexpr int SMEM_FIXED = 1024 + STAGES * (W_TILE + T_TILE) + 512;
+// 1-CTA kernel with 128-token tiles: half-size activation stages, so a deeper
+// ring (6 stages) fits — at small m its k-block rate is bound by the latency of
+// one stage's round trip (dequant/TMA -> MMA -> commit -> refill), not by MMA.
+#ifndef MLRA_STAGES128
+#define MLRA_STAGES128 6
+#endif
+__host__ __device__ constexpr int qgemm1_stages(int tbn) { return tbn == 128 ? MLRA_STAGES128 : STAGES; }
+__host__ __device__ constexpr int qgemm1_smem_fixed(int tbn) {
+  return 1024 + qgemm1_stages(tbn) * (W_TILE + tbn * BK * 2) + 512;
+}
 
 // Unit u (0..1023) of a stage -> byte offset of its 16-byte chunk inside the
 // SW128 operand tile, plus its position in the packed tile.

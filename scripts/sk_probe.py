@@ -1,6 +1,6 @@
 """Dev tool: fused-GEMM GPU time vs token count under each schedule — pair
 kernel whole tiles (MLRA_SK=0), stream-K (1), cost model (2), and the 1-CTA
-kernel (MLRA_GEMM=1). Each (op, mode) is captured in a CUDA graph of 10
+kernel (MLRA_GEMM=1: 256-token tiles, 3: 128-token tiles) and the cost model's own choice (auto). Each (op, mode) is captured in a CUDA graph of 10
 launches (no host overhead) and the modes are timed round-robin (3 rounds,
 best kept) so clock drift does not favour any order."""
 import json
@@ -13,7 +13,7 @@ import torch
 from paper_2309_16119_b200 import modulora as M
 from scripts.quick_perf import make_layer
 
-MODES = {"sk0": ("2", "0"), "sk1": ("2", "1"), "sk2": ("2", "2"), "cta1": ("1", "2")}
+MODES = {"sk0": ("2", "0"), "sk1": ("2", "1"), "sk2": ("2", "2"), "split": ("2", "4"), "cta1": ("1", "2"), "cta128": ("3", "2"), "auto": ("", "2")}
 ms_list = [int(v) for v in os.environ.get("MS", "512,1024,2048").split(",")]
 shapes = [(4096, 4096, 4), (11008, 4096, 3), (4096, 11008, 3)]
 for d_out, d_in, bits in shapes:
@@ -24,7 +24,11 @@ for d_out, d_in, bits in shapes:
         g = torch.randn(m, d_out, device="cuda").to(torch.bfloat16)
         graphs = {}
         for mode, (gem, sk) in MODES.items():
-            os.environ["MLRA_GEMM"], os.environ["MLRA_SK"] = gem, sk
+            os.environ["MLRA_SK"] = sk
+            if gem:
+                os.environ["MLRA_GEMM"] = gem
+            else:
+                os.environ.pop("MLRA_GEMM", None)
             for op, fn, a in (("fwd", M.lp_forward, x), ("dx", M.lp_backward, g)):
                 fn(ctx, a)
                 torch.cuda.synchronize()

@@ -85,8 +85,8 @@ class Lin:
         dx = M.layer_backward(L, x, xb, dy, dx_dtype=torch.float32)
         da, db = M.grads_of_adapter(L)
         assert torch.equal(dx16, dx.to(torch.bfloat16)), "bf16 dX epilogue != RN(fp32 epilogue)"
-        # dA / dB: fp32 atomics across token ranges -> equal to rounding
-        assert rel_fro(f64(da16), f64(da)) <= 1e-6 and rel_fro(f64(db16), f64(db)) <= 1e-6
+        # dA / dB: ordered (deterministic) reductions -> bitwise equal across runs
+        assert torch.equal(da16, da) and torch.equal(db16, db)
         return y, y16, xb, dx, dx16, da, db
 
     def check(self, x, dy, out, what):
@@ -152,7 +152,7 @@ def test_cfg3_decoder_stack():
         torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("gemm", ["1", "2"])
+@pytest.mark.parametrize("gemm", ["1", "2", "3"])
 def test_multi_wave_whole_tiles(gemm, monkeypatch):
     """more tiles than CTAs (4096² at m=4096: 128 pair tiles over 74
     pairs, 256 1-CTA tiles over 148 CTAs) with whole tiles, LoRA and bias; the
@@ -211,10 +211,10 @@ def test_cfg5_cb2_layer(strategy):
 
 def test_cfg1_single_layer_all_kernels(monkeypatch):
     """cfg1 (4096², 4-bit, r=8, m=512) under the cost-model choice, the forced
-    1-CTA kernel and the forced pair kernel with stream-K."""
+    1-CTA kernel (256- and 128-token tiles) and the forced pair kernel with stream-K."""
     lin = Lin(4096, 4096, 4, 8, seed=500, bias=True)
     x = _act(70, 512, 4096)
     dy = _act(71, 512, 4096)
-    for env in ({}, {"MLRA_GEMM": "1"}, {"MLRA_GEMM": "2", "MLRA_SK": "1"}):
+    for env in ({}, {"MLRA_GEMM": "1"}, {"MLRA_GEMM": "3"}, {"MLRA_GEMM": "2", "MLRA_SK": "1"}):
         _setenv(monkeypatch, env)
         lin.check(x, dy, lin.run(x, dy), f"cfg1 {env}")

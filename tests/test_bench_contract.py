@@ -118,3 +118,22 @@ def test_reference_arm_self_launches_ranks():
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["impl"] == "reference"
+
+
+@pytest.mark.gpu
+def test_bench_gpus_2_runs_two_ranks():
+    """`bench.py --gpus 2` launches two ranks itself and reports
+    n_gpus 2 (on the 1-GPU box both ranks share cuda:0 over gloo); strong
+    scaling splits cfg3's 8192 tokens."""
+    env = dict(os.environ, MLRA_DIST_BACKEND="gloo", MLRA_NO_NUMA_BIND="1")
+    for extra, tok in ((["--workload", "cfg1"], 512), (["--workload", "cfg3", "--scaling", "strong"], 4096)):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps",
+                            "2", "--warmup", "3", "--no-cpu-baseline", "--no-parity"] + extra,
+                           capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+        assert r.returncode == 0, r.stderr[-3000:]
+        lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+        assert len(lines) == 1, r.stdout[-2000:]
+        line = json.loads(lines[0])
+        assert line["n_gpus"] == 2 and line["comm"] == {"backend": "gloo", "nranks": 2}
+        assert line["arm"]["tokens_this_rank"] == tok and line["value"] > 0
+        assert line["scaling"] == ("strong" if "strong" in extra else "weak")

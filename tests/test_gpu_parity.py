@@ -264,11 +264,11 @@ def test_pair_kernel_matches_single_cta(bits, mn, monkeypatch):
     a = to_bf16_dev(orc.bf16_round(orc.gaussian(5, m, rows if mn else cols)))
     outs = []
     monkeypatch.setenv("MLRA_SK", "0")  # whole tiles: same K order as the 1-CTA kernel
-    for mode in ("1", "2"):
+    for mode in ("1", "2", "3"):
         monkeypatch.setenv("MLRA_GEMM", mode)
         f = M.lp_backward if mn else M.lp_forward
         outs.append(f64(f(ctx, a, out_dtype=torch.float32)))
-    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     wbf = deq_bf16_f64(words, rows, cols, bits, 128, sc, z)
     ref = f64(a) @ (wbf if mn else wbf.T)
     assert rel_fro(outs[1], ref) <= 1e-5
@@ -375,3 +375,30 @@ def test_fresh_adapter_equals_base_and_zero_base():
     s = 16.0 / r
     ref = orc.bf16_round(s * f64(xb)) @ orc.bf16_round(f64(zl.adapter.a)).T
     assert rel_fro(f64(yz), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("d_out,d_in,r,m,bias", [(1024, 2816, 16, 700, True), (4096, 4096, 8, 512, False),
+                                                 (512, 1024, 100, 4100, True), (256, 512, 8, 1, True)])
+def test_adapter_gradients_bitwise_reproducible(d_out, d_in, r, m, bias):
+    """the skinny products reduce in a fixed order (no atomics), so
+    xb, dA, dB, dbias, Y and dX are bitwise equal run to run, as the reference's
+    fixed-order loops are (matrix.cpp:81-97; test_train.cpp:328-387 asserts
+    bit-equal training trajectories)."""
+    q, *_ = random_quantized(d_out, d_in, 3, 128, seed=d_out + r)
+    dq = M.DeviceQuantizedMatrix(q)
+    a = (torch.randn(d_out, r, generator=torch.Generator().manual_seed(1)) * 0.02).cuda()
+    b = (torch.randn(d_in, r, generator=torch.Generator().manual_seed(2)) * 0.02).cuda()
+    layer = M.ModuLoraLayer("det", dq, M.LoraAdapter(a, b, r, 16.0),
+                            bias=torch.zeros(d_out).cuda() if bias else None, bias_trainable=bias)
+    x = torch.randn(m, d_in, generator=torch.Generator().manual_seed(3)).to(torch.bfloat16).cuda()
+    dy = torch.randn(m, d_out, generator=torch.Generator().manual_seed(4)).to(torch.bfloat16).cuda()
+    runs = []
+    for _ in range(3):
+        y, xb = M.layer_forward(layer, x)
+        dx = M.layer_backward(layer, x, xb, dy)
+        da, db = (t.clone() for t in M.grads_of_adapter(layer))
+        runs.append((y, xb, dx, da, db, None if layer.grad_bias is None else layer.grad_bias.clone()))
+        torch.cuda.synchronize()
+    for other in runs[1:]:
+        for u, v in zip(runs[0], other):
+            assert (u is None and v is None) or torch.equal(u, v)
