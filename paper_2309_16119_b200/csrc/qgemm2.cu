@@ -41,7 +41,7 @@ constexpr double kSkMinIdleBlocks = 50.0;  // stream-K only when it recovers mor
 constexpr int64_t kSkMinBlocksPerPair = 8;
 constexpr int64_t kSplitMinBlocks = 8;  // split-K: k-blocks per pair at least
 #ifndef MLRA_SPLIT_FIX
-#define MLRA_SPLIT_FIX 10.0
+#define MLRA_SPLIT_FIX 20.0
 #endif
 constexpr double kSplitFixUnits = MLRA_SPLIT_FIX;  // split-K drain + distributed fix-up
 constexpr double kSkMaxWaves = 1.25;  // stream-K only below this many waves of whole tiles
@@ -547,16 +547,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) d[j * BM] = __uint_as_float(r[j]);
         });
-        __threadfence();  // publish this CTA's partials to the tile's other pairs
+        if (tl && qd == 0 && lane == 0) tl[5] = gtime();
+        // publish: bar.sync orders the 128 threads' partial stores before one
+        // thread's gpu-scope release (cumulative); one thread acquires the other
+        // pairs' flags and the second bar.sync passes that on (per-thread fences
+        // and 128 spinning threads cost ~1 + ~3.5 us here)
         epi_bar_sync();
-        if (qd == 0 && lane == 0) st_release_gpu(&p.sk_flags[2 * cid + rank], 1u);
-        for (int q = q0; q < q0 + S; ++q)
-          if (q != cid)
-            while (ld_acquire_gpu(&p.sk_flags[2 * q + rank]) == 0) __nanosleep(64);
-        if (tl && qd == 0 && lane == 0) tl[3] = gtime();
+        const bool issuer = qd == 0 && lane == 0;
+        if (issuer) {
+          st_release_gpu(&p.sk_flags[2 * cid + rank], 1u);
+          if (tl) tl[6] = gtime();
+          for (int q = q0; q < q0 + S; ++q)
+            if (q != cid)
+              while (ld_acquire_gpu(&p.sk_flags[2 * q + rank]) == 0) __nanosleep(32);
+        }
+        epi_bar_sync();
+        if (tl && issuer) tl[3] = gtime();
         const int nq = S - 1, nc = c1 - c0;
         const int depth = kFixSlots / nq < nc ? (kFixSlots / nq > 0 ? kFixSlots / nq : 1) : nc;
-        const bool issuer = qd == 0 && lane == 0;
         const uint32_t ring = smem_u32(smem);
         auto issue = [&](int ci) {
           for (int i = 0; i < nq; ++i) {
@@ -586,6 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               const int i = qi - (qi > sidx ? 1 : 0);
               const int jb = ci * nq + i, slot = jb % kFixSlots;
               mbar_wait(&fixb[slot], static_cast<uint32_t>(jb / kFixSlots) & 1u);
+              if (tl && issuer && ci == 0 && i == nq - 1) tl[7] = gtime();
               const float* src =
                   reinterpret_cast<const float*>(smem + slot * kFixChunkBytes) + r_in;
 #pragma unroll

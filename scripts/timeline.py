@@ -29,7 +29,7 @@ t = buf.view(148, 8).cpu().numpy().astype(np.float64)
 used = t[:, 0] > 0
 t0 = t[used, 0].min()
 rel = np.where(t > 0, (t - t0) / 1e3, np.nan)[used]
-names = ["entry", "mma_done", "last_tfull", "flags_seen", "epi_done"]
+names = ["entry", "mma_done", "last_tfull", "flags_seen", "epi_done", "drained", "published", "chunk0_landed"]
 print(f"{used.sum()} CTAs; times in us from the first entry")
 for k, nm in enumerate(names):
     col = rel[:, k]
@@ -38,5 +38,5 @@ for k, nm in enumerate(names):
         print(f"  {nm:11s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f}  (n={col.size})")
 lead = rel[::2]
 print("per pair (leader): entry mma_done last_tfull flags_seen epi_done")
-for i in range(0, min(len(lead), 74), 6):
+for i in range(0, min(len(lead), 74), 6 if len(sys.argv) < 7 else 1000):
     print(" ", i, " ".join(f"{v:7.2f}" for v in lead[i, :5]))

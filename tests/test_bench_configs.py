@@ -41,7 +41,8 @@ pytestmark = pytest.mark.gpu
 
 ROW = M.MaterializationStrategy.RowMaterialize
 SCHEDULES = {"default": {}, "whole": {"MLRA_SK": "0", "MLRA_GEMM": "2"},
-             "streamk": {"MLRA_SK": "1", "MLRA_GEMM": "2"}}
+             "streamk": {"MLRA_SK": "1", "MLRA_GEMM": "2"},
+             "splitk": {"MLRA_SK": "4", "MLRA_GEMM": "2"}}
 
 
 def _setenv(monkeypatch, env):
@@ -211,10 +212,12 @@ def test_cfg5_cb2_layer(strategy):
 
 def test_cfg1_single_layer_all_kernels(monkeypatch):
     """cfg1 (4096², 4-bit, r=8, m=512) under the cost-model choice, the forced
-    1-CTA kernel (256- and 128-token tiles) and the forced pair kernel with stream-K."""
+    1-CTA kernel (256- and 128-token tiles) and the forced pair kernel with stream-K
+    and with split-K (distributed fix-up)."""
     lin = Lin(4096, 4096, 4, 8, seed=500, bias=True)
     x = _act(70, 512, 4096)
     dy = _act(71, 512, 4096)
-    for env in ({}, {"MLRA_GEMM": "1"}, {"MLRA_GEMM": "3"}, {"MLRA_GEMM": "2", "MLRA_SK": "1"}):
+    for env in ({}, {"MLRA_GEMM": "1"}, {"MLRA_GEMM": "3"}, {"MLRA_GEMM": "2", "MLRA_SK": "1"},
+                {"MLRA_GEMM": "2", "MLRA_SK": "4"}):
         _setenv(monkeypatch, env)
         lin.check(x, dy, lin.run(x, dy), f"cfg1 {env}")
