@@ -563,13 +563,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         epi_bar_sync();
         if (tl && issuer) tl[3] = gtime();
-        const int nq = S - 1, nc = c1 - c0;
-        const int depth = kFixSlots / nq < nc ? (kFixSlots / nq > 0 ? kFixSlots / nq : 1) : nc;
+        // staged slots: kFixSlots - 1 for the others' chunks, the last one is
+        // each thread's private spill of its own row of the current chunk (so
+        // only one 32-register chunk stays live: the kernel runs at the
+        // 128-register cap)
+        const int nq = S - 1, nc = c1 - c0, nslots = kFixSlots - 1;
+        const int depth = nslots / nq < nc ? (nslots / nq > 0 ? nslots / nq : 1) : nc;
         const uint32_t ring = smem_u32(smem);
+        float* own_row = reinterpret_cast<float*>(smem + nslots * kFixChunkBytes) + r_in;
         auto issue = [&](int ci) {
           for (int i = 0; i < nq; ++i) {
             const int q = q0 + i + (i >= sidx ? 1 : 0);
-            const int jb = ci * nq + i, slot = jb % kFixSlots;
+            const int jb = ci * nq + i, slot = jb % nslots;
             mbar_arrive_expect_tx(&fixb[slot], kFixChunkBytes);
             bulk_g2s(ring + slot * kFixChunkBytes, slot_of(q, c0 + ci) - r_in, kFixChunkBytes,
                      &fixb[slot]);
@@ -581,27 +586,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         for (int ci = 0; ci < nc; ++ci) {
           const int cc = c0 + ci;
-          uint32_t own[32], r[32];
-          tmem_ld_32x32b_x32(taddr + cc * 32, own);
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + cc * 32, r);
           tc_wait_ld();
-          for (int qi = 0; qi < S; ++qi) {  // pair order
-            if (qi == sidx) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                r[j] = qi == 0 ? own[j]
-                               : __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(own[j]));
+          for (int j = 0; j < 32; ++j) own_row[j * BM] = __uint_as_float(r[j]);
+          for (int qi = 0; qi < S; ++qi) {  // pair order
+            const float* src;
+            if (qi == sidx) {
+              src = own_row;
             } else {
               const int i = qi - (qi > sidx ? 1 : 0);
-              const int jb = ci * nq + i, slot = jb % kFixSlots;
-              mbar_wait(&fixb[slot], static_cast<uint32_t>(jb / kFixSlots) & 1u);
+              const int jb = ci * nq + i, slot = jb % nslots;
+              mbar_wait(&fixb[slot], static_cast<uint32_t>(jb / nslots) & 1u);
               if (tl && issuer && ci == 0 && i == nq - 1) tl[7] = gtime();
-              const float* src =
-                  reinterpret_cast<const float*>(smem + slot * kFixChunkBytes) + r_in;
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                r[j] = qi == 0 ? __float_as_uint(src[j * BM])
-                               : __float_as_uint(__uint_as_float(r[j]) + src[j * BM]);
+              src = reinterpret_cast<const float*>(smem + slot * kFixChunkBytes) + r_in;
             }
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              r[j] = qi == 0 ? __float_as_uint(src[j * BM])
+                             : __float_as_uint(__uint_as_float(r[j]) + src[j * BM]);
           }
           store_chunk(r, cc);
           epi_bar_sync();  // every epilogue thread is done with this chunk's slots
