@@ -41,14 +41,15 @@ constexpr double kSkMinIdleBlocks = 50.0;  // stream-K only when it recovers mor
 constexpr int64_t kSkMinBlocksPerPair = 8;
 constexpr int64_t kSplitMinBlocks = 8;  // split-K: k-blocks per pair at least
 #ifndef MLRA_SPLIT_FIX
-#define MLRA_SPLIT_FIX 20.0
+#define MLRA_SPLIT_FIX 24.0
 #endif
 constexpr double kSplitFixUnits = MLRA_SPLIT_FIX;  // split-K drain + distributed fix-up
 constexpr double kSkMaxWaves = 1.25;  // stream-K only below this many waves of whole tiles
 #ifndef MLRA_COST128
-#define MLRA_COST128 0.45
+#define MLRA_COST128 0.85
 #endif
 constexpr double kCost128 = MLRA_COST128;  // 1-CTA 128-token k-block wave, pair units
+constexpr double kCost256 = 0.8;           // 1-CTA 256-token k-block wave, pair units
 constexpr uint32_t TMEM_COLS = 512;  // two N=256 accumulators
 constexpr int kFixChunkBytes = 32 * 128 * 4;  // one stream-K partial chunk: 32 tokens x 128 rows
 constexpr int kFixSlots = STAGES * (W_TILE + T_TILE) / kFixChunkBytes;  // staged in the idle ring
@@ -906,8 +907,10 @@ void qgemm2_plan(GemmArgs& p) {
 // Kernel choice for a GEMM of p.tokens tokens (p's tile extents set, schedule
 // not yet planned). Costs in pair-k-block-wave units, fitted to graph-timed
 // sweeps at the LLaMA-7B shapes (scripts/sk_probe.py): a pair k-block wave
-// ~0.8 us, a 1-CTA k-block wave ~0.6 us (0.75 units) with 256-token tiles and
-// ~0.35 us (0.45 units) with 128-token tiles, stream-K's partial write +
+// ~0.8 us, a 1-CTA k-block wave ~0.6-0.7 us (0.8 units) with 256-token tiles
+// and ~0.7 us (0.85 units) with 128-token tiles — the 1-CTA MMA is bound by
+// shared-memory operand traffic (A 4 KB + B N·32 B per 16-deep step), not by N
+// — stream-K's partial write +
 // in-order fix-up ~56 units, split-K's distributed fix-up ~kSplitFixUnits.
 // Returns 2 (pair), 1 (1-CTA, 256) or 3 (1-CTA, 128).
 int qgemm_choose(const GemmArgs& p0) {
@@ -918,11 +921,11 @@ int qgemm_choose(const GemmArgs& p0) {
   const int64_t tiles2 = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
   const int64_t tiles1 = (p.m_total / BM) * ((p.tokens + 255) / 256);
   const int64_t tiles3 = (p.m_total / BM) * ((p.tokens + 127) / 128);
-  const double pair = p0.tokens <= 256 ? 1e30
+  const double pair = (p0.tokens <= 256 && !p.split) ? 1e30  // half-empty 512-token tiles
                       : p.sk_pairs ? static_cast<double>(tiles2) * n_kb / p.sk_pairs +
                                          (p.split ? kSplitFixUnits : 56.0)
                                    : static_cast<double>((tiles2 + slots - 1) / slots) * n_kb;
-  const double cta1 = static_cast<double>((tiles1 + sms - 1) / sms) * n_kb * 0.75;
+  const double cta1 = static_cast<double>((tiles1 + sms - 1) / sms) * n_kb * kCost256;
   const double cta3 = static_cast<double>((tiles3 + sms - 1) / sms) * n_kb * kCost128;
   if (cta3 < 0.95 * cta1 && cta3 < 0.95 * pair) return 3;
   return cta1 >= 0.95 * pair ? 2 : 1;
