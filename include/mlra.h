@@ -165,6 +165,34 @@ MLRA_API mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group_s
                                      const uint16_t* codes, const float* codebook,
                                      const float* scales, void* stream, mlra_qweight** out);
 
+/* Built-in plugin "e8p": QuIP#'s E8P lattice codebook (2 bits/weight) in the
+ * cb2 stream format — one u16 per 8 consecutive row entries: bits 0-7 index
+ * the 256-pattern abs table (mlra_e8p_abs_table), bits 8-14 negate entries
+ * 0-6, entry 7's sign makes the negation count congruent to the pattern's
+ * coordinate sum (mod 2: the point lies in E8's half-integer coset), bit 15
+ * shifts every entry by +1/4 (set) or -1/4 — and one f32 scale per (row,
+ * group). Ŵ = RN_f32(s · value) with value = sign·|a| + shift (exact in bf16).
+ * Decoded inside the fused GEMM (Q ring) for whole 256-multiples, through its
+ * hook otherwise. Reference: none (the interface must host
+ * such plugins; the decode law is pinned by oracle/mlra_oracle.c). */
+MLRA_API mlra_status mlra_e8p_create(int64_t rows, int64_t cols, int64_t group_size,
+                                     const uint16_t* codes, const float* scales, void* stream,
+                                     mlra_qweight** out);
+/* The E8P abs-pattern table (256 x 8 f32, row-major) and its 256 odd bits
+ * (8 words); returns 256. Either pointer may be NULL. */
+MLRA_API int mlra_e8p_abs_table(float* abs_out, uint32_t* odd_out);
+
+/* Block randomized Hadamard transform of bf16 activations [rows x cols] (QuIP#'s
+ * incoherence processing): per block of `block` columns
+ * (a power of two in [64, 1024] dividing cols), inverse = 0: out = H·diag(s)·in
+ * / sqrt(block); inverse = 1: out = diag(s)·H·in / sqrt(block) (H symmetric, so
+ * the two are each other's inverse). signs: device f32 [cols] of +-1. out is
+ * bf16 or f32 with leading dimension ld_out. A layer quantized in the rotated
+ * basis W~ = U W V^T runs y = U^T(W~(V x)), dx = V^T(W~^T(U dy)). */
+MLRA_API mlra_status mlra_rht(const void* in, int64_t rows, int64_t cols, int64_t ld_in,
+                              const float* signs, int inverse, int block, void* out,
+                              int64_t ld_out, mlra_dtype out_dtype, void* stream);
+
 /* Built-in "lut" plugin (non-uniform levels, e.g. QLoRA's NF4; a plugin behind
  * the reference's Quantizer interface, quantize.hpp:91-106, like cb2): codes
  * in the reference's b-bit bitstream (bitpack.cpp:25-35; words / word_count as

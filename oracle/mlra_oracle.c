@@ -302,6 +302,78 @@ ORC_EXPORT void orc_cb2_dequant_f32(const uint16_t* codes, uint64_t rows, uint64
   }
 }
 
+/* The built-in plugin "e8p" (include/mlra.h mlra_e8p_create): QuIP#'s E8P
+ * lattice codebook. Parity status: the reference ships no such plugin
+ * (SPEC.md:8, :251), so this restatement of the decode law is pinned by the
+ * hand-derived known answers and the lattice-membership checks of
+ * tests/test_e8p.py, not by reference output.
+ *
+ * Abs table: (i) every vector of {1/2, 3/2, 5/2}^8 with squared norm <= 10 in
+ * lexicographic order of 2|a| (227), then (ii) the 29 norm-12 patterns of
+ * {1/2, 3/2}^8 listed below (QuIP#'s E8P12 construction: 256 patterns). A code
+ * (one u16 per 8 row entries): bits 0-7 pattern index, bits 8-14 negate entries
+ * 0-6, entry 7 negated iff (number of negations among 0-6 + the pattern's
+ * coordinate sum) is odd, bit 15 = +1/4 shift (else -1/4). Then
+ *   out[i, 8u+j] = RN_f32(s[i, (8u+j)/g] * (sign_j * a_j + shift)). */
+static const uint8_t ORC_E8P_NORM12[29][8] = {
+    {3, 1, 1, 1, 3, 3, 3, 3}, {1, 3, 1, 1, 3, 3, 3, 3}, {1, 1, 3, 1, 3, 3, 3, 3},
+    {1, 1, 1, 3, 3, 3, 3, 3}, {3, 3, 3, 1, 3, 3, 1, 1}, {3, 3, 3, 1, 3, 1, 3, 1},
+    {3, 3, 3, 1, 1, 3, 3, 1}, {3, 3, 3, 1, 3, 1, 1, 3}, {3, 3, 3, 1, 1, 3, 1, 3},
+    {3, 3, 3, 1, 1, 1, 3, 3}, {3, 3, 1, 3, 3, 3, 1, 1}, {3, 3, 1, 3, 3, 1, 3, 1},
+    {3, 3, 1, 3, 1, 3, 3, 1}, {3, 3, 1, 3, 3, 1, 1, 3}, {3, 3, 1, 3, 1, 3, 1, 3},
+    {3, 3, 1, 3, 1, 1, 3, 3}, {3, 1, 3, 3, 3, 3, 1, 1}, {3, 1, 3, 3, 3, 1, 3, 1},
+    {3, 1, 3, 3, 1, 3, 3, 1}, {3, 1, 3, 3, 3, 1, 1, 3}, {3, 1, 3, 3, 1, 3, 1, 3},
+    {1, 3, 3, 3, 1, 1, 3, 3}, {1, 3, 3, 3, 3, 3, 1, 1}, {1, 3, 3, 3, 3, 1, 3, 1},
+    {1, 3, 3, 3, 1, 3, 3, 1}, {1, 3, 3, 3, 3, 1, 1, 3}, {1, 3, 3, 3, 1, 3, 1, 3},
+    {1, 1, 3, 3, 1, 3, 3, 3}, {3, 3, 1, 1, 3, 3, 3, 1}};
+
+/* 2|a| of the 256 patterns, row-major (the oracle's own enumeration). */
+ORC_EXPORT void orc_e8p_abs_table(int32_t* twice_abs) {
+  int n = 0;
+  for (int d0 = 1; d0 <= 5; d0 += 2)
+  for (int d1 = 1; d1 <= 5; d1 += 2)
+  for (int d2 = 1; d2 <= 5; d2 += 2)
+  for (int d3 = 1; d3 <= 5; d3 += 2)
+  for (int d4 = 1; d4 <= 5; d4 += 2)
+  for (int d5 = 1; d5 <= 5; d5 += 2)
+  for (int d6 = 1; d6 <= 5; d6 += 2)
+  for (int d7 = 1; d7 <= 5; d7 += 2) {
+    const int d[8] = {d0, d1, d2, d3, d4, d5, d6, d7};
+    int norm4 = 0;
+    for (int j = 0; j < 8; ++j) norm4 += d[j] * d[j];
+    if (norm4 > 40) continue;
+    for (int j = 0; j < 8; ++j) twice_abs[n * 8 + j] = d[j];
+    ++n;
+  }
+  for (int i = 0; i < 29; ++i, ++n)
+    for (int j = 0; j < 8; ++j) twice_abs[n * 8 + j] = ORC_E8P_NORM12[i][j];
+}
+
+ORC_EXPORT void orc_e8p_dequant_f32(const uint16_t* codes, uint64_t rows, uint64_t cols,
+                                    uint64_t group, const float* scales, float* out) {
+  int32_t t[256 * 8];
+  orc_e8p_abs_table(t);
+  const uint64_t ng = cols / group, cpr = cols / 8;
+  for (uint64_t i = 0; i < rows; ++i) {
+    for (uint64_t u = 0; u < cpr; ++u) {
+      const uint32_t code = codes[i * cpr + u];
+      const int32_t* a2 = t + (code & 0xFFu) * 8;
+      int sum2 = 0, flips = 0;
+      for (int j = 0; j < 8; ++j) sum2 += a2[j];
+      for (int j = 0; j < 7; ++j) flips += (code >> (8 + j)) & 1u;
+      const int neg7 = ((flips + sum2 / 2) & 1);  /* even total flips + coordinate sum */
+      for (int j = 0; j < 8; ++j) {
+        const int neg = j < 7 ? (int)((code >> (8 + j)) & 1u) : neg7;
+        /* value in quarters: sign * 2|a| * 2 +- 1, exact */
+        const int q4 = (neg ? -2 * a2[j] : 2 * a2[j]) + ((code >> 15) ? 1 : -1);
+        const float v = (float)q4 * 0.25f;
+        const float s = scales[i * ng + (8 * u + (uint64_t)j) / group];
+        out[i * cols + 8 * u + j] = s * v;
+      }
+    }
+  }
+}
+
 /* The built-in "lut" plugin (include/mlra.h mlra_lut_create; e.g. QLoRA's NF4):
  * codes in the reference's bitstream (bitpack.cpp:25-35), a per-matrix table of
  * 2^bits f32 levels and a per-(row, group) f32 scale:

@@ -80,6 +80,12 @@ class _Lib:
             lib.orc_adamw_step.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, _u64,
                                            C.c_double, _u64, _f64p, _f64p, _f64p, _f64p]
             lib.orc_lut_dequant_f32.argtypes = [_u32p, _u64, _u64, _int, _u64, _f32p, _f32p, _f32p]
+            lib.orc_e8p_abs_table.argtypes = [C.c_void_p]
+            lib.orc_e8p_abs_table.restype = None
+            lib.orc_e8p_dequant_f32.argtypes = [
+                np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS"), _u64, _u64, _u64, _f32p,
+                _f32p]
+            lib.orc_e8p_dequant_f32.restype = None
             cls._lib = lib
         return cls._lib
 
@@ -419,6 +425,22 @@ def cb2_dequantize_f32(codes, rows: int, cols: int, group: int, codebook, scales
     out = np.empty(rows * cols, np.float32)
     _Lib.get().orc_cb2_dequant_f32(_c(codes, np.uint16).ravel(), rows, cols, group,
                                    _c(codebook, np.float32).ravel(),
+                                   _c(scales, np.float32).ravel(), out)
+    return out.reshape(rows, cols)
+
+
+# --- e8p plugin decode law (include/mlra.h mlra_e8p_create) -------------------
+def e8p_abs_table() -> np.ndarray:
+    """orc_e8p_abs_table: the 256 E8P abs patterns, 2|a| as int32 [256, 8]."""
+    t = np.empty(256 * 8, np.int32)
+    _Lib.get().orc_e8p_abs_table(t.ctypes.data_as(C.c_void_p))
+    return t.reshape(256, 8)
+
+
+def e8p_dequantize_f32(codes, rows: int, cols: int, group: int, scales) -> np.ndarray:
+    """orc_e8p_dequant_f32: RN_f32(s * (sign * |a| +- 1/4)) per entry."""
+    out = np.empty(rows * cols, np.float32)
+    _Lib.get().orc_e8p_dequant_f32(_c(codes, np.uint16).ravel(), rows, cols, group,
                                    _c(scales, np.float32).ravel(), out)
     return out.reshape(rows, cols)
 

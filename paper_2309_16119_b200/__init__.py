@@ -7,7 +7,8 @@ from ._lib import MlraError, build, lib  # noqa: F401
 from .ledger import (  # noqa: F401
     LayerDims, LedgerEvent, LedgerReport, MemoryLedger, Phase, ledger_assert_single_materialization)
 from .modulora import (  # noqa: F401
-    Cb2Matrix, Codebook2Quantizer, DeviceQuantizedMatrix, DoublingQuantizer, LoraAdapter,
+    Cb2Matrix, Codebook2Quantizer, DeviceQuantizedMatrix, DoublingQuantizer, E8pMatrix,
+    E8pQuantizer, IncoherentLayer, LoraAdapter, e8p_abs_table, e8p_decode, random_signs, rht,
     LpLinearContext, LpLinearFunction, LutMatrix, LutQuantizer, MaterializationStrategy, NF4_LEVELS, OptqQuantizer, ModuLoraLayer, ModuLoraLinearFunction, PackedCodes,
     QuantizedMatrix, QuantizerHook, RtnQuantizer, default_cb2_codebook, dequantize,
     dequantize_row, dequantize_tile, grads_of_adapter, init_adapter, layer_backward, layer_forward,

@@ -32,7 +32,7 @@ EXPORTS = [
     "mlra_checkpoint_adapter", "mlra_checkpoint_assemble_check", "mlra_quantize_rtn",
     "mlra_dp_unique_id", "mlra_dp_init", "mlra_allreduce_lora_grads", "mlra_dp_destroy",
     "mlra_mix_seed", "mlra_gaussian_fill", "mlra_lut_create", "mlra_optq_workspace",
-    "mlra_quantize_optq",
+    "mlra_quantize_optq", "mlra_e8p_create", "mlra_e8p_abs_table", "mlra_rht",
 ]
 
 # mlra_hook.materialize(state, q, row0, nrows, col0, ncols, out, dtype, ld, stream)
@@ -131,6 +131,12 @@ def lib() -> C.CDLL:
                                                  C.POINTER(vp)]
         L.mlra_cb2_create.restype = i32
         L.mlra_cb2_create.argtypes = [i64, i64, i64, vp, vp, vp, vp, C.POINTER(vp)]
+        L.mlra_e8p_create.restype = i32
+        L.mlra_e8p_create.argtypes = [i64, i64, i64, vp, vp, vp, C.POINTER(vp)]
+        L.mlra_e8p_abs_table.restype = C.c_int
+        L.mlra_e8p_abs_table.argtypes = [vp, vp]
+        L.mlra_rht.restype = i32
+        L.mlra_rht.argtypes = [vp, i64, i64, i64, vp, C.c_int, C.c_int, vp, i64, C.c_int, vp]
         L.mlra_optq_workspace.restype = i32
         L.mlra_optq_workspace.argtypes = [vp, i64, i64, C.c_double, vp, vp, vp]
         L.mlra_quantize_optq.restype = i32

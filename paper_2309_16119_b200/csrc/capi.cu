@@ -212,6 +212,7 @@ struct GemmPlan {
   bool out_f32;
   const float* bias = nullptr;
   const void* cb2_codebook = nullptr;  // fused cb2 plugin decode (pair kernel, Q ring)
+  int e8p = 0;                         // with cb2_codebook: the e8p plugin's decode
   const float* lut = nullptr;          // fused lut plugin decode (pair kernel, Q ring)
 };
 
@@ -241,6 +242,7 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
   // the cost model; MLRA_GEMM=1|2|3 forces the 1-CTA (256) / pair / 1-CTA (128)
   // kernel (tests cover all three).
   a.cb2_codebook = gp.cb2_codebook;
+  a.e8p = gp.e8p;
   a.lut = gp.lut;
   int kind = mlra::qgemm_choose(a);
   if (const char* force = getenv("MLRA_GEMM")) kind = atoi(force);
@@ -274,7 +276,8 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
     a.q_stage_bytes = static_cast<int>(round_up(a.q_codes_bytes + a.q_grid_bytes, 128));
     a.q_stages = mlra::qgemm_max_q_stages(
         a.q_stage_bytes,
-        gp.cb2_codebook ? mlra::kCb2SmemBytes : (gp.lut ? mlra::kLutSmemBytes : 0));
+        gp.cb2_codebook ? (gp.e8p ? mlra::kE8pSmemBytes : mlra::kCb2SmemBytes)
+                        : (gp.lut ? mlra::kLutSmemBytes : 0));
     a.q_group_shift = g < 128 ? (g == 32 ? 5 : 6) : -1;
     a.q_group_div128 = g >= 128 ? static_cast<int>(g / 128) : 1;
     {
@@ -405,6 +408,7 @@ mlra_status run_gemm(const mlra_qweight* q, mlra_strategy strategy, const mlra_h
       !(strategy == MLRA_MATVEC && ctx_hook) && getenv("MLRA_CB2_HOOK") == nullptr) {
     GemmPlan g2 = gp;
     g2.cb2_codebook = q->cb2.codebook;
+    g2.e8p = q->cb2.e8p;
     return run_gemm_d(q->cb2_d, nullptr, 0, g2, sc);
   }
   if (const mlra_hook* hk = pick_hook(q, strategy, ctx_hook))
@@ -570,6 +574,131 @@ mlra_status side_stream(SideStream** out) {
   return MLRA_OK;
 }
 
+
+// The E8P abs-pattern table (QuIP#'s E8P12 construction): (i) every vector in
+// {1/2, 3/2, 5/2}^8 with squared norm <= 10, in lexicographic order of 2|a|
+// (227 patterns), then (ii) 29 patterns of squared norm 12 with entries in
+// {1/2, 3/2}; odd bit i = the coordinate sum of pattern i is odd. Restated in
+// oracle/mlra_oracle.c (orc_e8p_abs_table).
+void e8p_abs_table(float (*a)[8], uint32_t* odd) {
+  static const uint8_t kNorm12[29][8] = {
+      {3, 1, 1, 1, 3, 3, 3, 3}, {1, 3, 1, 1, 3, 3, 3, 3}, {1, 1, 3, 1, 3, 3, 3, 3},
+      {1, 1, 1, 3, 3, 3, 3, 3}, {3, 3, 3, 1, 3, 3, 1, 1}, {3, 3, 3, 1, 3, 1, 3, 1},
+      {3, 3, 3, 1, 1, 3, 3, 1}, {3, 3, 3, 1, 3, 1, 1, 3}, {3, 3, 3, 1, 1, 3, 1, 3},
+      {3, 3, 3, 1, 1, 1, 3, 3}, {3, 3, 1, 3, 3, 3, 1, 1}, {3, 3, 1, 3, 3, 1, 3, 1},
+      {3, 3, 1, 3, 1, 3, 3, 1}, {3, 3, 1, 3, 3, 1, 1, 3}, {3, 3, 1, 3, 1, 3, 1, 3},
+      {3, 3, 1, 3, 1, 1, 3, 3}, {3, 1, 3, 3, 3, 3, 1, 1}, {3, 1, 3, 3, 3, 1, 3, 1},
+      {3, 1, 3, 3, 1, 3, 3, 1}, {3, 1, 3, 3, 3, 1, 1, 3}, {3, 1, 3, 3, 1, 3, 1, 3},
+      {1, 3, 3, 3, 1, 1, 3, 3}, {1, 3, 3, 3, 3, 3, 1, 1}, {1, 3, 3, 3, 3, 1, 3, 1},
+      {1, 3, 3, 3, 1, 3, 3, 1}, {1, 3, 3, 3, 3, 1, 1, 3}, {1, 3, 3, 3, 1, 3, 1, 3},
+      {1, 1, 3, 3, 1, 3, 3, 3}, {3, 3, 1, 1, 3, 3, 3, 1}};
+  int n = 0;
+  for (int c = 0; c < 6561 && n < 227; ++c) {  // base-3 digits, most significant first
+    int d[8], v = c, norm4 = 0;
+    for (int j = 7; j >= 0; --j) {
+      d[j] = 2 * (v % 3) + 1;  // 1, 3, 5 = 2|a|
+      v /= 3;
+      norm4 += d[j] * d[j];
+    }
+    if (norm4 > 40) continue;
+    for (int j = 0; j < 8; ++j) a[n][j] = 0.5f * static_cast<float>(d[j]);
+    ++n;
+  }
+  for (int i = 0; i < 29; ++i, ++n)
+    for (int j = 0; j < 8; ++j) a[n][j] = 0.5f * static_cast<float>(kNorm12[i][j]);
+  for (int w = 0; w < 8; ++w) odd[w] = 0u;
+  for (int i = 0; i < 256; ++i) {
+    int twice = 0;  // 2 * coordinate sum
+    for (int j = 0; j < 8; ++j) twice += static_cast<int>(2.0f * a[i][j]);
+    if ((twice / 2) & 1) odd[i >> 5] |= 1u << (i & 31);
+  }
+}
+
+// Shared by the codebook plugins (cb2, e8p): validation, an opaque qweight whose
+// hook is k_cb2_materialize, the device codebook/codes/scales upload and, for
+// whole 256-multiples, the fused Q-ring view of the u16 code stream.
+mlra_status codebook_qweight_create(const char* name, int64_t rows, int64_t cols, int64_t group,
+                                    const uint16_t* codes, const std::vector<uint32_t>& cbdev,
+                                    bool cb16, bool e8p, const float* scales, void* stream,
+                                    mlra_qweight** out) {
+  if (!out) return fail(MLRA_ERR_CONTRACT, "null output handle");
+  *out = nullptr;
+  if (rows <= 0 || cols <= 0 || cols % 8 != 0)
+    return fail(MLRA_ERR_CONFIG, "%s: cols %lld must be a positive multiple of 8", name,
+                (long long)cols);
+  if (group <= 0 || group % 8 != 0 || cols % group != 0)
+    return fail(MLRA_ERR_CONFIG, "%s: group size %lld must be a multiple of 8 dividing cols %lld",
+                name, (long long)group, (long long)cols);
+  if (!codes || !scales) return fail(MLRA_ERR_CONTRACT, "%s: null buffers", name);
+  const int64_t ng = rows * (cols / group);
+  for (int64_t i = 0; i < ng; ++i)
+    if (!(scales[i] > 0.0f)) return fail(MLRA_ERR_NUMERIC, "%s: non-positive scale", name);
+  if (mlra_status st = check_device()) return st;
+  static const auto kHookFn = [](void*, const mlra_qweight* q, int64_t row0, int64_t nrows,
+                                 int64_t col0, int64_t ncols, void* o, mlra_dtype dtype,
+                                 int64_t ld, void* st) -> mlra_status {
+    if (col0 % 8 != 0 || ncols % 8 != 0)
+      return fail(MLRA_ERR_RANGE, "%s: tile columns must be 8-aligned", q->hook_name.c_str());
+    CUDA_TRY(mlra::launch_cb2_materialize(q->cb2, row0, nrows, col0, ncols, o, ld,
+                                          dtype == MLRA_F32, static_cast<cudaStream_t>(st)));
+    return MLRA_OK;
+  };
+  static const mlra_hook kCb2Hook = {"cb2", nullptr, kHookFn};
+  static const mlra_hook kE8pHook = {"e8p", nullptr, kHookFn};
+  mlra_qweight* q = nullptr;
+  if (mlra_status st = mlra_qweight_create_opaque(rows, cols, 2, e8p ? &kE8pHook : &kCb2Hook, &q))
+    return st;
+  const size_t cb_bytes = cbdev.size() * 4, code_bytes = static_cast<size_t>(rows * (cols / 8)) * 2,
+               sc_bytes = static_cast<size_t>(ng) * 4;
+  const size_t off_codes = cb_bytes, off_sc = round_up(off_codes + code_bytes, 16);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMalloc(&q->cb2_mem, off_sc + sc_bytes);
+  char* base = static_cast<char*>(q->cb2_mem);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(base, cbdev.data(), cb_bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(base + off_codes, codes, code_bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(base + off_sc, scales, sc_bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    mlra_qweight_destroy(q);
+    return fail(MLRA_ERR_CUDA, "%s upload: %s", name, cudaGetErrorString(e));
+  }
+  q->device_bytes = off_sc + sc_bytes;
+  q->d.group = group;
+  // fused path: whole 256-multiples (the u16 codes are then the row-aligned 2-bit
+  // stream the Q ring tiles), a bf16-exact codebook, a group the Q ring supports
+  const bool g_ok = group == 32 || group == 64 || group % 128 == 0;
+  if (cb16 && g_ok && rows % 256 == 0 && cols % 256 == 0) {
+    QWeightDev& fd = q->cb2_d;
+    fd.rows = fd.rows_pad = rows;
+    fd.cols = fd.cols_pad = cols;
+    fd.bits = 2;
+    fd.group = group;
+    fd.ng_pad = round_up(cols / group, 2);
+    fd.row_words = cols / 16;
+    fd.words = reinterpret_cast<const uint32_t*>(base + off_codes);
+    std::vector<float2> g(static_cast<size_t>(rows * fd.ng_pad), make_float2(1.0f, 0.0f));
+    for (int64_t i = 0; i < rows; ++i)
+      for (int64_t j = 0; j < cols / group; ++j)
+        g[static_cast<size_t>(i * fd.ng_pad + j)] = make_float2(scales[i * (cols / group) + j], 0.0f);
+    e = cudaMalloc(&q->cb2_grid, g.size() * sizeof(float2));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(q->cb2_grid, g.data(), g.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      mlra_qweight_destroy(q);
+      return fail(MLRA_ERR_CUDA, "%s grid upload: %s", name, cudaGetErrorString(e));
+    }
+    fd.grid = q->cb2_grid;
+    q->device_bytes += g.size() * sizeof(float2);
+    q->cb2_fused = true;
+  }
+  q->cb2 = mlra::Cb2Dev{rows, cols, group, cols / group,
+                        reinterpret_cast<const uint16_t*>(base + off_codes), base, cb16 ? 1 : 0,
+                        reinterpret_cast<const float*>(base + off_sc), e8p ? 1 : 0};
+  *out = q;
+  return MLRA_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -731,34 +860,10 @@ mlra_status mlra_qweight_create_opaque(int64_t rows, int64_t cols, int bits,
 mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group, const uint16_t* codes,
                             const float* codebook, const float* scales, void* stream,
                             mlra_qweight** out) {
-  if (!out) return fail(MLRA_ERR_CONTRACT, "null output handle");
-  *out = nullptr;
-  if (rows <= 0 || cols <= 0 || cols % 8 != 0)
-    return fail(MLRA_ERR_CONFIG, "cb2: cols %lld must be a positive multiple of 8",
-                (long long)cols);
-  if (group <= 0 || group % 8 != 0 || cols % group != 0)
-    return fail(MLRA_ERR_CONFIG, "cb2: group size %lld must be a multiple of 8 dividing cols %lld",
-                (long long)group, (long long)cols);
-  if (!codes || !codebook || !scales) return fail(MLRA_ERR_CONTRACT, "cb2: null buffers");
-  const int64_t ng = rows * (cols / group);
-  for (int64_t i = 0; i < ng; ++i)
-    if (!(scales[i] > 0.0f)) return fail(MLRA_ERR_NUMERIC, "cb2: non-positive scale");
+  if (!codebook) return fail(MLRA_ERR_CONTRACT, "cb2: null buffers");
   for (int i = 0; i < 256 * 8; ++i)
     if (!(codebook[i] >= 0.0f) || codebook[i] > 3.4e38f)
       return fail(MLRA_ERR_NUMERIC, "cb2: codebook magnitudes must be finite and >= 0");
-  if (mlra_status st = check_device()) return st;
-  static const mlra_hook kCb2Hook = {
-      "cb2", nullptr,
-      [](void*, const mlra_qweight* q, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols,
-         void* o, mlra_dtype dtype, int64_t ld, void* st) -> mlra_status {
-        if (col0 % 8 != 0 || ncols % 8 != 0)
-          return fail(MLRA_ERR_RANGE, "cb2: tile columns must be 8-aligned");
-        CUDA_TRY(mlra::launch_cb2_materialize(q->cb2, row0, nrows, col0, ncols, o, ld,
-                                              dtype == MLRA_F32, static_cast<cudaStream_t>(st)));
-        return MLRA_OK;
-      }};
-  mlra_qweight* q = nullptr;
-  if (mlra_status st = mlra_qweight_create_opaque(rows, cols, 2, &kCb2Hook, &q)) return st;
   // device codebook layout (common.cuh Cb2Dev): bf16-exact magnitudes -> 8 bf16
   // per code, else the two float4 halves in separate arrays
   bool cb16 = true;
@@ -777,56 +882,37 @@ mlra_status mlra_cb2_create(int64_t rows, int64_t cols, int64_t group, const uin
       else
         cbdev[(e / 4) * 1024 + i * 4 + (e & 3)] = u;
     }
-  const size_t cb_bytes = cbdev.size() * 4, code_bytes = static_cast<size_t>(rows * (cols / 8)) * 2,
-               sc_bytes = static_cast<size_t>(ng) * 4;
-  const size_t off_codes = cb_bytes, off_sc = round_up(off_codes + code_bytes, 16);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMalloc(&q->cb2_mem, off_sc + sc_bytes);
-  char* base = static_cast<char*>(q->cb2_mem);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(base, cbdev.data(), cb_bytes, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(base + off_codes, codes, code_bytes, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(base + off_sc, scales, sc_bytes, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) {
-    mlra_qweight_destroy(q);
-    return fail(MLRA_ERR_CUDA, "cb2 upload: %s", cudaGetErrorString(e));
-  }
-  q->device_bytes = off_sc + sc_bytes;
-  q->d.group = group;
-  // fused path: whole 256-multiples (the u16 codes are then the row-aligned 2-bit
-  // stream the Q ring tiles), a bf16-exact codebook, a group the Q ring supports
-  const bool g_ok = group == 32 || group == 64 || group % 128 == 0;
-  if (cb16 && g_ok && rows % 256 == 0 && cols % 256 == 0) {
-    QWeightDev& fd = q->cb2_d;
-    fd.rows = fd.rows_pad = rows;
-    fd.cols = fd.cols_pad = cols;
-    fd.bits = 2;
-    fd.group = group;
-    fd.ng_pad = round_up(cols / group, 2);
-    fd.row_words = cols / 16;
-    fd.words = reinterpret_cast<const uint32_t*>(base + off_codes);
-    std::vector<float2> g(static_cast<size_t>(rows * fd.ng_pad), make_float2(1.0f, 0.0f));
-    for (int64_t i = 0; i < rows; ++i)
-      for (int64_t j = 0; j < cols / group; ++j)
-        g[static_cast<size_t>(i * fd.ng_pad + j)] = make_float2(scales[i * (cols / group) + j], 0.0f);
-    e = cudaMalloc(&q->cb2_grid, g.size() * sizeof(float2));
-    if (e == cudaSuccess)
-      e = cudaMemcpy(q->cb2_grid, g.data(), g.size() * sizeof(float2), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      mlra_qweight_destroy(q);
-      return fail(MLRA_ERR_CUDA, "cb2 grid upload: %s", cudaGetErrorString(e));
-    }
-    fd.grid = q->cb2_grid;
-    q->device_bytes += g.size() * sizeof(float2);
-    q->cb2_fused = true;
-  }
-  q->cb2 = mlra::Cb2Dev{rows, cols, group, cols / group,
-                        reinterpret_cast<const uint16_t*>(base + off_codes), base, cb16 ? 1 : 0,
-                        reinterpret_cast<const float*>(base + off_sc)};
-  *out = q;
-  return MLRA_OK;
+  return codebook_qweight_create("cb2", rows, cols, group, codes, cbdev, cb16, false, scales,
+                                 stream, out);
+}
+
+int mlra_e8p_abs_table(float* abs_out, uint32_t* odd_out) {
+  float a[256][8];
+  uint32_t odd[8];
+  e8p_abs_table(a, odd);
+  if (abs_out) std::memcpy(abs_out, a, sizeof(a));
+  if (odd_out) std::memcpy(odd_out, odd, sizeof(odd));
+  return 256;
+}
+
+mlra_status mlra_e8p_create(int64_t rows, int64_t cols, int64_t group, const uint16_t* codes,
+                            const float* scales, void* stream, mlra_qweight** out) {
+  // device tables: bf16 rows of (|a| + 1/4), then of (|a| - 1/4), then the odd bits
+  float a[256][8];
+  uint32_t odd[8];
+  e8p_abs_table(a, odd);
+  std::vector<uint32_t> tab(2 * 256 * 4 + 32 / 4, 0u);
+  for (int h = 0; h < 2; ++h)
+    for (int i = 0; i < 256; ++i)
+      for (int e = 0; e < 8; ++e) {
+        const float m = a[i][e] + (h == 0 ? 0.25f : -0.25f);  // exact (multiples of 1/4)
+        uint32_t u;
+        std::memcpy(&u, &m, 4);
+        tab[h * 1024 + i * 4 + e / 2] |= (u >> 16) << (16 * (e & 1));
+      }
+  for (int w = 0; w < 8; ++w) tab[2048 + w] = odd[w];
+  return codebook_qweight_create("e8p", rows, cols, group, codes, tab, true, true, scales, stream,
+                                 out);
 }
 
 mlra_status mlra_lut_create(int64_t rows, int64_t cols, int bits, int64_t group,
@@ -1241,6 +1327,25 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
     CUDA_TRY(cudaStreamWaitEvent(s, side->join, 0));
   }
   return gst;
+}
+
+mlra_status mlra_rht(const void* in, int64_t rows, int64_t cols, int64_t ld_in, const float* signs,
+                     int inverse, int block, void* out, int64_t ld_out, mlra_dtype out_dtype,
+                     void* stream) {
+  if (!in || !out || !signs) return fail(MLRA_ERR_CONTRACT, "rht: null buffers");
+  if (block != 64 && block != 128 && block != 256 && block != 512 && block != 1024)
+    return fail(MLRA_ERR_CONFIG, "rht: block %d must be a power of two in [64, 1024]", block);
+  if (rows < 0 || cols <= 0 || cols % block != 0)
+    return fail(MLRA_ERR_DIMENSION, "rht: cols %lld is not a multiple of the block %d",
+                (long long)cols, block);
+  if (ld_in < cols || ld_out < cols || ld_in % 2 || ld_out % 2 ||
+      reinterpret_cast<uintptr_t>(in) % 4 || reinterpret_cast<uintptr_t>(out) % 8)
+    return fail(MLRA_ERR_DIMENSION, "rht: leading dimensions / alignment");
+  if (out_dtype != MLRA_BF16 && out_dtype != MLRA_F32) return fail(MLRA_ERR_CONFIG, "rht: bad dtype");
+  if (mlra_status st = check_device()) return st;
+  CUDA_TRY(mlra::launch_rht(in, rows, cols, ld_in, signs, inverse, block, out, ld_out,
+                            out_dtype == MLRA_F32, static_cast<cudaStream_t>(stream)));
+  return MLRA_OK;
 }
 
 mlra_status mlra_adamw_step(const mlra_adamw* opt, int64_t step_index, double lr,

@@ -1,4 +1,4 @@
-// codebook.cu — the built-in non-affine plugin "cb2" (include/mlra.h,
+// codebook.cu — the built-in non-affine plugins "cb2" and "e8p" (include/mlra.h,
 // mlra_cb2_create): a QuIP#-style 2-bit vector codebook behind the device
 // dequant hook (the GPU form of Quantizer::matvec, quantize.hpp:98-105).
 //
@@ -7,6 +7,10 @@
 // per (row, group) along cols. Ŵ[i, 8u+j] = RN_f32(s · ±cb[idx][j]) (one IEEE
 // multiply, so bit-exact against oracle/mlra_oracle.c orc_cb2_dequant), then
 // RN to bf16 for the GEMM operand.
+//
+// "e8p" (mlra_e8p_create) is QuIP#'s E8P lattice codebook in the same u16-per-8
+// format: the 16 bits select one of 2^16 points of E8 + 1/4 (common.cuh
+// e8p_decode_signs); Ŵ = RN_f32(s · value), value exact in bf16.
 //
 // k_cb2_materialize is HBM-bound: 0.25 B of code + 4/g B of scale read and
 // 2 (bf16) or 4 (f32) B written per entry. The codebook lives in shared memory
@@ -45,21 +49,41 @@ __device__ __forceinline__ void cb2_mags(uint32_t code, const uint4* cbh, const 
   }
 }
 
+// E8P: the 8 magnitudes of a code (|a| + 1/4 or |a| - 1/4 per entry, bf16-exact
+// tables in shared memory) and its negate byte (common.cuh e8p_decode_signs).
+__device__ __forceinline__ uint32_t e8p_mags(uint32_t code, const uint4* tab, const uint32_t* odd,
+                                             float (&m)[8]) {
+  const uint32_t i = code & 0xFFu;
+  uint32_t neg, plus;
+  e8p_decode_signs(code, (odd[i >> 5] >> (i & 31)) & 1u, &neg, &plus);
+  const uint4 P = tab[i], N = tab[256 + i];
+  const uint32_t pw[4] = {P.x, P.y, P.z, P.w}, nw[4] = {N.x, N.y, N.z, N.w};
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t lo = ((plus >> (2 * p)) & 1u) ? pw[p] : nw[p];
+    const uint32_t hi = ((plus >> (2 * p + 1)) & 1u) ? pw[p] : nw[p];
+    m[2 * p] = __uint_as_float(lo << 16);
+    m[2 * p + 1] = __uint_as_float(hi & 0xFFFF0000u);
+  }
+  return neg;
+}
+
 // One code -> 8 bf16 outputs. Products RN_f32(s·mag) (scalar IEEE
 // multiplies); the sign is applied after rounding (RN commutes with negation):
 // the mask of entries (2p, 2p+1) is ((code >> (8+2p)) & 3) * 0x40008000 &
 // 0x80008000 — bit 15 and bit 31 of the packed pair — 3 ops per pair.
 template <bool VEC>
-__device__ __forceinline__ void cb2_emit(void* __restrict__ out, int64_t o, uint32_t code, float s,
+__device__ __forceinline__ void cb2_emit(void* __restrict__ out, int64_t o, uint32_t sg, float s,
                                          const float (&m)[8]) {
+  // sg: negate bit per entry (cb2: code >> 8; e8p: e8p_decode_signs)
   float f[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) f[e] = __fmul_rn(s, m[e]);
   uint4 v;
-  v.x = pack_bf16x2(f[0], f[1]) ^ ((((code >> 8) & 3u) * 0x40008000u) & 0x80008000u);
-  v.y = pack_bf16x2(f[2], f[3]) ^ ((((code >> 10) & 3u) * 0x40008000u) & 0x80008000u);
-  v.z = pack_bf16x2(f[4], f[5]) ^ ((((code >> 12) & 3u) * 0x40008000u) & 0x80008000u);
-  v.w = pack_bf16x2(f[6], f[7]) ^ ((((code >> 14) & 3u) * 0x40008000u) & 0x80008000u);
+  v.x = pack_bf16x2(f[0], f[1]) ^ ((((sg) & 3u) * 0x40008000u) & 0x80008000u);
+  v.y = pack_bf16x2(f[2], f[3]) ^ ((((sg >> 2) & 3u) * 0x40008000u) & 0x80008000u);
+  v.z = pack_bf16x2(f[4], f[5]) ^ ((((sg >> 4) & 3u) * 0x40008000u) & 0x80008000u);
+  v.w = pack_bf16x2(f[6], f[7]) ^ ((((sg >> 6) & 3u) * 0x40008000u) & 0x80008000u);
   if constexpr (VEC) {
     *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + o) = v;
   } else {
@@ -73,13 +97,19 @@ __device__ __forceinline__ void cb2_emit(void* __restrict__ out, int64_t o, uint
 // f32 output, half a code per thread: entries 4h..4h+3 of the code, one
 // 16-B store — adjacent lanes write adjacent 16 B, so each warp store covers
 // a contiguous 512 B (a whole code per lane would leave 32-B gaps per store).
-template <bool VEC, bool CB16>
+template <bool VEC, bool CB16, bool E8P>
 __device__ __forceinline__ void cb2_emit_half(float* __restrict__ out, int64_t o, uint32_t code,
                                               float s, int h, const uint4* cbh, const float4* cb0,
-                                              const float4* cb1) {
+                                              const float4* cb1, const uint32_t* odd) {
   const uint32_t i = code & 0xFFu;
   float m[4];
-  if constexpr (CB16) {
+  uint32_t sg = code >> (8 + 4 * h);
+  if constexpr (E8P) {
+    float m8[8];
+    sg = e8p_mags(code, cbh, odd, m8) >> (4 * h);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m[e] = m8[4 * h + e];
+  } else if constexpr (CB16) {
     const uint4 q = cbh[i];
     const uint32_t a = h ? q.z : q.x, b = h ? q.w : q.y;
     m[0] = __uint_as_float(a << 16), m[1] = __uint_as_float(a & 0xFFFF0000u);
@@ -88,7 +118,6 @@ __device__ __forceinline__ void cb2_emit_half(float* __restrict__ out, int64_t o
     const float4 v = h ? cb1[i] : cb0[i];
     m[0] = v.x, m[1] = v.y, m[2] = v.z, m[3] = v.w;
   }
-  const uint32_t sg = code >> (8 + 4 * h);
   float f[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e)
@@ -109,15 +138,18 @@ __device__ __forceinline__ void cb2_emit_half(float* __restrict__ out, int64_t o
 // form was long-scoreboard bound at 32% of DRAM bandwidth). Within a pass a
 // thread owns kCbPerThread codes strided by the block size, so each warp store
 // covers a contiguous 512 B (bf16).
-template <bool F32, bool VEC, bool CB16>
+template <bool F32, bool VEC, bool CB16, bool E8P>
 __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
     const Cb2Dev c, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols,
     void* __restrict__ out, int64_t ld, int gshift) {
-  __shared__ float4 cbs[CB16 ? 256 : 512];
+  // cb2: 256 (bf16 rows) or 512 (f32 halves) float4; e8p: 512 uint4 + 8 odd words
+  constexpr int NCB = (CB16 && !E8P) ? 256 : 512;
+  __shared__ float4 cbs[NCB + (E8P ? 2 : 0)];
   const uint4* cbh = reinterpret_cast<const uint4*>(cbs);
   const float4* cb0 = cbs;
   const float4* cb1 = cbs + 256;
-  for (int i = threadIdx.x; i < (CB16 ? 256 : 512); i += kCbThreads)
+  const uint32_t* odd = reinterpret_cast<const uint32_t*>(cbs + NCB);
+  for (int i = threadIdx.x; i < NCB + (E8P ? 2 : 0); i += kCbThreads)
     cbs[i] = __ldg(reinterpret_cast<const float4*>(c.codebook) + i);
   constexpr int SH = F32 ? 1 : 0;  // work unit: a code (bf16) or half a code (f32)
   const int ncodes = static_cast<int>(ncols >> 3);
@@ -172,12 +204,18 @@ __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
       const int it = base + j * kCbThreads;
       if (it >= nunits) break;
       if constexpr (F32) {
-        cb2_emit_half<VEC, CB16>(static_cast<float*>(orow), static_cast<int64_t>(it) << 2, cur[j],
-                                 cs[j], it & 1, cbh, cb0, cb1);
+        cb2_emit_half<VEC, CB16, E8P>(static_cast<float*>(orow), static_cast<int64_t>(it) << 2,
+                                      cur[j], cs[j], it & 1, cbh, cb0, cb1, odd);
       } else {
         float m[8];
-        cb2_mags<CB16>(cur[j], cbh, cb0, cb1, m);
-        cb2_emit<VEC>(orow, static_cast<int64_t>(it) << 3, cur[j], cs[j], m);
+        uint32_t sg;
+        if constexpr (E8P) {
+          sg = e8p_mags(cur[j], cbh, odd, m);
+        } else {
+          cb2_mags<CB16>(cur[j], cbh, cb0, cb1, m);
+          sg = cur[j] >> 8;
+        }
+        cb2_emit<VEC>(orow, static_cast<int64_t>(it) << 3, sg, cs[j], m);
       }
     }
   }
@@ -197,7 +235,7 @@ cudaError_t launch_cb2_materialize(const Cb2Dev& c, int64_t row0, int64_t nrows,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 0;  // one resident wave
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cb2_materialize<false, true, false>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cb2_materialize<false, true, false, false>,
                                                     kCbThreads, 0) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   const int64_t cap = static_cast<int64_t>(sms) * per_sm;
@@ -205,20 +243,26 @@ cudaError_t launch_cb2_materialize(const Cb2Dev& c, int64_t row0, int64_t nrows,
   const int64_t items = nrows * ((nunits + kCbThreads * kCbPerThread - 1) / (kCbThreads * kCbPerThread));
   const dim3 grid(static_cast<unsigned>(items < cap ? items : cap));
   note_launch();
-#define MLRA_CB2_LAUNCH(F, V, H)                                                          \
-  k_cb2_materialize<F, V, H><<<grid, kCbThreads, 0, st>>>(c, row0, nrows, col0, ncols, out, \
-                                                          ld, gshift)
-  if (c.bf16) {
+#define MLRA_CB2_LAUNCH(F, V, H, E)                                                          \
+  k_cb2_materialize<F, V, H, E><<<grid, kCbThreads, 0, st>>>(c, row0, nrows, col0, ncols, out, \
+                                                             ld, gshift)
+  if (c.e8p) {
     if (f32) {
-      if (vec) MLRA_CB2_LAUNCH(true, true, true); else MLRA_CB2_LAUNCH(true, false, true);
+      if (vec) MLRA_CB2_LAUNCH(true, true, true, true); else MLRA_CB2_LAUNCH(true, false, true, true);
     } else {
-      if (vec) MLRA_CB2_LAUNCH(false, true, true); else MLRA_CB2_LAUNCH(false, false, true);
+      if (vec) MLRA_CB2_LAUNCH(false, true, true, true); else MLRA_CB2_LAUNCH(false, false, true, true);
+    }
+  } else if (c.bf16) {
+    if (f32) {
+      if (vec) MLRA_CB2_LAUNCH(true, true, true, false); else MLRA_CB2_LAUNCH(true, false, true, false);
+    } else {
+      if (vec) MLRA_CB2_LAUNCH(false, true, true, false); else MLRA_CB2_LAUNCH(false, false, true, false);
     }
   } else {
     if (f32) {
-      if (vec) MLRA_CB2_LAUNCH(true, true, false); else MLRA_CB2_LAUNCH(true, false, false);
+      if (vec) MLRA_CB2_LAUNCH(true, true, false, false); else MLRA_CB2_LAUNCH(true, false, false, false);
     } else {
-      if (vec) MLRA_CB2_LAUNCH(false, true, false); else MLRA_CB2_LAUNCH(false, false, false);
+      if (vec) MLRA_CB2_LAUNCH(false, true, false, false); else MLRA_CB2_LAUNCH(false, false, false, false);
     }
   }
 #undef MLRA_CB2_LAUNCH

@@ -48,7 +48,30 @@ struct Cb2Dev {
   const void* codebook;           // 16-B aligned
   int bf16;
   const float* scales;            // [rows x ng]
+  // e8p != 0: the E8P lattice codebook (mlra_e8p_create): codebook = uint4[256]
+  // of bf16 (|a| + 1/4) rows, uint4[256] of (|a| - 1/4) rows, then uint32[8]
+  // "odd" bits (the abs pattern's coordinate sum is odd); see e8p_decode_signs.
+  int e8p;
 };
+
+// E8P code -> (negate mask, use-(|a|+1/4) mask) of its 8 entries. Code bits:
+// 0-7 abs-pattern index, 8-14 signs of entries 0-6, 15 the shift (+1/4 when
+// set, -1/4 otherwise); entry 7's sign makes the count of negated entries
+// congruent to the pattern's coordinate sum mod 2, so sign(a)·|a| lies in E8's
+// half-integer coset (D8 + 1/2) before the shift. Entry j's value is
+// sign_j · (|a_j| + sign_j·shift): the magnitude is |a_j| + 1/4 exactly when
+// (negated_j XOR shift bit) is set.
+__host__ __device__ __forceinline__ void e8p_decode_signs(uint32_t code, uint32_t odd,
+                                                          uint32_t* neg, uint32_t* plus) {
+  const uint32_t sb = (code >> 8) & 0x7Fu;
+  uint32_t par = sb;
+  par ^= par >> 4;
+  par ^= par >> 2;
+  par ^= par >> 1;
+  const uint32_t n = sb | ((((par & 1u) ^ odd) & 1u) << 7);
+  *neg = n;
+  *plus = n ^ ((code >> 15) ? 0xFFu : 0u);
+}
 
 // Bits of the 8 consecutive codes of unit `u` (codes 8u..8u+7) of a
 // word-aligned row, at the LSB of the result (bitpack.cpp:25-35 restated for

@@ -113,6 +113,11 @@ struct PrepBlocks {
 };
 cudaError_t launch_prep(const PrepBatch& b, cudaStream_t st);
 
+// Block randomized Hadamard transform of bf16 activations (rht.cu).
+cudaError_t launch_rht(const void* in, int64_t rows, int64_t cols, int64_t ld_in,
+                       const float* signs, int inverse, int block, void* out, int64_t ld_out,
+                       bool f32, cudaStream_t st);
+
 // Skinny rank-r products on tensor cores (thin_mma.cu); r <= 64 per call. Factors are passed
 // transposed and split into bf16 hi/lo planes [thin_rows(r) x ld] (PrepBatch::split_t).
 int thin_rows(int64_t r, bool ones);

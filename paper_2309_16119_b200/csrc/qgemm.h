@@ -30,6 +30,7 @@ struct GemmArgs {
   const float* bias; // [m_valid] or nullptr
   int out_pairs;     // bf16 out with even ldo and 4-byte aligned base: paired-row stores
   const void* cb2_codebook;  // non-null: fused cb2 plugin decode (bf16 codebook, uint4[256])
+  int e8p;                   // with cb2_codebook: the e8p plugin's tables and decode
   const float* lut;          // non-null: fused lut plugin decode (16 f32 levels)
   // Q ring (fused path with TMA-fed codes); q_stages == 0 selects the LDG path
   int q_stages;
@@ -74,6 +75,7 @@ void qgemm2_plan(GemmArgs& p);
 int qgemm_choose(const GemmArgs& p);
 constexpr int kMaxSkPairs = 128;
 constexpr int kCb2SmemBytes = 256 * 16;  // the cb2 codebook staged in shared memory
+constexpr int kE8pSmemBytes = 2 * 256 * 16 + 128;  // e8p (|a| +- 1/4) tables + odd bits (padded)
 constexpr int kLutSmemBytes = 64;         // the lut plugin's 16 levels in shared memory
 constexpr int64_t kSkSlotFloats = 2LL * 512 * 128;  // per pair
 

@@ -168,11 +168,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sT = sW + STAGES * W_TILE;
   uint8_t* sQ = sT + STAGES * T_TILE;
   constexpr bool CB2 = BITS == kCb2Bits;
+  constexpr bool E8P = BITS == kE8pBits;
   constexpr bool LUT = is_lut<BITS>();
   constexpr int QB = q_geom_bits<BITS>();  // packed-stream geometry
   uint8_t* sCb = sQ + p.q_stages * p.q_stage_bytes;  // cb2 codebook / lut levels
   uint64_t* full = reinterpret_cast<uint64_t*>(
-      sCb + (CB2 ? kCb2SmemBytes : (LUT ? kLutSmemBytes : 0)));
+      sCb + (CB2 ? kCb2SmemBytes : (E8P ? kE8pSmemBytes : (LUT ? kLutSmemBytes : 0))));
   uint64_t* empty = full + STAGES;
   uint64_t* qfull = empty + STAGES;
   uint64_t* qempty = qfull + MAX_QS;
@@ -232,6 +233,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc2(tmem_slot, TMEM_COLS);
+  if constexpr (E8P) {  // stage the 8 KB e8p tables + odd bits
+    for (int i = threadIdx.x; i < (2 * 256 * 16 + 32) / 16; i += NUM_THREADS)
+      reinterpret_cast<uint4*>(sCb)[i] = __ldg(reinterpret_cast<const uint4*>(p.cb2_codebook) + i);
+  }
   if constexpr (CB2) {  // stage the 4 KB codebook (read by this CTA's dequant warps)
     if (threadIdx.x < kCb2SmemBytes / 16)
       reinterpret_cast<uint4*>(sCb)[threadIdx.x] =
@@ -736,6 +741,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               if constexpr (CB2)
                 dequant_units_cb2<UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox,
                                                  smem_u32(sCb));
+              else if constexpr (E8P)
+                dequant_units_e8p<UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox,
+                                                 smem_u32(sCb));
               else if constexpr (LUT)
                 dequant_units_lut<QB, UPT, ROW_STEP>(qc, qg, st, soff, unit, gsub, rbase, gbox,
                                                      smem_u32(sCb));
@@ -784,7 +792,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                   wrow = static_cast<int64_t>(kb) * BK + (u >> 4);
                   wunit = static_cast<int64_t>(cb) * (BM / 8) + (u & 15);
                 }
-                if constexpr (!CB2 && !LUT) {  // (the plugin decodes always run on the Q ring)
+                if constexpr (!CB2 && !E8P && !LUT) {  // (the plugin decodes always run on the Q ring)
                   const uint64_t v = load_unit<BITS>(q.words + wrow * q.row_words, wunit);
                   *reinterpret_cast<uint4*>(stile + unit_soff<MN>(u)) =
                       deq8_bf16_general<BITS>(v, q.grid + wrow * q.ng_pad, wunit * 8, q.group);
@@ -824,7 +832,9 @@ cudaError_t launch2_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs&
                       cudaStream_t stream) {
   auto kern = qgemm2_kernel<BITS, W_TMA, MN, OUT_F32, QTMA>;
   const int smem = SMEM_FIXED + p.q_stages * p.q_stage_bytes +
-                   (BITS == kCb2Bits ? kCb2SmemBytes : (is_lut<BITS>() ? kLutSmemBytes : 0));
+                   (BITS == kCb2Bits ? kCb2SmemBytes
+                                     : (BITS == kE8pBits ? kE8pSmemBytes
+                                                         : (is_lut<BITS>() ? kLutSmemBytes : 0)));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
@@ -936,6 +946,10 @@ cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmA
   if (p.tokens <= 0 || p.m_total <= 0) return cudaSuccess;
   if (w_tma) return launch2_mo<4, true, false>(maps, q, p, mn, out_f32, stream);
   const bool qtma = p.q_stages > 0;
+  if (p.cb2_codebook != nullptr && p.e8p) {
+    if (!qtma) return cudaErrorInvalidValue;  // the fused e8p decode needs the Q ring
+    return launch2_mo<kE8pBits, false, true>(maps, q, p, mn, out_f32, stream);
+  }
   if (p.cb2_codebook != nullptr) {
     if (!qtma) return cudaErrorInvalidValue;  // the fused cb2 decode needs the Q ring
     return launch2_mo<kCb2Bits, false, true>(maps, q, p, mn, out_f32, stream);

@@ -127,11 +127,14 @@ constexpr int kCb2Bits = 18;
 // The lut plugin (a per-matrix table of 2^b f32 levels, e.g. NF4): BITS tag
 // kLutTag + b; its codes are the plain b-bit stream, so only the decode differs.
 constexpr int kLutTag = 32;
+// The e8p plugin (E8P lattice codebook): the cb2 stream geometry, decode by
+// e8p_decode_signs over (|a| +- 1/4) tables (qgemm.h kE8pSmemBytes).
+constexpr int kE8pBits = 19;
 template <int BITS>
 constexpr bool is_lut() { return BITS > kLutTag; }
 template <int BITS>
 constexpr int q_geom_bits() {
-  return BITS == kCb2Bits ? 2 : (BITS > kLutTag ? BITS - kLutTag : BITS);
+  return (BITS == kCb2Bits || BITS == kE8pBits) ? 2 : (BITS > kLutTag ? BITS - kLutTag : BITS);
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
@@ -166,6 +169,44 @@ __device__ __forceinline__ void dequant_units_cb2(uint32_t qc, uint32_t qg, uint
       const float a = __fmul_rn(s, __uint_as_float(w[p] << 16));
       const float b = __fmul_rn(s, __uint_as_float(w[p] & 0xFFFF0000u));
       o[p] = pack_bf16x2(a, b) ^ ((((v[i] >> (8 + 2 * p)) & 3u) * 0x40008000u) & 0x80008000u);
+    }
+    sts128(st + soff[i], make_uint4(o[0], o[1], o[2], o[3]));
+  }
+}
+
+// The e8p plugin's tile decode: per code, the (|a| + 1/4) and (|a| - 1/4) bf16
+// rows of its abs pattern (tab, uint4[2][256]) blended per entry by the
+// e8p_decode_signs masks, scaled (one IEEE multiply per entry: the same law as
+// k_cb2_materialize's e8p path, so fused == materialized bit for bit), negated.
+template <int UPT, int ROW_STEP>
+__device__ __forceinline__ void dequant_units_e8p(uint32_t qc, uint32_t qg, uint32_t st,
+                                                  const uint32_t (&soff)[UPT], int unit, int gsub,
+                                                  int rbase, int gbox, uint32_t tab) {
+  constexpr int QROW = 32;  // 128 weights x 2 bits
+  uint32_t v[UPT];
+  float sc[UPT];
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int row = rbase + i * ROW_STEP;
+    v[i] = lds16(qc + row * QROW + unit * 2);
+    sc[i] = lds_f2(qg + row * gbox + gsub * 8).x;
+  }
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const uint32_t idx = v[i] & 0xFFu;
+    uint32_t neg, plus;
+    e8p_decode_signs(v[i], (lds32(tab + 8192 + ((idx >> 5) << 2)) >> (idx & 31)) & 1u, &neg, &plus);
+    const uint4 P = lds128(tab + (idx << 4)), N = lds128(tab + 4096 + (idx << 4));
+    const uint32_t pw[4] = {P.x, P.y, P.z, P.w}, nw[4] = {N.x, N.y, N.z, N.w};
+    const float s = fabsf(sc[i]);
+    uint32_t o[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t lo = ((plus >> (2 * p)) & 1u) ? pw[p] : nw[p];
+      const uint32_t hi = ((plus >> (2 * p + 1)) & 1u) ? pw[p] : nw[p];
+      const float a = __fmul_rn(s, __uint_as_float(lo << 16));
+      const float b = __fmul_rn(s, __uint_as_float(hi & 0xFFFF0000u));
+      o[p] = pack_bf16x2(a, b) ^ ((((neg >> (2 * p)) & 3u) * 0x40008000u) & 0x80008000u);
     }
     sts128(st + soff[i], make_uint4(o[0], o[1], o[2], o[3]));
   }

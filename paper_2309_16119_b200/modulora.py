@@ -415,6 +415,162 @@ class Codebook2Quantizer:
         return DeviceQuantizedMatrix._wrap(h, m.rows, m.cols, 2, m.group_size)
 
 
+def e8p_abs_table():
+    """The E8P abs-pattern table (include/mlra.h mlra_e8p_abs_table): 256 x 8 f32
+    |a| patterns and the 256 odd-coordinate-sum bits."""
+    a = np.empty((256, 8), np.float32)
+    odd = np.empty(8, np.uint32)
+    lib().mlra_e8p_abs_table(a.ctypes.data, odd.ctypes.data)
+    bits = ((odd[np.arange(256) >> 5] >> (np.arange(256) & 31).astype(np.uint32)) & 1).astype(bool)
+    return a, bits
+
+
+def e8p_decode(codes: np.ndarray) -> np.ndarray:
+    """E8P codes (u16) -> their 8-dim codewords (f64), the decode law of
+    mlra_e8p_create: sign_j * |a_j| + (+1/4 if bit 15 else -1/4)."""
+    a, odd = e8p_abs_table()
+    c = np.asarray(codes, np.uint32).ravel()
+    idx = c & 0xFF
+    neg = ((c[:, None] >> (8 + np.arange(7, dtype=np.uint32))) & 1).astype(np.int64)
+    n7 = (neg.sum(1) + odd[idx].astype(np.int64)) & 1
+    neg = np.concatenate([neg, n7[:, None]], 1)
+    sh = np.where((c >> 15) & 1, 0.25, -0.25)
+    return np.where(neg == 1, -1.0, 1.0) * a[idx].astype(np.float64) + sh[:, None]
+
+
+@dataclass
+class E8pMatrix:
+    """Host container of the e8p format (include/mlra.h mlra_e8p_create)."""
+    rows: int
+    cols: int
+    group_size: int
+    codes: np.ndarray   # uint16 [rows x cols/8]
+    scales: np.ndarray  # float32 [rows x cols/group]
+
+
+class E8pQuantizer:
+    """Quantizer plugin "e8p" (quantize.hpp:91-106 interface): QuIP#'s E8P
+    lattice codebook, 2 bits per weight — 2^16 points of E8 + 1/4 per 8
+    entries, a per-(row, group) scale. ``quantize`` is the exact nearest-point
+    search over the 256 abs patterns x 2 shifts (signs follow the residual,
+    one flip repairs the parity constraint); ``upload`` returns an opaque
+    DeviceQuantizedMatrix decoded inside the fused GEMM (whole 256-multiples)
+    or through the library's e8p materialize hook."""
+
+    def name(self) -> str:
+        return "e8p"
+
+    def quantize(self, w: np.ndarray, calib=None, bits: int = 2, group_size: int = 128) -> E8pMatrix:
+        if bits != 2:
+            raise MlraError(3, f"e8p: unsupported bit width {bits} (2 bits per weight)")
+        w = np.asarray(w, np.float64)
+        rows, cols = w.shape
+        if cols % 8 or group_size % 8 or cols % group_size:
+            raise MlraError(3, "e8p: cols and group size must be multiples of 8, group dividing cols")
+        a, odd = e8p_abs_table()
+        a = a.astype(np.float64)
+        ng = cols // group_size
+        # E8P codewords have RMS ~1.1 per coordinate; scale each group to match
+        rms = np.sqrt((w.reshape(rows, ng, group_size) ** 2).mean(-1))
+        scales = np.maximum(rms / 1.1, np.finfo(np.float32).tiny).astype(np.float32)
+        v = (w.reshape(rows, ng, group_size // 8, 8) /
+             scales.astype(np.float64)[:, :, None, None]).reshape(-1, 8)
+        codes = np.empty(v.shape[0], np.uint16)
+        for i in range(0, v.shape[0], 4096):
+            y = v[i:i + 4096]
+            best_err = np.full(y.shape[0], np.inf)
+            best = np.zeros(y.shape[0], np.uint32)
+            for shift_bit, delta in ((1, 0.25), (0, -0.25)):
+                z = y - delta                              # [n, 8]
+                az = np.abs(z)
+                neg = z < 0                                # unconstrained signs
+                err = ((az[:, None, :] - a[None, :, :]) ** 2).sum(-1)  # [n, 256]
+                par = (neg.sum(1)[:, None] + odd[None, :]) & 1       # parity violated
+                fix = 4.0 * (az[:, None, :] * a[None, :, :]).min(-1)  # cheapest flip
+                err = err + par * fix
+                k = err.argmin(1)
+                e = err[np.arange(len(k)), k]
+                # signs of the chosen pattern, with the parity flip applied
+                jflip = (az * a[k]).argmin(1)
+                s = neg.copy()
+                viol = par[np.arange(len(k)), k].astype(bool)
+                s[np.arange(len(k))[viol], jflip[viol]] ^= True
+                code = k.astype(np.uint32) | (s[:, :7].astype(np.uint32) << np.arange(8, 15, dtype=np.uint32)).sum(1) \
+                    | (np.uint32(shift_bit) << 15)
+                take = e < best_err
+                best_err[take] = e[take]
+                best[take] = code[take]
+            codes[i:i + 4096] = best.astype(np.uint16)
+        return E8pMatrix(rows, cols, group_size, codes.reshape(rows, cols // 8), scales.reshape(rows, ng))
+
+    def upload(self, m: E8pMatrix, stream: Optional[torch.cuda.Stream] = None) -> DeviceQuantizedMatrix:
+        codes = np.ascontiguousarray(m.codes, np.uint16)
+        sc = np.ascontiguousarray(m.scales, np.float32)
+        if codes.size != m.rows * (m.cols // 8) or sc.size != m.rows * (m.cols // m.group_size):
+            raise MlraError(7, "e8p: buffer sizes do not match the shape")
+        h = C.c_void_p()
+        check(lib().mlra_e8p_create(m.rows, m.cols, m.group_size, codes.ctypes.data, sc.ctypes.data,
+                                    _stream_ptr(stream), C.byref(h)))
+        return DeviceQuantizedMatrix._wrap(h, m.rows, m.cols, 2, m.group_size)
+
+
+def rht(x: torch.Tensor, signs: torch.Tensor, block: int = 512, inverse: bool = False,
+        out_dtype=torch.bfloat16) -> torch.Tensor:
+    """Block randomized Hadamard transform (include/mlra.h mlra_rht) of a bf16
+    [m x d] activation: H·diag(s)·x / sqrt(b) per b-wide block (inverse: the
+    transpose, diag(s)·H·x / sqrt(b))."""
+    if x.dim() != 2 or x.dtype != torch.bfloat16 or not x.is_cuda or x.stride(1) != 1:
+        raise MlraError(3, "rht: expected a row-major bf16 CUDA tensor")
+    if signs.dtype != torch.float32 or signs.numel() != x.shape[1] or not signs.is_contiguous():
+        raise MlraError(2, "rht: signs must be a contiguous f32 vector of length cols")
+    out = torch.empty(x.shape[0], x.shape[1], dtype=out_dtype, device=x.device)
+    check(lib().mlra_rht(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0), signs.data_ptr(),
+                         int(inverse), block, out.data_ptr(), out.shape[1], _dtype_code(out_dtype),
+                         _stream_ptr(None)))
+    return out
+
+
+def random_signs(n: int, seed: int, device="cuda") -> torch.Tensor:
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return (torch.randint(0, 2, (n,), generator=g) * 2 - 1).to(torch.float32).to(device)
+
+
+class IncoherentLayer:
+    """QuIP#-style incoherence processing around a ModuLoRA layer (PAPER.md:224,
+    :231: "orthogonal matrices multiplication in the forward and backward
+    passes"). The frozen weights were quantized in the rotated basis
+    W~ = U W V^T, U = H·diag(u), V = H·diag(v) (block-diagonal b-wide
+    Hadamard, random signs); the adapters live in the same basis (A~ = U A,
+    B~ = V B) and the bias enters as U·bias, so
+        y  = U^T (layer_forward(inner, V x))           (= W x + s·(xB)A^T + bias)
+        dx = V^T (layer_backward(inner, V x, ., U dy)) (dA~, dB~ from the inner layer).
+    Each transform is one mlra_rht launch; the inner layer is any ModuLoraLayer
+    (e8p / cb2 / affine weights)."""
+
+    def __init__(self, inner: ModuLoraLayer, u_signs: torch.Tensor, v_signs: torch.Tensor,
+                 block: int = 512):
+        if inner.bias_trainable:
+            raise MlraError(3, "IncoherentLayer: a trainable bias is not supported (frozen U·bias)")
+        self.inner, self.u, self.v, self.block = inner, u_signs, v_signs, block
+
+    @staticmethod
+    def rotated_bias(bias: torch.Tensor, u_signs: torch.Tensor, block: int = 512) -> torch.Tensor:
+        """U·bias (fp32) for the inner layer's bias."""
+        return rht(bias.reshape(1, -1).to(torch.bfloat16).contiguous(), u_signs, block,
+                   out_dtype=torch.float32).reshape(-1)
+
+    def forward(self, x: torch.Tensor):
+        xt = rht(x, self.v, self.block)
+        yt, xb = layer_forward(self.inner, xt)
+        return rht(yt, self.u, self.block, inverse=True), (xt, xb)
+
+    def backward(self, saved, dy: torch.Tensor, da=None, db=None):
+        xt, xb = saved
+        dyt = rht(dy, self.u, self.block)
+        dxt = layer_backward(self.inner, xt, xb, dyt, da=da, db=db)
+        return rht(dxt, self.v, self.block, inverse=True)
+
+
 # The QLoRA NF4 levels (Dettmers et al. 2023, "normal float 4"): the
 # published f32 table, sorted, normalised to [-1, 1] with an exact 0.
 NF4_LEVELS = np.array([
