@@ -174,6 +174,49 @@ def main():
                               "ms_per_step": ms, "tflops": flops / (ms / 1e3) / 1e12}),
                   flush=True)
 
+    if not only or "e8p" in only:
+        # the QuIP#-style path at cfg5 shapes: E8P lattice codebook (fused decode in the
+        # pair GEMM vs the hook's whole-matrix materialize) and the incoherent layer
+        # (block RHT of x / y / dY / dX around the E8P layer)
+        import numpy as np
+        rows, cols, m, r = 6656, 17920, 4096, 8
+        rng = np.random.default_rng(900)
+        em = M.E8pMatrix(rows, cols, 128,
+                         rng.integers(0, 1 << 16, (rows, cols // 8), dtype=np.uint32).astype(np.uint16),
+                         (0.01 * (0.5 + rng.random((rows, cols // 128)))).astype(np.float32))
+        eq = M.E8pQuantizer().upload(em)
+        for dt, eb in ((torch.bfloat16, 2), (torch.float32, 4)):
+            out = torch.empty(rows, cols, dtype=dt, device="cuda")
+            ms = time_steps(lambda: M.dequantize(eq, dt, out=out), flush)
+            nbytes = rows * cols * (2 / 8 + eb) + rows * (cols // 128) * 4 + 8224
+            print(json.dumps({"config": "cfg5_materialize", "format": "e8p plugin (hook)",
+                              "shape": [rows, cols], "bits": 2, "out": str(dt), "us": ms * 1e3,
+                              "gbs": nbytes / (ms / 1e3) / 1e9,
+                              "frac_measured_hbm": nbytes / (ms / 1e3) / 1e9 / hbm}), flush=True)
+            del out
+        a = torch.randn(rows, r, device="cuda") * 0.02
+        b = torch.randn(cols, r, device="cuda") * 0.02
+        flops = 4.0 * m * rows * cols + 6.0 * m * r * (rows + cols)
+        for sname in ("row", "weight"):
+            L = M.ModuLoraLayer("e8p", eq, M.LoraAdapter(a, b, r, 16.0), strategy=M.parse_strategy(sname))
+            ms = time_steps(graphed(independent_layers_step([L], m)), flush)
+            print(json.dumps({"config": "cfg5_e8p_layer", "shape": [rows, cols], "rank": r,
+                              "tokens": m, "strategy": sname, "launch": "cuda-graph",
+                              "ledger_bytes": M.LpLinearContext(eq, L.strategy).ledger_bytes(),
+                              "ms_per_step": ms, "tflops": flops / (ms / 1e3) / 1e12}), flush=True)
+        inc = M.IncoherentLayer(M.ModuLoraLayer("inc", eq, M.LoraAdapter(a, b, r, 16.0)),
+                                M.random_signs(rows, 1), M.random_signs(cols, 2), 512)
+        x = torch.randn(m, cols, device="cuda").to(torch.bfloat16)
+        dy = torch.randn(m, rows, device="cuda").to(torch.bfloat16)
+
+        def inc_step():
+            y, saved = inc.forward(x)
+            inc.backward(saved, dy)
+        ms = time_steps(graphed(inc_step), flush)
+        print(json.dumps({"config": "cfg5_e8p_incoherent_layer", "shape": [rows, cols], "rank": r,
+                          "tokens": m, "rht_block": 512, "launch": "cuda-graph",
+                          "ms_per_step": ms, "tflops": flops / (ms / 1e3) / 1e12}), flush=True)
+
     if not only or "nf4" in only:
         # the lut plugin (NF4 levels, absmax scale, g64) against the affine 4-bit
         # format at the cfg2 shapes (LLaMA-7B MLP up + down, r=16, m=4096), and its
