@@ -79,7 +79,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   // dev-only (MLRA_TRACE2): per CTA [0] total cycles, [1] MMA wait on full,
   // [2..4] / [5..7] dequant group 0 / 1: wait qfull, wait empty, compute+arrive
+#ifdef MLRA_DEV_TRACE  // dev-only instrumentation (MLRA_TRACE2), compiled in with -DMLRA_DEV_TRACE
   unsigned long long* tl = p.trace2 ? p.trace2 + 8 * blockIdx.x : nullptr;
+#else
+  constexpr unsigned long long* tl = nullptr;
+#endif
   const long long t_entry = clock64();
   const int n_kb_main = p.n_kb_main;
   const int n_kb = p.n_kb_main + p.n_kb_lora;
