@@ -27,6 +27,13 @@ using mlra::QWeightDev;
 namespace mlra {
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MLRA_PDL");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return on;
+}
 }  // namespace mlra
 
 struct mlra_qweight {
@@ -214,6 +221,13 @@ struct GemmPlan {
   const void* cb2_codebook = nullptr;  // fused cb2 plugin decode (pair kernel, Q ring)
   int e8p = 0;                         // with cb2_codebook: the e8p plugin's decode
   const float* lut = nullptr;          // fused lut plugin decode (pair kernel, Q ring)
+  // stream-K / split-K publish flags already zeroed by the pass's prep launch
+  // (so no memset node sits between the skinny product and the GEMM, which
+  // would break the programmatic launch chain); nullptr: zeroed here
+  unsigned* sk_flags_zeroed = nullptr;
+  // launch classically: a side stream's kernels (dA/dB) should get the SMs
+  // before this GEMM's CTAs, which a programmatic early launch would preempt
+  bool no_pdl = false;
 };
 
 // One GEMM over the quantized operand described by d. w_mat != nullptr: Ŵ is
@@ -242,6 +256,7 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
   // the cost model; MLRA_GEMM=1|2|3 forces the 1-CTA (256) / pair / 1-CTA (128)
   // kernel (tests cover all three).
   a.cb2_codebook = gp.cb2_codebook;
+  a.no_pdl = gp.no_pdl ? 1 : 0;
   a.e8p = gp.e8p;
   a.lut = gp.lut;
   int kind = mlra::qgemm_choose(a);
@@ -308,9 +323,11 @@ mlra_status run_gemm_d(const QWeightDev& d, const __nv_bfloat16* w_mat, int64_t 
     mlra::qgemm2_plan(a);
     if (a.sk_pairs) {  // stream-K: fp32 partial slots + zeroed publish flags
       a.sk_ws = sc.get<float>(static_cast<size_t>(a.sk_pairs * mlra::kSkSlotFloats));
-      a.sk_flags = sc.get<unsigned>(static_cast<size_t>(2 * a.sk_pairs));
+      a.sk_flags = gp.sk_flags_zeroed ? gp.sk_flags_zeroed
+                                      : sc.get<unsigned>(static_cast<size_t>(2 * a.sk_pairs));
       if (!a.sk_ws || !a.sk_flags) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-      CUDA_TRY(cudaMemsetAsync(a.sk_flags, 0, 2 * a.sk_pairs * sizeof(unsigned), sc.st));
+      if (!gp.sk_flags_zeroed)
+        CUDA_TRY(cudaMemsetAsync(a.sk_flags, 0, 2 * a.sk_pairs * sizeof(unsigned), sc.st));
     }
     CUDA_TRY(mlra::qgemm2_launch(maps, d, a, w_tma, gp.mn, gp.out_f32, sc.st));
   }
@@ -353,9 +370,11 @@ mlra_status call_hook(const mlra_hook* hk, const mlra_qweight* q, int64_t row0, 
 // slab's GEMM writes its own output columns), columns for dX (each slab's GEMM
 // writes its own dX columns) — so no slab needs a cross-slab reduction.
 mlra_status run_gemm_hooked(const mlra_qweight* q, const mlra_hook* hk, bool whole,
-                            const GemmPlan& gp, Scratch& sc) {
+                            const GemmPlan& gp0, Scratch& sc) {
   const QWeightDev& d = q->d;
   if (!hk->materialize) return fail(MLRA_ERR_CONTRACT, "quantizer hook without materialize()");
+  GemmPlan gp = gp0;
+  gp.sk_flags_zeroed = nullptr;  // one zeroed flag set cannot serve several slab GEMMs
   const int64_t esize = gp.out_f32 ? 4 : 2;
   if (!gp.mn) {
     const int64_t slab = slab_extent(d.rows_pad, d.cols_pad, whole);
@@ -503,6 +522,15 @@ mlra_status thin_ws(Scratch& sc, mlra::PrepBatch& pb, bool row, int64_t m, int64
   if (!w->ws || !w->cnt) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
   pb.zero_f32(reinterpret_cast<float*>(w->cnt), nc);
   return MLRA_OK;
+}
+
+// Publish flags for a stream-K / split-K GEMM of this pass (the most any plan
+// uses), zeroed by the pass's prep launch.
+unsigned* gemm_flags(Scratch& sc, mlra::PrepBatch& pb) {
+  constexpr int64_t n = 2 * mlra::kMaxSkPairs;
+  auto* f = sc.get<unsigned>(static_cast<size_t>(n));
+  if (f) pb.zero_f32(reinterpret_cast<float*>(f), n);
+  return f;
 }
 
 // out[m x r] = act[m x kd] · W   (K4 / K5a; W as planes). Optionally also the
@@ -1218,6 +1246,8 @@ mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, in
   if (mlra_status st = make_planes(sc, pb, L->b, d.cols, r, false, &bt)) return st;
   pb.pad(L->a, d.rows, r, r, 1.0f, apad, d.rows_pad, rp);
   if (mlra_status st = thin_ws(sc, pb, true, m, d.cols, r, false, &tw)) return st;
+  unsigned* flags = gemm_flags(sc, pb);
+  if (!flags) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
   CUDA_TRY(mlra::launch_prep(pb, s));
   // K4: xb = x·B (matmul(t, x, B), lora.cpp:68), finished with bf16(s·xb) zero
   // padded to rp columns: the extra-K LoRA operand of the GEMM
@@ -1234,6 +1264,7 @@ mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, in
   gp.ldo = ldy;
   gp.out_f32 = y_dtype == MLRA_F32;
   gp.bias = L->bias;
+  gp.sk_flags_zeroed = flags;
   // K2: y = x·Ŵᵀ + (s·xb)·Aᵀ + bias
   return run_gemm(L->q, L->strategy, L->hook, gp, sc);
 }
@@ -1282,6 +1313,8 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   if (mlra_status st = thin_ws(sc, pb, true, m, d.rows, r, false, &w_row)) return st;
   if (mlra_status st = thin_ws(sc, pb, false, m, d.rows, r, dbias != nullptr, &w_da)) return st;
   if (mlra_status st = thin_ws(sc, pb, false, m, d.cols, r, false, &w_db)) return st;
+  unsigned* flags = gemm_flags(sc, pb);
+  if (!flags) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
   CUDA_TRY(mlra::launch_prep(pb, s));
   // K5a: dyA = dy·A ; d(xb) = s·dyA (autodiff.cpp:150-152 on record lora.cpp:69),
   // finished with bf16(s·dyA) (the dX GEMM's extra-K operand) and dyA's
@@ -1319,6 +1352,8 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   gp.out = dx;
   gp.ldo = lddx;
   gp.out_f32 = dx_dtype == MLRA_F32;
+  gp.sk_flags_zeroed = flags;
+  gp.no_pdl = side != nullptr;
   // K3: dx = dy·Ŵ + (s·dyA)·Bᵀ   (lp_backward + matmul-bwd dx, lora.cpp:68)
   const mlra_status gst = run_gemm(L->q, L->strategy, L->hook, gp, sc);
   // join: the caller's stream (and the scratch frees queued on it) waits for dA/dB

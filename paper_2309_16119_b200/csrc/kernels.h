@@ -11,6 +11,28 @@ namespace mlra {
 // Counts every kernel this library launches (mlra_kernel_launches()).
 void note_launch();
 
+// Programmatic dependent launch for the layer-pass kernels (prep, skinny
+// products, fused GEMMs): the kernel may start while its stream predecessor
+// drains and synchronises with it through pdl_wait (ptx.cuh). MLRA_PDL=0
+// launches them classically (A/B switch).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 cudaError_t launch_relayout(const uint32_t* src, int64_t rows, int64_t cols, int bits,
                             int64_t row_words, int64_t rows_pad, uint32_t* dst, cudaStream_t st);
 cudaError_t launch_grid(const float* scales, const float* zeros, int64_t rows, int64_t ng,

@@ -31,6 +31,17 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
                : "memory");
 }
+// Programmatic dependent launch (the layer-pass kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, launch_pdl in kernels.h):
+// pdl_trigger lets the next kernel of the stream start its prologue; pdl_wait
+// blocks until the previous kernel has completed and its writes are visible.
+// Every PDL-launched kernel calls pdl_wait before touching anything an
+// earlier kernel of the stream may have written (transitively safe: a kernel
+// cannot complete before its own pdl_wait returned).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

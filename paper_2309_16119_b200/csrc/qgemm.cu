@@ -116,6 +116,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  pdl_trigger();
+  pdl_wait();  // every operand may come from earlier kernels
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -431,14 +433,16 @@ cudaError_t launch_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs& 
                      cudaStream_t stream) {
   auto kern = qgemm_kernel<BITS, W_TMA, MN, OUT_F32, QTMA, TBN>;
   const int smem = qgemm1_smem_fixed(TBN) + p.q_stages * p.q_stage_bytes;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  static int smem_set = 0;  // per instantiation: the opt-in only ever grows
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
   const int64_t tiles = (p.m_total / BM) * ((p.tokens + TBN - 1) / TBN);
   const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  note_launch();
-  kern<<<grid, NUM_THREADS, smem, stream>>>(maps.act, maps.act_lora, maps.w, maps.w_lora,
-                                            maps.codes, maps.grid, q, p);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(NUM_THREADS), smem, stream, p.no_pdl == 0, maps.act, maps.act_lora,
+                    maps.w, maps.w_lora, maps.codes, maps.grid, q, p);
 }
 
 template <int BITS, bool W_TMA, bool QTMA, int TBN>

@@ -50,6 +50,8 @@ struct GemmArgs {
   // needs no division and stays on the uniform datapath.
   int sk_pairs;
   int split;             // > 0: split-K mode, S pairs per tile (pair q = tile*S + s)
+  int tok256;            // split-K with 256-token pair tiles (one accumulator)
+  int no_pdl;            // host only: launch without programmatic dependent launch
   float* sk_ws;          // [sk_pairs x 2 CTAs x 512 tokens x 128 rows] fp32 partials
   unsigned* sk_flags;    // [sk_pairs x 2], zeroed before the launch
   int sk_tile[129];

@@ -57,6 +57,8 @@ constexpr bool kDevTrace = false;
 constexpr uint32_t TMEM_COLS = 512;  // two N=256 accumulators
 constexpr int kFixChunkBytes = 32 * 128 * 4;  // one stream-K partial chunk: 32 tokens x 128 rows
 constexpr int kFixSlots = STAGES * (W_TILE + T_TILE) / kFixChunkBytes;  // staged in the idle ring
+constexpr int kSplitMaxS = 8;  // split-K ways: (S - 1) partial slabs of one chunk fit the ring
+static_assert(kSplitMaxS - 1 <= kFixSlots, "split-K fix-up ring");
 constexpr int HB = 128;            // tokens per CTA per accumulator (MMA N=256 split in two)
 constexpr int HB_TILE = HB * BK * 2;  // 16 KB
 constexpr int PAIR_ROWS = 2 * BM;  // 256 weight-side rows per pair tile
@@ -156,6 +158,170 @@ __device__ __forceinline__ void epi_bar_sync() {  // the 4 epilogue warps only
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
+// One drained chunk (32 tokens x this thread's weight row) -> output (+bias).
+// bf16 output, paired rows: lanes 2i / 2i+1 swap half their tokens with one
+// shfl.xor so each stores a 32-bit word (rows 2i, 2i+1) for one token; the
+// pointer advances by ldo words. Needs even ldo and a 4-byte aligned output
+// (p.out_pairs) and every row of the warp valid (`pairs`, warp-uniform);
+// otherwise the scalar path.
+template <bool OUT_F32>
+__device__ __forceinline__ void epi_store(const GemmArgs& p, const uint32_t (&r)[32], int64_t t0,
+                                          int64_t wrow, bool row_ok, float bias, float bias_nb,
+                                          bool pairs, bool odd) {
+  if constexpr (!OUT_F32) {
+    if (pairs && t0 + 32 <= p.tokens) {
+      const float b_lo = odd ? bias_nb : bias, b_hi = odd ? bias : bias_nb;
+      uint32_t* o = reinterpret_cast<uint32_t*>(
+          reinterpret_cast<__nv_bfloat16*>(p.out) + (t0 + odd) * p.ldo + (wrow & ~1ll));
+      const int64_t step = p.ldo;  // two tokens = ldo 32-bit words
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float ev = __uint_as_float(r[2 * k]), ov = __uint_as_float(r[2 * k + 1]);
+        const float mine = odd ? ov : ev;
+        const float other = __shfl_xor_sync(0xffffffffu, odd ? ev : ov, 1);
+        const float lo = odd ? other : mine, hi = odd ? mine : other;
+        *o = pack_bf16x2(lo + b_lo, hi + b_hi);
+        o += step;
+      }
+      return;
+    }
+  }
+  if (!row_ok) return;
+  if (t0 + 32 <= p.tokens) {
+    if constexpr (OUT_F32) {
+      float* o = reinterpret_cast<float*>(p.out) + t0 * p.ldo + wrow;
+#pragma unroll
+      for (int j = 0; j < 32; ++j, o += p.ldo) *o = __uint_as_float(r[j]) + bias;
+    } else {
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + t0 * p.ldo + wrow;
+#pragma unroll
+      for (int j = 0; j < 32; ++j, o += p.ldo) *o = __float2bfloat16_rn(__uint_as_float(r[j]) + bias);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (t0 + j < p.tokens) {
+        const float v = __uint_as_float(r[j]) + bias;
+        if constexpr (OUT_F32)
+          reinterpret_cast<float*>(p.out)[(t0 + j) * p.ldo + wrow] = v;
+        else
+          reinterpret_cast<__nv_bfloat16*>(p.out)[(t0 + j) * p.ldo + wrow] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+// Split-K fix-up (p.split = S > 0: every pair runs one (tile, k-range) unit),
+// run by all 16 warps of the CTA once its MMAs are complete. The S pairs of a
+// tile each own 16/S of its 16 token chunks (32 tokens x 128 rows). Warp w
+// reads TMEM lane quadrant w & 3 and takes chunks w >> 2, +4, ...:
+//  1. non-owned chunks -> this pair's fp32 partial slots (coalesced rows);
+//  2. publish (one release after a CTA barrier), acquire the tile's other pairs;
+//  3. one thread stages every (owned chunk, other pair) 16 KB slab into the
+//     idle operand ring with cp.async.bulk (all in flight at once, rounds only
+//     when they exceed the ring), and each owned chunk is summed in pair order
+//     (deterministic: identical bits for identical inputs) with the TMEM
+//     accumulator and stored.
+template <bool OUT_F32>
+__device__ __forceinline__ void split_fixup(const GemmArgs& p, int cid, uint32_t rank, int m_pairs,
+                                            uint32_t tmem_base, uint64_t* tfull, uint64_t* fixb,
+                                            uint8_t* smem, unsigned long long* tl) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qd = warp & 3, wg = warp >> 2;
+  mbar_wait_backoff<EPI_NS>(tfull, 0);
+  tc_fence_after();
+  if (tl && threadIdx.x == 0) tl[2] = gtime();
+  const int S = p.split;
+  const int tile = cid / S, q0 = tile * S, sidx = cid - q0;
+  const int mp = tile % m_pairs, np = tile / m_pairs;
+  const int nch = p.tok256 ? 8 : 16;  // 32-token chunks per tile
+  const int tok_tile = 32 * nch;
+  const int c0 = nch * sidx / S, c1 = nch * (sidx + 1) / S;
+  const int r_in = qd * 32 + lane;
+  const int64_t wrow = static_cast<int64_t>(mp) * PAIR_ROWS + rank * BM + r_in;
+  const bool row_ok = wrow < p.m_valid;
+  const uint32_t taddr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
+  auto slot_of = [&](int q, int cc) {  // [512 tokens][128 rows] fp32 per CTA
+    return p.sk_ws + (2 * static_cast<int64_t>(q) + rank) * (PAIR_TOK * BM) +
+           static_cast<int64_t>(cc * 32) * BM;
+  };
+  // 1. partials of the chunks other pairs own
+  for (int cc = wg; cc < nch; cc += 4) {
+    if (cc >= c0 && cc < c1) continue;
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr + cc * 32, r);
+    tc_wait_ld();
+    if (row_ok) {
+      float* d = slot_of(cid, cc) + r_in;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) d[j * BM] = __uint_as_float(r[j]);
+    }
+  }
+  // 2. publish: the CTA barrier orders every thread's partial stores before one
+  // thread's gpu-scope release (cumulative); it acquires the other pairs' flags
+  __syncthreads();
+  if (tl && threadIdx.x == 0) tl[5] = gtime();
+  if (threadIdx.x == 0) {
+    st_release_gpu(&p.sk_flags[2 * cid + rank], 1u);
+    for (int q = q0; q < q0 + S; ++q)
+      if (q != cid)
+        while (ld_acquire_gpu(&p.sk_flags[2 * q + rank]) == 0) __nanosleep(32);
+    fence_proxy_async_global();  // acquired partials (generic writes) -> async-proxy reads
+    if (tl) tl[3] = gtime();
+  }
+  const float bias = (p.bias != nullptr && row_ok) ? p.bias[wrow] : 0.0f;
+  const float bias_nb = __shfl_xor_sync(0xffffffffu, bias, 1);
+  const bool odd = lane & 1;
+  const bool pairs = p.out_pairs && __all_sync(0xffffffffu, (wrow | 1) < p.m_valid);
+  const int nq = S - 1, nc = c1 - c0;
+  // owned chunks staged per round (S <= kSplitMaxS); S == 1: whole tiles, no partials
+  const int per_round = nq > 0 ? kFixSlots / nq : nc;
+  const uint32_t ring = smem_u32(smem);
+  int round = 0;
+  for (int b0 = 0; b0 < nc; b0 += per_round, ++round) {
+    const int nb = nc - b0 < per_round ? nc - b0 : per_round;
+    __syncthreads();  // the ring is free (round 0: every MMA has completed; else: consumed)
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < nb; ++i)
+        for (int k = 0; k < nq; ++k) {
+          const int q = q0 + k + (k >= sidx ? 1 : 0), slot = i * nq + k;
+          mbar_arrive_expect_tx(&fixb[slot], kFixChunkBytes);
+          bulk_g2s(ring + slot * kFixChunkBytes, slot_of(q, c0 + b0 + i), kFixChunkBytes,
+                   &fixb[slot]);
+        }
+    }
+    for (int i = wg; i < nb; i += 4) {
+      const int cc = c0 + b0 + i;
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + cc * 32, r);
+      tc_wait_ld();
+      float acc[32];
+      for (int qi = 0; qi < S; ++qi) {  // pair order
+        if (qi == sidx) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            acc[j] = qi == 0 ? __uint_as_float(r[j]) : acc[j] + __uint_as_float(r[j]);
+        } else {
+          const int slot = i * nq + qi - (qi > sidx ? 1 : 0);
+          mbar_wait(&fixb[slot], static_cast<uint32_t>(round & 1));
+          if (tl && round == 0 && i == 0 && lane == 0 && warp == 0) tl[7] = gtime();
+          const float* src = reinterpret_cast<const float*>(smem + slot * kFixChunkBytes) + r_in;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] = qi == 0 ? src[j * BM] : acc[j] + src[j * BM];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(acc[j]);
+      epi_store<OUT_F32>(p, r, static_cast<int64_t>(np) * tok_tile + cc * 32, wrow, row_ok, bias,
+                         bias_nb, pairs, odd);
+    }
+  }
+  if (tl) {
+    __syncthreads();
+    if (threadIdx.x == 0) tl[4] = gtime();
+  }
+}
+
 template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA, bool SK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     qgemm2_kernel(const __grid_constant__ CUtensorMap tm_act,
@@ -199,7 +365,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int n_kb_main = p.n_kb_main;
   const int n_kb = p.n_kb_main + p.n_kb_lora;
   const int m_pairs = static_cast<int>(p.m_total / PAIR_ROWS);
-  const int n_pairs = static_cast<int>((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
+  // split-K plans may use 256-token pair tiles (one accumulator, half the
+  // partial volume per split; p.tok256)
+  const bool one_acc = SK && p.tok256;
+  const int tok_tile = one_acc ? PAIR_TOK / 2 : PAIR_TOK;
+  const int n_pairs = static_cast<int>((p.tokens + tok_tile - 1) / tok_tile);
   const int n_tiles = m_pairs * n_pairs;
   SegSched<SK> sched;
   sched.init(p, cid, ncl, n_tiles, n_kb);
@@ -237,6 +407,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc2(tmem_slot, TMEM_COLS);
+  pdl_trigger();
+  pdl_wait();  // every operand (activations, LoRA planes, flags) may come from earlier kernels
   if constexpr (E8P) {  // stage the 8 KB e8p tables + odd bits
     for (int i = threadIdx.x; i < (2 * 256 * 16 + 32) / 16; i += NUM_THREADS)
       reinterpret_cast<uint4*>(sCb)[i] = __ldg(reinterpret_cast<const uint4*>(p.cb2_codebook) + i);
@@ -269,12 +441,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           mbar_wait_backoff<PROD_NS>(&empty[s], ph ^ 1);
           const bool lora = kb >= n_kb_main;
           const bool w_tma = lora || W_TMA;
-          if (leader) mbar_arrive_expect_tx(&full[s], 2 * (T_TILE + (w_tma ? W_TILE : 0)));
+          if (leader)
+            mbar_arrive_expect_tx(&full[s],
+                                  2 * ((one_acc ? HB_TILE : T_TILE) + (w_tma ? W_TILE : 0)));
           uint8_t* st = sT + s * T_TILE;
           uint8_t* sw = sW + s * W_TILE;
 #pragma unroll
           for (int a = 0; a < 2; ++a) {
-            const int tok = np * PAIR_TOK + a * 2 * HB + static_cast<int>(rank) * HB;
+            if (a == 1 && one_acc) break;
+            const int tok = np * tok_tile + a * 2 * HB + static_cast<int>(rank) * HB;
             if (!lora)
               tma_load_2d_2sm(st + a * HB_TILE, &tm_act, &full[s], kb * BK, tok);
             else
@@ -340,6 +515,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         // (tempty): the first `pre` k-blocks' accumulator-0 MMAs of this tile
         // run while accumulator 1 is still being drained; their stages are
         // released once accumulator 1's MMAs for them follow (tempty1).
+        if (one_acc) {  // (split-K only) one 256-token accumulator per tile
+          mbar_wait_acq_cluster(tempty, (sg & 1) ^ 1);
+          tc_fence_after();
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait_acq_cluster(&full[s], ph);
+            tc_fence_after();
+            issue(s, kb, kb0, 0, 0);
+            tc_commit_2sm_mc(&empty[s], 0x3);
+            if (++s == STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          tc_commit_2sm_mc(tfull, 0x3);
+          continue;
+        }
         const int pre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
         const unsigned long long tw0 = (kDevTrace && p.trace) ? clock64() : 0;
         mbar_wait_acq_cluster(tempty, (sg & 1) ^ 1);
@@ -433,12 +624,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int local = 0;
     SegSched<SK> sc = sched;
     int tile, kb0, kb1;
-    for (; sc.next(tile, kb0, kb1); ++local) {
+    // split-K: every warp of the CTA runs the fix-up after its role (below)
+    for (; !(SK && p.split > 0) && sc.next(tile, kb0, kb1); ++local) {
       const int mp = tile % m_pairs, np = tile / m_pairs;
       // stream-K roles: a segment starting mid-tile writes a partial; one that
       // starts at k-block 0 but ends early adds pairs [cid+1, q_end)'s partials
       const bool contrib = SK && kb0 != 0;
-      const bool split = SK && p.split > 0;  // split-K: one (tile, k-range) unit per pair
+      constexpr bool split = false;  // split-K runs in split_fixup (all warps)
       const int q_end = (SK && !split && !contrib && kb1 != n_kb) ? SegSched<SK>::contrib_end(p, cid, tile)
                                                             : cid + 1;
       const int r_in = qd * 32 + lane;
@@ -453,58 +645,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (tl && qd == 0 && lane == 0) tl[3] = gtime();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
       const int64_t tbase = static_cast<int64_t>(np) * PAIR_TOK;
-      // bf16 output, paired rows: lanes 2i / 2i+1 swap half their tokens with one
-      // shfl.xor so each stores a 32-bit word (rows 2i, 2i+1) for one token; the
-      // pointer advances by ldo words. Needs even ldo and a 4-byte aligned output
-      // (p.out_pairs) and every row of the warp valid; otherwise the scalar path.
       const float bias_nb = __shfl_xor_sync(0xffffffffu, bias, 1);
       const bool odd = lane & 1;
       const bool pairs = p.out_pairs && __all_sync(0xffffffffu, (wrow | 1) < p.m_valid);
       auto store_chunk = [&](const uint32_t(&r)[32], int cc) {
-        const int64_t t0 = tbase + cc * 32;
-        if constexpr (!OUT_F32) {
-          if (pairs && t0 + 32 <= p.tokens) {
-            const float b_lo = odd ? bias_nb : bias, b_hi = odd ? bias : bias_nb;
-            uint32_t* o = reinterpret_cast<uint32_t*>(
-                reinterpret_cast<__nv_bfloat16*>(p.out) + (t0 + odd) * p.ldo + (wrow & ~1ll));
-            const int64_t step = p.ldo;  // two tokens = ldo 32-bit words
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float ev = __uint_as_float(r[2 * k]), ov = __uint_as_float(r[2 * k + 1]);
-              const float mine = odd ? ov : ev;
-              const float other = __shfl_xor_sync(0xffffffffu, odd ? ev : ov, 1);
-              const float lo = odd ? other : mine, hi = odd ? mine : other;
-              *o = pack_bf16x2(lo + b_lo, hi + b_hi);
-              o += step;
-            }
-            return;
-          }
-        }
-        if (!row_ok) return;
-        if (t0 + 32 <= p.tokens) {
-          if constexpr (OUT_F32) {
-            float* o = reinterpret_cast<float*>(p.out) + t0 * p.ldo + wrow;
-#pragma unroll
-            for (int j = 0; j < 32; ++j, o += p.ldo) *o = __uint_as_float(r[j]) + bias;
-          } else {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + t0 * p.ldo + wrow;
-#pragma unroll
-            for (int j = 0; j < 32; ++j, o += p.ldo)
-              *o = __float2bfloat16_rn(__uint_as_float(r[j]) + bias);
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (t0 + j < p.tokens) {
-              const float v = __uint_as_float(r[j]) + bias;
-              if constexpr (OUT_F32)
-                reinterpret_cast<float*>(p.out)[(t0 + j) * p.ldo + wrow] = v;
-              else
-                reinterpret_cast<__nv_bfloat16*>(p.out)[(t0 + j) * p.ldo + wrow] =
-                    __float2bfloat16_rn(v);
-            }
-          }
-        }
+        epi_store<OUT_F32>(p, r, tbase + cc * 32, wrow, row_ok, bias, bias_nb, pairs, odd);
       };
       // stream-K partial slots of this CTA's rows: [512 tokens][128 rows] fp32
       auto slot_of = [&](int q, int cc) {
@@ -540,88 +685,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (cc + 2 < 16) tc_wait_ld();
         }
       };
-      if (split) {
-        // Split-K with a distributed fix-up: the S pairs of a tile each own
-        // 16/S of its 16 token chunks. Each drains the chunks it does not own
-        // as fp32 partials, publishes, waits for the tile's other pairs, then
-        // finishes its own chunks: its TMEM accumulator (no further segment
-        // overwrites it) plus the others' partials staged into its idle
-        // operand ring by bulk copies, summed in pair order (deterministic).
-        // Every pair reads ~(S-1)/S of one tile's partials instead of one
-        // owner reading all of them (the stream-K fix-up's tail).
-        const int S = p.split, q0 = tile * S, sidx = cid - q0;
-        const int c0 = 16 * sidx / S, c1 = 16 * (sidx + 1) / S;
-        drain([&](uint32_t(&r)[32], int cc) {
-          if (!row_ok || (cc >= c0 && cc < c1)) return;
-          float* d = slot_of(cid, cc);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) d[j * BM] = __uint_as_float(r[j]);
-        });
-        if (tl && qd == 0 && lane == 0) tl[5] = gtime();
-        // publish: bar.sync orders the 128 threads' partial stores before one
-        // thread's gpu-scope release (cumulative); one thread acquires the other
-        // pairs' flags and the second bar.sync passes that on (per-thread fences
-        // and 128 spinning threads cost ~1 + ~3.5 us here)
-        epi_bar_sync();
-        const bool issuer = qd == 0 && lane == 0;
-        if (issuer) {
-          st_release_gpu(&p.sk_flags[2 * cid + rank], 1u);
-          if (tl) tl[6] = gtime();
-          for (int q = q0; q < q0 + S; ++q)
-            if (q != cid)
-              while (ld_acquire_gpu(&p.sk_flags[2 * q + rank]) == 0) __nanosleep(32);
-        }
-        epi_bar_sync();
-        if (tl && issuer) tl[3] = gtime();
-        // staged slots: kFixSlots - 1 for the others' chunks, the last one is
-        // each thread's private spill of its own row of the current chunk (so
-        // only one 32-register chunk stays live: the kernel runs at the
-        // 128-register cap)
-        const int nq = S - 1, nc = c1 - c0, nslots = kFixSlots - 1;
-        const int depth = nslots / nq < nc ? (nslots / nq > 0 ? nslots / nq : 1) : nc;
-        const uint32_t ring = smem_u32(smem);
-        float* own_row = reinterpret_cast<float*>(smem + nslots * kFixChunkBytes) + r_in;
-        auto issue = [&](int ci) {
-          for (int i = 0; i < nq; ++i) {
-            const int q = q0 + i + (i >= sidx ? 1 : 0);
-            const int jb = ci * nq + i, slot = jb % nslots;
-            mbar_arrive_expect_tx(&fixb[slot], kFixChunkBytes);
-            bulk_g2s(ring + slot * kFixChunkBytes, slot_of(q, c0 + ci) - r_in, kFixChunkBytes,
-                     &fixb[slot]);
-          }
-        };
-        if (issuer) {
-          fence_proxy_async_global();  // acquired partials (generic writes) -> async-proxy reads
-          for (int ci = 0; ci < depth; ++ci) issue(ci);
-        }
-        for (int ci = 0; ci < nc; ++ci) {
-          const int cc = c0 + ci;
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + cc * 32, r);
-          tc_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) own_row[j * BM] = __uint_as_float(r[j]);
-          for (int qi = 0; qi < S; ++qi) {  // pair order
-            const float* src;
-            if (qi == sidx) {
-              src = own_row;
-            } else {
-              const int i = qi - (qi > sidx ? 1 : 0);
-              const int jb = ci * nq + i, slot = jb % nslots;
-              mbar_wait(&fixb[slot], static_cast<uint32_t>(jb / nslots) & 1u);
-              if (tl && issuer && ci == 0 && i == nq - 1) tl[7] = gtime();
-              src = reinterpret_cast<const float*>(smem + slot * kFixChunkBytes) + r_in;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              r[j] = qi == 0 ? __float_as_uint(src[j * BM])
-                             : __float_as_uint(__uint_as_float(r[j]) + src[j * BM]);
-          }
-          store_chunk(r, cc);
-          epi_bar_sync();  // every epilogue thread is done with this chunk's slots
-          if (issuer && ci + depth < nc) issue(ci + depth);
-        }
-      } else if (contrib) {
+      if (contrib) {
         drain([&](uint32_t(&r)[32], int cc) {
           if (!row_ok) return;
           float* d = slot_of(cid, cc);
@@ -816,6 +880,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   }
 
+  if constexpr (SK) {
+    if (p.split > 0) {
+      __syncwarp();
+      split_fixup<OUT_F32>(p, cid, rank, m_pairs, tmem_base, tfull, fixb, smem, tl);
+    }
+  }
+
   tc_fence_before();
   cluster_sync();
   if (warp == 1) tmem_dealloc2(tmem_base, TMEM_COLS);
@@ -839,14 +910,17 @@ cudaError_t launch2_t(const GemmMaps& maps, const QWeightDev& q, const GemmArgs&
                    (BITS == kCb2Bits ? kCb2SmemBytes
                                      : (BITS == kE8pBits ? kE8pSmemBytes
                                                          : (is_lut<BITS>() ? kLutSmemBytes : 0)));
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  static int smem_set = 0;  // per instantiation: the opt-in only ever grows
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
   const int64_t tiles = (p.m_total / PAIR_ROWS) * ((p.tokens + PAIR_TOK - 1) / PAIR_TOK);
   const int64_t pairs = p.sk_pairs ? p.sk_pairs : (tiles < sm_total() / 2 ? tiles : sm_total() / 2);
-  note_launch();
-  kern<<<static_cast<unsigned>(2 * pairs), NUM_THREADS, smem, stream>>>(
-      maps.act, maps.act_lora, maps.w, maps.w_lora, maps.codes, maps.grid, q, p);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(NUM_THREADS), smem, stream,
+                    p.no_pdl == 0,
+                    maps.act, maps.act_lora, maps.w, maps.w_lora, maps.codes, maps.grid, q, p);
 }
 
 template <bool MN, bool SK, int BITS, bool W_TMA, bool QTMA>

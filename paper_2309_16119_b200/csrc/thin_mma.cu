@@ -285,6 +285,12 @@ __global__ void __launch_bounds__(TTHREADS, 3)
   if (threadIdx.x == 0) {
     for (int s = 0; s < TNS; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
+    tma_prefetch_desc(&act_map);
+    tma_prefetch_desc(&fac_map);
+  }
+  pdl_trigger();
+  pdl_wait();  // activations / factor planes / counters come from earlier kernels
+  if (threadIdx.x == 0) {
     for (int c = 0; c < TNS - 1; ++c)
       if (u0 + c < u1) issue(u0 + c, c);
   }
@@ -352,6 +358,12 @@ __global__ void __launch_bounds__(TTHREADS, 3)
   if (threadIdx.x == 0) {
     for (int s = 0; s < TNS; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
+    tma_prefetch_desc(&act_map);
+    tma_prefetch_desc(&fac_map);
+  }
+  pdl_trigger();
+  pdl_wait();  // activations / factor planes / counters come from earlier kernels
+  if (threadIdx.x == 0) {
     for (int c = 0; c < TNS - 1; ++c)
       if (u0 + c < u1) issue(u0 + c, c);
   }
@@ -399,6 +411,8 @@ __global__ void __launch_bounds__(TTHREADS, 3)
 // computed), so each block resolves its task once and runs a 32-bit
 // grid-stride loop over that task's index space.
 __global__ void __launch_bounds__(256) k_prep(const PrepBatch b, const PrepBlocks pbk) {
+  pdl_trigger();
+  pdl_wait();
   int t = 0;
   while (static_cast<int>(blockIdx.x) >= pbk.first[t + 1]) ++t;
   const PrepTask& k = b.t[t];
@@ -542,10 +556,8 @@ cudaError_t rowmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   if (ctas <= 0 || o.ws_floats < static_cast<int64_t>(ctas) * 2 * TM * ROWS)
     return cudaErrorInvalidValue;
   o.rc = static_cast<int>(r);
-  note_launch();
-  k_rowmma<NT><<<ctas, TTHREADS, smem, st>>>(am, fm, m, static_cast<int>(kchunks),
-                                             static_cast<int>(units), o);
-  return cudaGetLastError();
+  return launch_pdl(k_rowmma<NT>, dim3(ctas), dim3(TTHREADS), smem, st, true, am, fm, m,
+                    static_cast<int>(kchunks), static_cast<int>(units), o);
 }
 
 template <int NT>
@@ -568,10 +580,8 @@ cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   if (ctas <= 0 || o.ws_floats < static_cast<int64_t>(ctas) * 2 * TM * ROWS)
     return cudaErrorInvalidValue;
   o.rc = static_cast<int>(r);
-  note_launch();
-  k_colmma<NT><<<ctas, TTHREADS, smem, st>>>(am, fm, nd, static_cast<int>(tchunks),
-                                             static_cast<int>(units), o);
-  return cudaGetLastError();
+  return launch_pdl(k_colmma<NT>, dim3(ctas), dim3(TTHREADS), smem, st, true, am, fm, nd,
+                    static_cast<int>(tchunks), static_cast<int>(units), o);
 }
 
 }  // namespace
@@ -590,9 +600,7 @@ cudaError_t launch_prep(const PrepBatch& b, cudaStream_t st) {
   }
   pbk.first[b.n] = nb;
   if (nb == 0) return cudaSuccess;
-  note_launch();
-  k_prep<<<nb, 256, 0, st>>>(b, pbk);
-  return cudaGetLastError();
+  return launch_pdl(k_prep, dim3(nb), dim3(256), 0, st, true, b, pbk);
 }
 
 int thin_rows(int64_t r, bool ones) { return static_cast<int>((r + (ones ? 1 : 0) + 7) / 8 * 8); }

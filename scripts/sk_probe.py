@@ -13,7 +13,7 @@ import torch
 from paper_2309_16119_b200 import modulora as M
 from scripts.quick_perf import make_layer
 
-MODES = {"sk0": ("2", "0"), "sk1": ("2", "1"), "sk2": ("2", "2"), "split": ("2", "4"), "cta1": ("1", "2"), "cta128": ("3", "2"), "auto": ("", "2")}
+MODES = {"sk0": ("2", "0"), "sk1": ("2", "1"), "sk2": ("2", "2"), "split": ("2", "4"), "split256": ("2", "5"), "cta1": ("1", "2"), "cta128": ("3", "2"), "auto": ("", "2")}
 ms_list = [int(v) for v in os.environ.get("MS", "512,1024,2048").split(",")]
 shapes = [(4096, 4096, 4), (11008, 4096, 3), (4096, 11008, 3)]
 for d_out, d_in, bits in shapes:

@@ -42,7 +42,8 @@ pytestmark = pytest.mark.gpu
 ROW = M.MaterializationStrategy.RowMaterialize
 SCHEDULES = {"default": {}, "whole": {"MLRA_SK": "0", "MLRA_GEMM": "2"},
              "streamk": {"MLRA_SK": "1", "MLRA_GEMM": "2"},
-             "splitk": {"MLRA_SK": "4", "MLRA_GEMM": "2"}}
+             "splitk": {"MLRA_SK": "4", "MLRA_GEMM": "2"},
+             "splitk256": {"MLRA_SK": "5", "MLRA_GEMM": "2"}}
 
 
 def _setenv(monkeypatch, env):
@@ -218,6 +219,6 @@ def test_cfg1_single_layer_all_kernels(monkeypatch):
     x = _act(70, 512, 4096)
     dy = _act(71, 512, 4096)
     for env in ({}, {"MLRA_GEMM": "1"}, {"MLRA_GEMM": "3"}, {"MLRA_GEMM": "2", "MLRA_SK": "1"},
-                {"MLRA_GEMM": "2", "MLRA_SK": "4"}):
+                {"MLRA_GEMM": "2", "MLRA_SK": "4"}, {"MLRA_GEMM": "2", "MLRA_SK": "5"}):
         _setenv(monkeypatch, env)
         lin.check(x, dy, lin.run(x, dy), f"cfg1 {env}")

@@ -292,13 +292,15 @@ def test_stream_k_matches_whole_tiles(rows, cols, m, bits, mn, monkeypatch):
     f = M.lp_backward if mn else M.lp_forward
     monkeypatch.setenv("MLRA_GEMM", "2")
     outs = {}
-    for sk in ("0", "1", "4"):  # whole tiles, stream-K, split-K (distributed fix-up)
+    # whole tiles, stream-K, split-K on 512- and on 256-token tiles (all-warp fix-up)
+    for sk in ("0", "1", "4", "5"):
         monkeypatch.setenv("MLRA_SK", sk)
         outs[sk] = f64(f(ctx, a, out_dtype=torch.float32))
-    assert rel_fro(outs["1"], outs["0"]) <= 1e-5  # fp32 order across the cut (~sqrt(K) ulp)
-    assert rel_fro(outs["4"], outs["0"]) <= 1e-5
-    monkeypatch.setenv("MLRA_SK", "4")
-    assert np.array_equal(f64(f(ctx, a, out_dtype=torch.float32)), outs["4"])
+    for sk in ("1", "4", "5"):
+        assert rel_fro(outs[sk], outs["0"]) <= 1e-5  # fp32 order across the cut (~sqrt(K) ulp)
+    for sk in ("4", "5"):  # the split fix-up adds partials in pair order: repeatable
+        monkeypatch.setenv("MLRA_SK", sk)
+        assert np.array_equal(f64(f(ctx, a, out_dtype=torch.float32)), outs[sk])
     wbf = deq_bf16_f64(words, rows, cols, bits, 128, sc, z)
     ref = f64(a) @ (wbf if mn else wbf.T)
     assert rel_fro(outs["1"], ref) <= 1e-5
@@ -319,7 +321,7 @@ def test_stream_k_layer_with_lora_and_bias(monkeypatch):
     g = to_bf16_dev(orc.bf16_round(orc.gaussian(82, m, d_out)))
     monkeypatch.setenv("MLRA_GEMM", "2")
     res = {}
-    for sk in ("0", "1", "4"):
+    for sk in ("0", "1", "4", "5"):
         monkeypatch.setenv("MLRA_SK", sk)
         ad = M.LoraAdapter(a=torch.from_numpy(a32).cuda(), b=torch.from_numpy(b32).cuda(), rank=r,
                            alpha=32.0)
@@ -328,7 +330,7 @@ def test_stream_k_layer_with_lora_and_bias(monkeypatch):
         y, xb = M.layer_forward(layer, x, out_dtype=torch.float32)
         dx = M.layer_backward(layer, x, xb, g, dx_dtype=torch.float32)
         res[sk] = (f64(y), f64(dx))
-    for sk in ("1", "4"):
+    for sk in ("1", "4", "5"):
         assert rel_fro(res[sk][0], res["0"][0]) <= 1e-5
         assert rel_fro(res[sk][1], res["0"][1]) <= 1e-5
 
