@@ -578,12 +578,15 @@ def main():
     gemm_flops = 2.0 * m * Lb.d_in() * Lb.d_out()
     peak_tf, peak_hbm, peak_src = _peaks()
     achieved = gemm_flops / (k_ms / 1e3) / 1e12
-    traffic = None
-    try:
+    traffic, traffic_split = None, None
+    try:  # ncu DRAM bytes of the same kernel at this workload (scripts/traffic.py)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
         if tj.get("workload") == w["name"]:
             traffic = tj.get("qgemm_dram_bytes_per_launch")
+            traffic_split = {k: {"dram": tj[k]["dram_read"] + tj[k]["dram_write"],
+                                 "algorithmic": tj[k]["alg_read"] + tj[k]["alg_write"]}
+                             for k in ("fwd", "dx") if k in tj}
     except Exception:
         pass
     flops = step_flops(w, m)
@@ -692,7 +695,7 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "qgemm2 (fused dequant tcgen05 GEMM)",
                          "layer": f"{w['layers'][big][0]} {Lb.d_out()}x{Lb.d_in()}",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "frac": achieved / peak_tf, "traffic": traffic, "traffic_by_launch": traffic_split,
                          "frac_sustained": (achieved / _sustained_peak()) if _sustained_peak() else None,
                          "frac_datasheet": achieved / DATASHEET_BF16_TFLOPS,
                          "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",

@@ -533,6 +533,13 @@ unsigned* gemm_flags(Scratch& sc, mlra::PrepBatch& pb) {
   return f;
 }
 
+// dev-only per-CTA timeline of the skinny kernels (MLRA_TRACE3 = device pointer
+// to 8 x CTAs u64, used only by a -DMLRA_DEV_TRACE build)
+unsigned long long* thin_trace() {
+  const char* e = getenv("MLRA_TRACE3");
+  return e ? reinterpret_cast<unsigned long long*>(strtoull(e, nullptr, 0)) : nullptr;
+}
+
 // out[m x r] = act[m x kd] · W   (K4 / K5a; W as planes). Optionally also the
 // padded bf16(pad_scale · out) operand [m x rp] and the transposed hi/lo planes
 // of out (tp, allocated by alloc_planes over m rows).
@@ -552,6 +559,7 @@ mlra_status rows_product(cudaStream_t st, const ThinWs& w, const __nv_bfloat16* 
       o.pad_cols = 64;
       o.pad_scale = pad_scale;
     }
+    o.trace = thin_trace();
     if (tp) {
       o.thi = tp->hi[c];
       o.ldt = tp->ldt;
@@ -572,6 +580,7 @@ mlra_status cols_product(cudaStream_t st, const ThinWs& w, const __nv_bfloat16* 
     o.ldo = r;
     o.scale = scale;
     o.colsum = c == 0 ? colsum : nullptr;
+    o.trace = thin_trace();
     o.ws = w.ws;
     o.ws_floats = w.ws_floats;
     o.cnt = w.cnt;

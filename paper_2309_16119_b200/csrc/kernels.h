@@ -162,6 +162,8 @@ struct ThinOut {
   int64_t ws_floats = 0;           // capacity of ws (checked against the launch's grid)
   int* cnt = nullptr;              // per-tile contributor counters, zero before the first
                                    // launch; the finisher resets its tile's counter to 0
+  unsigned long long* trace = nullptr;  // dev-only (-DMLRA_DEV_TRACE, MLRA_TRACE3): 8 globaltimer
+                                        // stamps per CTA
 };
 // Workspace of one launch: ws floats and counters (ints).
 void thin_ws_size(bool row, int64_t m, int64_t d, int64_t r, bool ones, int64_t* ws_floats,

@@ -38,6 +38,20 @@ namespace mlra {
 namespace {
 
 constexpr int TILE = 64;      // rows (tokens or n) per unit, and reduction chunk
+#ifdef MLRA_DEV_TRACE
+constexpr bool kThinTrace = true;
+#else
+constexpr bool kThinTrace = false;
+#endif
+// dev timeline (MLRA_TRACE3): per CTA [0] entry, [1] first unit landed, [2] last unit's MMAs
+// done, [3] exit, [4] 1 if this CTA finished a tile, [5] finisher start
+__device__ __forceinline__ void thin_stamp(const ThinOut& o, int k) {
+  if (kThinTrace && o.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    o.trace[8 * blockIdx.x + k] = t;
+  }
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -102,6 +116,12 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ int ld_acquire_gpu_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
   asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -117,17 +137,29 @@ __device__ __forceinline__ int first_tile_of(int c, int64_t units, int64_t G, in
   return static_cast<int>(c * units / G) / chunks;
 }
 
-// Flush of one output tile (all threads of the CTA, uniform): the fragment
+// Flush of one output tile (all threads of the CTA, uniform). The fragment
 // partials go to this CTA's slot (slot 0 when `tile` is the first tile of its
-// range, else slot 1; row-major [TM rows][ROWS cols], the output's own order);
-// when every contributor has written (counter), the last one sums the slots in
-// CTA order and stores.
+// range, else slot 1; row-major [TM rows][ROWS cols], the output's own order).
+// A tile covered by one CTA is finished by it at once. A shared tile (CTAs
+// c_lo..c_hi) is reduced by its PARTICIPANTS — the contributors whose range
+// ends in it (c_lo..c_hi-1, plus c_hi when its range also ends here), which
+// all reach it at about the kernel's end: every contributor arrives on the
+// tile's counter (acq_rel); each participant waits for all arrivals, then
+// reduces its own 1/n_part of the tile's float4 positions over every
+// contributor's slot (contributor groups per position combined in a fixed
+// order through shared memory: deterministic) and writes that piece of the
+// outputs. (The last arriver summing every slot alone was the launch's tail:
+// ~7 us at 512 tokens with 64 contributors per tile, scripts/thin_timeline.py.)
+// The last departing participant resets the tile's counters for the next
+// launch. Waiting needs every CTA of the grid resident: one wave (thin_ctas).
 template <int NT>
 __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
-                           const ThinOut& o, int64_t n_out) {
+                           const ThinOut& o, int64_t n_out, bool last, float4* scratch) {
   constexpr int ROWS = 8 * NT;
   constexpr int SLOT = TM * ROWS;
-  __shared__ int s_last;
+  constexpr int C4 = ROWS / 4;        // float4s per slot row
+  constexpr int P = SLOT / 4;         // float4 positions per tile
+  constexpr int QB = 4;               // loads in flight per thread (x float4)
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -143,70 +175,56 @@ __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
   }
   const int c_lo = cta_of_unit(static_cast<int64_t>(tile) * chunks, units, G);
   const int c_hi = cta_of_unit(static_cast<int64_t>(tile + 1) * chunks - 1, units, G);
+  const int n_con = c_hi - c_lo + 1;
+  int n_part = 1, k_part = 0;
+  int* arrive = o.cnt + tile;
+  int* depart = o.cnt + units / chunks + tile;
   // bar.sync orders the CTA's slot stores before thread 0's acq_rel atomic (a
-  // cumulative gpu-scope release); the finisher's thread 0 acquires every other
+  // cumulative gpu-scope release); a participant's thread 0 acquires every
   // contributor's release through the same counter and the second bar.sync
   // passes that on to its threads, whose L2 (.cg) loads then see the slots.
-  // (A per-thread __threadfence() here is a fence.sc per thread: measured
-  // ~3x slower for the whole kernel.)
   __syncthreads();
-  if (c_lo != c_hi) {
-    if (threadIdx.x == 0) {
-      const int old = atom_add_acq_rel_gpu(o.cnt + tile, 1);
-      s_last = old == c_hi - c_lo;
-      if (s_last) o.cnt[tile] = 0;  // self-resetting for the next launch on this stream
-    }
+  if (n_con > 1) {
+    const int hi_last = (static_cast<int>(static_cast<int64_t>(c_hi + 1) * units / G) - 1) / chunks;
+    n_part = n_con - (hi_last == tile ? 0 : 1);
+    if (threadIdx.x == 0) atom_add_acq_rel_gpu(arrive, 1);
+    if (!last) return;  // c == c_hi continuing past this tile: contributes only
+    k_part = c - c_lo;
+    thin_stamp(o, 5);
+    if (threadIdx.x == 0)
+      while (ld_acquire_gpu_s32(arrive) < n_con) __nanosleep(64);
     __syncthreads();
-    if (!s_last) return;
+    if (kThinTrace && o.trace && threadIdx.x == 0) o.trace[8 * blockIdx.x + 4] = 1;
   }
-  // Finisher: v(row, j) = Σ_{q = c_lo..c_hi} slot_q(row, j), in CTA order. Every
-  // contributor after c_lo starts its range inside this tile, so its slot is 0;
-  // c_lo's is 0 only when the tile is its first. The finisher is the launch's
-  // tail, so it is built for memory-level parallelism and coalescing: each
-  // thread owns PER float4s = 4 consecutive columns of one row, keeps QB·PER
-  // loads in flight, and stores row-major (16-B fp32 / 8-B bf16 stores; measured:
-  // scattered 4-B stores made the tail ~10 us of a 28 us launch).
-  constexpr int C4 = ROWS / 4;                  // float4s per slot row
-  constexpr int PER = SLOT / (4 * TTHREADS);    // float4 positions per thread (= NT)
-  static_assert(SLOT % (4 * TTHREADS) == 0, "slot must tile the CTA in float4s");
-  constexpr int QB = 8 / PER > 0 ? 8 / PER : 1;
-  const float* s0 = o.ws + (static_cast<int64_t>(c_lo) * 2 +
-                            (tile == first_tile_of(c_lo, units, G, chunks) ? 0 : 1)) * SLOT;
-  float4 acc4[PER];
+  // this participant's positions [p0, p1) of the tile, over contributors c_lo..c_hi
+  const int p0 = k_part * P / n_part, p1 = (k_part + 1) * P / n_part, pc = p1 - p0;
+  auto slot_of = [&](int q) {
+    const int wq = (q == c_lo && tile != first_tile_of(c_lo, units, G, chunks)) ? 1 : 0;
+    return reinterpret_cast<const float4*>(o.ws + (static_cast<int64_t>(q) * 2 + wq) * SLOT);
+  };
+  auto sum_over = [&](int p, int q_first, int q_step, float4& s) {  // contributors in order
+    s = __ldcg(slot_of(q_first) + p);
+    for (int q0 = q_first + q_step; q0 <= c_hi; q0 += QB * q_step) {
+      float4 buf[QB];
 #pragma unroll
-  for (int k = 0; k < PER; ++k)
-    acc4[k] = __ldcg(reinterpret_cast<const float4*>(s0) + threadIdx.x + k * TTHREADS);
-  for (int q0 = c_lo + 1; q0 <= c_hi; q0 += QB) {
-    float4 buf[QB][PER];
+      for (int i = 0; i < QB; ++i)
+        if (q0 + i * q_step <= c_hi) buf[i] = __ldcg(slot_of(q0 + i * q_step) + p);
 #pragma unroll
-    for (int i = 0; i < QB; ++i) {
-      if (q0 + i <= c_hi) {
-        const float4* p = reinterpret_cast<const float4*>(o.ws + static_cast<int64_t>(q0 + i) * 2 * SLOT);
-#pragma unroll
-        for (int k = 0; k < PER; ++k) buf[i][k] = __ldcg(p + threadIdx.x + k * TTHREADS);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < QB; ++i) {
-      if (q0 + i <= c_hi) {
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          acc4[k].x += buf[i][k].x;
-          acc4[k].y += buf[i][k].y;
-          acc4[k].z += buf[i][k].z;
-          acc4[k].w += buf[i][k].w;
+      for (int i = 0; i < QB; ++i)
+        if (q0 + i * q_step <= c_hi) {
+          s.x += buf[i].x;
+          s.y += buf[i].y;
+          s.z += buf[i].z;
+          s.w += buf[i].w;
         }
-      }
     }
-  }
+  };
   const bool vec_out = (o.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0;
   const bool vec_pad = o.pad && (o.ldp & 3) == 0 && (reinterpret_cast<uintptr_t>(o.pad) & 7) == 0;
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int p4 = threadIdx.x + k * TTHREADS;
+  auto finish = [&](int p4, const float4& a) {  // outputs of one float4 position
     const int tr = p4 / C4, j = 4 * (p4 - tr * C4);
     const int64_t row = static_cast<int64_t>(tile) * TM + tr;
-    const float vv[4] = {acc4[k].x, acc4[k].y, acc4[k].z, acc4[k].w};
+    const float vv[4] = {a.x, a.y, a.z, a.w};
     if (row < n_out) {
       if (vec_out && j + 4 <= o.rc) {
         *reinterpret_cast<float4*>(o.out + row * o.ldo + j) =
@@ -243,11 +261,43 @@ __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
         }
       }
     }
+  };
+  if (pc >= TTHREADS || n_con == 1) {
+    // enough positions for every thread: each sums its positions over all contributors
+    for (int p = p0 + threadIdx.x; p < p1; p += TTHREADS) {
+      float4 s;
+      sum_over(p, c_lo, 1, s);
+      finish(p, s);
+    }
+  } else {
+    // few positions (many participants): contributor groups per position, then
+    // the groups' partials combined in group order (scratch: the idle TMA ring)
+    int ng = TTHREADS / pc;
+    if (ng > n_con) ng = n_con;
+    const int t = threadIdx.x, pi = t % pc, gi = t / pc;
+    if (gi < ng) {
+      float4 s;
+      sum_over(p0 + pi, c_lo + gi, ng, s);
+      scratch[gi * pc + pi] = s;
+    }
+    __syncthreads();
+    if (t < pc) {
+      float4 s = scratch[t];
+      for (int k = 1; k < ng; ++k) {
+        const float4 v = scratch[k * pc + t];
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+      finish(p0 + t, s);
+    }
   }
-  if (o.pad && o.pad_cols > ROWS) {  // zero pad columns [ROWS, pad_cols): 8-B stores
+  if (o.pad && o.pad_cols > ROWS) {  // zero pad columns [ROWS, pad_cols) of this piece's rows
+    const int r0 = k_part * TM / n_part, r1 = (k_part + 1) * TM / n_part;
     const int pc4 = (o.pad_cols - ROWS) / 4;
-    for (int idx = threadIdx.x; idx < TM * pc4; idx += TTHREADS) {
-      const int tr = idx / pc4, j = ROWS + 4 * (idx - tr * pc4);
+    for (int idx = threadIdx.x; idx < (r1 - r0) * pc4; idx += TTHREADS) {
+      const int tr = r0 + idx / pc4, j = ROWS + 4 * (idx % pc4);
       const int64_t row = static_cast<int64_t>(tile) * TM + tr;
       if (row < n_out) {
         if (vec_pad)
@@ -257,7 +307,13 @@ __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
       }
     }
   }
-  __syncthreads();  // the slot is rewritten by this CTA's next flush
+  __syncthreads();  // the slot / scratch are reused by this CTA's next flush
+  if (n_con > 1 && threadIdx.x == 0) {
+    if (atom_add_acq_rel_gpu(depart, 1) == n_part - 1) {  // every participant has read the slots
+      *arrive = 0;  // self-resetting for the next launch on this stream
+      *depart = 0;
+    }
+  }
 }
 
 // out[t, j] (+)= Σ_k act[t, k] · Wt[j, k]   (Wt = W transposed, hi/lo bf16 planes)
@@ -273,6 +329,7 @@ __global__ void __launch_bounds__(TTHREADS, 3)
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + TNS * L::STAGE_AL);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
+  thin_stamp(o, 0);
   const int u0 = static_cast<int>(static_cast<int64_t>(blockIdx.x) * units / gridDim.x);
   const int u1 = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * units / gridDim.x);
   auto issue = [&](int u, int slot) {
@@ -306,6 +363,8 @@ __global__ void __launch_bounds__(TTHREADS, 3)
       issue(u + TNS - 1, (i + TNS - 1) % TNS);
     }
     mbar_wait(&full[b], static_cast<uint32_t>((i / TNS) & 1));
+    if (i == 0) thin_stamp(o, 1);
+    if (u + 1 == u1) thin_stamp(o, 2);
     const uint32_t abase = smem_u32(sm + b * L::STAGE_AL);
     const uint32_t fbase = abase + L::ACT;
 #pragma unroll
@@ -326,8 +385,10 @@ __global__ void __launch_bounds__(TTHREADS, 3)
     __syncthreads();
     const int tile = u / kchunks;
     if (u + 1 == u1 || (u + 1) / kchunks != tile)  // leaving this token tile
-      thin_flush<NT>(acc, tile, kchunks, units, o, m);
+      thin_flush<NT>(acc, tile, kchunks, units, o, m, u + 1 == u1,
+                     reinterpret_cast<float4*>(sm));
   }
+  thin_stamp(o, 3);
 }
 
 // out[n, j] += scale · Σ_t act[t, n] · Vt[j, t]   (Vt = V transposed, hi/lo bf16 planes)
@@ -344,6 +405,7 @@ __global__ void __launch_bounds__(TTHREADS, 3)
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + TNS * L::STAGE_AL);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
+  thin_stamp(o, 0);
   const int u0 = static_cast<int>(static_cast<int64_t>(blockIdx.x) * units / gridDim.x);
   const int u1 = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * units / gridDim.x);
   auto issue = [&](int u, int slot) {
@@ -382,6 +444,8 @@ __global__ void __launch_bounds__(TTHREADS, 3)
       issue(u + TNS - 1, (i + TNS - 1) % TNS);
     }
     mbar_wait(&full[b], static_cast<uint32_t>((i / TNS) & 1));
+    if (i == 0) thin_stamp(o, 1);
+    if (u + 1 == u1) thin_stamp(o, 2);
     const uint32_t abase = smem_u32(sm + b * L::STAGE_AL);
     const uint32_t fbase = abase + L::ACT;
 #pragma unroll
@@ -402,8 +466,10 @@ __global__ void __launch_bounds__(TTHREADS, 3)
     __syncthreads();
     const int nt = u / tchunks;
     if (u + 1 == u1 || (u + 1) / tchunks != nt)  // leaving this n tile
-      thin_flush<NT>(acc, nt, tchunks, units, o, nd);
+      thin_flush<NT>(acc, nt, tchunks, units, o, nd, u + 1 == u1,
+                     reinterpret_cast<float4*>(sm));
   }
+  thin_stamp(o, 3);
 }
 
 // One launch for a layer pass's small conversion / zeroing jobs (PrepBatch):
@@ -533,7 +599,7 @@ void ws_size_nt(bool row, int64_t m, int64_t d, int64_t* ws_floats, int64_t* n_c
   const int64_t units = tiles * chunks;
   const int64_t ctas = units > 0 ? thin_ctas<NT>(row, units) : 0;
   *ws_floats = ctas * 2 * TM * 8 * NT;
-  *n_cnt = tiles;
+  *n_cnt = 2 * tiles;  // arrival + departure counters per output tile
 }
 
 template <int NT>

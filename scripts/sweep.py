@@ -4,6 +4,7 @@ headline bench; writes one JSON line per config).
   cfg1  4096x4096, 4-bit g128, r=8, m=512, fwd+bwd
   cfg2  LLaMA-7B MLP up+down, 3-bit, r=16, m=4096 (the bench.py headline)
   cfg3  LLaMA-7B decoder linear stack Q,K,V,O,gate,up,down, 3-bit, r=8, m=8192
+  cfg3_1k  the same stack at 1024 tokens (one rank's share of cfg3 strong-scaled over 8 GPUs)
   cfg4  LLaMA-65B up 22016x8192 + down 8192x22016, b in {3,4}, r=64, m=2048 (per GPU of 8)
   cfg5  2-bit 6656x17920 materialize() bandwidth sweep (bf16 and f32 out): the affine
         2-bit format and the black-box "cb2" codebook plugin (hook), plus the cb2 layer
@@ -93,6 +94,8 @@ def main():
         "cfg1": ([(4096, 4096)], 4, 8, 512),
         "cfg2": ([(11008, 4096), (4096, 11008)], 3, 16, 4096),
         "cfg3": ([(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)], 3, 8, 8192),
+        # one rank's share of cfg3 strong-scaled over 8 GPUs (8192 / 8 tokens)
+        "cfg3_1k": ([(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)], 3, 8, 1024),
         "cfg4_b3": ([(22016, 8192), (8192, 22016)], 3, 64, 2048),
         "cfg4_b4": ([(22016, 8192), (8192, 22016)], 4, 64, 2048),
     }
