@@ -15,6 +15,7 @@
 //   mode 1 (inverse): out = diag(s) · H_b · in / sqrt(b)      (V^T d~x, U^T y~)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "../../include/mlra.h"
 #include "kernels.h"
@@ -84,6 +85,162 @@ __global__ void __launch_bounds__(256) k_rht(const __nv_bfloat16* __restrict__ i
   }
 }
 
+// Tensor-core form for b = 16·A (A in {16, 32, 64}: b = 256, 512, 1024). A
+// block x (b elements) is the A x 16 matrix M[a][c] = x[16a + c]; with Sylvester
+// ordering H_b = H_A (x) H_16, so H_b·x = vec(H_A · M · H_16) (H symmetric).
+// One warp per block, two bf16 mma.sync m16n8k16 stages, fp32 accumulation:
+//  1. M1^T = H_16 · M^T: the x values are exact bf16 operands (B fragments
+//     loaded straight from global, sign flips applied to the bf16 bits);
+//  2. Y = H_A · M1: step 1's fp32 accumulator fragments are exactly step 2's
+//     B fragments (row/col of the m16n8 C layout = k/n of the B layout of the
+//     transpose), split into three bf16 parts (hi + mid + lo = the full 24-bit
+//     fp32 value), so the product of the +-1 entries stays fp32-exact.
+// H entries are (-1)^popc(i & j). Output fragments hold 2 consecutive
+// elements per lane. Same law as the butterfly kernel up to fp32 summation
+// order; no shuffles (the butterfly kernel's 5 cross-lane stages made it
+// shuffle-bound at ~1 TB/s).
+__device__ __forceinline__ uint32_t h_pair(int i, int j) {  // bf16x2 {H[i][j], H[i][j+1]}
+  const uint32_t lo = (__popc(i & j) & 1) ? 0xBF80u : 0x3F80u;
+  const uint32_t hi = (__popc(i & (j + 1)) & 1) ? 0xBF80u : 0x3F80u;
+  return lo | (hi << 16);
+}
+
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t sign_mask2(const float* s) {  // flip bf16 sign bits where s < 0
+  const float2 v = __ldg(reinterpret_cast<const float2*>(s));
+  return (v.x < 0.0f ? 0x8000u : 0u) | (v.y < 0.0f ? 0x80000000u : 0u);
+}
+
+// three-way bf16 split of two fp32 values: parts[p] = bf16x2 of part p
+__device__ __forceinline__ void split3(float x, float y, uint32_t (&parts)[3]) {
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+    parts[p] = *reinterpret_cast<const uint32_t*>(&h);
+    x -= __bfloat162float(h.x);
+    y -= __bfloat162float(h.y);
+  }
+}
+
+template <int A, bool OUT_F32>
+__global__ void __launch_bounds__(256, A <= 32 ? 3 : 1) k_rht_tc(const __nv_bfloat16* __restrict__ in, int64_t rows,
+                                               int64_t cols, int64_t ld_in,
+                                               const float* __restrict__ signs, int inverse,
+                                               void* __restrict__ out, int64_t ld_out) {
+  constexpr int B = 16 * A, NT1 = A / 8, MT = A / 16;
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t nblk = cols / B, total = rows * nblk;
+  const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  // H_16 A fragments (step 1), loop invariant
+  const uint32_t h0 = h_pair(g, 2 * tq), h1 = h_pair(g + 8, 2 * tq), h2 = h_pair(g, 2 * tq + 8),
+                 h3 = h_pair(g + 8, 2 * tq + 8);
+  const float norm = rsqrtf(static_cast<float>(B));
+  // the next block's operands are loaded before this block's MMAs (two blocks'
+  // loads in flight per warp)
+  uint32_t nb0[NT1], nb1[NT1];
+  auto load = [&](int64_t b) {
+    const int64_t r = b / nblk, c0 = (b - r * nblk) * B;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(in + r * ld_in + c0);
+#pragma unroll
+    for (int j = 0; j < NT1; ++j) {
+      const int e = 16 * (8 * j + g) + 2 * tq;  // element of b0 (b1: e + 8)
+      nb0[j] = __ldg(src + e / 2);
+      nb1[j] = __ldg(src + e / 2 + 4);
+    }
+  };
+  if (warp0 < total) load(warp0);
+  for (int64_t blk = warp0; blk < total; blk += nwarps) {
+    const int64_t r = blk / nblk, c0 = (blk - r * nblk) * B;
+    uint32_t cb0[NT1], cb1[NT1];
+#pragma unroll
+    for (int j = 0; j < NT1; ++j) {
+      cb0[j] = nb0[j];
+      cb1[j] = nb1[j];
+    }
+    if (blk + nwarps < total) load(blk + nwarps);
+    // step 1: C1[j] = (H_16 · M^T) restricted to a in [8j, 8j + 8)
+    float c1[NT1][4];
+#pragma unroll
+    for (int j = 0; j < NT1; ++j) {
+      const int e = 16 * (8 * j + g) + 2 * tq;
+      uint32_t b0 = cb0[j], b1 = cb1[j];
+      if (!inverse) {
+        b0 ^= sign_mask2(signs + c0 + e);
+        b1 ^= sign_mask2(signs + c0 + e + 8);
+      }
+      c1[j][0] = c1[j][1] = c1[j][2] = c1[j][3] = 0.0f;
+      mma16816(c1[j], h0, h1, h2, h3, b0, b1);
+    }
+    // step 2: Y = H_A · M1, B fragments from C1 (three bf16 parts each)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int kt = 0; kt < MT; ++kt) {
+          const uint32_t a0 = h_pair(16 * mt + g, 16 * kt + 2 * tq),
+                         a1 = h_pair(16 * mt + g + 8, 16 * kt + 2 * tq),
+                         a2 = h_pair(16 * mt + g, 16 * kt + 2 * tq + 8),
+                         a3 = h_pair(16 * mt + g + 8, 16 * kt + 2 * tq + 8);
+          uint32_t p0[3], p1[3];
+          split3(c1[2 * kt][2 * nt], c1[2 * kt][2 * nt + 1], p0);
+          split3(c1[2 * kt + 1][2 * nt], c1[2 * kt + 1][2 * nt + 1], p1);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) mma16816(acc, a0, a1, a2, a3, p0[p], p1[p]);
+        }
+        // acc: Y[16mt + g][8nt + 2tq .. +1] and Y[16mt + g + 8][...] -> elements i, i + 128
+        const int i0 = 16 * (16 * mt + g) + 8 * nt + 2 * tq;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = i0 + 128 * h;
+          float y0 = acc[2 * h] * norm, y1 = acc[2 * h + 1] * norm;
+          if (inverse) {
+            const float2 s = __ldg(reinterpret_cast<const float2*>(signs + c0 + i));
+            y0 *= s.x;
+            y1 *= s.y;
+          }
+          if constexpr (OUT_F32) {
+            *reinterpret_cast<float2*>(reinterpret_cast<float*>(out) + r * ld_out + c0 + i) =
+                make_float2(y0, y1);
+          } else {
+            *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(out) + r * ld_out +
+                                               c0 + i) = __floats2bfloat162_rn(y0, y1);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int A>
+cudaError_t rht_tc(const void* in, int64_t rows, int64_t cols, int64_t ld_in, const float* signs,
+                   int inverse, void* out, int64_t ld_out, bool f32, cudaStream_t st) {
+  const int64_t total = rows * (cols / (16 * A));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t blocks = (total + 7) / 8;
+  if (blocks > 3LL * sms) blocks = 3LL * sms;  // resident 8-warp CTAs, grid-stride
+  note_launch();
+  if (f32)
+    k_rht_tc<A, true><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(in), rows, cols, ld_in, signs, inverse, out, ld_out);
+  else
+    k_rht_tc<A, false><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(in), rows, cols, ld_in, signs, inverse, out, ld_out);
+  return cudaGetLastError();
+}
+
 template <int E>
 cudaError_t rht_e(const void* in, int64_t rows, int64_t cols, int64_t ld_in, const float* signs,
                   int inverse, void* out, int64_t ld_out, bool f32, cudaStream_t st) {
@@ -106,12 +263,17 @@ cudaError_t launch_rht(const void* in, int64_t rows, int64_t cols, int64_t ld_in
                        const float* signs, int inverse, int block, void* out, int64_t ld_out,
                        bool f32, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
+  // tensor-core form for b >= 256 (MLRA_RHT_BUTTERFLY=1: the butterfly kernel, A/B)
+  static const bool use_tc = getenv("MLRA_RHT_BUTTERFLY") == nullptr;
   switch (block) {
     case 64: return rht_e<2>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st);
     case 128: return rht_e<4>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st);
-    case 256: return rht_e<8>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st);
-    case 512: return rht_e<16>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st);
-    case 1024: return rht_e<32>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st);
+    case 256: return use_tc ? rht_tc<16>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st)
+                            : rht_e<8>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st);
+    case 512: return use_tc ? rht_tc<32>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st)
+                            : rht_e<16>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st);
+    case 1024: return use_tc ? rht_tc<64>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st)
+                             : rht_e<32>(in, rows, cols, ld_in, signs, inverse, out, ld_out, f32, st);
     default: return cudaErrorInvalidValue;
   }
 }
