@@ -49,23 +49,22 @@ __device__ __forceinline__ void cb2_mags(uint32_t code, const uint4* cbh, const 
   }
 }
 
-// E8P: the 8 magnitudes of a code (|a| + 1/4 or |a| - 1/4 per entry, bf16-exact
-// tables in shared memory) and its negate byte (common.cuh e8p_decode_signs).
-__device__ __forceinline__ uint32_t e8p_mags(uint32_t code, const uint4* tab, const uint32_t* odd,
-                                             float (&m)[8]) {
-  const uint32_t i = code & 0xFFu;
-  uint32_t neg, plus;
-  e8p_decode_signs(code, (odd[i >> 5] >> (i & 31)) & 1u, &neg, &plus);
-  const uint4 P = tab[i], N = tab[256 + i];
-  const uint32_t pw[4] = {P.x, P.y, P.z, P.w}, nw[4] = {N.x, N.y, N.z, N.w};
+// E8P: the 8 magnitudes |a_j| + t·(1 - 2·neg_j) of a code (t = +-1/4 from bit
+// 15; exact) and its negate byte (common.cuh e8p_decode_signs), from ONE
+// shared-memory gather: `tab` = the 256 bf16 |a| rows with the pattern's
+// odd-sum bit in the (zero) sign bit of entry 0 (staged by k_cb2_materialize).
+__device__ __forceinline__ uint32_t e8p_mags(uint32_t code, const uint4* tab, float (&m)[8]) {
+  const uint4 A = tab[code & 0xFFu];
+  const uint32_t sb = (code >> 8) & 0x7Fu;
+  const uint32_t n = sb | (((__popc(sb) ^ (A.x >> 15)) & 1u) << 7);
+  const float t = (code >> 15) ? 0.25f : -0.25f;
+  const uint32_t w[4] = {A.x & 0xFFFF7FFFu, A.y, A.z, A.w};
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    const uint32_t lo = ((plus >> (2 * p)) & 1u) ? pw[p] : nw[p];
-    const uint32_t hi = ((plus >> (2 * p + 1)) & 1u) ? pw[p] : nw[p];
-    m[2 * p] = __uint_as_float(lo << 16);
-    m[2 * p + 1] = __uint_as_float(hi & 0xFFFF0000u);
+    m[2 * p] = __uint_as_float(w[p] << 16) + (((n >> (2 * p)) & 1u) ? -t : t);
+    m[2 * p + 1] = __uint_as_float(w[p] & 0xFFFF0000u) + (((n >> (2 * p + 1)) & 1u) ? -t : t);
   }
-  return neg;
+  return n;
 }
 
 // One code -> 8 bf16 outputs. Products RN_f32(s·mag) (scalar IEEE
@@ -106,7 +105,7 @@ __device__ __forceinline__ void cb2_emit_half(float* __restrict__ out, int64_t o
   uint32_t sg = code >> (8 + 4 * h);
   if constexpr (E8P) {
     float m8[8];
-    sg = e8p_mags(code, cbh, odd, m8) >> (4 * h);
+    sg = e8p_mags(code, cbh, m8) >> (4 * h);
 #pragma unroll
     for (int e = 0; e < 4; ++e) m[e] = m8[4 * h + e];
   } else if constexpr (CB16) {
@@ -142,15 +141,31 @@ template <bool F32, bool VEC, bool CB16, bool E8P>
 __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
     const Cb2Dev c, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols,
     void* __restrict__ out, int64_t ld, int gshift) {
-  // cb2: 256 (bf16 rows) or 512 (f32 halves) float4; e8p: 512 uint4 + 8 odd words
-  constexpr int NCB = (CB16 && !E8P) ? 256 : 512;
-  __shared__ float4 cbs[NCB + (E8P ? 2 : 0)];
+  // cb2: 256 (bf16 rows) or 512 (f32 halves) float4; e8p: the 256 |a| rows (e8p_mags)
+  constexpr int NCB = CB16 ? 256 : 512;
+  __shared__ float4 cbs[NCB];
   const uint4* cbh = reinterpret_cast<const uint4*>(cbs);
   const float4* cb0 = cbs;
   const float4* cb1 = cbs + 256;
-  const uint32_t* odd = reinterpret_cast<const uint32_t*>(cbs + NCB);
-  for (int i = threadIdx.x; i < NCB + (E8P ? 2 : 0); i += kCbThreads)
-    cbs[i] = __ldg(reinterpret_cast<const float4*>(c.codebook) + i);
+  const uint32_t* odd = nullptr;
+  if constexpr (E8P) {  // |a| = (|a| + 1/4) - 1/4 (bf16-exact), odd bit -> sign bit of entry 0
+    const uint4* src = reinterpret_cast<const uint4*>(c.codebook);
+    const uint32_t* oddw = reinterpret_cast<const uint32_t*>(src + 512);
+    for (int i = threadIdx.x; i < 256; i += kCbThreads) {
+      const uint4 pr = __ldg(src + i);
+      const uint32_t pw[4] = {pr.x, pr.y, pr.z, pr.w};
+      uint32_t aw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        aw[q] = pack_bf16x2(__uint_as_float(pw[q] << 16) - 0.25f,
+                            __uint_as_float(pw[q] & 0xFFFF0000u) - 0.25f);
+      aw[0] |= ((__ldg(oddw + (i >> 5)) >> (i & 31)) & 1u) << 15;
+      reinterpret_cast<uint4*>(cbs)[i] = make_uint4(aw[0], aw[1], aw[2], aw[3]);
+    }
+  } else {
+    for (int i = threadIdx.x; i < NCB; i += kCbThreads)
+      cbs[i] = __ldg(reinterpret_cast<const float4*>(c.codebook) + i);
+  }
   constexpr int SH = F32 ? 1 : 0;  // work unit: a code (bf16) or half a code (f32)
   const int ncodes = static_cast<int>(ncols >> 3);
   const int nunits = ncodes << SH;
@@ -210,7 +225,7 @@ __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
         float m[8];
         uint32_t sg;
         if constexpr (E8P) {
-          sg = e8p_mags(cur[j], cbh, odd, m);
+          sg = e8p_mags(cur[j], cbh, m);
         } else {
           cb2_mags<CB16>(cur[j], cbh, cb0, cb1, m);
           sg = cur[j] >> 8;

@@ -409,9 +409,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) tmem_alloc2(tmem_slot, TMEM_COLS);
   pdl_trigger();
   pdl_wait();  // every operand (activations, LoRA planes, flags) may come from earlier kernels
-  if constexpr (E8P) {  // stage the 8 KB e8p tables + odd bits
-    for (int i = threadIdx.x; i < (2 * 256 * 16 + 32) / 16; i += NUM_THREADS)
-      reinterpret_cast<uint4*>(sCb)[i] = __ldg(reinterpret_cast<const uint4*>(p.cb2_codebook) + i);
+  if constexpr (E8P) {  // the e8p decode table (dequant_units_e8p), from the (|a| +- 1/4) rows
+    if (threadIdx.x < 256) {  // |a| = (|a| + 1/4) - 1/4, bf16-exact; odd bit -> sign bit of entry 0
+      const uint4* src = reinterpret_cast<const uint4*>(p.cb2_codebook);
+      const uint4 pr = __ldg(src + threadIdx.x);
+      const uint32_t odd = (__ldg(reinterpret_cast<const uint32_t*>(src + 512) + (threadIdx.x >> 5)) >>
+                            (threadIdx.x & 31)) & 1u;
+      const uint32_t pw[4] = {pr.x, pr.y, pr.z, pr.w};
+      uint32_t aw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        aw[q] = pack_bf16x2(__uint_as_float(pw[q] << 16) - 0.25f,
+                            __uint_as_float(pw[q] & 0xFFFF0000u) - 0.25f);
+      reinterpret_cast<uint4*>(sCb)[threadIdx.x] = make_uint4(aw[0] | (odd << 15), aw[1], aw[2], aw[3]);
+    }
   }
   if constexpr (CB2) {  // stage the 4 KB codebook (read by this CTA's dequant warps)
     if (threadIdx.x < kCb2SmemBytes / 16)

@@ -174,10 +174,14 @@ __device__ __forceinline__ void dequant_units_cb2(uint32_t qc, uint32_t qg, uint
   }
 }
 
-// The e8p plugin's tile decode: per code, the (|a| + 1/4) and (|a| - 1/4) bf16
-// rows of its abs pattern (tab, uint4[2][256]) blended per entry by the
-// e8p_decode_signs masks, scaled (one IEEE multiply per entry: the same law as
-// k_cb2_materialize's e8p path, so fused == materialized bit for bit), negated.
+// The e8p plugin's tile decode. Entry j of a code is sign_j·(|a_j| + sign_j·t)
+// = sign_j·|a_j| + t (t = +-1/4 from bit 15, sign_j^2 = 1), exact in fp32, so
+// w_j = RN_f32(s · (sign_j·|a_j| + t)) — bit for bit the law of
+// k_cb2_materialize's e8p path (sign_j·RN(s·(|a_j| +- 1/4)); RN is odd-symmetric).
+// ONE shared-memory gather per code, as in the cb2 decode: `tab` holds the 256
+// bf16 |a| rows (built by the kernel prologue from the (|a| +- 1/4) tables)
+// with the pattern's odd-sum bit in the (otherwise zero) sign bit of entry 0;
+// the negate byte (e8p_decode_signs) and its sign-bit masks are ALU work.
 template <int UPT, int ROW_STEP>
 __device__ __forceinline__ void dequant_units_e8p(uint32_t qc, uint32_t qg, uint32_t st,
                                                   const uint32_t (&soff)[UPT], int unit, int gsub,
@@ -193,20 +197,18 @@ __device__ __forceinline__ void dequant_units_e8p(uint32_t qc, uint32_t qg, uint
   }
 #pragma unroll
   for (int i = 0; i < UPT; ++i) {
-    const uint32_t idx = v[i] & 0xFFu;
-    uint32_t neg, plus;
-    e8p_decode_signs(v[i], (lds32(tab + 8192 + ((idx >> 5) << 2)) >> (idx & 31)) & 1u, &neg, &plus);
-    const uint4 P = lds128(tab + (idx << 4)), N = lds128(tab + 4096 + (idx << 4));
-    const uint32_t pw[4] = {P.x, P.y, P.z, P.w}, nw[4] = {N.x, N.y, N.z, N.w};
+    const uint4 A = lds128(tab + ((v[i] & 0xFFu) << 4));
+    const uint32_t sb = (v[i] >> 8) & 0x7Fu;
+    const uint32_t n = sb | (((__popc(sb) ^ (A.x >> 15)) & 1u) << 7);  // negate byte
+    const uint32_t w[4] = {A.x & 0xFFFF7FFFu, A.y, A.z, A.w};
+    const float t = (v[i] >> 15) ? 0.25f : -0.25f;
     const float s = fabsf(sc[i]);
     uint32_t o[4];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      const uint32_t lo = ((plus >> (2 * p)) & 1u) ? pw[p] : nw[p];
-      const uint32_t hi = ((plus >> (2 * p + 1)) & 1u) ? pw[p] : nw[p];
-      const float a = __fmul_rn(s, __uint_as_float(lo << 16));
-      const float b = __fmul_rn(s, __uint_as_float(hi & 0xFFFF0000u));
-      o[p] = pack_bf16x2(a, b) ^ ((((neg >> (2 * p)) & 3u) * 0x40008000u) & 0x80008000u);
+      const uint32_t ws = w[p] ^ ((((n >> (2 * p)) & 3u) * 0x40008000u) & 0x80008000u);
+      o[p] = pack_bf16x2(__fmul_rn(s, __uint_as_float(ws << 16) + t),
+                         __fmul_rn(s, __uint_as_float(ws & 0xFFFF0000u) + t));
     }
     sts128(st + soff[i], make_uint4(o[0], o[1], o[2], o[3]));
   }
