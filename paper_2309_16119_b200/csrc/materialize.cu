@@ -154,32 +154,48 @@ __global__ void __launch_bounds__(128) k_materialize_fast(const QWeightDev q, in
                                                           void* __restrict__ out, int64_t ld,
                                                           int64_t items, int gshift) {
   constexpr int CODES = F32 ? 4 : 8;
+  constexpr int IPT = 4;  // items per thread, strided by 32: every warp store covers 512 B
   const int64_t rr = blockIdx.y;
   const int64_t r = row0 + rr;
   const uint32_t* rw = q.words + r * q.row_words;
   const float2* grow = q.grid + r * q.ng_pad;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * 512 + (threadIdx.x >> 5) * 128 + (threadIdx.x & 31);
+  const int base = static_cast<int>(blockIdx.x) * 512 + (threadIdx.x >> 5) * 128 + (threadIdx.x & 31);
+  const int n = static_cast<int>(items);
+  // every item's code bits and grid entry are requested before any is decoded
+  // (the loop with an early exit issued them one at a time: long-scoreboard bound)
+  uint64_t v[IPT];
+  float2 g[IPT];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int64_t it = base + 32 * j;
-    if (it >= items) break;
-    const int64_t k0 = it * CODES;
-    const float2 g = __ldg(grow + (gshift >= 0 ? (k0 >> gshift) : k0 / q.group));
+  for (int j = 0; j < IPT; ++j) {
+    const int it = base + 32 * j;
+    if (it < n) {
+      const int k0 = it * CODES;
+      g[j] = __ldg(grow + (gshift >= 0 ? (k0 >> gshift) : k0 / static_cast<int>(q.group)));
+      if constexpr (F32)
+        v[j] = quad_bits<BITS>(rw, it);
+      else
+        v[j] = load_unit<BITS>(rw, it);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const int it = base + 32 * j;
+    if (it >= n) break;
+    const int k0 = it * CODES;
     if constexpr (F32) {
-      const uint32_t v = quad_bits<BITS>(rw, it);
       constexpr uint32_t mask = (1u << BITS) - 1u;
+      const uint32_t vv = static_cast<uint32_t>(v[j]);
       float f[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) f[i] = deq_entry((v >> (BITS * i)) & mask, g.x, g.y);
+      for (int i = 0; i < 4; ++i) f[i] = deq_entry((vv >> (BITS * i)) & mask, g[j].x, g[j].y);
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * ld + k0) =
           make_float4(f[0], f[1], f[2], f[3]);
     } else {
-      const uint64_t v = load_unit<BITS>(rw, it);
       uint4 o;
       if constexpr (BITS <= 4)
-        o = deq8_bf16_fast<BITS>(static_cast<uint32_t>(v), g);
+        o = deq8_bf16_fast<BITS>(static_cast<uint32_t>(v[j]), g[j]);
       else
-        o = deq8_bf16<BITS>(v, g);
+        o = deq8_bf16<BITS>(v[j], g[j]);
       *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * ld + k0) = o;
     }
   }
