@@ -1331,23 +1331,31 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   if (mlra_status st = rows_product(s, w_row, dya, lddya, m, d.rows, at, dyA, r, dyas, rp,
                                     scaling, &dyat))
     return st;
-  // K5b / K6 go to the side stream when a dX GEMM follows (overlap), else inline
+  // K5b / K6 go to the side stream when a dX GEMM follows, else inline. The GEMM is
+  // enqueued FIRST: its persistent pairs take the SMs, and dA / dB fill the SMs
+  // its under-filled last wave leaves idle (e.g. 128 tiles over 74 pairs) and its
+  // tail, instead of delaying its start (MLRA_SIDE_FIRST=1: the old order).
   SideStream* side = nullptr;
-  cudaStream_t cs = s;
-  static const bool no_side = getenv("MLRA_NO_SIDE") != nullptr;  // dev A/B switch
+  static const bool no_side = getenv("MLRA_NO_SIDE") != nullptr;        // dev A/B switch
+  static const bool side_first = getenv("MLRA_SIDE_FIRST") != nullptr;  // dev A/B switch
   if (dx && !no_side) {
     if (mlra_status st = side_stream(&side)) return st;
-    cs = side->st;
     CUDA_TRY(cudaEventRecord(side->fork, s));
-    CUDA_TRY(cudaStreamWaitEvent(cs, side->fork, 0));
+    CUDA_TRY(cudaStreamWaitEvent(side->st, side->fork, 0));
   }
-  // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
-  if (mlra_status st = cols_product(cs, w_da, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias))
-    return st;
-  // K6: dB = s·xᵀ·dyA   (autodiff.cpp:153-155 on record lora.cpp:68)
-  if (mlra_status st = cols_product(cs, w_db, xa, ldxa, m, d.cols, dyat, scaling, db, r, nullptr))
-    return st;
-  if (!dx) return MLRA_OK;  // frozen input: no dX (autodiff.cpp:136)
+  auto adapter_grads = [&](cudaStream_t cs) -> mlra_status {
+    // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
+    if (mlra_status st = cols_product(cs, w_da, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias))
+      return st;
+    // K6: dB = s·xᵀ·dyA   (autodiff.cpp:153-155 on record lora.cpp:68)
+    return cols_product(cs, w_db, xa, ldxa, m, d.cols, dyat, scaling, db, r, nullptr);
+  };
+  if (!dx) return adapter_grads(s);  // frozen input: no dX (autodiff.cpp:136)
+  if (!side) {
+    if (mlra_status st = adapter_grads(s)) return st;
+  } else if (side_first) {
+    if (mlra_status st = adapter_grads(side->st)) return st;
+  }
   GemmPlan gp{};
   gp.mn = true;
   gp.act = dya;
@@ -1365,9 +1373,12 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   gp.no_pdl = side != nullptr;
   // K3: dx = dy·Ŵ + (s·dyA)·Bᵀ   (lp_backward + matmul-bwd dx, lora.cpp:68)
   const mlra_status gst = run_gemm(L->q, L->strategy, L->hook, gp, sc);
-  // join: the caller's stream (and the scratch frees queued on it) waits for dA/dB
   if (side) {
-    CUDA_TRY(cudaEventRecord(side->join, cs));
+    if (!side_first && gst == MLRA_OK) {
+      if (mlra_status st = adapter_grads(side->st)) return st;
+    }
+    // join: the caller's stream (and the scratch frees queued on it) waits for dA/dB
+    CUDA_TRY(cudaEventRecord(side->join, side->st));
     CUDA_TRY(cudaStreamWaitEvent(s, side->join, 0));
   }
   return gst;
