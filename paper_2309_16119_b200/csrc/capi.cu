@@ -13,10 +13,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
 #include "../../include/mlra.h"
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "qgemm.h"
@@ -27,6 +32,38 @@ using mlra::QWeightDev;
 namespace mlra {
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// Dev-only host-side profile of the API calls (MLRA_HOSTPROF=1): wall time in
+// workspace allocation, tensor-map encoding, kernel launches and whole calls,
+// printed to stderr at exit.
+struct HostProf {
+  std::atomic<uint64_t> ns[5]{}, n[5]{};
+  const bool on = getenv("MLRA_HOSTPROF") != nullptr;
+  ~HostProf() {
+    if (!on) return;
+    const char* nm[5] = {"alloc", "tmap", "launch", "call", "free"};
+    for (int i = 0; i < 5; ++i)
+      fprintf(stderr, "mlra hostprof %-6s %8.2f us total-per-call-avg %llu events\n", nm[i],
+              n[3] ? ns[i].load() / 1e3 / n[3].load() : 0.0, (unsigned long long)n[i].load());
+  }
+};
+HostProf g_prof;
+struct ProfScope {
+  int k;
+  std::chrono::steady_clock::time_point t0;
+  explicit ProfScope(int kk) : k(kk) {
+    if (g_prof.on) t0 = std::chrono::steady_clock::now();
+  }
+  ~ProfScope() {
+    if (!g_prof.on) return;
+    g_prof.ns[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::steady_clock::now() - t0).count();
+    g_prof.n[k] += 1;
+  }
+};
+
+HostLaunchTimer::HostLaunchTimer() : impl(g_prof.on ? new ProfScope(2) : nullptr) {}
+HostLaunchTimer::~HostLaunchTimer() { delete static_cast<ProfScope*>(impl); }
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("MLRA_PDL");
@@ -35,6 +72,7 @@ bool pdl_enabled() {
   return on;
 }
 }  // namespace mlra
+using mlra::ProfScope;
 
 struct mlra_qweight {
   QWeightDev d{};
@@ -147,6 +185,7 @@ mlra_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
                      uint64_t ld, uint32_t box_inner, uint32_t box_outer,
                      CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                      uint32_t esize = 2, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+  ProfScope ps(1);
   auto enc = get_encode();
   if (!enc) return fail(MLRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
@@ -163,18 +202,87 @@ mlra_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
   return MLRA_OK;
 }
 
+// Per-stream workspace arena: one device block reused by every API call on the
+// stream (bump allocation; stream order makes reuse safe — a call's side-stream
+// work is joined back into the stream before the call returns). A call that
+// needs more than the block gets the excess from the stream-ordered pool and
+// the block is regrown (stream-ordered free + alloc) for the next call. Calls
+// under stream capture, or concurrent calls on one stream, use the pool only.
+// (Per-call cudaMallocAsync was ~10 us of host time per buffer, ~11 buffers
+// per layer pass: MLRA_HOSTPROF.)
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0;
+  bool busy = false;
+};
+std::mutex g_arena_mu;
+constexpr size_t kArenaMaxItem = size_t{64} << 20;  // bigger buffers (a whole Ŵ, hook slabs): pool
+struct ArenaKey {
+  int dev;
+  cudaStream_t st;
+  bool operator==(const ArenaKey& o) const { return dev == o.dev && st == o.st; }
+};
+struct ArenaKeyHash {
+  size_t operator()(const ArenaKey& k) const {
+    return std::hash<const void*>()(k.st) * 31u + static_cast<size_t>(k.dev);
+  }
+};
+std::unordered_map<ArenaKey, Arena, ArenaKeyHash>& arenas() {
+  static std::unordered_map<ArenaKey, Arena, ArenaKeyHash> m;
+  return m;
+}
+
 // Stream-ordered scratch owned by one API call.
 struct Scratch {
   cudaStream_t st;
-  std::vector<void*> ptrs;
-  explicit Scratch(cudaStream_t s) : st(s) {}
+  std::vector<void*> ptrs;  // pool allocations (freed on the stream at the end)
+  Arena* ar = nullptr;
+  size_t used = 0, want = 0;
+  explicit Scratch(cudaStream_t s) : st(s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_arena_mu);
+    Arena& a = arenas()[ArenaKey{dev, s}];
+    if (!a.busy) {
+      a.busy = true;
+      ar = &a;
+    }
+  }
   ~Scratch() {
+    ProfScope ps(4);
     for (void* p : ptrs) cudaFreeAsync(p, st);
+    if (!ar) return;
+    if (want > ar->cap) {  // regrow for the next call on this stream
+      if (ar->base) cudaFreeAsync(ar->base, st);
+      const size_t cap = want + want / 4;
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, cap, st) == cudaSuccess) {
+        ar->base = static_cast<char*>(p);
+        ar->cap = cap;
+      } else {
+        ar->base = nullptr;
+        ar->cap = 0;
+      }
+    }
+    std::lock_guard<std::mutex> lk(g_arena_mu);
+    ar->busy = false;
   }
   template <typename T>
   T* get(size_t count) {
+    ProfScope ps(0);
+    const size_t bytes = (count * sizeof(T) + 16 + 255) & ~size_t{255};
+    if (ar && bytes <= kArenaMaxItem) {
+      want += bytes;
+      if (used + bytes <= ar->cap) {
+        void* p = ar->base + used;
+        used += bytes;
+        return static_cast<T*>(p);
+      }
+    }
     void* p = nullptr;
-    if (cudaMallocAsync(&p, count * sizeof(T) + 16, st) != cudaSuccess) return nullptr;
+    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) return nullptr;
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -1228,6 +1336,7 @@ mlra_status mlra_lp_backward_ex(const mlra_qweight* q, mlra_strategy strategy,
 
 mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, int64_t m, void* y,
                               mlra_dtype y_dtype, int64_t ldy, float* xb, void* stream) {
+  ProfScope call_scope(3);
   if (mlra_status st = check_lora(L)) return st;
   const QWeightDev& d = L->q->d;
   if (m < 0) return fail(MLRA_ERR_DIMENSION, "layer: negative token count");
@@ -1282,6 +1391,7 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
                                const void* dy, int64_t lddy, int64_t m, void* dx,
                                mlra_dtype dx_dtype, int64_t lddx, float* da, float* db,
                                float* dbias, void* stream) {
+  ProfScope call_scope(3);
   if (mlra_status st = check_lora(L)) return st;
   const QWeightDev& d = L->q->d;
   if (m < 0) return fail(MLRA_ERR_DIMENSION, "layer: negative token count");

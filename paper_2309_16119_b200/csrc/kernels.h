@@ -16,6 +16,12 @@ void note_launch();
 // drains and synchronises with it through pdl_wait (ptx.cuh). MLRA_PDL=0
 // launches them classically (A/B switch).
 bool pdl_enabled();
+// dev-only host profile of launches (MLRA_HOSTPROF, capi.cu)
+struct HostLaunchTimer {
+  void* impl;
+  HostLaunchTimer();
+  ~HostLaunchTimer();
+};
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, bool pdl, Args&&... args) {
@@ -30,6 +36,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.attrs = at;
   cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
   note_launch();
+  HostLaunchTimer lt;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

@@ -42,20 +42,18 @@ struct GemmArgs {
   uint32_t q_group_magic; // ceil(2^32 / (group/128)) when group/128 > 1, else 0
   unsigned long long* trace;  // dev-only: per-CTA MMA-thread wait cycles (MLRA_TRACE), else null
   unsigned long long* trace2; // dev-only: per-CTA globaltimer timeline, 8 slots (MLRA_TRACE2)
-  // Stream-K (pair kernel only): 0 = whole tiles strided over the grid; else
-  // the tile x k-block space is cut into sk_pairs contiguous ranges. Split
-  // tiles are finished by their first segment's pair from fp32 partials.
-  // Pair q's range starts at k-block sk_off[q] of tile sk_tile[q] (q = 0..sk_pairs;
-  // entry sk_pairs is the end). Precomputed on the host so the device schedule
-  // needs no division and stays on the uniform datapath.
+  // Stream-K / split-K (pair kernel only): 0 = whole tiles strided over the
+  // grid; else the tile x k-block space is cut into sk_pairs contiguous ranges
+  // (split > 0: S equal cuts per tile). Pair q's range start is a closed form
+  // of (q, sk_pairs, split, tiles, k-blocks) evaluated by the kernel once
+  // (sk_cut in qgemm2_kernel.cuh; the host planner uses the same formula), so
+  // the launch carries no per-pair tables (kernel parameters stay small).
   int sk_pairs;
   int split;             // > 0: split-K mode, S pairs per tile (pair q = tile*S + s)
   int tok256;            // split-K with 256-token pair tiles (one accumulator)
   int no_pdl;            // host only: launch without programmatic dependent launch
   float* sk_ws;          // [sk_pairs x 2 CTAs x 512 tokens x 128 rows] fp32 partials
   unsigned* sk_flags;    // [sk_pairs x 2], zeroed before the launch
-  int sk_tile[129];
-  int sk_off[129];
 };
 
 // true when the fused path can stream codes/grids through the TMA Q ring

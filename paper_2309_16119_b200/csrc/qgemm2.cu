@@ -36,13 +36,7 @@ namespace {
 // Split-K schedule: every pair one (tile, k-range) unit, tiles of 512 or 256
 // tokens (tok256: one accumulator), S pairs per tile.
 void set_split(GemmArgs& p, int64_t tiles, int64_t S, int64_t n_kb, bool tok256) {
-  for (int64_t q = 0; q <= tiles * S; ++q) {
-    const int64_t t = q / S, sp = q % S;
-    int64_t b = n_kb * sp / S;
-    if (b & 1) ++b;  // even offset: a Q-ring stage holds two k-blocks
-    p.sk_tile[q] = static_cast<int>(t);
-    p.sk_off[q] = static_cast<int>(b);
-  }
+  (void)n_kb;  // pair q: tile q / S, k-blocks from n_kb * (q % S) / S (sk_cut)
   p.sk_pairs = static_cast<int>(tiles * S);
   p.split = static_cast<int>(S);
   p.tok256 = tok256 ? 1 : 0;
@@ -129,12 +123,7 @@ double plan_pair(GemmArgs& p) {
     if (total / pairs < kSkMinBlocksPerPair) pairs = total / kSkMinBlocksPerPair;
     const double c = pairs >= 2 ? static_cast<double>(total) / pairs + kSkFixUnits : 1e30;
     if (pairs >= 2 && (mode == 1 || c <= best)) {
-      for (int64_t q = 0; q <= pairs; ++q) {
-        int64_t b = total * q / pairs;
-        if ((b % n_kb) & 1) ++b;  // even offset: a Q-ring stage holds two k-blocks
-        p.sk_tile[q] = static_cast<int>(b / n_kb);
-        p.sk_off[q] = static_cast<int>(b % n_kb);
-      }
+      // pair q starts at k-block total * q / pairs (sk_cut)
       p.sk_pairs = static_cast<int>(pairs);
       return c;
     }

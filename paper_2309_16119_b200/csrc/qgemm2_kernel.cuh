@@ -78,6 +78,26 @@ static_assert(kSkSlotFloats == 2LL * PAIR_TOK * BM, "stream-K slot = both CTAs' 
 //    stores the result. A pair's first segment may start mid-tile: it writes
 //    its accumulators as a partial and publishes a flag. Owners process their
 //    part last in their range, so the partials they need are normally ready.
+// Start (tile, k-block) of pair q's range (q = sk_pairs: the end of the space).
+// Same formula as the host planner (qgemm2.cu set_split / stream-K cuts): cuts
+// land on even k-block offsets (a Q-ring stage holds two k-blocks).
+__device__ __forceinline__ void sk_cut(const GemmArgs& p, int n_kb, int n_tiles, int q, int& t,
+                                       int& kb) {
+  if (p.split > 0) {
+    const int S = p.split;
+    t = q / S;
+    int b = n_kb * (q - t * S) / S;
+    if (b & 1) ++b;
+    kb = b;
+  } else {
+    const long long total = static_cast<long long>(n_tiles) * n_kb;
+    long long b = total * q / p.sk_pairs;
+    if ((b % n_kb) & 1) ++b;
+    t = static_cast<int>(b / n_kb);
+    kb = static_cast<int>(b % n_kb);
+  }
+}
+
 template <bool SK>
 struct SegSched {
   int t, kb, t_end, kb_end, n_kb, n_tiles, stride;
@@ -89,12 +109,13 @@ struct SegSched {
       // called by full, converged warps: the REDUX broadcast puts the cuts in
       // uniform registers, keeping the MMA issuer's loop (and its smem
       // descriptors) on the uniform datapath instead of an R2UR waterfall
-      t = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_tile[cid])));
-      kb = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_off[cid])));
-      t_end = static_cast<int>(
-          __reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_tile[cid + 1])));
-      kb_end = static_cast<int>(
-          __reduce_min_sync(0xffffffffu, static_cast<unsigned>(p.sk_off[cid + 1])));
+      int t0, k0, t1, k1;
+      sk_cut(p, nkb, tiles, cid, t0, k0);
+      sk_cut(p, nkb, tiles, cid + 1, t1, k1);
+      t = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(t0)));
+      kb = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(k0)));
+      t_end = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(t1)));
+      kb_end = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(k1)));
     } else {
       t = cid;
       stride = ncl;
@@ -124,9 +145,14 @@ struct SegSched {
     return t_end - t + (kb_end > 0 ? 1 : 0);
   }
   // pairs (cid, q_end) whose ranges start inside `tile` (the owner's contributors)
-  __device__ static int contrib_end(const GemmArgs& p, int cid, int tile) {
+  __device__ int contrib_end(const GemmArgs& p, int cid, int tile) const {
     int q = cid + 1;
-    while (q < p.sk_pairs && p.sk_tile[q] == tile) ++q;
+    while (q < p.sk_pairs) {
+      int tq, kq;
+      sk_cut(p, n_kb, n_tiles, q, tq, kq);
+      if (tq != tile) break;
+      ++q;
+    }
     return q;
   }
 };
@@ -642,7 +668,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       // starts at k-block 0 but ends early adds pairs [cid+1, q_end)'s partials
       const bool contrib = SK && kb0 != 0;
       constexpr bool split = false;  // split-K runs in split_fixup (all warps)
-      const int q_end = (SK && !split && !contrib && kb1 != n_kb) ? SegSched<SK>::contrib_end(p, cid, tile)
+      const int q_end = (SK && !split && !contrib && kb1 != n_kb) ? sc.contrib_end(p, cid, tile)
                                                             : cid + 1;
       const int r_in = qd * 32 + lane;
       mbar_wait_backoff<EPI_NS>(tfull, local & 1);
