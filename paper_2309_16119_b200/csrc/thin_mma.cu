@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -137,29 +138,21 @@ __device__ __forceinline__ int first_tile_of(int c, int64_t units, int64_t G, in
   return static_cast<int>(c * units / G) / chunks;
 }
 
-// Flush of one output tile (all threads of the CTA, uniform). The fragment
+// Flush of one output tile (all threads of the CTA, uniform): the fragment
 // partials go to this CTA's slot (slot 0 when `tile` is the first tile of its
-// range, else slot 1; row-major [TM rows][ROWS cols], the output's own order).
-// A tile covered by one CTA is finished by it at once. A shared tile (CTAs
-// c_lo..c_hi) is reduced by its PARTICIPANTS — the contributors whose range
-// ends in it (c_lo..c_hi-1, plus c_hi when its range also ends here), which
-// all reach it at about the kernel's end: every contributor arrives on the
-// tile's counter (acq_rel); each participant waits for all arrivals, then
-// reduces its own 1/n_part of the tile's float4 positions over every
-// contributor's slot (contributor groups per position combined in a fixed
-// order through shared memory: deterministic) and writes that piece of the
-// outputs. (The last arriver summing every slot alone was the launch's tail:
-// ~7 us at 512 tokens with 64 contributors per tile, scripts/thin_timeline.py.)
-// The last departing participant resets the tile's counters for the next
-// launch. Waiting needs every CTA of the grid resident: one wave (thin_ctas).
+// range, else slot 1; row-major [TM rows][ROWS cols], the output's own order);
+// when every contributor has written (counter), the last one sums the slots in
+// CTA order and stores.
+// Lock-free on purpose: no CTA ever waits for another (a spin-waiting
+// reduction deadlocks when two such grids are co-scheduled on different
+// streams and each holds the SMs the other's unscheduled CTAs need); the
+// launcher caps the contributors per tile instead (kMinUnitsPerCta).
 template <int NT>
 __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
-                           const ThinOut& o, int64_t n_out, bool last, float4* scratch) {
+                           const ThinOut& o, int64_t n_out, bool /*last*/, float4* /*scratch*/) {
   constexpr int ROWS = 8 * NT;
   constexpr int SLOT = TM * ROWS;
-  constexpr int C4 = ROWS / 4;        // float4s per slot row
-  constexpr int P = SLOT / 4;         // float4 positions per tile
-  constexpr int QB = 4;               // loads in flight per thread (x float4)
+  __shared__ int s_last;
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -175,56 +168,72 @@ __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
   }
   const int c_lo = cta_of_unit(static_cast<int64_t>(tile) * chunks, units, G);
   const int c_hi = cta_of_unit(static_cast<int64_t>(tile + 1) * chunks - 1, units, G);
-  const int n_con = c_hi - c_lo + 1;
-  int n_part = 1, k_part = 0;
-  int* arrive = o.cnt + tile;
-  int* depart = o.cnt + units / chunks + tile;
   // bar.sync orders the CTA's slot stores before thread 0's acq_rel atomic (a
-  // cumulative gpu-scope release); a participant's thread 0 acquires every
+  // cumulative gpu-scope release); the finisher's thread 0 acquires every other
   // contributor's release through the same counter and the second bar.sync
   // passes that on to its threads, whose L2 (.cg) loads then see the slots.
+  // (A per-thread __threadfence() here is a fence.sc per thread: measured
+  // ~3x slower for the whole kernel.)
   __syncthreads();
-  if (n_con > 1) {
-    const int hi_last = (static_cast<int>(static_cast<int64_t>(c_hi + 1) * units / G) - 1) / chunks;
-    n_part = n_con - (hi_last == tile ? 0 : 1);
-    if (threadIdx.x == 0) atom_add_acq_rel_gpu(arrive, 1);
-    if (!last) return;  // c == c_hi continuing past this tile: contributes only
-    k_part = c - c_lo;
-    thin_stamp(o, 5);
-    if (threadIdx.x == 0)
-      while (ld_acquire_gpu_s32(arrive) < n_con) __nanosleep(64);
-    __syncthreads();
-    if (kThinTrace && o.trace && threadIdx.x == 0) o.trace[8 * blockIdx.x + 4] = 1;
-  }
-  // this participant's positions [p0, p1) of the tile, over contributors c_lo..c_hi
-  const int p0 = k_part * P / n_part, p1 = (k_part + 1) * P / n_part, pc = p1 - p0;
-  auto slot_of = [&](int q) {
-    const int wq = (q == c_lo && tile != first_tile_of(c_lo, units, G, chunks)) ? 1 : 0;
-    return reinterpret_cast<const float4*>(o.ws + (static_cast<int64_t>(q) * 2 + wq) * SLOT);
-  };
-  auto sum_over = [&](int p, int q_first, int q_step, float4& s) {  // contributors in order
-    s = __ldcg(slot_of(q_first) + p);
-    for (int q0 = q_first + q_step; q0 <= c_hi; q0 += QB * q_step) {
-      float4 buf[QB];
-#pragma unroll
-      for (int i = 0; i < QB; ++i)
-        if (q0 + i * q_step <= c_hi) buf[i] = __ldcg(slot_of(q0 + i * q_step) + p);
-#pragma unroll
-      for (int i = 0; i < QB; ++i)
-        if (q0 + i * q_step <= c_hi) {
-          s.x += buf[i].x;
-          s.y += buf[i].y;
-          s.z += buf[i].z;
-          s.w += buf[i].w;
-        }
+  if (c_lo != c_hi) {
+    if (threadIdx.x == 0) {
+      const int old = atom_add_acq_rel_gpu(o.cnt + tile, 1);
+      s_last = old == c_hi - c_lo;
+      if (s_last) o.cnt[tile] = 0;  // self-resetting for the next launch on this stream
     }
-  };
+    __syncthreads();
+    if (!s_last) return;
+  }
+  thin_stamp(o, 5);
+  if (kThinTrace && o.trace && threadIdx.x == 0) o.trace[8 * blockIdx.x + 4] = 1;
+  // Finisher: v(row, j) = Σ_{q = c_lo..c_hi} slot_q(row, j), in CTA order. Every
+  // contributor after c_lo starts its range inside this tile, so its slot is 0;
+  // c_lo's is 0 only when the tile is its first. The finisher is the launch's
+  // tail, so it is built for memory-level parallelism and coalescing: each
+  // thread owns PER float4s = 4 consecutive columns of one row, keeps QB·PER
+  // loads in flight, and stores row-major (16-B fp32 / 8-B bf16 stores; measured:
+  // scattered 4-B stores made the tail ~10 us of a 28 us launch).
+  constexpr int C4 = ROWS / 4;                  // float4s per slot row
+  constexpr int PER = SLOT / (4 * TTHREADS);    // float4 positions per thread (= NT)
+  static_assert(SLOT % (4 * TTHREADS) == 0, "slot must tile the CTA in float4s");
+  constexpr int QB = 8 / PER > 0 ? 8 / PER : 1;
+  const float* s0 = o.ws + (static_cast<int64_t>(c_lo) * 2 +
+                            (tile == first_tile_of(c_lo, units, G, chunks) ? 0 : 1)) * SLOT;
+  float4 acc4[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k)
+    acc4[k] = __ldcg(reinterpret_cast<const float4*>(s0) + threadIdx.x + k * TTHREADS);
+  for (int q0 = c_lo + 1; q0 <= c_hi; q0 += QB) {
+    float4 buf[QB][PER];
+#pragma unroll
+    for (int i = 0; i < QB; ++i) {
+      if (q0 + i <= c_hi) {
+        const float4* p = reinterpret_cast<const float4*>(o.ws + static_cast<int64_t>(q0 + i) * 2 * SLOT);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) buf[i][k] = __ldcg(p + threadIdx.x + k * TTHREADS);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < QB; ++i) {
+      if (q0 + i <= c_hi) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          acc4[k].x += buf[i][k].x;
+          acc4[k].y += buf[i][k].y;
+          acc4[k].z += buf[i][k].z;
+          acc4[k].w += buf[i][k].w;
+        }
+      }
+    }
+  }
   const bool vec_out = (o.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0;
   const bool vec_pad = o.pad && (o.ldp & 3) == 0 && (reinterpret_cast<uintptr_t>(o.pad) & 7) == 0;
-  auto finish = [&](int p4, const float4& a) {  // outputs of one float4 position
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int p4 = threadIdx.x + k * TTHREADS;
     const int tr = p4 / C4, j = 4 * (p4 - tr * C4);
     const int64_t row = static_cast<int64_t>(tile) * TM + tr;
-    const float vv[4] = {a.x, a.y, a.z, a.w};
+    const float vv[4] = {acc4[k].x, acc4[k].y, acc4[k].z, acc4[k].w};
     if (row < n_out) {
       if (vec_out && j + 4 <= o.rc) {
         *reinterpret_cast<float4*>(o.out + row * o.ldo + j) =
@@ -261,43 +270,11 @@ __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
         }
       }
     }
-  };
-  if (pc >= TTHREADS || n_con == 1) {
-    // enough positions for every thread: each sums its positions over all contributors
-    for (int p = p0 + threadIdx.x; p < p1; p += TTHREADS) {
-      float4 s;
-      sum_over(p, c_lo, 1, s);
-      finish(p, s);
-    }
-  } else {
-    // few positions (many participants): contributor groups per position, then
-    // the groups' partials combined in group order (scratch: the idle TMA ring)
-    int ng = TTHREADS / pc;
-    if (ng > n_con) ng = n_con;
-    const int t = threadIdx.x, pi = t % pc, gi = t / pc;
-    if (gi < ng) {
-      float4 s;
-      sum_over(p0 + pi, c_lo + gi, ng, s);
-      scratch[gi * pc + pi] = s;
-    }
-    __syncthreads();
-    if (t < pc) {
-      float4 s = scratch[t];
-      for (int k = 1; k < ng; ++k) {
-        const float4 v = scratch[k * pc + t];
-        s.x += v.x;
-        s.y += v.y;
-        s.z += v.z;
-        s.w += v.w;
-      }
-      finish(p0 + t, s);
-    }
   }
-  if (o.pad && o.pad_cols > ROWS) {  // zero pad columns [ROWS, pad_cols) of this piece's rows
-    const int r0 = k_part * TM / n_part, r1 = (k_part + 1) * TM / n_part;
+  if (o.pad && o.pad_cols > ROWS) {  // zero pad columns [ROWS, pad_cols): 8-B stores
     const int pc4 = (o.pad_cols - ROWS) / 4;
-    for (int idx = threadIdx.x; idx < (r1 - r0) * pc4; idx += TTHREADS) {
-      const int tr = r0 + idx / pc4, j = ROWS + 4 * (idx % pc4);
+    for (int idx = threadIdx.x; idx < TM * pc4; idx += TTHREADS) {
+      const int tr = idx / pc4, j = ROWS + 4 * (idx - tr * pc4);
       const int64_t row = static_cast<int64_t>(tile) * TM + tr;
       if (row < n_out) {
         if (vec_pad)
@@ -307,13 +284,7 @@ __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
       }
     }
   }
-  __syncthreads();  // the slot / scratch are reused by this CTA's next flush
-  if (n_con > 1 && threadIdx.x == 0) {
-    if (atom_add_acq_rel_gpu(depart, 1) == n_part - 1) {  // every participant has read the slots
-      *arrive = 0;  // self-resetting for the next launch on this stream
-      *depart = 0;
-    }
-  }
+  __syncthreads();  // the slot is rewritten by this CTA's next flush
 }
 
 // out[t, j] (+)= Σ_k act[t, k] · Wt[j, k]   (Wt = W transposed, hi/lo bf16 planes)
@@ -535,14 +506,26 @@ int blocks_for(int64_t work) {
   return static_cast<int>(b < 1 ? 1 : b);
 }
 
-// One resident wave: CTAs = min(units, resident CTAs per SM x SMs).
+// CTAs per launch: at most one resident wave, and at most kMaxContrib CTAs per
+// output tile (the tile's last arriver reads every contributor's slot: with a
+// resident wave over few tiles — 4 token tiles at 512 tokens — that serial
+// read was most of the launch).
+int max_contrib() {
+  static const int v = [] {
+    const char* e = getenv("MLRA_THIN_MAXC");
+    return e && atoi(e) > 0 ? atoi(e) : 16;
+  }();
+  return v;
+}
 template <typename K>
-int wave_ctas(K kernel, int smem, int64_t units) {
+int wave_ctas(K kernel, int smem, int64_t units, int64_t tiles) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TTHREADS, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  const int64_t cap = static_cast<int64_t>(per_sm) * sms();
+  int64_t cap = static_cast<int64_t>(per_sm) * sms();
+  const int64_t by_tiles = tiles * max_contrib();
+  if (by_tiles < cap) cap = by_tiles;
   return static_cast<int>(units < cap ? units : cap);
 }
 
@@ -578,7 +561,7 @@ cudaError_t thin_map(CUtensorMap* m, const void* base, int64_t inner, int64_t ou
 // Grid of one launch: one resident wave. The dynamic-smem opt-in is set first,
 // so the occupancy query (and the workspace sized from it) matches the launch.
 template <int NT>
-int thin_ctas(bool row, int64_t units) {
+int thin_ctas(bool row, int64_t units, int64_t tiles) {
   const int smem = ThinSmem<NT>::BYTES;
   static bool attr_row = false, attr_col = false;
   bool& attr = row ? attr_row : attr_col;
@@ -589,7 +572,8 @@ int thin_ctas(bool row, int64_t units) {
     if (e != cudaSuccess) return 0;
     attr = true;
   }
-  return row ? wave_ctas(k_rowmma<NT>, smem, units) : wave_ctas(k_colmma<NT>, smem, units);
+  return row ? wave_ctas(k_rowmma<NT>, smem, units, tiles)
+             : wave_ctas(k_colmma<NT>, smem, units, tiles);
 }
 
 template <int NT>
@@ -597,9 +581,9 @@ void ws_size_nt(bool row, int64_t m, int64_t d, int64_t* ws_floats, int64_t* n_c
   const int64_t tiles = row ? (m + TM - 1) / TM : (d + TM - 1) / TM;
   const int64_t chunks = row ? (d + TILE - 1) / TILE : (m + TILE - 1) / TILE;
   const int64_t units = tiles * chunks;
-  const int64_t ctas = units > 0 ? thin_ctas<NT>(row, units) : 0;
+  const int64_t ctas = units > 0 ? thin_ctas<NT>(row, units, tiles) : 0;
   *ws_floats = ctas * 2 * TM * 8 * NT;
-  *n_cnt = 2 * tiles;  // arrival + departure counters per output tile
+  *n_cnt = tiles;
 }
 
 template <int NT>
@@ -618,7 +602,7 @@ cudaError_t rowmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   if (e == cudaSuccess) e = thin_map(&fm, hi, ldw, 2 * ROWS, ldw, 2 * ROWS);
   if (e != cudaSuccess) return e;
   const int smem = ThinSmem<NT>::BYTES;
-  const int ctas = thin_ctas<NT>(true, units);
+  const int ctas = thin_ctas<NT>(true, units, tb);
   if (ctas <= 0 || o.ws_floats < static_cast<int64_t>(ctas) * 2 * TM * ROWS)
     return cudaErrorInvalidValue;
   o.rc = static_cast<int>(r);
@@ -642,7 +626,7 @@ cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   if (e == cudaSuccess) e = thin_map(&fm, hi, ldv, 2 * ROWS, ldv, 2 * ROWS);
   if (e != cudaSuccess) return e;
   const int smem = ThinSmem<NT>::BYTES;
-  const int ctas = thin_ctas<NT>(false, units);
+  const int ctas = thin_ctas<NT>(false, units, nb);
   if (ctas <= 0 || o.ws_floats < static_cast<int64_t>(ctas) * 2 * TM * ROWS)
     return cudaErrorInvalidValue;
   o.rc = static_cast<int>(r);
