@@ -408,3 +408,44 @@ def test_adapter_gradients_bitwise_reproducible(d_out, d_in, r, m, bias):
     for other in runs[1:]:
         for u, v in zip(runs[0], other):
             assert (u is None and v is None) or torch.equal(u, v)
+
+
+def test_workspace_arena_across_streams_sizes_and_capture():
+    """The per-stream workspace arena (capi.cu Scratch): a pass gives the same bits
+    on any stream, across arena regrowth (small -> large -> small on one stream),
+    and under CUDA graph capture (which takes the pool path)."""
+
+    def make(d_out, d_in, r, seed):
+        q, *_ = random_quantized(d_out, d_in, 3, 128, seed=seed)
+        a = (torch.randn(d_out, r, generator=torch.Generator().manual_seed(seed)) * 0.02).cuda()
+        b = (torch.randn(d_in, r, generator=torch.Generator().manual_seed(seed + 1)) * 0.02).cuda()
+        return M.ModuLoraLayer("arena", M.DeviceQuantizedMatrix(q), M.LoraAdapter(a, b, r, 16.0))
+
+    def run(layer, m, seed):
+        x = torch.randn(m, layer.d_in(), generator=torch.Generator().manual_seed(seed)).to(torch.bfloat16).cuda()
+        dy = torch.randn(m, layer.d_out(), generator=torch.Generator().manual_seed(seed + 7)).to(torch.bfloat16).cuda()
+        y, xb = M.layer_forward(layer, x)
+        dx = M.layer_backward(layer, x, xb, dy)
+        return [t.clone() for t in (y, xb, dx, *M.grads_of_adapter(layer))]
+
+    small, big = make(256, 512, 8, 11), make(4096, 4096, 16, 12)
+    ref_small, ref_big = run(small, 300, 1), run(big, 1024, 2)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for st, layer, m, seed, ref in ((s1, small, 300, 1, ref_small), (s2, big, 1024, 2, ref_big),
+                                    (s1, big, 1024, 2, ref_big), (s1, small, 300, 1, ref_small)):
+        with torch.cuda.stream(st):
+            got = run(layer, m, seed)
+        st.synchronize()
+        for u, v in zip(got, ref):
+            assert torch.equal(u, v)
+    # graph capture (pool path), replayed
+    x = torch.randn(300, 512, generator=torch.Generator().manual_seed(1)).to(torch.bfloat16).cuda()
+    M.layer_forward(small, x)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        yg, xbg = M.layer_forward(small, x)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(yg, ref_small[0]) and torch.equal(xbg, ref_small[1])
