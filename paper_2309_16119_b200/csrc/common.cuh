@@ -173,6 +173,20 @@ __device__ __forceinline__ void unit_magic(uint32_t v, uint32_t (&m)[8]) {
       m[2 * j] = __byte_perm(lo, 0x4B000000u, 0x7540u | j);
       m[2 * j + 1] = __byte_perm(hi, 0x4B000000u, 0x7540u | j);
     }
+  } else if constexpr (BITS == 2) {
+    // spread the 2-bit fields into nibbles (x: codes 0,2,4,6; y: codes 1,3,5,7),
+    // then the 4-bit byte-permute path: lo byte j = nibble 2j, hi byte j = nibble 2j+1
+    const uint32_t w = (v & 0x3333u) | (((v >> 2) & 0x3333u) << 16);
+    const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
+    // lo bytes = codes (0, 4, 1, 5), hi bytes = codes (2, 6, 3, 7)
+    m[0] = __byte_perm(lo, 0x4B000000u, 0x7540u);
+    m[1] = __byte_perm(lo, 0x4B000000u, 0x7542u);
+    m[2] = __byte_perm(hi, 0x4B000000u, 0x7540u);
+    m[3] = __byte_perm(hi, 0x4B000000u, 0x7542u);
+    m[4] = __byte_perm(lo, 0x4B000000u, 0x7541u);
+    m[5] = __byte_perm(lo, 0x4B000000u, 0x7543u);
+    m[6] = __byte_perm(hi, 0x4B000000u, 0x7541u);
+    m[7] = __byte_perm(hi, 0x4B000000u, 0x7543u);
   } else {
     constexpr uint32_t mask = (1u << BITS) - 1u;
 #pragma unroll

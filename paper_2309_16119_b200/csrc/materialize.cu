@@ -149,18 +149,25 @@ __device__ __forceinline__ uint32_t quad_bits(const uint32_t* __restrict__ rw, i
   return __funnelshift_r(lo, hi, off) & qmask;
 }
 
-template <int BITS, bool F32>
+// Uncertified groups (rare: the per-group fp32-FMA exactness check failed at
+// upload) take the exact f64 path out of line, so the hot loop keeps few registers.
+template <int BITS>
+__device__ __noinline__ uint4 deq8_bf16_slow(uint32_t v, float2 g) {
+  return deq8_bf16<BITS>(v, g);
+}
+
+template <int BITS, bool F32, int GSHIFT>
 __global__ void __launch_bounds__(128) k_materialize_fast(const QWeightDev q, int64_t row0,
                                                           void* __restrict__ out, int64_t ld,
                                                           int64_t items, int gshift) {
   constexpr int CODES = F32 ? 4 : 8;
   constexpr int IPT = 4;  // items per thread, strided by 32: every warp store covers 512 B
-  const int64_t rr = blockIdx.y;
-  const int64_t r = row0 + rr;
+  const int64_t r = row0 + blockIdx.y;
   const uint32_t* rw = q.words + r * q.row_words;
   const float2* grow = q.grid + r * q.ng_pad;
   const int base = static_cast<int>(blockIdx.x) * 512 + (threadIdx.x >> 5) * 128 + (threadIdx.x & 31);
   const int n = static_cast<int>(items);
+  const int gs = GSHIFT >= 0 ? GSHIFT : gshift;
   // every item's code bits and grid entry are requested before any is decoded
   // (the loop with an early exit issued them one at a time: long-scoreboard bound)
   uint64_t v[IPT];
@@ -170,33 +177,39 @@ __global__ void __launch_bounds__(128) k_materialize_fast(const QWeightDev q, in
     const int it = base + 32 * j;
     if (it < n) {
       const int k0 = it * CODES;
-      g[j] = __ldg(grow + (gshift >= 0 ? (k0 >> gshift) : k0 / static_cast<int>(q.group)));
+      g[j] = __ldg(grow + (gs >= 0 ? (k0 >> gs) : k0 / static_cast<int>(q.group)));
       if constexpr (F32)
         v[j] = quad_bits<BITS>(rw, it);
       else
         v[j] = load_unit<BITS>(rw, it);
     }
   }
+  if constexpr (F32) {
+    float* orow = reinterpret_cast<float*>(out) + static_cast<int64_t>(blockIdx.y) * ld;
 #pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const int it = base + 32 * j;
-    if (it >= n) break;
-    const int k0 = it * CODES;
-    if constexpr (F32) {
+    for (int j = 0; j < IPT; ++j) {
+      const int it = base + 32 * j;
+      if (it >= n) break;
       constexpr uint32_t mask = (1u << BITS) - 1u;
       const uint32_t vv = static_cast<uint32_t>(v[j]);
       float f[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) f[i] = deq_entry((vv >> (BITS * i)) & mask, g[j].x, g[j].y);
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + rr * ld + k0) =
-          make_float4(f[0], f[1], f[2], f[3]);
-    } else {
+      *reinterpret_cast<float4*>(orow + it * CODES) = make_float4(f[0], f[1], f[2], f[3]);
+    }
+  } else {
+    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(out) + static_cast<int64_t>(blockIdx.y) * ld;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const int it = base + 32 * j;
+      if (it >= n) break;
       uint4 o;
       if constexpr (BITS <= 4)
-        o = deq8_bf16_fast<BITS>(static_cast<uint32_t>(v[j]), g[j]);
+        o = g[j].x > 0.0f ? deq8_bf16_cert<BITS>(static_cast<uint32_t>(v[j]), g[j])
+                          : deq8_bf16_slow<BITS>(static_cast<uint32_t>(v[j]), g[j]);
       else
         o = deq8_bf16<BITS>(v[j], g[j]);
-      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + rr * ld + k0) = o;
+      *reinterpret_cast<uint4*>(orow + it * CODES) = o;
     }
   }
 }
@@ -362,10 +375,18 @@ cudaError_t materialize_bits(const QWeightDev& q, int64_t row0, int64_t nrows, v
       if ((int64_t{1} << sft) == q.group) gshift = sft;
     dim3 grid(static_cast<unsigned>((items + 511) / 512), static_cast<unsigned>(nrows));
     note_launch();
-    if (f32)
-      k_materialize_fast<BITS, true><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
-    else
-      k_materialize_fast<BITS, false><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
+    // the LLaMA group (128) gets a compile-time shift
+    if (f32) {
+      if (gshift == 7)
+        k_materialize_fast<BITS, true, 7><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
+      else
+        k_materialize_fast<BITS, true, -1><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
+    } else {
+      if (gshift == 7)
+        k_materialize_fast<BITS, false, 7><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
+      else
+        k_materialize_fast<BITS, false, -1><<<grid, 128, 0, st>>>(q, row0, out, ld, items, gshift);
+    }
     return cudaGetLastError();
   }
   return materialize_tile_bits<BITS>(q, row0, nrows, 0, q.cols, out, ld, f32, vec, st);
