@@ -702,7 +702,7 @@ mlra_status cols_product(cudaStream_t st, const ThinWs& w, const __nv_bfloat16* 
 // leaves idle) and are joined back to the caller's stream before return.
 struct SideStream {
   cudaStream_t st = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, mid = nullptr;
 };
 mlra_status side_stream(SideStream** out) {
   thread_local SideStream per_dev[64];
@@ -714,6 +714,7 @@ mlra_status side_stream(SideStream** out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ss.st, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ss.mid, cudaEventDisableTiming));
   }
   *out = &ss;
   return MLRA_OK;
@@ -1435,6 +1436,27 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   unsigned* flags = gemm_flags(sc, pb);
   if (!flags) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
   CUDA_TRY(mlra::launch_prep(pb, s));
+  // dA early: the side stream starts dA = s·dyᵀ·xb right after the prep launch,
+  // concurrently with dY·A — both stream dY, so the second reader finds much of
+  // it in L2; dB follows once dYA exists (cfg2 step 1166 -> 1139 us, cfg3 -2 %;
+  // MLRA_DA_EARLY=0: dA after dY·A, for A/B)
+  static const bool da_early = getenv("MLRA_DA_EARLY") == nullptr || atoi(getenv("MLRA_DA_EARLY")) != 0;
+  SideStream* side = nullptr;
+  static const bool no_side = getenv("MLRA_NO_SIDE") != nullptr;        // dev A/B switch
+  static const bool side_first = getenv("MLRA_SIDE_FIRST") != nullptr;  // dev A/B switch
+  if (dx && !no_side) {
+    if (mlra_status st = side_stream(&side)) return st;
+    CUDA_TRY(cudaEventRecord(side->fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(side->st, side->fork, 0));
+  }
+  const bool early = side != nullptr && da_early;
+  auto grad_a = [&](cudaStream_t cs) -> mlra_status {
+    // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
+    return cols_product(cs, w_da, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias);
+  };
+  if (early) {
+    if (mlra_status st = grad_a(side->st)) return st;
+  }
   // K5a: dyA = dy·A ; d(xb) = s·dyA (autodiff.cpp:150-152 on record lora.cpp:69),
   // finished with bf16(s·dyA) (the dX GEMM's extra-K operand) and dyA's
   // transposed hi/lo planes (the dB product's factor)
@@ -1445,18 +1467,14 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   // enqueued FIRST: its persistent pairs take the SMs, and dA / dB fill the SMs
   // its under-filled last wave leaves idle (e.g. 128 tiles over 74 pairs) and its
   // tail, instead of delaying its start (MLRA_SIDE_FIRST=1: the old order).
-  SideStream* side = nullptr;
-  static const bool no_side = getenv("MLRA_NO_SIDE") != nullptr;        // dev A/B switch
-  static const bool side_first = getenv("MLRA_SIDE_FIRST") != nullptr;  // dev A/B switch
-  if (dx && !no_side) {
-    if (mlra_status st = side_stream(&side)) return st;
-    CUDA_TRY(cudaEventRecord(side->fork, s));
-    CUDA_TRY(cudaStreamWaitEvent(side->st, side->fork, 0));
+  if (early) {  // dB needs dYA: the side stream waits for the row product
+    CUDA_TRY(cudaEventRecord(side->mid, s));
+    CUDA_TRY(cudaStreamWaitEvent(side->st, side->mid, 0));
   }
   auto adapter_grads = [&](cudaStream_t cs) -> mlra_status {
-    // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
-    if (mlra_status st = cols_product(cs, w_da, dya, lddya, m, d.rows, xbt, scaling, da, r, dbias))
-      return st;
+    if (!early) {
+      if (mlra_status st = grad_a(cs)) return st;
+    }
     // K6: dB = s·xᵀ·dyA   (autodiff.cpp:153-155 on record lora.cpp:68)
     return cols_product(cs, w_db, xa, ldxa, m, d.cols, dyat, scaling, db, r, nullptr);
   };
