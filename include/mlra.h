@@ -21,6 +21,15 @@
  * thread-local string (mlra_last_error). There is no CPU fallback: on a
  * device that is not sm_100 every compute entry point returns
  * MLRA_ERR_UNSUPPORTED.
+ *
+ * Streams and workspace: a layer pass enqueues its kernels on `stream` (the
+ * backward also uses an internal side stream that is joined back into `stream`
+ * before the call returns). Temporary device memory comes from a per-(device,
+ * stream) arena kept by the library across calls (regrown on demand; the
+ * stream-ordered pool under stream capture or for buffers > 64 MB), so calls
+ * are capturable into CUDA graphs. The small-token GEMM schedules (split-K /
+ * stream-K) need all CTAs of their grid resident at once: do not run two layer
+ * passes concurrently on different streams of one device.
  */
 #ifndef MLRA_H_
 #define MLRA_H_
