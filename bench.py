@@ -483,6 +483,10 @@ def main():
     if world > 1:
         backend = os.environ.get("MLRA_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # NCCL's own communicator-init lines (nRanks per rank) in the log, also
+            # when the driver (not self_launch) started the ranks
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)

@@ -67,6 +67,26 @@ __device__ __forceinline__ uint32_t e8p_mags(uint32_t code, const uint4* tab, fl
   return n;
 }
 
+// E8P bf16 output straight from the signed |a| row: w_j = RN_f32(s·(sign_j·|a_j| + t))
+// (the fused GEMM decode's law, qgemm_dev.cuh dequant_units_e8p; identical bits
+// to sign_j·RN(s·(|a_j| +- 1/4)) since RN is odd-symmetric) — no per-entry
+// magnitude select, one sign-mask XOR per pair.
+__device__ __forceinline__ uint4 e8p_bf16(uint32_t code, const uint4* tab, float s) {
+  const uint4 A = tab[code & 0xFFu];
+  const uint32_t sb = (code >> 8) & 0x7Fu;
+  const uint32_t n = sb | (((__popc(sb) ^ (A.x >> 15)) & 1u) << 7);
+  const float t = (code >> 15) ? 0.25f : -0.25f;
+  const uint32_t w[4] = {A.x & 0xFFFF7FFFu, A.y, A.z, A.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t ws = w[p] ^ ((((n >> (2 * p)) & 3u) * 0x40008000u) & 0x80008000u);
+    o[p] = pack_bf16x2(__fmul_rn(s, __uint_as_float(ws << 16) + t),
+                       __fmul_rn(s, __uint_as_float(ws & 0xFFFF0000u) + t));
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 // One code -> 8 bf16 outputs. Products RN_f32(s·mag) (scalar IEEE
 // multiplies); the sign is applied after rounding (RN commutes with negation):
 // the mask of entries (2p, 2p+1) is ((code >> (8+2p)) & 3) * 0x40008000 &
@@ -222,15 +242,22 @@ __global__ void __launch_bounds__(kCbThreads) k_cb2_materialize(
         cb2_emit_half<VEC, CB16, E8P>(static_cast<float*>(orow), static_cast<int64_t>(it) << 2,
                                       cur[j], cs[j], it & 1, cbh, cb0, cb1, odd);
       } else {
-        float m[8];
-        uint32_t sg;
         if constexpr (E8P) {
-          sg = e8p_mags(cur[j], cbh, m);
+          const uint4 v = e8p_bf16(cur[j], cbh, cs[j]);
+          const int64_t o = static_cast<int64_t>(it) << 3;
+          if constexpr (VEC) {
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(orow) + o) = v;
+          } else {
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              reinterpret_cast<uint16_t*>(orow)[o + e] = static_cast<uint16_t>(w[e >> 1] >> (16 * (e & 1)));
+          }
         } else {
+          float m[8];
           cb2_mags<CB16>(cur[j], cbh, cb0, cb1, m);
-          sg = cur[j] >> 8;
+          cb2_emit<VEC>(orow, static_cast<int64_t>(it) << 3, cur[j] >> 8, cs[j], m);
         }
-        cb2_emit<VEC>(orow, static_cast<int64_t>(it) << 3, sg, cs[j], m);
       }
     }
   }
