@@ -130,12 +130,27 @@ __device__ __forceinline__ void split3(float x, float y, uint32_t (&parts)[3]) {
   }
 }
 
-template <int A, bool OUT_F32>
+constexpr int kRhtRing = 4;  // blocks in flight per warp (cp.async ring)
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// RING: every warp keeps kRhtRing blocks in flight through a shared-memory ring
+// filled by cp.async (16-B aligned rows; the register-prefetch form had one
+// block of prefetch per warp and was latency-bound: ncu 27 % DRAM, 30 % tensor)
+template <int A, bool OUT_F32, bool RING>
 __global__ void __launch_bounds__(256, A <= 32 ? 3 : 1) k_rht_tc(const __nv_bfloat16* __restrict__ in, int64_t rows,
                                                int64_t cols, int64_t ld_in,
                                                const float* __restrict__ signs, int inverse,
                                                void* __restrict__ out, int64_t ld_out) {
   constexpr int B = 16 * A, NT1 = A / 8, MT = A / 16;
+  constexpr int SLOT = B * 2;              // bytes of one block
+  constexpr int CPL = SLOT / (16 * 32);    // 16-B copies per lane per block
+  extern __shared__ __align__(16) unsigned char rht_ring[];
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t nblk = cols / B, total = rows * nblk;
   const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -144,8 +159,18 @@ __global__ void __launch_bounds__(256, A <= 32 ? 3 : 1) k_rht_tc(const __nv_bflo
   const uint32_t h0 = h_pair(g, 2 * tq), h1 = h_pair(g + 8, 2 * tq), h2 = h_pair(g, 2 * tq + 8),
                  h3 = h_pair(g + 8, 2 * tq + 8);
   const float norm = rsqrtf(static_cast<float>(B));
-  // the next block's operands are loaded before this block's MMAs (two blocks'
-  // loads in flight per warp)
+  const uint32_t wring = static_cast<uint32_t>(__cvta_generic_to_shared(rht_ring)) +
+                         static_cast<uint32_t>(threadIdx.x >> 5) * (kRhtRing * SLOT);
+  auto issue = [&](int64_t b, int slot) {  // block b -> ring slot (one commit group)
+    if (b < total) {
+      const int64_t r = b / nblk, c0 = (b - r * nblk) * B;
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(in + r * ld_in + c0);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        cp_async16(wring + slot * SLOT + (lane + 32 * c) * 16, src + (lane + 32 * c) * 16);
+    }
+    cp_async_commit();
+  };
   uint32_t nb0[NT1], nb1[NT1];
   auto load = [&](int64_t b) {
     const int64_t r = b / nblk, c0 = (b - r * nblk) * B;
@@ -157,16 +182,36 @@ __global__ void __launch_bounds__(256, A <= 32 ? 3 : 1) k_rht_tc(const __nv_bflo
       nb1[j] = __ldg(src + e / 2 + 4);
     }
   };
-  if (warp0 < total) load(warp0);
-  for (int64_t blk = warp0; blk < total; blk += nwarps) {
+  if constexpr (RING) {
+#pragma unroll
+    for (int d = 0; d < kRhtRing - 1; ++d) issue(warp0 + d * nwarps, d);
+  } else {
+    if (warp0 < total) load(warp0);
+  }
+  int it = 0;
+  for (int64_t blk = warp0; blk < total; blk += nwarps, ++it) {
     const int64_t r = blk / nblk, c0 = (blk - r * nblk) * B;
     uint32_t cb0[NT1], cb1[NT1];
+    if constexpr (RING) {
+      issue(blk + (kRhtRing - 1) * nwarps, (it + kRhtRing - 1) % kRhtRing);
+      cp_async_wait<kRhtRing - 1>();  // this block's group has landed (own copies)
+      __syncwarp();                    // ... and every lane's
+      const uint32_t sl = wring + (it % kRhtRing) * SLOT;
 #pragma unroll
-    for (int j = 0; j < NT1; ++j) {
-      cb0[j] = nb0[j];
-      cb1[j] = nb1[j];
+      for (int j = 0; j < NT1; ++j) {
+        const int e = 16 * (8 * j + g) + 2 * tq;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cb0[j]) : "r"(sl + e * 2));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cb1[j]) : "r"(sl + e * 2 + 16));
+      }
+      __syncwarp();  // the slot is refilled by the next iteration's issue
+    } else {
+#pragma unroll
+      for (int j = 0; j < NT1; ++j) {
+        cb0[j] = nb0[j];
+        cb1[j] = nb1[j];
+      }
+      if (blk + nwarps < total) load(blk + nwarps);
     }
-    if (blk + nwarps < total) load(blk + nwarps);
     // step 1: C1[j] = (H_16 · M^T) restricted to a in [8j, 8j + 8)
     float c1[NT1][4];
 #pragma unroll
@@ -220,6 +265,7 @@ __global__ void __launch_bounds__(256, A <= 32 ? 3 : 1) k_rht_tc(const __nv_bflo
       }
     }
   }
+  if constexpr (RING) cp_async_wait<0>();
 }
 
 template <int A>
@@ -229,15 +275,33 @@ cudaError_t rht_tc(const void* in, int64_t rows, int64_t cols, int64_t ld_in, co
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_sm = A <= 32 ? 3 : 1;
   int64_t blocks = (total + 7) / 8;
-  if (blocks > 3LL * sms) blocks = 3LL * sms;  // resident 8-warp CTAs, grid-stride
+  if (blocks > per_sm * static_cast<int64_t>(sms)) blocks = per_sm * static_cast<int64_t>(sms);
+  const bool ring = ld_in % 8 == 0 && reinterpret_cast<uintptr_t>(in) % 16 == 0 &&
+                    getenv("MLRA_RHT_NORING") == nullptr;
+  const int smem = ring ? 8 * kRhtRing * 16 * A * 2 : 0;
   note_launch();
-  if (f32)
-    k_rht_tc<A, true><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(in), rows, cols, ld_in, signs, inverse, out, ld_out);
-  else
-    k_rht_tc<A, false><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(in), rows, cols, ld_in, signs, inverse, out, ld_out);
+  const auto* x = static_cast<const __nv_bfloat16*>(in);
+  const dim3 grid(static_cast<unsigned>(blocks));
+#define MLRA_RHT_LAUNCH(F, R)                                                                  \
+  do {                                                                                         \
+    if (R) {                                                                                   \
+      static bool attr = false;                                                                \
+      if (!attr) {                                                                             \
+        cudaFuncSetAttribute(k_rht_tc<A, F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                             smem);                                                            \
+        attr = true;                                                                           \
+      }                                                                                        \
+    }                                                                                          \
+    k_rht_tc<A, F, R><<<grid, 256, smem, st>>>(x, rows, cols, ld_in, signs, inverse, out, ld_out); \
+  } while (0)
+  if (f32) {
+    if (ring) MLRA_RHT_LAUNCH(true, true); else MLRA_RHT_LAUNCH(true, false);
+  } else {
+    if (ring) MLRA_RHT_LAUNCH(false, true); else MLRA_RHT_LAUNCH(false, false);
+  }
+#undef MLRA_RHT_LAUNCH
   return cudaGetLastError();
 }
 
