@@ -149,7 +149,7 @@ __device__ __forceinline__ int first_tile_of(int c, int64_t units, int64_t G, in
 // launcher caps the contributors per tile instead (kMinUnitsPerCta).
 template <int NT>
 __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
-                           const ThinOut& o, int64_t n_out, bool /*last*/, float4* /*scratch*/) {
+                           const ThinOut& o, int64_t n_out) {
   constexpr int ROWS = 8 * NT;
   constexpr int SLOT = TM * ROWS;
   __shared__ int s_last;
@@ -356,8 +356,7 @@ __global__ void __launch_bounds__(TTHREADS, 3)
     __syncthreads();
     const int tile = u / kchunks;
     if (u + 1 == u1 || (u + 1) / kchunks != tile)  // leaving this token tile
-      thin_flush<NT>(acc, tile, kchunks, units, o, m, u + 1 == u1,
-                     reinterpret_cast<float4*>(sm));
+      thin_flush<NT>(acc, tile, kchunks, units, o, m);
   }
   thin_stamp(o, 3);
 }
@@ -437,8 +436,7 @@ __global__ void __launch_bounds__(TTHREADS, 3)
     __syncthreads();
     const int nt = u / tchunks;
     if (u + 1 == u1 || (u + 1) / tchunks != nt)  // leaving this n tile
-      thin_flush<NT>(acc, nt, tchunks, units, o, nd, u + 1 == u1,
-                     reinterpret_cast<float4*>(sm));
+      thin_flush<NT>(acc, nt, tchunks, units, o, nd);
   }
   thin_stamp(o, 3);
 }
