@@ -161,6 +161,26 @@ def test_rht_matches_f64_and_inverts(block):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("block", [256, 512])
+def test_rht_strided_rows_take_the_register_path(block):
+    """Rows whose stride is not a 16-B multiple cannot feed the cp.async ring: the
+    tensor-core RHT falls back to register prefetch — same values as the ring
+    path on a contiguous copy (bit for bit) and as the f64 transform."""
+    m, d = 37, 4 * block
+    x64 = orc.bf16_round(orc.gaussian(block + 1, m, d))
+    wide = torch.zeros(m, d + 2, dtype=torch.bfloat16, device="cuda")
+    wide[:, :d] = to_bf16_dev(x64)
+    strided = wide[:, :d]  # row stride d + 2 elements: 4-B but not 16-B aligned rows
+    s = M.random_signs(d, 11)
+    for inv in (False, True):
+        y_str = M.rht(strided, s, block, inverse=inv, out_dtype=torch.float32)
+        y_con = M.rht(strided.contiguous(), s, block, inverse=inv, out_dtype=torch.float32)
+        assert torch.equal(y_str, y_con)
+        want = _np_rht(x64, s.cpu().numpy().astype(np.float64), block, inv)
+        assert rel_fro(f64(y_str), want) <= 1e-6
+
+
+@pytest.mark.gpu
 def test_incoherent_e8p_layer_is_the_unrotated_linear():
     """y = U^T(W~ V x) + s(xB)A^T + bias with W~ quantized by E8P in the rotated
     basis equals the layer on W = U^T W~ V (exactly, in f64) with A = U^T A~,
