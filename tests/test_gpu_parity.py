@@ -449,3 +449,30 @@ def test_workspace_arena_across_streams_sizes_and_capture():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(yg, ref_small[0]) and torch.equal(xbg, ref_small[1])
+
+
+@pytest.mark.parametrize("env", [{"MLRA_PDL": "0"}, {"MLRA_DA_EARLY": "0"}, {"MLRA_SIDE_FIRST": "1"},
+                                 {"MLRA_NO_SIDE": "1"}, {"MLRA_THIN_MAXC": "1000"}])
+def test_launch_switches_bit_identical(env, tmp_path):
+    """The launch-order / launch-mode switches (programmatic dependent launch, the
+    side-stream schedule of dA/dB, the skinny-product CTA cap) change only when
+    kernels run, never what they compute: bitwise-equal outputs."""
+    import os
+    import subprocess
+    import sys
+    helper = os.path.join(os.path.dirname(__file__), "helpers", "layer_pass_dump.py")
+    ref_p, alt_p = tmp_path / "ref.npz", tmp_path / "alt.npz"
+    base = {k: v for k, v in os.environ.items() if not k.startswith("MLRA_")}
+    for path, extra in ((ref_p, {}), (alt_p, env)):
+        r = subprocess.run([sys.executable, helper, str(path)], env=dict(base, **extra),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+    ref, alt = np.load(ref_p), np.load(alt_p)
+    for k in ref.files:
+        if env.get("MLRA_THIN_MAXC"):
+            # a different CTA count changes the skinny products' fp32 summation order (and
+            # through bf16(s·xb) the bf16 outputs by at most an ulp here and there)
+            bound = 1e-3 if k.split("_")[0] in ("y", "dx") else 1e-5
+            assert rel_fro(alt[k].astype(np.float64), ref[k].astype(np.float64)) <= bound, k
+        else:
+            assert np.array_equal(ref[k], alt[k]), k
