@@ -52,6 +52,8 @@ struct GemmArgs {
   int split;             // > 0: split-K mode, S pairs per tile (pair q = tile*S + s)
   int tok256;            // split-K with 256-token pair tiles (one accumulator)
   int no_pdl;            // host only: launch without programmatic dependent launch
+  int sk_owner4;         // dev A/B (MLRA_SK_OWNER4=1): stream-K owner fix-up by the 4
+                         // epilogue warps instead of all 16 (set by qgemm2_launch)
   float* sk_ws;          // [sk_pairs x 2 CTAs x 512 tokens x 128 rows] fp32 partials
   unsigned* sk_flags;    // [sk_pairs x 2], zeroed before the launch
 };

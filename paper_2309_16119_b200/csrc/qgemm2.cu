@@ -165,6 +165,13 @@ cudaError_t qgemm2_launch(const GemmMaps& maps, const QWeightDev& q, const GemmA
                           bool w_tma, bool mn, bool out_f32, cudaStream_t stream) {
   if (p.tokens <= 0 || p.m_total <= 0) return cudaSuccess;
   const bool sk = p.sk_pairs != 0;
+  const char* o4 = sk ? getenv("MLRA_SK_OWNER4") : nullptr;  // read per launch, like MLRA_SK
+  if (o4 && o4[0] == '1') {
+    GemmArgs p4 = p;
+    p4.sk_owner4 = 1;
+    return mn ? qgemm2_launch_d1(maps, q, p4, w_tma, out_f32, stream)
+              : qgemm2_launch_f1(maps, q, p4, w_tma, out_f32, stream);
+  }
   if (mn) return sk ? qgemm2_launch_d1(maps, q, p, w_tma, out_f32, stream)
                     : qgemm2_launch_d0(maps, q, p, w_tma, out_f32, stream);
   return sk ? qgemm2_launch_f1(maps, q, p, w_tma, out_f32, stream)

@@ -348,6 +348,81 @@ __device__ __forceinline__ void split_fixup(const GemmArgs& p, int cid, uint32_t
   }
 }
 
+// Stream-K owner fix-up of the pair's LAST segment (tile, k-blocks [0, kb_end)),
+// run by all 16 warps once every MMA of the CTA has completed (the 4 epilogue
+// warps alone took ~12 us after the last MMA at 1024 tokens, profiles/r03x).
+// Contributors (pairs cid+1 .. cid+nc) each published the fp32 partial of the
+// tile's remaining k-blocks. One thread acquires their flags and stages the
+// (chunk, contributor) 16 KB slabs into the idle operand ring in rounds of
+// kFixSlots / nc chunks; warp w (TMEM lane quadrant w & 3) takes chunks
+// w >> 2, +4, ... of each round and sums own + partials in pair order — the
+// same order as the 4-warp path, so the bits are unchanged.
+template <bool OUT_F32>
+__device__ __forceinline__ void sk_owner_fixup(const GemmArgs& p, int cid, uint32_t rank,
+                                               int m_pairs, int tile, int nc, uint32_t tfull_par,
+                                               uint32_t tmem_base, uint64_t* tfull, uint64_t* fixb,
+                                               uint8_t* smem, unsigned long long* tl) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qd = warp & 3, wg = warp >> 2;
+  mbar_wait_backoff<EPI_NS>(tfull, tfull_par);
+  tc_fence_after();
+  if (tl && threadIdx.x == 0) tl[2] = gtime();
+  const int mp = tile % m_pairs, np = tile / m_pairs;
+  const int r_in = qd * 32 + lane;
+  const int64_t wrow = static_cast<int64_t>(mp) * PAIR_ROWS + rank * BM + r_in;
+  const bool row_ok = wrow < p.m_valid;
+  const uint32_t taddr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
+  auto slot_of = [&](int q, int cc) {  // [512 tokens][128 rows] fp32 per CTA
+    return p.sk_ws + (2 * static_cast<int64_t>(q) + rank) * (PAIR_TOK * BM) +
+           static_cast<int64_t>(cc * 32) * BM;
+  };
+  if (threadIdx.x == 0) {
+    for (int q = cid + 1; q <= cid + nc; ++q)
+      while (ld_acquire_gpu(&p.sk_flags[2 * q + rank]) == 0) __nanosleep(64);
+    fence_proxy_async_global();  // acquired partials (generic writes) -> async-proxy reads
+    if (tl) tl[3] = gtime();
+  }
+  const float bias = (p.bias != nullptr && row_ok) ? p.bias[wrow] : 0.0f;
+  const float bias_nb = __shfl_xor_sync(0xffffffffu, bias, 1);
+  const bool odd = lane & 1;
+  const bool pairs = p.out_pairs && __all_sync(0xffffffffu, (wrow | 1) < p.m_valid);
+  const int per_round = kFixSlots / nc;
+  const uint32_t ring = smem_u32(smem);
+  int round = 0;
+  for (int b0 = 0; b0 < 16; b0 += per_round, ++round) {
+    const int nb = 16 - b0 < per_round ? 16 - b0 : per_round;
+    __syncthreads();  // the ring is free (round 0: every MMA has completed; else: consumed)
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < nb; ++i)
+        for (int k = 0; k < nc; ++k) {
+          const int slot = i * nc + k;
+          mbar_arrive_expect_tx(&fixb[slot], kFixChunkBytes);
+          bulk_g2s(ring + slot * kFixChunkBytes, slot_of(cid + 1 + k, b0 + i), kFixChunkBytes,
+                   &fixb[slot]);
+        }
+    }
+    for (int i = wg; i < nb; i += 4) {
+      const int cc = b0 + i;
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + cc * 32, r);
+      tc_wait_ld();
+      for (int k = 0; k < nc; ++k) {  // pair order: deterministic sums
+        const int slot = i * nc + k;
+        mbar_wait(&fixb[slot], static_cast<uint32_t>(round & 1));
+        const float* src = reinterpret_cast<const float*>(smem + slot * kFixChunkBytes) + r_in;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + src[j * BM]);
+      }
+      epi_store<OUT_F32>(p, r, static_cast<int64_t>(np) * PAIR_TOK + cc * 32, wrow, row_ok, bias,
+                         bias_nb, pairs, odd);
+    }
+  }
+  if (tl) {
+    __syncthreads();
+    if (threadIdx.x == 0) tl[4] = gtime();
+  }
+}
+
 template <int BITS, bool W_TMA, bool MN, bool OUT_F32, bool QTMA, bool SK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     qgemm2_kernel(const __grid_constant__ CUtensorMap tm_act,
@@ -406,6 +481,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       __reduce_min_sync(0xffffffffu, static_cast<unsigned>(sched.sk ? sched.kb : 0)));
   const int mma_kb_last = static_cast<int>(
       __reduce_min_sync(0xffffffffu, static_cast<unsigned>(sched.sk ? sched.kb_end : 0)));
+  // stream-K: a last segment [0, kb_end) of tile t_end owns that tile and adds
+  // the partials of pairs cid+1 .. cid+own_nc; all 16 warps run its fix-up
+  // (sk_owner_fixup) unless the ring cannot stage one chunk of every partial
+  const bool own_last = SK && p.split == 0 && !p.sk_owner4 && sched.kb_end > 0 &&
+                        (sched.t_end != sched.t || sched.kb == 0);
+  auto own_count = [&]() {  // contributors of the last segment's tile (0: 4-warp path)
+    const int nc = sched.contrib_end(p, cid, sched.t_end) - cid - 1;
+    return nc <= kFixSlots ? nc : 0;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_act);
@@ -663,6 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int tile, kb0, kb1;
     // split-K: every warp of the CTA runs the fix-up after its role (below)
     for (; !(SK && p.split > 0) && sc.next(tile, kb0, kb1); ++local) {
+      if (own_last && sc.count() == 0 && own_count() > 0) break;  // -> sk_owner_fixup
       const int mp = tile % m_pairs, np = tile / m_pairs;
       // stream-K roles: a segment starting mid-tile writes a partial; one that
       // starts at k-block 0 but ends early adds pairs [cid+1, q_end)'s partials
@@ -921,6 +1006,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (p.split > 0) {
       __syncwarp();
       split_fixup<OUT_F32>(p, cid, rank, m_pairs, tmem_base, tfull, fixb, smem, tl);
+    } else if (own_last) {
+      __syncwarp();
+      const int own_nc = own_count();
+      if (own_nc > 0)
+        sk_owner_fixup<OUT_F32>(p, cid, rank, m_pairs, sched.t_end, own_nc,
+                                static_cast<uint32_t>(sched.count() - 1) & 1u, tmem_base, tfull,
+                                fixb, smem, tl);
     }
   }
 

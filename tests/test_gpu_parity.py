@@ -307,6 +307,12 @@ def test_stream_k_matches_whole_tiles(rows, cols, m, bits, mn, monkeypatch):
     # repeatable: the owner adds partials in pair order
     monkeypatch.setenv("MLRA_SK", "1")
     assert np.array_equal(f64(f(ctx, a, out_dtype=torch.float32)), outs["1"])
+    # the all-warp owner fix-up and the 4-epilogue-warp one sum in the same order
+    monkeypatch.setenv("MLRA_SK_OWNER4", "1")
+    assert np.array_equal(f64(f(ctx, a, out_dtype=torch.float32)), outs["1"])
+    y4 = f64(f(ctx, a))  # bf16 output (paired-row stores)
+    monkeypatch.delenv("MLRA_SK_OWNER4")
+    assert np.array_equal(f64(f(ctx, a)), y4)
 
 
 def test_stream_k_layer_with_lora_and_bias(monkeypatch):
@@ -321,8 +327,9 @@ def test_stream_k_layer_with_lora_and_bias(monkeypatch):
     g = to_bf16_dev(orc.bf16_round(orc.gaussian(82, m, d_out)))
     monkeypatch.setenv("MLRA_GEMM", "2")
     res = {}
-    for sk in ("0", "1", "4", "5"):
-        monkeypatch.setenv("MLRA_SK", sk)
+    for sk in ("0", "1", "4", "5", "1o4"):
+        monkeypatch.setenv("MLRA_SK", sk[0])
+        monkeypatch.setenv("MLRA_SK_OWNER4", "1" if sk == "1o4" else "0")
         ad = M.LoraAdapter(a=torch.from_numpy(a32).cuda(), b=torch.from_numpy(b32).cuda(), rank=r,
                            alpha=32.0)
         layer = M.ModuLoraLayer("k", dq, ad, bias=torch.from_numpy(bias).cuda(),
@@ -333,6 +340,8 @@ def test_stream_k_layer_with_lora_and_bias(monkeypatch):
     for sk in ("1", "4", "5"):
         assert rel_fro(res[sk][0], res["0"][0]) <= 1e-5
         assert rel_fro(res[sk][1], res["0"][1]) <= 1e-5
+    # stream-K owner fix-up: all 16 warps vs the 4 epilogue warps, same bits
+    assert np.array_equal(res["1"][0], res["1o4"][0]) and np.array_equal(res["1"][1], res["1o4"][1])
 
 
 @pytest.mark.parametrize("strategy", STRATS)
