@@ -1358,21 +1358,35 @@ mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, in
   auto* xbs = sc.get<__nv_bfloat16>(static_cast<size_t>(m * rp));
   auto* apad = sc.get<__nv_bfloat16>(static_cast<size_t>(d.rows_pad * rp));
   if (!xbs || !apad) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  // one launch: B -> transposed hi/lo planes, A -> padded bf16 operand, counters = 0
   mlra::PrepBatch pb;
-  Planes bt;
-  ThinWs tw;
-  if (mlra_status st = make_planes(sc, pb, L->b, d.cols, r, false, &bt)) return st;
-  pb.pad(L->a, d.rows, r, r, 1.0f, apad, d.rows_pad, rp);
-  if (mlra_status st = thin_ws(sc, pb, true, m, d.cols, r, false, &tw)) return st;
+  pb.pad(L->a, d.rows, r, r, 1.0f, apad, d.rows_pad, rp);  // A -> padded bf16 GEMM operand
   unsigned* flags = gemm_flags(sc, pb);
   if (!flags) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  CUDA_TRY(mlra::launch_prep(pb, s));
   // K4: xb = x·B (matmul(t, x, B), lora.cpp:68), finished with bf16(s·xb) zero
   // padded to rp columns: the extra-K LoRA operand of the GEMM
-  if (mlra_status st = rows_product(s, tw, gp.act, gp.ld_act, m, d.cols, bt, xb, r, xbs, rp,
-                                    scaling, nullptr))
-    return st;
+  if (mlra::thin_fused_ok(r)) {
+    // one launch: B is split in the kernel, A's padded operand and the flags
+    // are the launch's post jobs (no prep launch in front of it)
+    mlra::ThinOut o;
+    o.out = xb;
+    o.ldo = r;
+    o.pad = xbs;
+    o.ldp = rp;
+    o.pad_cols = static_cast<int>(rp);
+    o.pad_scale = scaling;
+    o.trace = thin_trace();
+    CUDA_TRY(mlra::launch_rowmma_fused(gp.act, gp.ld_act, m, d.cols, L->b, r, r, o, pb, s));
+  } else {
+    // prep launch: B -> transposed hi/lo planes, A's operand, counters = 0
+    Planes bt;
+    ThinWs tw;
+    if (mlra_status st = make_planes(sc, pb, L->b, d.cols, r, false, &bt)) return st;
+    if (mlra_status st = thin_ws(sc, pb, true, m, d.cols, r, false, &tw)) return st;
+    CUDA_TRY(mlra::launch_prep(pb, s));
+    if (mlra_status st = rows_product(s, tw, gp.act, gp.ld_act, m, d.cols, bt, xb, r, xbs, rp,
+                                      scaling, nullptr))
+      return st;
+  }
   gp.k_red_valid = d.cols;
   gp.act_lora = xbs;
   gp.w_lora = apad;
@@ -1421,21 +1435,28 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   auto* dyas = sc.get<__nv_bfloat16>(static_cast<size_t>(m * rp));
   auto* bpad = dx ? sc.get<__nv_bfloat16>(static_cast<size_t>(d.cols_pad * rp)) : nullptr;
   if (!dyA || !dyas || (dx && !bpad)) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  // one launch: A, xb -> transposed hi/lo planes, B -> padded operand, counters = 0
-  // (dA, dB, dbias, dyA are stored by the skinny kernels' finishers: no zero-fill)
-  mlra::PrepBatch pb;
+  // A, xb -> transposed hi/lo planes, B -> the dX GEMM's padded operand, counters = 0
+  // (dA, dB, dbias, dyA are stored by the skinny kernels' finishers: no zero-fill).
+  // Fused row product (r <= 64): A is split inside it and B's operand and the
+  // flags are its post jobs; the planes of xb and the column products' counters
+  // (the side stream's inputs) are a prep launch on the side stream.
+  const bool fused = mlra::thin_fused_ok(r);
+  mlra::PrepBatch pb, pbs;  // pb: main stream (prep launch or the row kernel's post jobs)
   Planes at, xbt, dyat;
   ThinWs w_row, w_da, w_db;
-  if (mlra_status st = make_planes(sc, pb, L->a, d.rows, r, false, &at)) return st;
-  if (mlra_status st = make_planes(sc, pb, xb, m, r, dbias != nullptr, &xbt)) return st;
+  mlra::PrepBatch& cpb = fused ? pbs : pb;  // column-product inputs
+  if (mlra_status st = make_planes(sc, cpb, xb, m, r, dbias != nullptr, &xbt)) return st;
   if (mlra_status st = alloc_planes(sc, m, r, false, &dyat)) return st;
+  if (mlra_status st = thin_ws(sc, cpb, false, m, d.rows, r, dbias != nullptr, &w_da)) return st;
+  if (mlra_status st = thin_ws(sc, cpb, false, m, d.cols, r, false, &w_db)) return st;
   if (dx) pb.pad(L->b, d.cols, r, r, 1.0f, bpad, d.cols_pad, rp);
-  if (mlra_status st = thin_ws(sc, pb, true, m, d.rows, r, false, &w_row)) return st;
-  if (mlra_status st = thin_ws(sc, pb, false, m, d.rows, r, dbias != nullptr, &w_da)) return st;
-  if (mlra_status st = thin_ws(sc, pb, false, m, d.cols, r, false, &w_db)) return st;
+  if (!fused) {
+    if (mlra_status st = make_planes(sc, pb, L->a, d.rows, r, false, &at)) return st;
+    if (mlra_status st = thin_ws(sc, pb, true, m, d.rows, r, false, &w_row)) return st;
+  }
   unsigned* flags = gemm_flags(sc, pb);
   if (!flags) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
-  CUDA_TRY(mlra::launch_prep(pb, s));
+  if (!fused) CUDA_TRY(mlra::launch_prep(pb, s));
   // dA early: the side stream starts dA = s·dyᵀ·xb right after the prep launch,
   // concurrently with dY·A — both stream dY, so the second reader finds much of
   // it in L2; dB follows once dYA exists (cfg2 step 1166 -> 1139 us, cfg3 -2 %;
@@ -1449,6 +1470,7 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
     CUDA_TRY(cudaEventRecord(side->fork, s));
     CUDA_TRY(cudaStreamWaitEvent(side->st, side->fork, 0));
   }
+  if (fused) CUDA_TRY(mlra::launch_prep(pbs, side ? side->st : s));
   const bool early = side != nullptr && da_early;
   auto grad_a = [&](cudaStream_t cs) -> mlra_status {
     // K5b: dA = s·dyᵀ·xb (+ dbias = Σ_t dy)   (autodiff.cpp:153-155, 315-320, 183-191)
@@ -1460,9 +1482,23 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   // K5a: dyA = dy·A ; d(xb) = s·dyA (autodiff.cpp:150-152 on record lora.cpp:69),
   // finished with bf16(s·dyA) (the dX GEMM's extra-K operand) and dyA's
   // transposed hi/lo planes (the dB product's factor)
-  if (mlra_status st = rows_product(s, w_row, dya, lddya, m, d.rows, at, dyA, r, dyas, rp,
-                                    scaling, &dyat))
+  if (fused) {
+    mlra::ThinOut o;
+    o.out = dyA;
+    o.ldo = r;
+    o.pad = dyas;
+    o.ldp = rp;
+    o.pad_cols = static_cast<int>(rp);
+    o.pad_scale = scaling;
+    o.thi = dyat.hi[0];
+    o.ldt = dyat.ldt;
+    o.t_rows = static_cast<int>(dyat.rows_t[0]);
+    o.trace = thin_trace();
+    CUDA_TRY(mlra::launch_rowmma_fused(dya, lddya, m, d.rows, L->a, r, r, o, pb, s));
+  } else if (mlra_status st = rows_product(s, w_row, dya, lddya, m, d.rows, at, dyA, r, dyas, rp,
+                                           scaling, &dyat)) {
     return st;
+  }
   // K5b / K6 go to the side stream when a dX GEMM follows, else inline. The GEMM is
   // enqueued FIRST: its persistent pairs take the SMs, and dA / dB fill the SMs
   // its under-filled last wave leaves idle (e.g. 128 tiles over 74 pairs) and its

@@ -179,6 +179,13 @@ void thin_ws_size(bool row, int64_t m, int64_t d, int64_t r, bool ones, int64_t*
 cudaError_t launch_rowmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
                           const __nv_bfloat16* wt_hi, const __nv_bfloat16* wt_lo, int64_t ldw,
                           int64_t r, const ThinOut& o, cudaStream_t st);
+// out[m x r] = act[m x kd] · F for an fp32 factor F [kd x r] (ld ldf), r <= 64, on
+// the cluster kernel (k_rowmma_cl: factor split in-kernel, no counters); `post`
+// (the pass's small jobs) runs inside the launch after its PDL wait.
+bool thin_fused_ok(int64_t r);
+cudaError_t launch_rowmma_fused(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
+                                const float* F, int64_t ldf, int64_t r, const ThinOut& o,
+                                const PrepBatch& post, cudaStream_t st);
 // out[nd x r] = scale · actᵀ · V    (V given as Vt hi/lo [rows x ldv]); colsum[n] = Σ_t act
 cudaError_t launch_colmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t nd,
                           const __nv_bfloat16* vt_hi, const __nv_bfloat16* vt_lo, int64_t ldv,

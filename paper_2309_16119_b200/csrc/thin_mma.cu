@@ -97,14 +97,14 @@ constexpr int TW = MLRA_THIN_WARPS;   // warps per CTA; each owns 16 output rows
 constexpr int TM = 16 * TW;           // output-tile rows per unit (tokens or n)
 constexpr int TTHREADS = 32 * TW;
 
-template <int NT>
+template <int NT, int NS = TNS>
 struct ThinSmem {
   static constexpr int ROWS = 8 * NT;
   static constexpr int ACT = TM * 128;          // TM x 64 bf16
   static constexpr int FAC = 2 * ROWS * 128;    // hi + lo planes, 64 columns
   static constexpr int STAGE = ACT + FAC;       // multiple of 1024 when NT is even
   static constexpr int STAGE_AL = (STAGE + 1023) / 1024 * 1024;
-  static constexpr int BYTES = 1024 + TNS * STAGE_AL + 64;  // + alignment slack + barriers
+  static constexpr int BYTES = 1024 + NS * STAGE_AL + 8 * NS;  // + alignment slack + barriers
 };
 
 __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
@@ -136,6 +136,68 @@ __device__ __forceinline__ int cta_of_unit(int64_t u, int64_t units, int64_t G) 
 }
 __device__ __forceinline__ int first_tile_of(int c, int64_t units, int64_t G, int chunks) {
   return static_cast<int>(c * units / G) / chunks;
+}
+
+// The finished value of 4 consecutive columns [j, j+4) of output row `row`:
+// out = scale·v, colsum (the ones column), the GEMM's padded bf16(pad_scale·v)
+// operand and the transposed hi/lo planes (zero beyond n_out up to ldt).
+__device__ __forceinline__ void thin_store4(const ThinOut& o, int64_t row, int j,
+                                            const float (&vv)[4], int64_t n_out, bool vec_out,
+                                            bool vec_pad) {
+  if (row < n_out) {
+    if (vec_out && j + 4 <= o.rc) {
+      *reinterpret_cast<float4*>(o.out + row * o.ldo + j) =
+          make_float4(o.scale * vv[0], o.scale * vv[1], o.scale * vv[2], o.scale * vv[3]);
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        if (j + kk < o.rc) o.out[row * o.ldo + j + kk] = o.scale * vv[kk];
+    }
+    if (o.colsum && j <= o.rc && o.rc < j + 4) o.colsum[row] = vv[o.rc - j];
+    if (o.pad) {  // bf16(pad_scale · v), zero beyond rc (the padded extra-K operand)
+      __nv_bfloat16 h[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        h[kk] = __float2bfloat16_rn(j + kk < o.rc ? o.pad_scale * vv[kk] : 0.0f);
+      if (vec_pad && j + 4 <= o.pad_cols) {
+        *reinterpret_cast<uint2*>(o.pad + row * o.ldp + j) = *reinterpret_cast<const uint2*>(h);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (j + kk < o.pad_cols) o.pad[row * o.ldp + j + kk] = h[kk];
+      }
+    }
+  }
+  if (o.thi && row < o.ldt) {  // transposed hi/lo planes [t_rows x ldt] (zero padded)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      if (j + kk < o.t_rows) {
+        const float tv = (row < n_out && j + kk < o.rc) ? vv[kk] : 0.0f;
+        const __nv_bfloat16 h = __float2bfloat16_rn(tv);
+        o.thi[static_cast<int64_t>(j + kk) * o.ldt + row] = h;
+        o.thi[static_cast<int64_t>(o.t_rows + j + kk) * o.ldt + row] =
+            __float2bfloat16_rn(tv - __bfloat162float(h));
+      }
+    }
+  }
+}
+
+// Zero pad columns [ROWS, pad_cols) of rows [row0, row0 + nrows) (8-B stores).
+template <int ROWS>
+__device__ __forceinline__ void thin_pad_zero(const ThinOut& o, int64_t row0, int nrows,
+                                              int64_t n_out, bool vec_pad) {
+  if (!o.pad || o.pad_cols <= ROWS) return;
+  const int pc4 = (o.pad_cols - ROWS) / 4;
+  for (int idx = threadIdx.x; idx < nrows * pc4; idx += TTHREADS) {
+    const int tr = idx / pc4, j = ROWS + 4 * (idx - tr * pc4);
+    const int64_t row = row0 + tr;
+    if (row < n_out) {
+      if (vec_pad)
+        *reinterpret_cast<uint2*>(o.pad + row * o.ldp + j) = make_uint2(0u, 0u);
+      else
+        for (int kk = 0; kk < 4; ++kk) o.pad[row * o.ldp + j + kk] = __float2bfloat16_rn(0.0f);
+    }
+  }
 }
 
 // Flush of one output tile (all threads of the CTA, uniform): the fragment
@@ -232,58 +294,10 @@ __device__ void thin_flush(float (&acc)[NT][4], int tile, int chunks, int units,
   for (int k = 0; k < PER; ++k) {
     const int p4 = threadIdx.x + k * TTHREADS;
     const int tr = p4 / C4, j = 4 * (p4 - tr * C4);
-    const int64_t row = static_cast<int64_t>(tile) * TM + tr;
     const float vv[4] = {acc4[k].x, acc4[k].y, acc4[k].z, acc4[k].w};
-    if (row < n_out) {
-      if (vec_out && j + 4 <= o.rc) {
-        *reinterpret_cast<float4*>(o.out + row * o.ldo + j) =
-            make_float4(o.scale * vv[0], o.scale * vv[1], o.scale * vv[2], o.scale * vv[3]);
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          if (j + kk < o.rc) o.out[row * o.ldo + j + kk] = o.scale * vv[kk];
-      }
-      if (o.colsum && j <= o.rc && o.rc < j + 4) o.colsum[row] = vv[o.rc - j];
-      if (o.pad) {  // bf16(pad_scale · v), zero beyond rc (the padded extra-K operand)
-        __nv_bfloat16 h[4];
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          h[kk] = __float2bfloat16_rn(j + kk < o.rc ? o.pad_scale * vv[kk] : 0.0f);
-        if (vec_pad && j + 4 <= o.pad_cols) {
-          *reinterpret_cast<uint2*>(o.pad + row * o.ldp + j) = *reinterpret_cast<const uint2*>(h);
-        } else {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            if (j + kk < o.pad_cols) o.pad[row * o.ldp + j + kk] = h[kk];
-        }
-      }
-    }
-    if (o.thi && row < o.ldt) {  // transposed hi/lo planes [t_rows x ldt] (zero padded)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        if (j + kk < o.t_rows) {
-          const float tv = (row < n_out && j + kk < o.rc) ? vv[kk] : 0.0f;
-          const __nv_bfloat16 h = __float2bfloat16_rn(tv);
-          o.thi[static_cast<int64_t>(j + kk) * o.ldt + row] = h;
-          o.thi[static_cast<int64_t>(o.t_rows + j + kk) * o.ldt + row] =
-              __float2bfloat16_rn(tv - __bfloat162float(h));
-        }
-      }
-    }
+    thin_store4(o, static_cast<int64_t>(tile) * TM + tr, j, vv, n_out, vec_out, vec_pad);
   }
-  if (o.pad && o.pad_cols > ROWS) {  // zero pad columns [ROWS, pad_cols): 8-B stores
-    const int pc4 = (o.pad_cols - ROWS) / 4;
-    for (int idx = threadIdx.x; idx < TM * pc4; idx += TTHREADS) {
-      const int tr = idx / pc4, j = ROWS + 4 * (idx - tr * pc4);
-      const int64_t row = static_cast<int64_t>(tile) * TM + tr;
-      if (row < n_out) {
-        if (vec_pad)
-          *reinterpret_cast<uint2*>(o.pad + row * o.ldp + j) = make_uint2(0u, 0u);
-        else
-          for (int kk = 0; kk < 4; ++kk) o.pad[row * o.ldp + j + kk] = __float2bfloat16_rn(0.0f);
-      }
-    }
-  }
+  thin_pad_zero<ROWS>(o, static_cast<int64_t>(tile) * TM, TM, n_out, vec_pad);
   __syncthreads();  // the slot is rewritten by this CTA's next flush
 }
 
@@ -359,6 +373,230 @@ __global__ void __launch_bounds__(TTHREADS, 3)
       thin_flush<NT>(acc, tile, kchunks, units, o, m);
   }
   thin_stamp(o, 3);
+}
+
+// Row products on clusters: out[t, j] = Σ_k act[t,k]·F[k,j] for an fp32 factor
+// F [kd x r] (B for x·B, A for dY·A). The CL CTAs of a cluster split one
+// 128-token tile's reduction (kd / 64 chunks) into equal contiguous ranges and
+// reduce their fp32 partials through distributed shared memory: CTA s sums rows
+// [s·TM/CL, (s+1)·TM/CL) of the tile over the cluster's slabs in rank order
+// (deterministic) and finishes them (thin_store4). No global partial slots,
+// counters or finisher round trips, and no CTA waits for one outside its own
+// co-scheduled cluster. CL = 8 when the token tiles x 8 fill the SMs, else 16.
+//
+// The factor is converted in the kernel: each unit's 64 x r fp32 chunk is
+// loaded (L2-resident: every tile's CTAs read the same F) one unit ahead and
+// split into the bf16 hi/lo planes of the stage, so no prep launch stands
+// between the previous kernel and this one. `post` carries the pass's other
+// small jobs (the GEMM's padded LoRA operand, its stream-K flags), run by the
+// whole grid after the PDL wait while the first activation tiles load.
+#ifndef MLRA_THIN_CL_NS
+#define MLRA_THIN_CL_NS 3
+#endif
+constexpr int kClNS = MLRA_THIN_CL_NS;  // TMA ring depth of the cluster kernel
+
+__device__ __forceinline__ void run_prep_task(const PrepTask& k, uint32_t j) {
+  const uint32_t ldd = static_cast<uint32_t>(k.ldd);
+  switch (k.kind) {
+    case PrepTask::kZeroF32:
+      reinterpret_cast<float*>(k.dst)[j] = 0.0f;
+      break;
+    case PrepTask::kZeroBf16:
+      reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = __float2bfloat16_rn(0.0f);
+      break;
+    case PrepTask::kSplitT: {  // hi/lo planes [rows_out x ldd] of src^T (cols = r)
+      const uint32_t row = j / ldd, col = j - row * ldd;
+      float v = 0.0f;
+      if (col < k.rows) {
+        if (row < k.cols)
+          v = k.src[static_cast<int64_t>(col) * k.lds + row];
+        else if (row == k.cols && k.ones)
+          v = 1.0f;
+      }
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = h;
+      reinterpret_cast<__nv_bfloat16*>(k.dst2)[j] = __float2bfloat16_rn(v - __bfloat162float(h));
+      break;
+    }
+    case PrepTask::kPadBf16: {  // dst [rows_out x ldd] = bf16(scale * src) zero-padded
+      const uint32_t row = j / ldd, col = j - row * ldd;
+      const float v = (row < k.rows && col < k.cols)
+                          ? k.scale * k.src[static_cast<int64_t>(row) * k.lds + col]
+                          : 0.0f;
+      reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = __float2bfloat16_rn(v);
+      break;
+    }
+  }
+}
+
+// One unit's factor chunk: rows k of F [kd x ldf] (fp32) -> the stage's bf16
+// hi / lo planes [ROWS][64] (SWIZZLE_128B layout, as the TMA path stores them).
+// Thread idx handles float4 (k = idx / (ROWS/4), j = 4·(idx % (ROWS/4))).
+template <int NT>
+struct FacRegs {
+  static constexpr int ROWS = 8 * NT;
+  static constexpr int N4 = 64 * ROWS / 4;                        // float4s per chunk
+  static constexpr int PER = (N4 + TTHREADS - 1) / TTHREADS;      // per thread
+  float4 v[PER];
+  __device__ __forceinline__ void load(const float* F, int64_t ldf, int64_t kd, int rc, int ch,
+                                       bool vec) {
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int idx = threadIdx.x + p * TTHREADS;
+      const int kk = idx / (ROWS / 4), j = 4 * (idx % (ROWS / 4));
+      const int64_t k = static_cast<int64_t>(ch) * 64 + kk;
+      float4 x = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      if (idx < N4 && k < kd && j < rc) {
+        const float* src = F + k * ldf + j;
+        if (vec && j + 4 <= rc) {
+          x = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          x.x = __ldg(src);
+          if (j + 1 < rc) x.y = __ldg(src + 1);
+          if (j + 2 < rc) x.z = __ldg(src + 2);
+          if (j + 3 < rc) x.w = __ldg(src + 3);
+        }
+      }
+      v[p] = x;
+    }
+  }
+  __device__ __forceinline__ void store(uint32_t fbase) const {
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int idx = threadIdx.x + p * TTHREADS;
+      if (idx >= N4) break;
+      const int kk = idx / (ROWS / 4), j = 4 * (idx % (ROWS / 4));
+      const float f[4] = {v[p].x, v[p].y, v[p].z, v[p].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(f[i]);
+        const __nv_bfloat16 l = __float2bfloat16_rn(f[i] - __bfloat162float(h));
+        const uint32_t off = (kk & 7) * 2;
+        asm volatile("st.shared.b16 [%0], %1;" ::"r"(swz(fbase, j + i, kk >> 3) + off),
+                     "h"(*reinterpret_cast<const unsigned short*>(&h)));
+        asm volatile("st.shared.b16 [%0], %1;" ::"r"(swz(fbase, ROWS + j + i, kk >> 3) + off),
+                     "h"(*reinterpret_cast<const unsigned short*>(&l)));
+      }
+    }
+  }
+};
+
+template <int NT, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(TTHREADS, 3)
+    k_rowmma_cl(const __grid_constant__ CUtensorMap act_map, const float* F, int64_t ldf,
+                int64_t kd, int64_t m, int kchunks, const ThinOut o, const PrepBatch post) {
+  using L = ThinSmem<NT, kClNS>;
+  constexpr int ROWS = L::ROWS;
+  constexpr int RP = TM / CL;  // output rows finished per CTA
+  static_assert(TM % CL == 0, "cluster rows");
+  static_assert(TM * ROWS * 4 <= kClNS * L::STAGE_AL, "partial slab fits the ring");
+  extern __shared__ __align__(16) unsigned char thin_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(thin_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kClNS * L::STAGE_AL);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int s = static_cast<int>(cluster_ctarank());
+  const int tile = blockIdx.x / CL;
+  const int c0 = kchunks * s / CL, c1 = kchunks * (s + 1) / CL;
+  const bool vecf = (ldf & 3) == 0 && (reinterpret_cast<uintptr_t>(F) & 15) == 0;
+  auto issue = [&](int ch, int slot) {
+    mbar_arrive_expect_tx(&full[slot], L::ACT);
+    tma_load_2d(sm + slot * L::STAGE_AL, &act_map, &full[slot], ch * TILE, tile * TM);
+  };
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kClNS; ++b) mbar_init(&full[b], 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&act_map);
+  }
+  pdl_trigger();
+  pdl_wait();  // activations and the factor may come from earlier kernels
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kClNS - 1; ++b)
+      if (c0 + b < c1) issue(c0 + b, b);
+  }
+  FacRegs<NT> fr;
+  if (c0 < c1) {
+    fr.load(F, ldf, kd, o.rc, c0, vecf);
+    fr.store(smem_u32(sm) + L::ACT);
+  }
+  // the pass's small jobs, spread over the grid, while the first tiles load
+  if (post.n > 0) {
+    const uint32_t gt = blockIdx.x * TTHREADS + threadIdx.x, gs = gridDim.x * TTHREADS;
+    for (int t = 0; t < post.n; ++t) {
+      const uint32_t cnt = static_cast<uint32_t>(post.offs[t + 1] - post.offs[t]);
+      for (uint32_t j = gt; j < cnt; j += gs) run_prep_task(post.t[t], j);
+    }
+  }
+  __syncthreads();
+  float acc[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.0f;
+  const int arow = warp * 16 + (lane & 15);
+  for (int ch = c0; ch < c1; ++ch) {
+    const int i = ch - c0, b = i % kClNS;
+    if (threadIdx.x == 0 && ch + kClNS - 1 < c1) {
+      fence_proxy_async_smem();  // the slot's last generic reads (iteration i-1) before TMA
+      issue(ch + kClNS - 1, (i + kClNS - 1) % kClNS);
+    }
+    const bool more = ch + 1 < c1;
+    if (more) fr.load(F, ldf, kd, o.rc, ch + 1, vecf);  // next unit's factor, in flight
+    mbar_wait(&full[b], static_cast<uint32_t>((i / kClNS) & 1));
+    const uint32_t abase = smem_u32(sm + b * L::STAGE_AL);
+    const uint32_t fbase = abase + L::ACT;
+#pragma unroll
+    for (int k16 = 0; k16 < 4; ++k16) {
+      uint32_t a[4];
+      ldsm_x4(swz(abase, arow, k16 * 2 + (lane >> 4)), a);
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int rh = n * 8 + g, rl = rh + ROWS;
+        const uint32_t h0 = lds_u32(swz(fbase, rh, k16 * 2) + 4 * tq);
+        const uint32_t h1 = lds_u32(swz(fbase, rh, k16 * 2 + 1) + 4 * tq);
+        const uint32_t l0 = lds_u32(swz(fbase, rl, k16 * 2) + 4 * tq);
+        const uint32_t l1 = lds_u32(swz(fbase, rl, k16 * 2 + 1) + 4 * tq);
+        mma_bf16(acc[n], a, h0, h1);
+        mma_bf16(acc[n], a, l0, l1);
+      }
+    }
+    // the next stage's factor planes (its previous unit was consumed two
+    // barriers ago); the barrier below publishes them
+    if (more) fr.store(smem_u32(sm + ((i + 1) % kClNS) * L::STAGE_AL) + L::ACT);
+    __syncthreads();
+  }
+  // this CTA's partial slab [TM][ROWS] fp32 in the (drained) ring
+  float* slab = reinterpret_cast<float*>(sm);
+  const int ra = warp * 16 + g;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int j = n * 8 + 2 * tq;
+    *reinterpret_cast<float2*>(slab + ra * ROWS + j) = make_float2(acc[n][0], acc[n][1]);
+    *reinterpret_cast<float2*>(slab + (ra + 8) * ROWS + j) = make_float2(acc[n][2], acc[n][3]);
+  }
+  cluster_sync();  // every slab of the cluster written (release / acquire at cluster scope)
+  const bool vec_out = (o.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0;
+  const bool vec_pad = o.pad && (o.ldp & 3) == 0 && (reinterpret_cast<uintptr_t>(o.pad) & 7) == 0;
+  constexpr int C4 = ROWS / 4;
+  const uint32_t slab_u32 = smem_u32(slab);
+  for (int idx = threadIdx.x; idx < RP * C4; idx += TTHREADS) {
+    const int tr = s * RP + idx / C4, j = 4 * (idx % C4);
+    const uint32_t off = slab_u32 + static_cast<uint32_t>((tr * ROWS + j) * 4);
+    float vv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int q = 0; q < CL; ++q) {  // rank order: deterministic sums
+      float x0, x1, x2, x3;
+      asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
+                   : "r"(mapa(off, static_cast<uint32_t>(q))));
+      vv[0] += x0;
+      vv[1] += x1;
+      vv[2] += x2;
+      vv[3] += x3;
+    }
+    thin_store4(o, static_cast<int64_t>(tile) * TM + tr, j, vv, m, vec_out, vec_pad);
+  }
+  thin_pad_zero<ROWS>(o, static_cast<int64_t>(tile) * TM + s * RP, RP, m, vec_pad);
+  cluster_sync();  // no CTA leaves while a peer may still read its slab
 }
 
 // out[n, j] += scale · Σ_t act[t, n] · Vt[j, t]   (Vt = V transposed, hi/lo bf16 planes)
@@ -453,39 +691,8 @@ __global__ void __launch_bounds__(256) k_prep(const PrepBatch b, const PrepBlock
   const PrepTask& k = b.t[t];
   const uint32_t count = static_cast<uint32_t>(b.offs[t + 1] - b.offs[t]);
   const uint32_t stride = static_cast<uint32_t>(pbk.first[t + 1] - pbk.first[t]) * blockDim.x;
-  const uint32_t ldd = static_cast<uint32_t>(k.ldd);
-  for (uint32_t j = (blockIdx.x - pbk.first[t]) * blockDim.x + threadIdx.x; j < count; j += stride) {
-    switch (k.kind) {
-      case PrepTask::kZeroF32:
-        reinterpret_cast<float*>(k.dst)[j] = 0.0f;
-        break;
-      case PrepTask::kZeroBf16:
-        reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = __float2bfloat16_rn(0.0f);
-        break;
-      case PrepTask::kSplitT: {  // hi/lo planes [rows_out x ldd] of src^T (cols = r)
-        const uint32_t row = j / ldd, col = j - row * ldd;
-        float v = 0.0f;
-        if (col < k.rows) {
-          if (row < k.cols)
-            v = k.src[static_cast<int64_t>(col) * k.lds + row];
-          else if (row == k.cols && k.ones)
-            v = 1.0f;
-        }
-        const __nv_bfloat16 h = __float2bfloat16_rn(v);
-        reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = h;
-        reinterpret_cast<__nv_bfloat16*>(k.dst2)[j] = __float2bfloat16_rn(v - __bfloat162float(h));
-        break;
-      }
-      case PrepTask::kPadBf16: {  // dst [rows_out x ldd] = bf16(scale * src) zero-padded
-        const uint32_t row = j / ldd, col = j - row * ldd;
-        const float v = (row < k.rows && col < k.cols)
-                            ? k.scale * k.src[static_cast<int64_t>(row) * k.lds + col]
-                            : 0.0f;
-        reinterpret_cast<__nv_bfloat16*>(k.dst)[j] = __float2bfloat16_rn(v);
-        break;
-      }
-    }
-  }
+  for (uint32_t j = (blockIdx.x - pbk.first[t]) * blockDim.x + threadIdx.x; j < count; j += stride)
+    run_prep_task(k, j);
 }
 
 int sms() {
@@ -600,10 +807,10 @@ cudaError_t rowmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   if (e == cudaSuccess) e = thin_map(&fm, hi, ldw, 2 * ROWS, ldw, 2 * ROWS);
   if (e != cudaSuccess) return e;
   const int smem = ThinSmem<NT>::BYTES;
+  o.rc = static_cast<int>(r);
   const int ctas = thin_ctas<NT>(true, units, tb);
   if (ctas <= 0 || o.ws_floats < static_cast<int64_t>(ctas) * 2 * TM * ROWS)
     return cudaErrorInvalidValue;
-  o.rc = static_cast<int>(r);
   return launch_pdl(k_rowmma<NT>, dim3(ctas), dim3(TTHREADS), smem, st, true, am, fm, m,
                     static_cast<int>(kchunks), static_cast<int>(units), o);
 }
@@ -630,6 +837,30 @@ cudaError_t colmma_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t 
   o.rc = static_cast<int>(r);
   return launch_pdl(k_colmma<NT>, dim3(ctas), dim3(TTHREADS), smem, st, true, am, fm, nd,
                     static_cast<int>(tchunks), static_cast<int>(units), o);
+}
+
+template <int NT, int CL>
+cudaError_t rowmma_cl_nt(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
+                         const float* F, int64_t ldf, int64_t r, ThinOut o, const PrepBatch& post,
+                         cudaStream_t st) {
+  const int64_t tb = (m + TM - 1) / TM;
+  const int64_t kchunks = (kd + TILE - 1) / TILE;
+  if (tb * CL > INT32_MAX || kchunks > INT32_MAX || !o.out) return cudaErrorInvalidValue;
+  CUtensorMap am;
+  cudaError_t e = thin_map(&am, act, kd, m, lda, TM);
+  if (e != cudaSuccess) return e;
+  constexpr int smem = ThinSmem<NT, kClNS>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_rowmma_cl<NT, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess && CL > 8)
+      e = cudaFuncSetAttribute(k_rowmma_cl<NT, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  o.rc = static_cast<int>(r);
+  return launch_pdl(k_rowmma_cl<NT, CL>, dim3(static_cast<unsigned>(tb * CL)), dim3(TTHREADS), smem,
+                    st, true, am, F, ldf, kd, m, static_cast<int>(kchunks), o, post);
 }
 
 }  // namespace
@@ -703,6 +934,26 @@ cudaError_t launch_colmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int6
 #define CALL_COL(N) colmma_nt<N>(act, lda, m, nd, vt_hi, vt_lo, ldv, r, o, st)
   MLRA_NT_DISPATCH(thin_rows(r, o.colsum != nullptr) / 8, CALL_COL)
 #undef CALL_COL
+}
+
+// The fused row product (k_rowmma_cl) serves ranks <= 64 unless MLRA_THIN_CL=0
+// (the range kernel + prep launch; read per call for A/B runs and tests).
+bool thin_fused_ok(int64_t r) {
+  const char* e = getenv("MLRA_THIN_CL");
+  return r > 0 && r <= 64 && !(e && e[0] == '0');
+}
+
+cudaError_t launch_rowmma_fused(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
+                                const float* F, int64_t ldf, int64_t r, const ThinOut& o,
+                                const PrepBatch& post, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  if (r <= 0 || r > 64 || post.n > kMaxPrep) return cudaErrorInvalidValue;
+  // 8 CTAs per 128-token tile when that fills the SMs, else 16
+  const bool c8 = (m + TM - 1) / TM * 8 >= sms();
+#define CALL_CL(N) (c8 ? rowmma_cl_nt<N, 8>(act, lda, m, kd, F, ldf, r, o, post, st) \
+                       : rowmma_cl_nt<N, 16>(act, lda, m, kd, F, ldf, r, o, post, st))
+  MLRA_NT_DISPATCH(thin_rows(r, false) / 8, CALL_CL)
+#undef CALL_CL
 }
 
 }  // namespace mlra

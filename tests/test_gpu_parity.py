@@ -419,6 +419,53 @@ def test_adapter_gradients_bitwise_reproducible(d_out, d_in, r, m, bias):
             assert (u is None and v is None) or torch.equal(u, v)
 
 
+@pytest.mark.parametrize("d_out,d_in,r,m", [
+    (1024, 1024, 16, 4100),  # ragged last token tile
+    (512, 384, 8, 300),      # 6 reduction chunks over 8 CTAs: empty ranges
+    (768, 4096, 72, 2048),   # NT = 9 (r = 72), 72 -> 128 padded GEMM operand
+    (256, 512, 8, 1),
+])
+def test_row_products_cluster_vs_range_kernel(d_out, d_in, r, m, monkeypatch):
+    """The row products (xb = x·B, dyA = dy·A and their derived GEMM operands /
+    transposed planes) on the cluster kernel (k_rowmma_cl: kThinCl CTAs split one
+    token tile's reduction, DSMEM reduction in rank order) and on the range
+    kernel: both match the f64 oracle to fp32-order rounding, and each is bitwise
+    repeatable."""
+    q, words, sc, z = random_quantized(d_out, d_in, 3, 128, seed=d_out + d_in + r)
+    dq = M.DeviceQuantizedMatrix(q)
+    a = (torch.randn(d_out, r, generator=torch.Generator().manual_seed(5)) * 0.02).cuda()
+    b = (torch.randn(d_in, r, generator=torch.Generator().manual_seed(6)) * 0.02).cuda()
+    layer = M.ModuLoraLayer("cl", dq, M.LoraAdapter(a, b, r, 16.0))
+    x = to_bf16_dev(orc.bf16_round(orc.gaussian(7, m, d_in)))
+    dy = to_bf16_dev(orc.bf16_round(orc.gaussian(8, m, d_out)))
+    res = {}
+    for cl in ("0", "1"):
+        monkeypatch.setenv("MLRA_THIN_CL", cl)
+        outs = []
+        for _ in range(2):
+            y, xb = M.layer_forward(layer, x, out_dtype=torch.float32)
+            dx = M.layer_backward(layer, x, xb, dy, dx_dtype=torch.float32)
+            outs.append([f64(t) for t in (y, xb, dx, *M.grads_of_adapter(layer))])
+        for u, v in zip(*outs):
+            assert np.array_equal(u, v)
+        res[cl] = outs[0]
+    s = 16.0 / r
+    xb_ref = f64(x) @ f64(b)
+    dya_ref = f64(dy) @ f64(a)
+    wbf = deq_bf16_f64(words, d_out, d_in, 3, 128, sc, z)
+    y_ref = f64(x) @ wbf.T + orc.bf16_round(s * xb_ref) @ orc.bf16_round(f64(a)).T
+    dx_ref = f64(dy) @ wbf + orc.bf16_round(s * dya_ref) @ orc.bf16_round(f64(b)).T
+    db_ref = s * f64(x).T @ dya_ref
+    for cl in ("0", "1"):
+        y, xb, dx, da, db = res[cl]
+        assert rel_fro(xb, xb_ref) <= 1e-5, cl
+        assert rel_fro(db, db_ref) <= 1e-5, cl
+        # bf16(s·xb) / bf16(s·dyA) may round differently from the f64 reference's
+        assert rel_fro(y, y_ref) <= 1e-3 and rel_fro(dx, dx_ref) <= 1e-3, cl
+    for u, v in zip(res["0"], res["1"]):  # fp32 summation order only
+        assert rel_fro(u, v) <= 1e-3
+
+
 def test_workspace_arena_across_streams_sizes_and_capture():
     """The per-stream workspace arena (capi.cu Scratch): a pass gives the same bits
     on any stream, across arena regrowth (small -> large -> small on one stream),
@@ -461,7 +508,8 @@ def test_workspace_arena_across_streams_sizes_and_capture():
 
 
 @pytest.mark.parametrize("env", [{"MLRA_PDL": "0"}, {"MLRA_DA_EARLY": "0"}, {"MLRA_SIDE_FIRST": "1"},
-                                 {"MLRA_NO_SIDE": "1"}, {"MLRA_THIN_MAXC": "1000"}])
+                                 {"MLRA_NO_SIDE": "1"}, {"MLRA_THIN_MAXC": "1000"},
+                                 {"MLRA_THIN_CL": "1"}])
 def test_launch_switches_bit_identical(env, tmp_path):
     """The launch-order / launch-mode switches (programmatic dependent launch, the
     side-stream schedule of dA/dB, the skinny-product CTA cap) change only when
@@ -478,8 +526,8 @@ def test_launch_switches_bit_identical(env, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
     ref, alt = np.load(ref_p), np.load(alt_p)
     for k in ref.files:
-        if env.get("MLRA_THIN_MAXC"):
-            # a different CTA count changes the skinny products' fp32 summation order (and
+        if env.get("MLRA_THIN_MAXC") or env.get("MLRA_THIN_CL"):
+            # a different CTA count (or the cluster row-product kernel) changes the skinny products' fp32 summation order (and
             # through bf16(s·xb) the bf16 outputs by at most an ulp here and there)
             bound = 1e-3 if k.split("_")[0] in ("y", "dx") else 1e-5
             assert rel_fro(alt[k].astype(np.float64), ref[k].astype(np.float64)) <= bound, k
