@@ -44,8 +44,9 @@ constexpr bool kThinTrace = true;
 #else
 constexpr bool kThinTrace = false;
 #endif
-// dev timeline (MLRA_TRACE3): per CTA [0] entry, [1] first unit landed, [2] last unit's MMAs
-// done, [3] exit, [4] 1 if this CTA finished a tile, [5] finisher start
+// dev timeline (MLRA_TRACE3): per CTA [0] entry, [1] first unit landed (k_rowmma_cl: PDL
+// wait passed), [2] last unit's MMAs done (k_rowmma_cl: main loop done), [3] exit,
+// [4] 1 if this CTA finished a tile, [5] finisher start
 __device__ __forceinline__ void thin_stamp(const ThinOut& o, int k) {
   if (kThinTrace && o.trace && threadIdx.x == 0) {
     unsigned long long t;
@@ -509,8 +510,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(TTHREADS, 3)
     fence_mbar_init();
     tma_prefetch_desc(&act_map);
   }
+  thin_stamp(o, 0);
   pdl_trigger();
   pdl_wait();  // activations and the factor may come from earlier kernels
+  thin_stamp(o, 1);
   if (threadIdx.x == 0) {
     for (int b = 0; b < kClNS - 1; ++b)
       if (c0 + b < c1) issue(c0 + b, b);
@@ -564,6 +567,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(TTHREADS, 3)
     if (more) fr.store(smem_u32(sm + ((i + 1) % kClNS) * L::STAGE_AL) + L::ACT);
     __syncthreads();
   }
+  thin_stamp(o, 2);
   // this CTA's partial slab [TM][ROWS] fp32 in the (drained) ring
   float* slab = reinterpret_cast<float*>(sm);
   const int ra = warp * 16 + g;
@@ -597,6 +601,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(TTHREADS, 3)
   }
   thin_pad_zero<ROWS>(o, static_cast<int64_t>(tile) * TM + s * RP, RP, m, vec_pad);
   cluster_sync();  // no CTA leaves while a peer may still read its slab
+  thin_stamp(o, 3);
 }
 
 // out[n, j] += scale · Σ_t act[t, n] · Vt[j, t]   (Vt = V transposed, hi/lo bf16 planes)
