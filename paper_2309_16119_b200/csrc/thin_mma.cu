@@ -432,52 +432,51 @@ __device__ __forceinline__ void run_prep_task(const PrepTask& k, uint32_t j) {
 
 // One unit's factor chunk: rows k of F [kd x ldf] (fp32) -> the stage's bf16
 // hi / lo planes [ROWS][64] (SWIZZLE_128B layout, as the TMA path stores them).
-// Thread idx handles float4 (k = idx / (ROWS/4), j = 4·(idx % (ROWS/4))).
+// Task (j, kq): the 8 values F[64 ch + 8 kq + i][j] — one 16-B swizzle chunk of
+// row j in each plane, stored with one 16-B st.shared per plane. Consecutive
+// threads take consecutive j, so each scalar load instruction of a warp reads
+// consecutive floats of one F row.
 template <int NT>
 struct FacRegs {
   static constexpr int ROWS = 8 * NT;
-  static constexpr int N4 = 64 * ROWS / 4;                        // float4s per chunk
-  static constexpr int PER = (N4 + TTHREADS - 1) / TTHREADS;      // per thread
-  float4 v[PER];
+  static constexpr int TASKS = 8 * ROWS;                          // (j, k-octet) pairs
+  static constexpr int PER = (TASKS + TTHREADS - 1) / TTHREADS;   // per thread
+  float v[PER][8];
   __device__ __forceinline__ void load(const float* F, int64_t ldf, int64_t kd, int rc, int ch,
-                                       bool vec) {
+                                       bool /*vec*/) {
 #pragma unroll
     for (int p = 0; p < PER; ++p) {
-      const int idx = threadIdx.x + p * TTHREADS;
-      const int kk = idx / (ROWS / 4), j = 4 * (idx % (ROWS / 4));
-      const int64_t k = static_cast<int64_t>(ch) * 64 + kk;
-      float4 x = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      if (idx < N4 && k < kd && j < rc) {
-        const float* src = F + k * ldf + j;
-        if (vec && j + 4 <= rc) {
-          x = __ldg(reinterpret_cast<const float4*>(src));
-        } else {
-          x.x = __ldg(src);
-          if (j + 1 < rc) x.y = __ldg(src + 1);
-          if (j + 2 < rc) x.z = __ldg(src + 2);
-          if (j + 3 < rc) x.w = __ldg(src + 3);
-        }
-      }
-      v[p] = x;
+      const int t = threadIdx.x + p * TTHREADS;
+      const int j = t % ROWS, kq = t / ROWS;
+      const int64_t k0 = static_cast<int64_t>(ch) * 64 + kq * 8;
+      const bool ok = t < TASKS && j < rc;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[p][i] = (ok && k0 + i < kd) ? __ldg(F + (k0 + i) * ldf + j) : 0.0f;
     }
   }
   __device__ __forceinline__ void store(uint32_t fbase) const {
 #pragma unroll
     for (int p = 0; p < PER; ++p) {
-      const int idx = threadIdx.x + p * TTHREADS;
-      if (idx >= N4) break;
-      const int kk = idx / (ROWS / 4), j = 4 * (idx % (ROWS / 4));
-      const float f[4] = {v[p].x, v[p].y, v[p].z, v[p].w};
+      const int t = threadIdx.x + p * TTHREADS;
+      if (t >= TASKS) break;
+      const int j = t % ROWS, kq = t / ROWS;
+      uint32_t hi[4], lo[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const __nv_bfloat16 h = __float2bfloat16_rn(f[i]);
-        const __nv_bfloat16 l = __float2bfloat16_rn(f[i] - __bfloat162float(h));
-        const uint32_t off = (kk & 7) * 2;
-        asm volatile("st.shared.b16 [%0], %1;" ::"r"(swz(fbase, j + i, kk >> 3) + off),
-                     "h"(*reinterpret_cast<const unsigned short*>(&h)));
-        asm volatile("st.shared.b16 [%0], %1;" ::"r"(swz(fbase, ROWS + j + i, kk >> 3) + off),
-                     "h"(*reinterpret_cast<const unsigned short*>(&l)));
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(v[p][2 * i]);
+        const __nv_bfloat16 h1 = __float2bfloat16_rn(v[p][2 * i + 1]);
+        const __nv_bfloat16 l0 = __float2bfloat16_rn(v[p][2 * i] - __bfloat162float(h0));
+        const __nv_bfloat16 l1 = __float2bfloat16_rn(v[p][2 * i + 1] - __bfloat162float(h1));
+        hi[i] = static_cast<uint32_t>(*reinterpret_cast<const unsigned short*>(&h0)) |
+                (static_cast<uint32_t>(*reinterpret_cast<const unsigned short*>(&h1)) << 16);
+        lo[i] = static_cast<uint32_t>(*reinterpret_cast<const unsigned short*>(&l0)) |
+                (static_cast<uint32_t>(*reinterpret_cast<const unsigned short*>(&l1)) << 16);
       }
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(swz(fbase, j, kq)), "r"(hi[0]),
+                   "r"(hi[1]), "r"(hi[2]), "r"(hi[3]));
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(swz(fbase, ROWS + j, kq)),
+                   "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]));
     }
   }
 };
@@ -941,11 +940,16 @@ cudaError_t launch_colmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int6
 #undef CALL_COL
 }
 
-// The fused row product (k_rowmma_cl) serves ranks <= 64 unless MLRA_THIN_CL=0
-// (the range kernel + prep launch; read per call for A/B runs and tests).
+// The fused row product (k_rowmma_cl) serves ranks <= 32 by default: at r = 64
+// its in-kernel factor split (64 x 64 fp32 per unit) costs more than the prep
+// launch it saves (cfg4, r = 64: 2.38 vs 2.28 ms per step; cfg2 / cfg3 at r = 16 / 8
+// gain, profiles/r04/). MLRA_THIN_CL=1 forces it for r <= 64, MLRA_THIN_CL=0
+// selects the range kernel + prep launch (read per call: A/B runs and tests).
 bool thin_fused_ok(int64_t r) {
   const char* e = getenv("MLRA_THIN_CL");
-  return r > 0 && r <= 64 && !(e && e[0] == '0');
+  if (e && e[0] == '0') return false;
+  const int64_t max_r = (e && e[0] == '1') ? 64 : 32;
+  return r > 0 && r <= max_r;
 }
 
 cudaError_t launch_rowmma_fused(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
