@@ -1364,7 +1364,7 @@ mlra_status mlra_lora_forward(const mlra_lora* L, const void* x, int64_t ldx, in
   if (!flags) return fail(MLRA_ERR_CUDA, "workspace allocation failed");
   // K4: xb = x·B (matmul(t, x, B), lora.cpp:68), finished with bf16(s·xb) zero
   // padded to rp columns: the extra-K LoRA operand of the GEMM
-  if (mlra::thin_fused_ok(r)) {
+  if (mlra::thin_fused_ok(r, m)) {
     // one launch: B is split in the kernel, A's padded operand and the flags
     // are the launch's post jobs (no prep launch in front of it)
     mlra::ThinOut o;
@@ -1440,7 +1440,7 @@ mlra_status mlra_lora_backward(const mlra_lora* L, const void* x, int64_t ldx, c
   // Fused row product (r <= 64): A is split inside it and B's operand and the
   // flags are its post jobs; the planes of xb and the column products' counters
   // (the side stream's inputs) are a prep launch on the side stream.
-  const bool fused = mlra::thin_fused_ok(r);
+  const bool fused = mlra::thin_fused_ok(r, m);
   mlra::PrepBatch pb, pbs;  // pb: main stream (prep launch or the row kernel's post jobs)
   Planes at, xbt, dyat;
   ThinWs w_row, w_da, w_db;

@@ -182,7 +182,7 @@ cudaError_t launch_rowmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int6
 // out[m x r] = act[m x kd] · F for an fp32 factor F [kd x r] (ld ldf), r <= 64, on
 // the cluster kernel (k_rowmma_cl: factor split in-kernel, no counters); `post`
 // (the pass's small jobs) runs inside the launch after its PDL wait.
-bool thin_fused_ok(int64_t r);
+bool thin_fused_ok(int64_t r, int64_t m);
 cudaError_t launch_rowmma_fused(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
                                 const float* F, int64_t ldf, int64_t r, const ThinOut& o,
                                 const PrepBatch& post, cudaStream_t st);

@@ -940,16 +940,21 @@ cudaError_t launch_colmma(const __nv_bfloat16* act, int64_t lda, int64_t m, int6
 #undef CALL_COL
 }
 
-// The fused row product (k_rowmma_cl) serves ranks <= 32 by default: at r = 64
-// its in-kernel factor split (64 x 64 fp32 per unit) costs more than the prep
-// launch it saves (cfg4, r = 64: 2.38 vs 2.28 ms per step; cfg2 / cfg3 at r = 16 / 8
-// gain, profiles/r04/). MLRA_THIN_CL=1 forces it for r <= 64, MLRA_THIN_CL=0
-// selects the range kernel + prep launch (read per call: A/B runs and tests).
-bool thin_fused_ok(int64_t r) {
+// The fused row product (k_rowmma_cl) serves ranks <= 32 above 512 tokens by
+// default: at r = 64 its in-kernel factor split (64 x 64 fp32 per unit) costs
+// more than the prep launch it saves (cfg4, r = 64: 2.38 vs 2.28 ms per step),
+// and at <= 512 tokens (<= 4 token tiles: <= 64 CTAs in 16-CTA clusters) its
+// serial phases cost more than the prep launch too (cfg1: 98.0 vs 96.5 us per
+// graphed step); cfg2 / cfg3 at r = 16 / 8 and 1024+ tokens gain (profiles/r04/,
+// profiles/r05/). MLRA_THIN_CL=1 forces it for r <= 64 at any token count,
+// MLRA_THIN_CL=0 selects the range kernel + prep launch (read per call: A/B
+// runs and tests).
+constexpr int64_t kThinFusedMinTokens = 513;
+bool thin_fused_ok(int64_t r, int64_t m) {
   const char* e = getenv("MLRA_THIN_CL");
   if (e && e[0] == '0') return false;
-  const int64_t max_r = (e && e[0] == '1') ? 64 : 32;
-  return r > 0 && r <= max_r;
+  if (e && e[0] == '1') return r > 0 && r <= 64;
+  return r > 0 && r <= 32 && m >= kThinFusedMinTokens;
 }
 
 cudaError_t launch_rowmma_fused(const __nv_bfloat16* act, int64_t lda, int64_t m, int64_t kd,
